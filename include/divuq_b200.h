@@ -1,0 +1,215 @@
+/* divuq_b200.h -- C ABI of the B200-native divergence-uncertainty hot path.
+ *
+ * Drop-in boundary for the reference package `divuq`
+ * (/root/reference/pkg/src/divuq).  The reference is pure Python and has no
+ * FFI; its only pluggable seam is the per-index kernel run by
+ * parallel_map (parallel.py:65-116) under the public functions re-exported by
+ * __init__.py:9-96.  Each entry point below replaces one of those functions
+ * (file:line cited) and is what a ctypes binding inside the reference would
+ * call (INTEGRATION.md shows the stub).
+ *
+ * Conventions
+ *   - plain pointers + sizes only; no torch or CUDA types in signatures
+ *     (`stream` is a cudaStream_t passed as void*, NULL = legacy default);
+ *   - `divuq_*`      : DEVICE pointers, asynchronous on `stream`, caller owns
+ *                      every buffer, inputs are never modified;
+ *   - `divuq_host_*` : HOST pointers (pinned or pageable), synchronous; the
+ *                      library stages device memory itself and checks the
+ *                      validation word before returning;
+ *   - arrays are flat row-major, x fastest: 2D index j*nx+i (grid.py:3-8),
+ *     3D index (k*ny+j)*nx+i; ensembles are member-major (M, C, N) like the
+ *     DIVUQ1 container (io.py:51-53);
+ *   - grids need >= 2 vertices per axis and positive spacing (grid.py:42-46);
+ *   - `err_word` (device int32, may be NULL) receives DIVUQ_ERRBIT_* bits
+ *     when an input is non-finite or a sigma is negative -- the reference's
+ *     construction-time checks (grid.py:26-27, divergence.py:34-35,
+ *     gaussian.py:28-29) folded into the kernels at zero extra HBM traffic;
+ *   - return value: 0 ok, < 0 DIVUQ_E* argument/validation error, > 0 a
+ *     cudaError_t.
+ *   - optional outputs may be NULL (not computed / not written).
+ *
+ * Probability maps: the reference has no public name for them; they are its
+ * private _tail_probs (lcp.py:48-68): p_src = P(div > t) = "above" at
+ * theta = t, p_snk = P(div < -t) = "below" at theta = -t (P(div <= -t) on
+ * the sigma == 0 tie, lcp.py:56-59).
+ */
+#ifndef DIVUQ_B200_H
+#define DIVUQ_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DIVUQ_ABI_VERSION 1
+
+#define DIVUQ_OK 0
+#define DIVUQ_EINVAL (-1)          /* null pointer / bad size */
+#define DIVUQ_EGRID (-2)           /* grid smaller than 2 per axis or spacing <= 0 */
+#define DIVUQ_EMEMBERS (-3)        /* fewer than 2 ensemble members */
+#define DIVUQ_ESAMPLES (-4)        /* fewer than 2 Monte Carlo samples */
+#define DIVUQ_ENONFINITE (-10)     /* an input value is NaN / inf */
+#define DIVUQ_ENEGSIGMA (-11)      /* a sigma input is negative */
+
+#define DIVUQ_ERRBIT_NONFINITE 1
+#define DIVUQ_ERRBIT_NEGSIGMA 2
+
+int divuq_abi_version(void);
+const char* divuq_status_string(int status);
+
+/* ---- K2: analytic propagation + probability map ----------------------
+ * Replaces propagate_divergence (divergence.py:48-70; per-index body
+ * stencils.py:54-84) and _tail_probs (lcp.py:48-68).  fp64 results are
+ * bit-identical to the reference.  s_u/s_v may be NULL only when
+ * out_sigma/out_p_src/out_p_snk are all NULL: that is
+ * divergence_deterministic (divergence.py:41-45). */
+int divuq_propagate2d_f64(const double* mu_u, const double* mu_v,
+                          const double* s_u, const double* s_v,
+                          int64_t nx, int64_t ny, double dx, double dy, double t,
+                          double* out_mu, double* out_sigma,
+                          double* out_p_src, double* out_p_snk,
+                          int32_t* err_word, void* stream);
+int divuq_propagate2d_f32(const float* mu_u, const float* mu_v,
+                          const float* s_u, const float* s_v,
+                          int64_t nx, int64_t ny, double dx, double dy, double t,
+                          float* out_mu, float* out_sigma,
+                          float* out_p_src, float* out_p_snk,
+                          int32_t* err_word, void* stream);
+
+/* 3D (no reference code; restates stencils.py:46-51 for z).  Arrays hold the
+ * z-slab [z0, z0+nz_local) of a grid with nz_global planes.  halo_* are the
+ * (mu_w, s_w) planes at global z0-1 / z0+nz_local, required only when those
+ * planes exist (z0 > 0 / z0+nz_local < nz_global).  Only local planes
+ * [k_begin, k_end) are computed (lets a caller overlap the halo exchange
+ * with the interior). */
+int divuq_propagate3d_f32(const float* mu_u, const float* mu_v, const float* mu_w,
+                          const float* s_u, const float* s_v, const float* s_w,
+                          const float* halo_lo_mu_w, const float* halo_lo_s_w,
+                          const float* halo_hi_mu_w, const float* halo_hi_s_w,
+                          int64_t nx, int64_t ny, int64_t nz_local,
+                          int64_t z0, int64_t nz_global, int64_t k_begin, int64_t k_end,
+                          double dx, double dy, double dz, double t,
+                          float* out_mu, float* out_sigma,
+                          float* out_p_src, float* out_p_snk,
+                          int32_t* err_word, void* stream);
+int divuq_propagate3d_f64(const double* mu_u, const double* mu_v, const double* mu_w,
+                          const double* s_u, const double* s_v, const double* s_w,
+                          const double* halo_lo_mu_w, const double* halo_lo_s_w,
+                          const double* halo_hi_mu_w, const double* halo_hi_s_w,
+                          int64_t nx, int64_t ny, int64_t nz_local,
+                          int64_t z0, int64_t nz_global, int64_t k_begin, int64_t k_end,
+                          double dx, double dy, double dz, double t,
+                          double* out_mu, double* out_sigma,
+                          double* out_p_src, double* out_p_snk,
+                          int32_t* err_word, void* stream);
+
+/* Probability map of an existing Gaussian scalar field: _tail_probs
+ * (lcp.py:48-68) elementwise.  out_below = P(X <= theta), out_above =
+ * P(X > theta); either may be NULL. */
+int divuq_tail_probs_f64(const double* mu, const double* sigma, int64_t n, double theta,
+                         double* out_below, double* out_above, int32_t* err_word, void* stream);
+int divuq_tail_probs_f32(const float* mu, const float* sigma, int64_t n, double theta,
+                         float* out_below, float* out_above, int32_t* err_word, void* stream);
+
+/* ---- K1: ensemble moments ---------------------------------------------
+ * Replaces fit_gaussian (gaussian.py:35-45): mean = sequential sum / M,
+ * sigma = sqrt(two-pass sum of squared deviations / (M-1)); fp64 is
+ * bit-identical to numpy's mean / std(ddof=1).  members: (M, C, n_points)
+ * with member stride C*n_points; outputs (C, n_points). */
+int divuq_fit_gaussian_f64(const double* members, int64_t n_members, int64_t n_components,
+                           int64_t n_points, double* out_mu, double* out_sigma,
+                           int32_t* err_word, void* stream);
+int divuq_fit_gaussian_f32(const float* members, int64_t n_members, int64_t n_components,
+                           int64_t n_points, float* out_mu, float* out_sigma,
+                           int32_t* err_word, void* stream);
+
+/* ---- K3: fused ensemble -> moments -> divergence -> probabilities --------
+ * fit_gaussian followed by propagate_divergence and _tail_probs in one pass
+ * over the members.  members: (M, 2, nx*ny) [2D] or (M, 3, nx*ny*nz_local)
+ * [3D slab].  out_mom_mu/out_mom_sigma (optional, (C, N)) receive the
+ * fitted moments.  3D halos are REDUCED w moments (mu_w, s_w) of the
+ * neighbouring planes (compute them with divuq_fit_gaussian_f32 on the
+ * owner's edge plane). */
+int divuq_ensemble_divergence2d_f32(const float* members, int64_t n_members,
+                                    int64_t nx, int64_t ny, double dx, double dy, double t,
+                                    float* out_mu, float* out_sigma,
+                                    float* out_p_src, float* out_p_snk,
+                                    float* out_mom_mu, float* out_mom_sigma,
+                                    int32_t* err_word, void* stream);
+int divuq_ensemble_divergence3d_f32(const float* members, int64_t n_members,
+                                    const float* halo_lo_mu_w, const float* halo_lo_s_w,
+                                    const float* halo_hi_mu_w, const float* halo_hi_s_w,
+                                    int64_t nx, int64_t ny, int64_t nz_local,
+                                    int64_t z0, int64_t nz_global, int64_t k_begin, int64_t k_end,
+                                    double dx, double dy, double dz, double t,
+                                    float* out_mu, float* out_sigma,
+                                    float* out_p_src, float* out_p_snk,
+                                    float* out_mom_mu, float* out_mom_sigma,
+                                    int32_t* err_word, void* stream);
+
+/* ---- K4: Monte Carlo estimator ------------------------------------------
+ * Replaces mc_divergence (mc.py:94-117) with a Philox4x32-10 + Box-Muller
+ * stream (contract: oracle/philox.py).  Inputs: the full grid model (fp64).
+ * Rows [row_begin, row_end) are estimated (vertex sharding needs no
+ * communication: draws are keyed by global vertex).  Outputs hold
+ * (row_end-row_begin)*nx values.  scratch: divuq_mc_scratch_bytes() bytes of
+ * device memory. */
+int64_t divuq_mc_scratch_bytes(int64_t nx, int64_t row_begin, int64_t row_end, int64_t n_samples);
+int divuq_mc_divergence2d_f64(const double* mu_u, const double* mu_v,
+                              const double* s_u, const double* s_v,
+                              int64_t nx, int64_t ny, double dx, double dy,
+                              int64_t n_samples, uint64_t seed,
+                              int64_t row_begin, int64_t row_end,
+                              double* out_mean, double* out_std, void* scratch,
+                              int32_t* err_word, void* stream);
+
+/* ---- K5: synthetic inputs (bench only; BASELINE.json configs) -----------
+ * bumps: n_bumps x 5 floats (cx, cy, cz, amp, 1/width^2) in world units on
+ * the device.  Writes the model (n_members == 0: mu_u, mu_v[, mu_w], s_u,
+ * s_v[, s_w] into out[0..2C-1]) or the members (M, C, nx*ny*nz_local). */
+int divuq_gen_field_f32(const float* bumps, int n_bumps, int dims,
+                        int64_t nx, int64_t ny, int64_t nz_local, int64_t z0,
+                        double dx, double dy, double dz,
+                        double vortex_amp, double vortex_cx, double vortex_cy, double vortex_r,
+                        double shear_amp, uint64_t seed, double sig_lo, double sig_hi,
+                        int sigma_mode, int64_t n_members, float* const* out, float* members,
+                        void* stream);
+
+/* ---- host-buffer entry points (the reference-facing path) ----------------
+ * Same semantics as the device versions; synchronous; `device` = CUDA
+ * ordinal.  Host buffers may be pinned (direct DMA) or pageable.  The 3D
+ * variant pipelines z-chunks: host->device copies, the kernel and
+ * device->host copies of consecutive chunks overlap on separate streams. */
+int divuq_host_propagate2d_f64(const double* mu_u, const double* mu_v,
+                               const double* s_u, const double* s_v,
+                               int64_t nx, int64_t ny, double dx, double dy, double t,
+                               double* out_mu, double* out_sigma,
+                               double* out_p_src, double* out_p_snk, int device);
+int divuq_host_propagate3d_f32(const float* mu_u, const float* mu_v, const float* mu_w,
+                               const float* s_u, const float* s_v, const float* s_w,
+                               int64_t nx, int64_t ny, int64_t nz,
+                               double dx, double dy, double dz, double t,
+                               float* out_mu, float* out_sigma,
+                               float* out_p_src, float* out_p_snk,
+                               int64_t chunk_planes, int device);
+int divuq_host_tail_probs_f64(const double* mu, const double* sigma, int64_t n, double theta,
+                              double* out_below, double* out_above, int device);
+int divuq_host_fit_gaussian_f64(const double* members, int64_t n_members, int64_t n_components,
+                                int64_t n_points, double* out_mu, double* out_sigma, int device);
+int divuq_host_ensemble_divergence2d_f32(const float* members, int64_t n_members,
+                                         int64_t nx, int64_t ny, double dx, double dy, double t,
+                                         float* out_mu, float* out_sigma,
+                                         float* out_p_src, float* out_p_snk,
+                                         float* out_mom_mu, float* out_mom_sigma, int device);
+int divuq_host_mc_divergence2d_f64(const double* mu_u, const double* mu_v,
+                                   const double* s_u, const double* s_v,
+                                   int64_t nx, int64_t ny, double dx, double dy,
+                                   int64_t n_samples, uint64_t seed,
+                                   double* out_mean, double* out_std, int device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DIVUQ_B200_H */

@@ -1,0 +1,91 @@
+"""ctypes binding of libdivuq_b200.so (declared in include/divuq_b200.h).
+
+There is deliberately no fallback: if the CUDA library is missing or does not
+load, importing the package raises.  Build it with
+``python -c "import __graft_entry__ as g; g.build()"`` (or ``make -C
+paper_2510_01190_b200/csrc``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdivuq_b200.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: the B200 CUDA library has not been built "
+        "(run __graft_entry__.build()); there is no CPU fallback"
+    )
+
+lib = ctypes.CDLL(LIB_PATH)
+
+_p = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_u64 = ctypes.c_uint64
+_f64 = ctypes.c_double
+_int = ctypes.c_int
+
+# name -> (restype, argtypes)
+SIGNATURES = {
+    "divuq_abi_version": (_int, []),
+    "divuq_status_string": (ctypes.c_char_p, [_int]),
+    "divuq_propagate2d_f64": (_int, [_p] * 4 + [_i64, _i64, _f64, _f64, _f64] + [_p] * 4 + [_p, _p]),
+    "divuq_propagate2d_f32": (_int, [_p] * 4 + [_i64, _i64, _f64, _f64, _f64] + [_p] * 4 + [_p, _p]),
+    "divuq_propagate3d_f32": (
+        _int, [_p] * 10 + [_i64] * 7 + [_f64] * 4 + [_p] * 4 + [_p, _p]),
+    "divuq_propagate3d_f64": (
+        _int, [_p] * 10 + [_i64] * 7 + [_f64] * 4 + [_p] * 4 + [_p, _p]),
+    "divuq_fit_gaussian_f64": (_int, [_p, _i64, _i64, _i64, _p, _p, _p, _p]),
+    "divuq_fit_gaussian_f32": (_int, [_p, _i64, _i64, _i64, _p, _p, _p, _p]),
+    "divuq_ensemble_divergence2d_f32": (
+        _int, [_p, _i64, _i64, _i64, _f64, _f64, _f64] + [_p] * 6 + [_p, _p]),
+    "divuq_ensemble_divergence3d_f32": (
+        _int, [_p, _i64] + [_p] * 4 + [_i64] * 7 + [_f64] * 4 + [_p] * 6 + [_p, _p]),
+    "divuq_tail_probs_f64": (_int, [_p, _p, _i64, _f64, _p, _p, _p, _p]),
+    "divuq_tail_probs_f32": (_int, [_p, _p, _i64, _f64, _p, _p, _p, _p]),
+    "divuq_host_tail_probs_f64": (_int, [_p, _p, _i64, _f64, _p, _p, _int]),
+    "divuq_mc_scratch_bytes": (_i64, [_i64, _i64, _i64, _i64]),
+    "divuq_mc_divergence2d_f64": (
+        _int, [_p] * 4 + [_i64, _i64, _f64, _f64, _i64, _u64, _i64, _i64] + [_p] * 3 + [_p, _p]),
+    "divuq_gen_field_f32": (
+        _int, [_p, _int, _int, _i64, _i64, _i64, _i64, _f64, _f64, _f64, _f64, _f64, _f64, _f64,
+               _f64, _u64, _f64, _f64, _int, _i64, _p, _p, _p]),
+    "divuq_host_propagate2d_f64": (
+        _int, [_p] * 4 + [_i64, _i64, _f64, _f64, _f64] + [_p] * 4 + [_int]),
+    "divuq_host_propagate3d_f32": (
+        _int, [_p] * 6 + [_i64] * 3 + [_f64] * 4 + [_p] * 4 + [_i64, _int]),
+    "divuq_host_fit_gaussian_f64": (_int, [_p, _i64, _i64, _i64, _p, _p, _int]),
+    "divuq_host_ensemble_divergence2d_f32": (
+        _int, [_p, _i64, _i64, _i64, _f64, _f64, _f64] + [_p] * 6 + [_int]),
+    "divuq_host_mc_divergence2d_f64": (
+        _int, [_p] * 4 + [_i64, _i64, _f64, _f64, _i64, _u64, _p, _p, _int]),
+}
+
+for _name, (_res, _args) in SIGNATURES.items():
+    _fn = getattr(lib, _name)  # AttributeError here = header/library mismatch
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+ABI_VERSION = lib.divuq_abi_version()
+if ABI_VERSION != 1:
+    raise ImportError(f"libdivuq_b200 ABI {ABI_VERSION} != 1")
+
+# status codes (include/divuq_b200.h)
+OK, EINVAL, EGRID, EMEMBERS, ESAMPLES, ENONFINITE, ENEGSIGMA = 0, -1, -2, -3, -4, -10, -11
+
+
+class DivuqError(RuntimeError):
+    """CUDA-side failure (status > 0 is a cudaError_t)."""
+
+
+def check(status: int) -> None:
+    """Map a C status to the reference's exception types."""
+    if status == OK:
+        return
+    msg = lib.divuq_status_string(status).decode()
+    if status < 0:
+        raise ValueError(msg)
+    raise DivuqError(f"CUDA error {status}: {msg}")

@@ -1,0 +1,234 @@
+"""Drop-in replacements for the reference's public hot-path functions.
+
+Same names, signatures, return types and exceptions as
+/root/reference/pkg/src/divuq (re-exported by its __init__.py:9-96).  Each
+function hands host (numpy) buffers to a ``divuq_host_*`` entry point of the
+C ABI (include/divuq_b200.h), which stages them into HBM, runs the sm_100a
+kernel and copies the result back -- the "reference-facing" path the e2e
+benchmark times.  There is no CPU fallback: without the CUDA library the
+package does not import.
+"""
+
+from __future__ import annotations
+
+from typing import NamedTuple
+
+import numpy as np
+
+from ._lib import check as _check
+from ._lib import lib
+from .types import (
+    Ensemble2,
+    GaussianScalarField,
+    GaussianScalarField3,
+    GaussianVectorField,
+    GaussianVectorField3,
+    McConfig,
+    McDivergenceEstimate,
+    ParallelConfig,
+    ScalarField2,
+    VectorField2,
+)
+
+_DEVICE = 0
+
+
+def set_device(ordinal: int) -> None:
+    """CUDA device used by the host-buffer entry points (default 0)."""
+    global _DEVICE
+    _DEVICE = int(ordinal)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data
+
+
+def _c64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def fit_gaussian(ensemble: Ensemble2) -> GaussianVectorField:
+    """Sample mean and ddof=1 std per vertex/component (gaussian.py:35-45).
+
+    Bit-identical to the reference (sequential member sum, two-pass variance).
+    """
+    stacked = _c64(ensemble.stacked())  # (M, 2, N)
+    m, c, n = stacked.shape
+    mu = np.empty((c, n))
+    sg = np.empty((c, n))
+    _check(lib.divuq_host_fit_gaussian_f64(_p(stacked), m, c, n, _p(mu), _p(sg), _DEVICE))
+    return GaussianVectorField(ensemble.grid, mu[0], mu[1], sg[0], sg[1])
+
+
+def propagate_divergence(model, config: ParallelConfig | None = None):
+    """Divergence distribution of an independent-Gaussian model (divergence.py:48-70).
+
+    2D (``GaussianVectorField``) results are bit-identical to the reference;
+    ``config`` is accepted and ignored (one launch covers every vertex, and the
+    output is the same for any setting -- the reference's own contract,
+    parallel.py:1-6).  A ``GaussianVectorField3`` runs the 3D restatement.
+    """
+    if isinstance(model, GaussianVectorField3):
+        res = propagate_with_probabilities3d(model, 0.0, probabilities=False)
+        return res.field
+    return propagate_with_probabilities(model, 0.0, probabilities=False).field
+
+
+class Propagation(NamedTuple):
+    field: object          # GaussianScalarField / GaussianScalarField3
+    p_src: np.ndarray | None   # P(div > t)
+    p_snk: np.ndarray | None   # P(div < -t)
+
+
+def propagate_with_probabilities(model: GaussianVectorField, t: float = 0.0, *,
+                                 probabilities: bool = True) -> Propagation:
+    """Fused hot path: mu_div, sigma_div and the source/sink maps in one pass.
+
+    p_src = P(div > t) and p_snk = P(div < -t) with the reference's
+    ``_tail_probs`` semantics (lcp.py:48-68), computed in the same kernel.
+    """
+    g = model.grid
+    n = g.n_vertices
+    mu = np.empty(n)
+    sg = np.empty(n)
+    ps = np.empty(n) if probabilities else None
+    pk = np.empty(n) if probabilities else None
+    _check(lib.divuq_host_propagate2d_f64(
+        _p(model.mu_u), _p(model.mu_v), _p(model.sigma_u), _p(model.sigma_v), g.nx, g.ny,
+        float(g.dx), float(g.dy), float(t), _p(mu), _p(sg), _p(ps), _p(pk), _DEVICE))
+    return Propagation(GaussianScalarField(g, mu, sg), ps, pk)
+
+
+def propagate_with_probabilities3d(model: GaussianVectorField3, t: float = 0.0, *,
+                                   probabilities: bool = True, chunk_planes: int = 32) -> Propagation:
+    """3D twin (fp32 models use the pipelined host entry point; fp64 models
+    are staged through torch and run the fp64 kernel)."""
+    g = model.grid
+    n = g.n_vertices
+    dt = model.dtype
+    ins = [model.mu_u, model.mu_v, model.mu_w, model.sigma_u, model.sigma_v, model.sigma_w]
+    mu = np.empty(n, dtype=dt)
+    sg = np.empty(n, dtype=dt)
+    ps = np.empty(n, dtype=dt) if probabilities else None
+    pk = np.empty(n, dtype=dt) if probabilities else None
+    if dt == np.float32:
+        _check(lib.divuq_host_propagate3d_f32(
+            *(_p(a) for a in ins), g.nx, g.ny, g.nz, float(g.dx), float(g.dy), float(g.dz),
+            float(t), _p(mu), _p(sg), _p(ps), _p(pk), int(chunk_planes), _DEVICE))
+    else:
+        import torch
+
+        from . import device as dev
+
+        with torch.cuda.device(_DEVICE):
+            tens = [torch.from_numpy(np.array(a)).cuda() for a in ins]
+            outs = ("mu", "sigma", "p_src", "p_snk") if probabilities else ("mu", "sigma")
+            o = dev.propagate3d(*tens, g.nx, g.ny, g.nz, g.dx, g.dy, g.dz, t, outputs=outs)
+            mu[:] = o["mu"].cpu().numpy()
+            sg[:] = o["sigma"].cpu().numpy()
+            if probabilities:
+                ps[:] = o["p_src"].cpu().numpy()
+                pk[:] = o["p_snk"].cpu().numpy()
+    return Propagation(GaussianScalarField3(g, mu, sg), ps, pk)
+
+
+def divergence_deterministic(fld: VectorField2) -> ScalarField2:
+    """du/dx + dv/dy with the one-sided boundary rule (divergence.py:41-45)."""
+    g = fld.grid
+    out = np.empty(g.n_vertices)
+    _check(lib.divuq_host_propagate2d_f64(
+        _p(fld.u), _p(fld.v), None, None, g.nx, g.ny, float(g.dx), float(g.dy), 0.0, _p(out),
+        None, None, None, _DEVICE))
+    return ScalarField2(g, out)
+
+
+def stencil_distribution(neighbors, spacing: tuple[float, float]) -> tuple[float, float]:
+    """Single interior vertex (divergence.py:73-85): four scalars, host-side by
+    design -- a kernel launch would cost more than the math."""
+    (mu_um, s_um), (mu_up, s_up), (mu_vm, s_vm), (mu_vp, s_vp) = neighbors
+    dx, dy = spacing
+    cx, cy = 1.0 / (2.0 * dx), 1.0 / (2.0 * dy)
+    mu = mu_up * cx - mu_um * cx + mu_vp * cy - mu_vm * cy
+    var = (s_up * cx) ** 2 + (s_um * cx) ** 2 + (s_vp * cy) ** 2 + (s_vm * cy) ** 2
+    return float(mu), float(np.sqrt(var))
+
+
+def tail_probs(mu, sigma, isovalue: float):
+    """(P[X <= theta], P[X > theta]) per vertex (lcp.py:48-68), on the GPU."""
+    mu = _c64(mu)
+    sigma = _c64(sigma)
+    if mu.shape != sigma.shape:
+        raise ValueError("mu and sigma must have the same shape")
+    below = np.empty_like(mu)
+    above = np.empty_like(mu)
+    _check(lib.divuq_host_tail_probs_f64(_p(mu), _p(sigma), mu.size, float(isovalue), _p(below),
+                                         _p(above), _DEVICE))
+    return below, above
+
+
+def source_probability(fld: GaussianScalarField, t: float = 0.0) -> np.ndarray:
+    """P(div > t) per vertex: the reference's 'above' tail at isovalue t."""
+    return tail_probs(fld.mu, fld.sigma, t)[1]
+
+
+def sink_probability(fld: GaussianScalarField, t: float = 0.0) -> np.ndarray:
+    """P(div < -t) per vertex (P(div <= -t) on the sigma == 0 tie, lcp.py:56-59)."""
+    return tail_probs(fld.mu, fld.sigma, -t)[0]
+
+
+def mc_divergence(model: GaussianVectorField, config: McConfig) -> McDivergenceEstimate:
+    """Per-vertex empirical divergence mean/std (mc.py:94-117), Philox stream.
+
+    Statistically equivalent to the reference (its splitmix64 + AS241 draws
+    are replaced by Philox4x32-10 + Box-Muller as the north star mandates);
+    deterministic in (model, seed, n) and invariant to launch shape.
+    """
+    if config.n_samples < 2:
+        raise ValueError("mc_divergence needs n_samples >= 2")
+    g = model.grid
+    n = g.n_vertices
+    mean = np.empty(n)
+    std = np.empty(n)
+    _check(lib.divuq_host_mc_divergence2d_f64(
+        _p(model.mu_u), _p(model.mu_v), _p(model.sigma_u), _p(model.sigma_v), g.nx, g.ny,
+        float(g.dx), float(g.dy), int(config.n_samples), int(config.seed), _p(mean), _p(std),
+        _DEVICE))
+    return McDivergenceEstimate(g, mean, std, config.n_samples)
+
+
+def error_metrics(estimate: McDivergenceEstimate, analytic: GaussianScalarField):
+    """(e_m, e_sigma, sse) between estimate and model (mc.py:159-175)."""
+    if estimate.grid != analytic.grid:
+        raise ValueError("estimate and analytic fields are on different grids")
+    dm = estimate.mean - analytic.mu
+    ds = estimate.std - analytic.sigma
+    return (
+        float(np.abs(dm).mean()),
+        float(np.abs(ds).mean()),
+        float(np.sum(dm**2) + np.sum(ds**2)),
+    )
+
+
+class EnsembleDivergence(NamedTuple):
+    model: GaussianVectorField      # fitted moments (fp32-rounded, returned as fp64)
+    field: GaussianScalarField
+    p_src: np.ndarray
+    p_snk: np.ndarray
+
+
+def ensemble_divergence(ensemble: Ensemble2, t: float = 0.0) -> EnsembleDivergence:
+    """Fused fp32 pipeline fit_gaussian -> propagate_divergence -> tail maps
+    (BASELINE config 1): one pass over the members on the GPU."""
+    g = ensemble.grid
+    stacked = np.ascontiguousarray(ensemble.stacked(), dtype=np.float32)
+    m = stacked.shape[0]
+    n = g.n_vertices
+    o = [np.empty(n, dtype=np.float32) for _ in range(4)]
+    mom_mu = np.empty((2, n), dtype=np.float32)
+    mom_sg = np.empty((2, n), dtype=np.float32)
+    _check(lib.divuq_host_ensemble_divergence2d_f32(
+        _p(stacked), m, g.nx, g.ny, float(g.dx), float(g.dy), float(t), *(_p(a) for a in o),
+        _p(mom_mu), _p(mom_sg), _DEVICE))
+    model = GaussianVectorField(g, mom_mu[0], mom_mu[1], mom_sg[0], mom_sg[1])
+    return EnsembleDivergence(model, GaussianScalarField(g, o[0], o[1]), o[2].astype(np.float64),
+                              o[3].astype(np.float64))

@@ -1,0 +1,698 @@
+// C ABI of the divergence-uncertainty hot path: launchers + host pipelines.
+// Declarations and reference citations: include/divuq_b200.h.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/divuq_b200.h"
+#include "gen.cuh"
+#include "mc.cuh"
+#include "stencil.cuh"
+
+using namespace divuq;
+
+namespace {
+
+#define DIVUQ_CUDA(call)                         \
+  do {                                           \
+    const int e_ = int(call);                    \
+    if (e_ != 0) return e_;                      \
+  } while (0)
+
+int sm_count() {
+  static std::mutex mu;
+  static std::unordered_map<int, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  cache[dev] = n > 0 ? n : 1;
+  return cache[dev];
+}
+
+template <typename K>
+int blocks_per_sm(K kernel, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> cache;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(reinterpret_cast<const void*>(kernel));
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem);
+  cache[reinterpret_cast<const void*>(kernel)] = n > 0 ? n : 1;
+  return cache[reinterpret_cast<const void*>(kernel)];
+}
+
+int64_t env_int(const char* name, int64_t dflt) {
+  const char* s = std::getenv(name);
+  return s ? std::atoll(s) : dflt;
+}
+
+bool aligned(const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+int grid_ok(int64_t nx, int64_t ny, double dx, double dy) {
+  if (nx < 2 || ny < 2) return DIVUQ_EGRID;
+  if (!(dx > 0.0) || !(dy > 0.0)) return DIVUQ_EGRID;
+  return DIVUQ_OK;
+}
+
+template <typename T>
+void set_coeffs(StencilParams<T>& p, double dx, double dy, double dz) {
+  // stencils.py:48-50: interior 1/(2h), boundary 1/h, evaluated in fp64
+  p.cx_in = T(1.0 / (2.0 * dx)); p.cx_bd = T(1.0 / dx);
+  p.cy_in = T(1.0 / (2.0 * dy)); p.cy_bd = T(1.0 / dy);
+  p.cz_in = T(1.0 / (2.0 * dz)); p.cz_bd = T(1.0 / dz);
+}
+
+template <typename T, int VEC, bool HAS_W, bool HAS_SIGMA, int SRC, int MR>
+int launch_stencil_impl(StencilParams<T> p, cudaStream_t s) {
+  using K = StencilKernel<T, VEC, HAS_W, HAS_SIGMA, SRC, MR>;
+  auto kern = stencil_kernel<T, VEC, HAS_W, HAS_SIGMA, SRC, MR>;
+  const int threads = 32 * kStencilTY;
+  const int64_t nk = p.kend - p.kbeg;
+  if (nk <= 0) return DIVUQ_OK;
+  p.tiles_x = (p.nx + K::TX - 1) / K::TX;
+  p.tiles_y = (p.ny + K::TY - 1) / K::TY;
+  const int64_t tiles = p.tiles_x * p.tiles_y;
+  const int64_t cap = int64_t(blocks_per_sm(kern, threads, 0)) * sm_count();
+  int64_t zc = env_int("DIVUQ_ZCHUNK", 0);
+  if (zc <= 0) {
+    // ~16 items per resident CTA keeps the round-robin tail small; >= 8
+    // planes per item amortises the 2-plane w prologue
+    const int64_t target = cap * 16;
+    zc = std::max<int64_t>(8, (nk * tiles + target - 1) / target);
+  }
+  p.zchunk = std::min<int64_t>(zc, nk);
+  p.n_items = tiles * ((nk + p.zchunk - 1) / p.zchunk);
+  const int64_t grid = std::min<int64_t>(p.n_items, cap);
+  kern<<<dim3(unsigned(grid)), dim3(32, kStencilTY), 0, s>>>(p);
+  return int(cudaGetLastError());
+}
+
+template <typename T, int VEC, bool HAS_W, int SRC>
+int dispatch_sigma(const StencilParams<T>& p, bool has_sigma, cudaStream_t s) {
+  if constexpr (SRC == kEnsemble) {
+    const int64_t m = p.n_members;
+    if (m <= 8) return launch_stencil_impl<T, VEC, HAS_W, true, SRC, 8>(p, s);
+    if (m <= 16) return launch_stencil_impl<T, VEC, HAS_W, true, SRC, 16>(p, s);
+    if (m <= 24) return launch_stencil_impl<T, VEC, HAS_W, true, SRC, 24>(p, s);
+    return launch_stencil_impl<T, VEC, HAS_W, true, SRC, 32>(p, s);
+  } else {
+    if (has_sigma) return launch_stencil_impl<T, VEC, HAS_W, true, SRC, 1>(p, s);
+    return launch_stencil_impl<T, VEC, HAS_W, false, SRC, 1>(p, s);
+  }
+}
+
+template <typename T, bool HAS_W, int SRC>
+int dispatch_vec(const StencilParams<T>& p, bool has_sigma, cudaStream_t s) {
+  constexpr int VW = (sizeof(T) == 4) ? 4 : 2;
+  bool vec = (p.nx % VW) == 0;
+  const void* ptrs[] = {p.mu_u, p.mu_v, p.mu_w, p.s_u, p.s_v, p.s_w, p.members,
+                        p.halo_lo_mu_w, p.halo_lo_s_w, p.halo_hi_mu_w, p.halo_hi_s_w,
+                        p.out_mu, p.out_sigma, p.out_psrc, p.out_psnk, p.out_mom_mu, p.out_mom_sigma};
+  for (const void* q : ptrs) vec = vec && aligned(q, 16);
+  if (SRC == kEnsemble) vec = vec && ((p.comp_stride % VW) == 0);
+  if (vec) return dispatch_sigma<T, VW, HAS_W, SRC>(p, has_sigma, s);
+  return dispatch_sigma<T, 1, HAS_W, SRC>(p, has_sigma, s);
+}
+
+template <typename T>
+StencilParams<T> blank_params() {
+  StencilParams<T> p;
+  std::memset(&p, 0, sizeof(p));
+  return p;
+}
+
+template <typename T>
+int propagate2d(const T* mu_u, const T* mu_v, const T* s_u, const T* s_v, int64_t nx, int64_t ny,
+                double dx, double dy, double t, T* out_mu, T* out_sigma, T* out_ps, T* out_pk,
+                int32_t* err, void* stream) {
+  if (int r = grid_ok(nx, ny, dx, dy)) return r;
+  if (!mu_u || !mu_v) return DIVUQ_EINVAL;
+  const bool has_sigma = out_sigma || out_ps || out_pk;
+  if (has_sigma && (!s_u || !s_v)) return DIVUQ_EINVAL;
+  StencilParams<T> p = blank_params<T>();
+  p.mu_u = mu_u; p.mu_v = mu_v; p.s_u = s_u; p.s_v = s_v;
+  p.nx = nx; p.ny = ny; p.nzl = 1; p.z0 = 0; p.nzg = 1; p.kbeg = 0; p.kend = 1;
+  set_coeffs(p, dx, dy, 1.0);
+  p.theta = T(t);
+  p.out_mu = out_mu; p.out_sigma = out_sigma; p.out_psrc = out_ps; p.out_psnk = out_pk;
+  p.err = err;
+  return dispatch_vec<T, false, kMoments>(p, has_sigma, static_cast<cudaStream_t>(stream));
+}
+
+template <typename T>
+int propagate3d(const T* mu_u, const T* mu_v, const T* mu_w, const T* s_u, const T* s_v, const T* s_w,
+                const T* hl_mu, const T* hl_s, const T* hh_mu, const T* hh_s, int64_t nx, int64_t ny,
+                int64_t nzl, int64_t z0, int64_t nzg, int64_t kb, int64_t ke, double dx, double dy,
+                double dz, double t, T* out_mu, T* out_sigma, T* out_ps, T* out_pk, int32_t* err,
+                void* stream) {
+  if (int r = grid_ok(nx, ny, dx, dy)) return r;
+  if (nzg < 2 || !(dz > 0.0)) return DIVUQ_EGRID;
+  if (nzl < 1 || z0 < 0 || z0 + nzl > nzg || kb < 0 || ke > nzl || kb > ke) return DIVUQ_EINVAL;
+  if (!mu_u || !mu_v || !mu_w) return DIVUQ_EINVAL;
+  const bool has_sigma = out_sigma || out_ps || out_pk;
+  if (has_sigma && (!s_u || !s_v || !s_w)) return DIVUQ_EINVAL;
+  if (z0 > 0 && (!hl_mu || (has_sigma && !hl_s))) return DIVUQ_EINVAL;
+  if (z0 + nzl < nzg && (!hh_mu || (has_sigma && !hh_s))) return DIVUQ_EINVAL;
+  StencilParams<T> p = blank_params<T>();
+  p.mu_u = mu_u; p.mu_v = mu_v; p.mu_w = mu_w; p.s_u = s_u; p.s_v = s_v; p.s_w = s_w;
+  p.halo_lo_mu_w = hl_mu; p.halo_lo_s_w = hl_s; p.halo_hi_mu_w = hh_mu; p.halo_hi_s_w = hh_s;
+  p.nx = nx; p.ny = ny; p.nzl = nzl; p.z0 = z0; p.nzg = nzg; p.kbeg = kb; p.kend = ke;
+  set_coeffs(p, dx, dy, dz);
+  p.theta = T(t);
+  p.out_mu = out_mu; p.out_sigma = out_sigma; p.out_psrc = out_ps; p.out_psnk = out_pk;
+  p.err = err;
+  return dispatch_vec<T, true, kMoments>(p, has_sigma, static_cast<cudaStream_t>(stream));
+}
+
+// ---- K1: per-point moments over members, all components ----------------
+template <typename T, int VEC, int MR>
+__global__ void __launch_bounds__(256) fit_kernel(const T* __restrict__ members, int64_t M, int64_t C,
+                                                  int64_t N, T* __restrict__ out_mu,
+                                                  T* __restrict__ out_sigma, int* err) {
+  const int64_t groups = N / VEC;
+  int errbits = 0;
+  for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < groups;
+       g += int64_t(gridDim.x) * blockDim.x) {
+    for (int64_t c = 0; c < C; ++c) {
+      Vec<T, VEC> mu, sg;
+      member_moments<T, VEC, MR>(members + c * N + g * VEC, C * N, int(M), mu, sg, errbits);
+      st_stream<T, VEC>(out_mu + c * N + g * VEC, mu);
+      st_stream<T, VEC>(out_sigma + c * N + g * VEC, sg);
+    }
+  }
+  flush_error(err, errbits);
+}
+
+template <typename T, int VEC, int MR>
+int launch_fit(const T* m, int64_t M, int64_t C, int64_t N, T* mu, T* sg, int32_t* err, cudaStream_t s) {
+  auto kern = fit_kernel<T, VEC, MR>;
+  const int64_t groups = N / VEC;
+  const int64_t cap = int64_t(blocks_per_sm(kern, 256, 0)) * sm_count();
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((groups + 255) / 256, cap));
+  kern<<<unsigned(grid), 256, 0, s>>>(m, M, C, N, mu, sg, err);
+  return int(cudaGetLastError());
+}
+
+template <typename T, int VEC>
+int fit_mr(const T* m, int64_t M, int64_t C, int64_t N, T* mu, T* sg, int32_t* err, cudaStream_t s) {
+  if (M <= 8) return launch_fit<T, VEC, 8>(m, M, C, N, mu, sg, err, s);
+  if (M <= 16) return launch_fit<T, VEC, 16>(m, M, C, N, mu, sg, err, s);
+  if (M <= 24) return launch_fit<T, VEC, 24>(m, M, C, N, mu, sg, err, s);
+  return launch_fit<T, VEC, 32>(m, M, C, N, mu, sg, err, s);
+}
+
+template <typename T>
+int fit_gaussian(const T* members, int64_t M, int64_t C, int64_t N, T* out_mu, T* out_sigma,
+                 int32_t* err, void* stream) {
+  if (!members || !out_mu || !out_sigma || C < 1 || N < 1) return DIVUQ_EINVAL;
+  if (M < 2) return DIVUQ_EMEMBERS;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  constexpr int VW = (sizeof(T) == 4) ? 4 : 2;
+  // wide vectors only while the M register-resident values stay small
+  const bool vec = M <= 16 && (N % VW) == 0 && aligned(members, 16) && aligned(out_mu, 16) &&
+                   aligned(out_sigma, 16);
+  if (vec) return fit_mr<T, VW>(members, M, C, N, out_mu, out_sigma, err, s);
+  return fit_mr<T, 1>(members, M, C, N, out_mu, out_sigma, err, s);
+}
+
+// ---- probability map on an existing Gaussian scalar field (lcp.py:48-68)
+template <typename T>
+__global__ void tail_probs_kernel(const T* __restrict__ mu, const T* __restrict__ sigma, int64_t n,
+                                  T theta, T* __restrict__ below, T* __restrict__ above, int* err) {
+  int errbits = 0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const T m = mu[i], s = sigma[i];
+    errbits |= check_value(m) | check_sigma(s);
+    if (below) below[i] = prob_below(m, s, theta);
+    if (above) above[i] = prob_above(m, s, theta);
+  }
+  flush_error(err, errbits);
+}
+
+template <typename T>
+int tail_probs(const T* mu, const T* sigma, int64_t n, double theta, T* below, T* above, int32_t* err,
+               void* stream) {
+  if (!mu || !sigma || n < 0) return DIVUQ_EINVAL;
+  if (n == 0 || (!below && !above)) return DIVUQ_OK;
+  const int64_t grid = std::min<int64_t>((n + 255) / 256, int64_t(sm_count()) * 8);
+  tail_probs_kernel<T><<<unsigned(grid), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      mu, sigma, n, T(theta), below, above, err);
+  return int(cudaGetLastError());
+}
+
+int check_err_word(const int32_t* d_err, cudaStream_t s, int* status) {
+  int32_t h = 0;
+  DIVUQ_CUDA(cudaMemcpyAsync(&h, d_err, sizeof(h), cudaMemcpyDeviceToHost, s));
+  DIVUQ_CUDA(cudaStreamSynchronize(s));
+  *status = (h & DIVUQ_ERRBIT_NONFINITE) ? DIVUQ_ENONFINITE
+            : (h & DIVUQ_ERRBIT_NEGSIGMA) ? DIVUQ_ENEGSIGMA : DIVUQ_OK;
+  return 0;
+}
+
+// RAII device scratch from the stream-ordered pool; released with a
+// synchronising cudaFree so no stream of the call can still be using it
+struct DevBuf {
+  void* p = nullptr;
+  cudaError_t alloc(size_t bytes, cudaStream_t st) { return cudaMallocAsync(&p, bytes ? bytes : 1, st); }
+  ~DevBuf() { if (p) cudaFree(p); }
+  template <typename T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct StreamGuard {
+  cudaStream_t s = nullptr;
+  ~StreamGuard() { if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); } }
+};
+
+}  // namespace
+
+// =====================================================================
+extern "C" {
+
+int divuq_abi_version(void) { return DIVUQ_ABI_VERSION; }
+
+const char* divuq_status_string(int status) {
+  switch (status) {
+    case DIVUQ_OK: return "ok";
+    case DIVUQ_EINVAL: return "invalid argument (null pointer or bad size)";
+    case DIVUQ_EGRID: return "grid must be at least 2 per axis with positive spacing";
+    case DIVUQ_EMEMBERS: return "ensemble needs at least 2 members";
+    case DIVUQ_ESAMPLES: return "mc_divergence needs n_samples >= 2";
+    case DIVUQ_ENONFINITE: return "non-finite values are not allowed";
+    case DIVUQ_ENEGSIGMA: return "sigma must be non-negative";
+    default: return status > 0 ? cudaGetErrorString(cudaError_t(status)) : "unknown status";
+  }
+}
+
+int divuq_propagate2d_f64(const double* mu_u, const double* mu_v, const double* s_u, const double* s_v,
+                          int64_t nx, int64_t ny, double dx, double dy, double t, double* out_mu,
+                          double* out_sigma, double* out_p_src, double* out_p_snk, int32_t* err,
+                          void* stream) {
+  return propagate2d<double>(mu_u, mu_v, s_u, s_v, nx, ny, dx, dy, t, out_mu, out_sigma, out_p_src,
+                             out_p_snk, err, stream);
+}
+
+int divuq_propagate2d_f32(const float* mu_u, const float* mu_v, const float* s_u, const float* s_v,
+                          int64_t nx, int64_t ny, double dx, double dy, double t, float* out_mu,
+                          float* out_sigma, float* out_p_src, float* out_p_snk, int32_t* err,
+                          void* stream) {
+  return propagate2d<float>(mu_u, mu_v, s_u, s_v, nx, ny, dx, dy, t, out_mu, out_sigma, out_p_src,
+                            out_p_snk, err, stream);
+}
+
+int divuq_propagate3d_f32(const float* mu_u, const float* mu_v, const float* mu_w, const float* s_u,
+                          const float* s_v, const float* s_w, const float* hl_mu, const float* hl_s,
+                          const float* hh_mu, const float* hh_s, int64_t nx, int64_t ny, int64_t nzl,
+                          int64_t z0, int64_t nzg, int64_t kb, int64_t ke, double dx, double dy,
+                          double dz, double t, float* out_mu, float* out_sigma, float* out_p_src,
+                          float* out_p_snk, int32_t* err, void* stream) {
+  return propagate3d<float>(mu_u, mu_v, mu_w, s_u, s_v, s_w, hl_mu, hl_s, hh_mu, hh_s, nx, ny, nzl, z0,
+                            nzg, kb, ke, dx, dy, dz, t, out_mu, out_sigma, out_p_src, out_p_snk, err,
+                            stream);
+}
+
+int divuq_propagate3d_f64(const double* mu_u, const double* mu_v, const double* mu_w, const double* s_u,
+                          const double* s_v, const double* s_w, const double* hl_mu, const double* hl_s,
+                          const double* hh_mu, const double* hh_s, int64_t nx, int64_t ny, int64_t nzl,
+                          int64_t z0, int64_t nzg, int64_t kb, int64_t ke, double dx, double dy,
+                          double dz, double t, double* out_mu, double* out_sigma, double* out_p_src,
+                          double* out_p_snk, int32_t* err, void* stream) {
+  return propagate3d<double>(mu_u, mu_v, mu_w, s_u, s_v, s_w, hl_mu, hl_s, hh_mu, hh_s, nx, ny, nzl,
+                             z0, nzg, kb, ke, dx, dy, dz, t, out_mu, out_sigma, out_p_src, out_p_snk,
+                             err, stream);
+}
+
+int divuq_fit_gaussian_f64(const double* members, int64_t M, int64_t C, int64_t N, double* out_mu,
+                           double* out_sigma, int32_t* err, void* stream) {
+  return fit_gaussian<double>(members, M, C, N, out_mu, out_sigma, err, stream);
+}
+
+int divuq_fit_gaussian_f32(const float* members, int64_t M, int64_t C, int64_t N, float* out_mu,
+                           float* out_sigma, int32_t* err, void* stream) {
+  return fit_gaussian<float>(members, M, C, N, out_mu, out_sigma, err, stream);
+}
+
+int divuq_ensemble_divergence2d_f32(const float* members, int64_t M, int64_t nx, int64_t ny, double dx,
+                                    double dy, double t, float* out_mu, float* out_sigma,
+                                    float* out_p_src, float* out_p_snk, float* out_mom_mu,
+                                    float* out_mom_sigma, int32_t* err, void* stream) {
+  if (int r = grid_ok(nx, ny, dx, dy)) return r;
+  if (!members) return DIVUQ_EINVAL;
+  if (M < 2) return DIVUQ_EMEMBERS;
+  if ((out_mom_mu == nullptr) != (out_mom_sigma == nullptr)) return DIVUQ_EINVAL;
+  StencilParams<float> p = blank_params<float>();
+  p.members = members; p.n_members = M; p.comp_stride = nx * ny; p.member_stride = 2 * nx * ny;
+  p.nx = nx; p.ny = ny; p.nzl = 1; p.z0 = 0; p.nzg = 1; p.kbeg = 0; p.kend = 1;
+  set_coeffs(p, dx, dy, 1.0);
+  p.theta = float(t);
+  p.out_mu = out_mu; p.out_sigma = out_sigma; p.out_psrc = out_p_src; p.out_psnk = out_p_snk;
+  p.out_mom_mu = out_mom_mu; p.out_mom_sigma = out_mom_sigma;
+  p.err = err;
+  return dispatch_vec<float, false, kEnsemble>(p, true, static_cast<cudaStream_t>(stream));
+}
+
+int divuq_ensemble_divergence3d_f32(const float* members, int64_t M, const float* hl_mu,
+                                    const float* hl_s, const float* hh_mu, const float* hh_s,
+                                    int64_t nx, int64_t ny, int64_t nzl, int64_t z0, int64_t nzg,
+                                    int64_t kb, int64_t ke, double dx, double dy, double dz, double t,
+                                    float* out_mu, float* out_sigma, float* out_p_src,
+                                    float* out_p_snk, float* out_mom_mu, float* out_mom_sigma,
+                                    int32_t* err, void* stream) {
+  if (int r = grid_ok(nx, ny, dx, dy)) return r;
+  if (nzg < 2 || !(dz > 0.0)) return DIVUQ_EGRID;
+  if (nzl < 1 || z0 < 0 || z0 + nzl > nzg || kb < 0 || ke > nzl || kb > ke) return DIVUQ_EINVAL;
+  if (!members) return DIVUQ_EINVAL;
+  if (M < 2) return DIVUQ_EMEMBERS;
+  if (z0 > 0 && (!hl_mu || !hl_s)) return DIVUQ_EINVAL;
+  if (z0 + nzl < nzg && (!hh_mu || !hh_s)) return DIVUQ_EINVAL;
+  if ((out_mom_mu == nullptr) != (out_mom_sigma == nullptr)) return DIVUQ_EINVAL;
+  StencilParams<float> p = blank_params<float>();
+  const int64_t nl = nx * ny * nzl;
+  p.members = members; p.n_members = M; p.comp_stride = nl; p.member_stride = 3 * nl;
+  p.halo_lo_mu_w = hl_mu; p.halo_lo_s_w = hl_s; p.halo_hi_mu_w = hh_mu; p.halo_hi_s_w = hh_s;
+  p.nx = nx; p.ny = ny; p.nzl = nzl; p.z0 = z0; p.nzg = nzg; p.kbeg = kb; p.kend = ke;
+  set_coeffs(p, dx, dy, dz);
+  p.theta = float(t);
+  p.out_mu = out_mu; p.out_sigma = out_sigma; p.out_psrc = out_p_src; p.out_psnk = out_p_snk;
+  p.out_mom_mu = out_mom_mu; p.out_mom_sigma = out_mom_sigma;
+  p.err = err;
+  return dispatch_vec<float, true, kEnsemble>(p, true, static_cast<cudaStream_t>(stream));
+}
+
+int divuq_tail_probs_f64(const double* mu, const double* sigma, int64_t n, double theta,
+                         double* out_below, double* out_above, int32_t* err, void* stream) {
+  return tail_probs<double>(mu, sigma, n, theta, out_below, out_above, err, stream);
+}
+
+int divuq_tail_probs_f32(const float* mu, const float* sigma, int64_t n, double theta,
+                         float* out_below, float* out_above, int32_t* err, void* stream) {
+  return tail_probs<float>(mu, sigma, n, theta, out_below, out_above, err, stream);
+}
+
+int64_t divuq_mc_scratch_bytes(int64_t nx, int64_t row_begin, int64_t row_end, int64_t n_samples) {
+  if (nx < 1 || row_end <= row_begin || n_samples < 1) return 0;
+  const int64_t chunks = (n_samples + kMcChunk - 1) / kMcChunk;
+  return 2 * chunks * (row_end - row_begin) * nx * int64_t(sizeof(double));
+}
+
+int divuq_mc_divergence2d_f64(const double* mu_u, const double* mu_v, const double* s_u,
+                              const double* s_v, int64_t nx, int64_t ny, double dx, double dy,
+                              int64_t n_samples, uint64_t seed, int64_t row_begin, int64_t row_end,
+                              double* out_mean, double* out_std, void* scratch, int32_t* err,
+                              void* stream) {
+  if (int r = grid_ok(nx, ny, dx, dy)) return r;
+  if (n_samples < 2) return DIVUQ_ESAMPLES;
+  if (!mu_u || !mu_v || !s_u || !s_v || !out_mean || !out_std || !scratch) return DIVUQ_EINVAL;
+  if (row_begin < 0 || row_end > ny || row_begin >= row_end) return DIVUQ_EINVAL;
+  McParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.mu_u = mu_u; p.mu_v = mu_v; p.s_u = s_u; p.s_v = s_v;
+  p.nx = nx; p.ny = ny; p.row_begin = row_begin; p.row_end = row_end;
+  p.n_samples = n_samples; p.n_chunks = (n_samples + kMcChunk - 1) / kMcChunk;
+  p.seed = seed;
+  p.cx_in = 1.0 / (2.0 * dx); p.cx_bd = 1.0 / dx; p.cy_in = 1.0 / (2.0 * dy); p.cy_bd = 1.0 / dy;
+  const int64_t nv = (row_end - row_begin) * nx;
+  p.part_mean = static_cast<double*>(scratch);
+  p.part_m2 = p.part_mean + p.n_chunks * nv;
+  p.out_mean = out_mean; p.out_std = out_std; p.err = err;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  dim3 grid(unsigned((nx + kMcTX - 1) / kMcTX), unsigned((row_end - row_begin + kMcTY - 1) / kMcTY),
+            unsigned(p.n_chunks));
+  mc_chunk_kernel<<<grid, dim3(kMcTX, kMcTY), 0, s>>>(p);
+  DIVUQ_CUDA(cudaGetLastError());
+  const int64_t threads = 256;
+  mc_merge_kernel<<<unsigned((nv * 32 + threads - 1) / threads), unsigned(threads), 0, s>>>(p);
+  return int(cudaGetLastError());
+}
+
+int divuq_gen_field_f32(const float* bumps, int n_bumps, int dims, int64_t nx, int64_t ny, int64_t nzl,
+                        int64_t z0, double dx, double dy, double dz, double vortex_amp,
+                        double vortex_cx, double vortex_cy, double vortex_r, double shear_amp,
+                        uint64_t seed, double sig_lo, double sig_hi, int sigma_mode,
+                        int64_t n_members, float* const* out, float* members, void* stream) {
+  if ((dims != 2 && dims != 3) || nx < 1 || ny < 1 || nzl < 1) return DIVUQ_EINVAL;
+  if (n_members == 0 && !out) return DIVUQ_EINVAL;
+  if (n_members > 0 && !members) return DIVUQ_EINVAL;
+  GenParams p;
+  std::memset(&p, 0, sizeof(p));
+  p.bumps = reinterpret_cast<const Bump*>(bumps); p.n_bumps = n_bumps;
+  p.nx = nx; p.ny = ny; p.nzl = nzl; p.z0 = z0;
+  p.dx = float(dx); p.dy = float(dy); p.dz = float(dz); p.dims = dims;
+  p.vortex_amp = float(vortex_amp); p.vortex_cx = float(vortex_cx); p.vortex_cy = float(vortex_cy);
+  p.vortex_inv_r2 = vortex_r > 0 ? float(1.0 / (vortex_r * vortex_r)) : 0.f;
+  p.shear_amp = float(shear_amp); p.shear_ly = float(double(ny - 1) * dy);
+  p.seed = seed; p.sig_lo = float(sig_lo); p.sig_hi = float(sig_hi); p.sigma_mode = sigma_mode;
+  p.n_members = n_members;
+  if (n_members == 0)
+    for (int c = 0; c < 2 * dims; ++c) {
+      if (!out[c]) return DIVUQ_EINVAL;
+      p.out[c] = out[c];
+    }
+  p.members = members;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t nl = nx * ny * nzl;
+  const int64_t grid = std::min<int64_t>((nl + 255) / 256, int64_t(sm_count()) * 16);
+  gen_kernel<<<unsigned(grid), 256, 0, s>>>(p);
+  return int(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------
+// host-buffer entry points
+// ---------------------------------------------------------------------
+
+int divuq_host_propagate2d_f64(const double* mu_u, const double* mu_v, const double* s_u,
+                               const double* s_v, int64_t nx, int64_t ny, double dx, double dy,
+                               double t, double* out_mu, double* out_sigma, double* out_p_src,
+                               double* out_p_snk, int device) {
+  if (int r = grid_ok(nx, ny, dx, dy)) return r;
+  if (!mu_u || !mu_v) return DIVUQ_EINVAL;
+  const bool has_sigma = out_sigma || out_p_src || out_p_snk;
+  if (has_sigma && (!s_u || !s_v)) return DIVUQ_EINVAL;
+  DIVUQ_CUDA(cudaSetDevice(device));
+  StreamGuard sg;
+  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  const int64_t n = nx * ny;
+  const size_t b = size_t(n) * sizeof(double);
+  DevBuf d;
+  DIVUQ_CUDA(d.alloc(8 * b + 256, sg.s));
+  double* base = d.as<double>();
+  double *dmu = base, *dmv = base + n, *dsu = base + 2 * n, *dsv = base + 3 * n;
+  double* outs[4] = {base + 4 * n, base + 5 * n, base + 6 * n, base + 7 * n};
+  int32_t* derr = reinterpret_cast<int32_t*>(base + 8 * n);
+  DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
+  DIVUQ_CUDA(cudaMemcpyAsync(dmu, mu_u, b, cudaMemcpyHostToDevice, sg.s));
+  DIVUQ_CUDA(cudaMemcpyAsync(dmv, mu_v, b, cudaMemcpyHostToDevice, sg.s));
+  if (has_sigma) {
+    DIVUQ_CUDA(cudaMemcpyAsync(dsu, s_u, b, cudaMemcpyHostToDevice, sg.s));
+    DIVUQ_CUDA(cudaMemcpyAsync(dsv, s_v, b, cudaMemcpyHostToDevice, sg.s));
+  }
+  double* host_out[4] = {out_mu, out_sigma, out_p_src, out_p_snk};
+  int r = propagate2d<double>(dmu, dmv, has_sigma ? dsu : nullptr, has_sigma ? dsv : nullptr, nx, ny,
+                              dx, dy, t, out_mu ? outs[0] : nullptr, out_sigma ? outs[1] : nullptr,
+                              out_p_src ? outs[2] : nullptr, out_p_snk ? outs[3] : nullptr, derr,
+                              sg.s);
+  if (r) return r;
+  for (int q = 0; q < 4; ++q)
+    if (host_out[q]) DIVUQ_CUDA(cudaMemcpyAsync(host_out[q], outs[q], b, cudaMemcpyDeviceToHost, sg.s));
+  int status = 0;
+  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  return status;
+}
+
+int divuq_host_tail_probs_f64(const double* mu, const double* sigma, int64_t n, double theta,
+                              double* out_below, double* out_above, int device) {
+  if (!mu || !sigma || n < 0) return DIVUQ_EINVAL;
+  if (n == 0) return DIVUQ_OK;
+  DIVUQ_CUDA(cudaSetDevice(device));
+  StreamGuard sg;
+  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  const size_t b = size_t(n) * sizeof(double);
+  DevBuf d;
+  DIVUQ_CUDA(d.alloc(4 * b + 256, sg.s));
+  double* base = d.as<double>();
+  int32_t* derr = reinterpret_cast<int32_t*>(base + 4 * n);
+  DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
+  DIVUQ_CUDA(cudaMemcpyAsync(base, mu, b, cudaMemcpyHostToDevice, sg.s));
+  DIVUQ_CUDA(cudaMemcpyAsync(base + n, sigma, b, cudaMemcpyHostToDevice, sg.s));
+  if (int r = tail_probs<double>(base, base + n, n, theta, out_below ? base + 2 * n : nullptr,
+                                 out_above ? base + 3 * n : nullptr, derr, sg.s))
+    return r;
+  if (out_below) DIVUQ_CUDA(cudaMemcpyAsync(out_below, base + 2 * n, b, cudaMemcpyDeviceToHost, sg.s));
+  if (out_above) DIVUQ_CUDA(cudaMemcpyAsync(out_above, base + 3 * n, b, cudaMemcpyDeviceToHost, sg.s));
+  int status = 0;
+  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  return status;
+}
+
+int divuq_host_fit_gaussian_f64(const double* members, int64_t M, int64_t C, int64_t N, double* out_mu,
+                                double* out_sigma, int device) {
+  if (!members || !out_mu || !out_sigma || C < 1 || N < 1) return DIVUQ_EINVAL;
+  if (M < 2) return DIVUQ_EMEMBERS;
+  DIVUQ_CUDA(cudaSetDevice(device));
+  StreamGuard sg;
+  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  const size_t in_b = size_t(M * C * N) * sizeof(double), out_b = size_t(C * N) * sizeof(double);
+  DevBuf d;
+  DIVUQ_CUDA(d.alloc(in_b + 2 * out_b + 256, sg.s));
+  double* dm = d.as<double>();
+  double* dmu = dm + M * C * N;
+  double* dsg = dmu + C * N;
+  int32_t* derr = reinterpret_cast<int32_t*>(dsg + C * N);
+  DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
+  DIVUQ_CUDA(cudaMemcpyAsync(dm, members, in_b, cudaMemcpyHostToDevice, sg.s));
+  if (int r = fit_gaussian<double>(dm, M, C, N, dmu, dsg, derr, sg.s)) return r;
+  DIVUQ_CUDA(cudaMemcpyAsync(out_mu, dmu, out_b, cudaMemcpyDeviceToHost, sg.s));
+  DIVUQ_CUDA(cudaMemcpyAsync(out_sigma, dsg, out_b, cudaMemcpyDeviceToHost, sg.s));
+  int status = 0;
+  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  return status;
+}
+
+int divuq_host_ensemble_divergence2d_f32(const float* members, int64_t M, int64_t nx, int64_t ny,
+                                         double dx, double dy, double t, float* out_mu,
+                                         float* out_sigma, float* out_p_src, float* out_p_snk,
+                                         float* out_mom_mu, float* out_mom_sigma, int device) {
+  if (int r = grid_ok(nx, ny, dx, dy)) return r;
+  if (!members) return DIVUQ_EINVAL;
+  if (M < 2) return DIVUQ_EMEMBERS;
+  if ((out_mom_mu == nullptr) != (out_mom_sigma == nullptr)) return DIVUQ_EINVAL;
+  DIVUQ_CUDA(cudaSetDevice(device));
+  StreamGuard sg;
+  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  const int64_t n = nx * ny;
+  const size_t in_b = size_t(M * 2 * n) * sizeof(float), b = size_t(n) * sizeof(float);
+  DevBuf d;
+  DIVUQ_CUDA(d.alloc(in_b + 8 * b + 256, sg.s));
+  float* dm = d.as<float>();
+  float* o = dm + M * 2 * n;
+  float* outs[4] = {o, o + n, o + 2 * n, o + 3 * n};
+  float* mom_mu = o + 4 * n;      // (2, n)
+  float* mom_sg = o + 6 * n;      // (2, n)
+  int32_t* derr = reinterpret_cast<int32_t*>(o + 8 * n);
+  DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
+  DIVUQ_CUDA(cudaMemcpyAsync(dm, members, in_b, cudaMemcpyHostToDevice, sg.s));
+  float* host_out[4] = {out_mu, out_sigma, out_p_src, out_p_snk};
+  int r = divuq_ensemble_divergence2d_f32(dm, M, nx, ny, dx, dy, t, out_mu ? outs[0] : nullptr,
+                                          out_sigma ? outs[1] : nullptr, out_p_src ? outs[2] : nullptr,
+                                          out_p_snk ? outs[3] : nullptr, out_mom_mu ? mom_mu : nullptr,
+                                          out_mom_mu ? mom_sg : nullptr, derr, sg.s);
+  if (r) return r;
+  for (int q = 0; q < 4; ++q)
+    if (host_out[q]) DIVUQ_CUDA(cudaMemcpyAsync(host_out[q], outs[q], b, cudaMemcpyDeviceToHost, sg.s));
+  if (out_mom_mu) {
+    DIVUQ_CUDA(cudaMemcpyAsync(out_mom_mu, mom_mu, 2 * b, cudaMemcpyDeviceToHost, sg.s));
+    DIVUQ_CUDA(cudaMemcpyAsync(out_mom_sigma, mom_sg, 2 * b, cudaMemcpyDeviceToHost, sg.s));
+  }
+  int status = 0;
+  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  return status;
+}
+
+int divuq_host_mc_divergence2d_f64(const double* mu_u, const double* mu_v, const double* s_u,
+                                   const double* s_v, int64_t nx, int64_t ny, double dx, double dy,
+                                   int64_t n_samples, uint64_t seed, double* out_mean,
+                                   double* out_std, int device) {
+  if (int r = grid_ok(nx, ny, dx, dy)) return r;
+  if (n_samples < 2) return DIVUQ_ESAMPLES;
+  if (!mu_u || !mu_v || !s_u || !s_v || !out_mean || !out_std) return DIVUQ_EINVAL;
+  DIVUQ_CUDA(cudaSetDevice(device));
+  StreamGuard sg;
+  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  const int64_t n = nx * ny;
+  const size_t b = size_t(n) * sizeof(double);
+  const int64_t scratch = divuq_mc_scratch_bytes(nx, 0, ny, n_samples);
+  DevBuf d;
+  DIVUQ_CUDA(d.alloc(6 * b + size_t(scratch) + 256, sg.s));
+  double* base = d.as<double>();
+  double *dmu = base, *dmv = base + n, *dsu = base + 2 * n, *dsv = base + 3 * n;
+  double *dmean = base + 4 * n, *dstd = base + 5 * n;
+  int32_t* derr = reinterpret_cast<int32_t*>(base + 6 * n);
+  void* dscr = reinterpret_cast<char*>(base + 6 * n) + 256;
+  DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
+  DIVUQ_CUDA(cudaMemcpyAsync(dmu, mu_u, b, cudaMemcpyHostToDevice, sg.s));
+  DIVUQ_CUDA(cudaMemcpyAsync(dmv, mu_v, b, cudaMemcpyHostToDevice, sg.s));
+  DIVUQ_CUDA(cudaMemcpyAsync(dsu, s_u, b, cudaMemcpyHostToDevice, sg.s));
+  DIVUQ_CUDA(cudaMemcpyAsync(dsv, s_v, b, cudaMemcpyHostToDevice, sg.s));
+  int r = divuq_mc_divergence2d_f64(dmu, dmv, dsu, dsv, nx, ny, dx, dy, n_samples, seed, 0, ny, dmean,
+                                    dstd, dscr, derr, sg.s);
+  if (r) return r;
+  DIVUQ_CUDA(cudaMemcpyAsync(out_mean, dmean, b, cudaMemcpyDeviceToHost, sg.s));
+  DIVUQ_CUDA(cudaMemcpyAsync(out_std, dstd, b, cudaMemcpyDeviceToHost, sg.s));
+  int status = 0;
+  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  return status;
+}
+
+// 3D host pipeline: z-chunks of `chunk_planes` planes; chunk c uses buffer
+// set c % 2 and stream c % 2, so chunk c+1's host->device copies overlap
+// chunk c's kernel and device->host copies (two copy engines + SMs busy).
+int divuq_host_propagate3d_f32(const float* mu_u, const float* mu_v, const float* mu_w,
+                               const float* s_u, const float* s_v, const float* s_w, int64_t nx,
+                               int64_t ny, int64_t nz, double dx, double dy, double dz, double t,
+                               float* out_mu, float* out_sigma, float* out_p_src, float* out_p_snk,
+                               int64_t chunk_planes, int device) {
+  if (int r = grid_ok(nx, ny, dx, dy)) return r;
+  if (nz < 2 || !(dz > 0.0)) return DIVUQ_EGRID;
+  const float* in[6] = {mu_u, mu_v, mu_w, s_u, s_v, s_w};
+  for (const float* q : in)
+    if (!q) return DIVUQ_EINVAL;
+  float* host_out[4] = {out_mu, out_sigma, out_p_src, out_p_snk};
+  DIVUQ_CUDA(cudaSetDevice(device));
+  const int64_t plane = nx * ny;
+  const int64_t cz = std::max<int64_t>(1, std::min<int64_t>(chunk_planes > 0 ? chunk_planes : 32, nz));
+  const int64_t nchunks = (nz + cz - 1) / cz;
+  StreamGuard sg[2];
+  for (auto& g : sg) DIVUQ_CUDA(cudaStreamCreateWithFlags(&g.s, cudaStreamNonBlocking));
+  // per buffer set: u, v, su, sv: cz planes; w, sw: cz + 2 planes; 4 outputs: cz planes
+  const int64_t set_elems = 4 * cz * plane + 2 * (cz + 2) * plane + 4 * cz * plane;
+  DevBuf d;
+  DIVUQ_CUDA(d.alloc(size_t(2 * set_elems) * sizeof(float) + 256, sg[0].s));
+  DIVUQ_CUDA(cudaStreamSynchronize(sg[0].s));
+  int32_t* derr = reinterpret_cast<int32_t*>(d.as<float>() + 2 * set_elems);
+  DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg[0].s));
+  DIVUQ_CUDA(cudaStreamSynchronize(sg[0].s));
+  for (int64_t c = 0; c < nchunks; ++c) {
+    cudaStream_t s = sg[c % 2].s;
+    float* set = d.as<float>() + (c % 2) * set_elems;
+    float* uv[4] = {set, set + cz * plane, set + 2 * cz * plane, set + 3 * cz * plane};  // u v su sv
+    float* wbuf = set + 4 * cz * plane;                 // (cz+2) planes
+    float* swbuf = wbuf + (cz + 2) * plane;
+    float* outs = swbuf + (cz + 2) * plane;
+    const int64_t z0 = c * cz, nzl = std::min(cz, nz - z0);
+    const size_t nb = size_t(nzl * plane) * sizeof(float);
+    const int src_idx[4] = {0, 1, 3, 4};
+    for (int q = 0; q < 4; ++q)
+      DIVUQ_CUDA(cudaMemcpyAsync(uv[q], in[src_idx[q]] + z0 * plane, nb, cudaMemcpyHostToDevice, s));
+    // w with one ghost plane each side (slot 0 = z0-1, slot 1.. = z0..)
+    const int64_t wlo = std::max<int64_t>(0, z0 - 1), whi = std::min<int64_t>(nz, z0 + nzl + 1);
+    const int64_t slot0 = 1 - (z0 - wlo);
+    const size_t wb = size_t((whi - wlo) * plane) * sizeof(float);
+    DIVUQ_CUDA(cudaMemcpyAsync(wbuf + slot0 * plane, mu_w + wlo * plane, wb, cudaMemcpyHostToDevice, s));
+    DIVUQ_CUDA(cudaMemcpyAsync(swbuf + slot0 * plane, s_w + wlo * plane, wb, cudaMemcpyHostToDevice, s));
+    float* o[4];
+    for (int q = 0; q < 4; ++q) o[q] = host_out[q] ? outs + q * cz * plane : nullptr;
+    int r = propagate3d<float>(uv[0], uv[1], wbuf + plane, uv[2], uv[3], swbuf + plane, wbuf, swbuf,
+                               wbuf + (nzl + 1) * plane, swbuf + (nzl + 1) * plane, nx, ny, nzl, z0, nz,
+                               0, nzl, dx, dy, dz, t, o[0], o[1], o[2], o[3], derr, s);
+    if (r) return r;
+    for (int q = 0; q < 4; ++q)
+      if (host_out[q])
+        DIVUQ_CUDA(cudaMemcpyAsync(host_out[q] + z0 * plane, o[q], nb, cudaMemcpyDeviceToHost, s));
+  }
+  DIVUQ_CUDA(cudaStreamSynchronize(sg[1].s));
+  int status = 0;
+  DIVUQ_CUDA(check_err_word(derr, sg[0].s, &status));
+  return status;
+}
+
+}  // extern "C"
