@@ -1,0 +1,432 @@
+#!/usr/bin/env python
+"""Benchmark of the divergence-uncertainty hot path on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config {1,3,4}] [--impl {ours,reference}]
+
+Default workload = BASELINE.json config 3 (the metric's "1/2/4/8 B200" config):
+3D analytic divergence mean + sigma + P(div>0) + P(div<0) on a 512^3 fp32
+grid, z-slab sharded over N GPUs (strong scaling; NCCL halo exchange of the
+w edge planes overlapped with the interior planes).  One "step" = one pass of
+the hot path over the whole grid with inputs resident in HBM.
+
+Prints ONE JSON line (rank 0).  Keys beyond the base contract:
+  roofline      dominant kernel: algorithmic bytes per launch / its average
+                CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the oracle restatement of the reference on this box's cores
+  e2e           the same metric through the host-buffer C-ABI entry point
+                (pinned host buffers, H2D + D2H inside the timed region)
+  gpu_launches  our kernel launches inside the timed region
+  clocks        NVML SM clock / throttle reasons sampled during the timed region
+
+``--impl reference`` times the reference's CPU algorithm (the oracle port,
+``oracle/cpu_baseline.py``; the Python reference cannot travel to this box) on
+a bounded sample of the same workload with all host threads; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "grid points/sec (analytic div mean+var+prob) and % HBM roofline at 1/2/4/8 B200"
+UNIT = "grid points/s"
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def committed_traffic(key):
+    """dram bytes per launch from the committed ncu --set full capture, or None."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(key)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML SM clock + clocks-event reasons, polled every ~2 ms in a thread."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x2: "applications_clocks_setting", 0x1: "gpu_idle"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self.stop_evt = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _run(self):
+        while not self.stop_evt.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.th = threading.Thread(target=self._run, daemon=True)
+            self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self.stop_evt.set()
+            self.th.join()
+            try:  # one more sample right at the end of the timed region
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            except Exception:
+                pass
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        names = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "n_samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+
+def run_reference(args):
+    if int(os.environ.get("RANK", "0")) != 0:
+        return  # rank 0 alone runs the CPU reference
+    from oracle import cpu_baseline as cb
+
+    cid = args.config
+    threads = os.cpu_count() or 1
+    steps, warm = args.steps, args.warmup
+    budget = 150.0  # seconds for warm-up + steps: the arm must end within minutes
+    if cid == 4:
+        make = lambda p: cb.ensemble3d_thunk(1024, 1024, p, 16, threads=threads)
+        sample = "fit_gaussian(M=16) + 3D propagation + P(div>0.1), P(div<-0.1) on 1024x1024x{p}"
+    elif cid == 1:
+        make = lambda p: cb.ensemble3d_thunk(1024, 64, p, 20, threads=threads)
+        sample = "fit_gaussian(M=20) + propagation + tails on 1024x64x{p}"
+    else:
+        make = lambda p: cb.propagate3d_thunk(512, 512, p, threads=threads)
+        sample = "3D propagation + P(div>0) + P(div<0) on 512x512x{p} sub-volume"
+    thunk, n, _ = make(2)
+    thunk()
+    t0 = time.perf_counter()
+    thunk()
+    per_plane = (time.perf_counter() - t0) / 2.0
+    planes = int(max(2, min(64, budget / max(1, steps + warm) / max(per_plane, 1e-6))))
+    thunk, n, _ = make(planes)
+    times = []
+    for it in range(warm + steps):
+        t0 = time.perf_counter()
+        thunk()
+        if it >= warm:
+            times.append(time.perf_counter() - t0)
+    mean_s = sum(times) / len(times)
+    value = n / mean_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": warm, "ms_per_step": mean_s * 1e3, "higher_is_better": True,
+        "scaling": "strong" if cid == 3 else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": f"config{cid} (bounded CPU sample)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample.format(p=planes) + f", {threads} threads, fp64 like the reference"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", type=int, default=3, choices=(1, 3, 4))
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--planes-per-gpu", type=int, default=128, help="config 4 slab depth")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import __graft_entry__
+
+    if rank == 0:
+        __graft_entry__.build()
+    if world > 1:
+        dist.barrier()
+    from paper_2510_01190_b200 import configs, device as dev
+    from paper_2510_01190_b200._lib import lib
+    from paper_2510_01190_b200.shard import SlabStep
+
+    cfg = configs.CONFIGS[args.config]
+    stream = torch.cuda.current_stream()
+    kernel_events = []  # (start, end) of the dominant launch per step
+
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
+
+    if args.config == 3:
+        nx, ny, nz = cfg.nx, cfg.ny, cfg.nz
+        step = SlabStep(nx, ny, nz, rank, world, device="cuda")
+        fields = configs.config3_slab(step.z0, step.nzl, nx, ny, nz, seed=cfg.seed)
+        n_local = nx * ny * step.nzl
+        out = {k: torch.empty(n_local, dtype=torch.float32, device="cuda") for k in dev.ALL_OUTPUTS}
+        plane = nx * ny
+        mu_w, s_w = fields[2], fields[5]
+        total_pts = nx * ny * nz
+        scaling = "strong"
+
+        def edges():
+            return ((mu_w[:plane], s_w[:plane]), (mu_w[-plane:], s_w[-plane:]))
+
+        def compute(k_range, lo, hi, timed):
+            dominant = (k_range[1] - k_range[0]) > 1 or step.nzl == 1
+            e0 = ev() if timed and dominant else None
+            dev.propagate3d(*fields, nx, ny, step.nzl, 1.0, 1.0, 1.0, cfg.t, z0=step.z0,
+                            nz_global=nz, halo_lo=step.halo_lo, halo_hi=step.halo_hi,
+                            k_range=k_range, out=out, check=False)
+            if e0 is not None:
+                kernel_events.append((e0, ev(), (k_range[1] - k_range[0]) * plane))
+            return 1
+
+        def one_step(timed):
+            return step.run(edges, lambda kr, lo, hi: compute(kr, lo, hi, timed))
+
+        bpp = cfg.bytes_per_point
+        workload = ("config3: 3D analytic divergence mean+sigma+P(div>0)+P(div<0), fp32, "
+                    f"512^3, z-slab x{world}")
+    elif args.config == 4:
+        nx, ny = cfg.nx, cfg.ny
+        nz = args.planes_per_gpu * world
+        step = SlabStep(nx, ny, nz, rank, world, device="cuda")
+        members = configs.config4_slab(step.z0, step.nzl, nx, ny, nz, cfg.members, cfg.seed)
+        n_local = nx * ny * step.nzl
+        out = {k: torch.empty(n_local, dtype=torch.float32, device="cuda") for k in dev.ALL_OUTPUTS}
+        total_pts = nx * ny * nz
+        scaling = "weak"
+
+        def edges():
+            first = dev.w_moments_plane(members, nx, ny, step.nzl, 0, check=False)
+            last = dev.w_moments_plane(members, nx, ny, step.nzl, step.nzl - 1, check=False)
+            return first, last
+
+        def compute(k_range, lo, hi, timed):
+            dominant = (k_range[1] - k_range[0]) > 1
+            e0 = ev() if timed and dominant else None
+            dev.ensemble_divergence3d(members, nx, ny, step.nzl, 1.0, 1.0, 1.0, cfg.t, z0=step.z0,
+                                      nz_global=nz, halo_lo=step.halo_lo, halo_hi=step.halo_hi,
+                                      k_range=k_range, out=out, check=False)
+            if e0 is not None:
+                kernel_events.append((e0, ev(), (k_range[1] - k_range[0]) * nx * ny))
+            return 1
+
+        def one_step(timed):
+            n = step.run(edges, lambda kr, lo, hi: compute(kr, lo, hi, timed))
+            return n + (4 if world > 1 else 0)
+
+        bpp = cfg.bytes_per_point
+        workload = (f"config4 slab: fused ensemble (M=16) -> moments -> divergence -> P(div>0.1), "
+                    f"P(div<-0.1), fp32, 1024x1024x{args.planes_per_gpu} per GPU "
+                    f"(N=8 -> the full 1024^3 config 4)")
+    else:  # config 1: 2D fused ensemble, replicas only
+        nx, ny = cfg.nx, cfg.ny
+        members = configs.config1_members(nx, ny, cfg.members, cfg.seed)
+        n_local = nx * ny
+        out = {k: torch.empty(n_local, dtype=torch.float32, device="cuda")
+               for k in ("mu", "sigma", "p_src")}
+        total_pts = nx * ny * world
+        scaling = "weak"
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+        def one_step(timed):
+            if timed:
+                flush.zero_()  # L2 flush (inputs 168 MB are ~L2-sized); outside the kernel events
+            e0 = ev() if timed else None
+            dev.ensemble_divergence2d(members, nx, ny, 1.0, 1.0, cfg.t, outputs=("mu", "sigma", "p_src"),
+                                      out=out, check=False)
+            if timed:
+                kernel_events.append((e0, ev(), nx * ny))
+            return 1
+
+        bpp = cfg.bytes_per_point
+        workload = "config1: 2D fused ensemble M=20 -> moments -> divergence -> P(div>0), fp32, 1024^2"
+
+    # correctness guard on the real inputs before timing (validation word)
+    torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        one_step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = 0
+    with ClockSampler(local) as clocks:
+        t_start = ev()
+        for _ in range(args.steps):
+            launches += one_step(True)
+        t_end = ev()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    elapsed_ms = t_start.elapsed_time(t_end)
+    if args.config == 1:  # flushes excluded: sum of kernel intervals
+        elapsed_ms = sum(a.elapsed_time(b) for a, b, _ in kernel_events)
+    if world > 1:
+        t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    ms_per_step = elapsed_ms / args.steps
+    value = total_pts / (ms_per_step * 1e-3)
+
+    # roofline of the dominant kernel (rank 0's launches)
+    k_ms = [a.elapsed_time(b) for a, b, _ in kernel_events]
+    k_pts = kernel_events[0][2] if kernel_events else n_local
+    avg_k_s = (sum(k_ms) / len(k_ms)) * 1e-3 if k_ms else ms_per_step * 1e-3
+    peak, peak_src = measured_peak()
+    achieved = bpp * k_pts / avg_k_s / 1e9
+    traffic = committed_traffic(f"config{args.config}")
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "bytes_per_point": bpp, "points_per_launch": k_pts,
+                "avg_launch_ms": avg_k_s * 1e3, "peak_source": peak_src}
+
+    # e2e through the host-buffer C ABI (pinned host buffers, copies timed)
+    e2e = None
+    if not args.no_e2e and args.config == 3:
+        host_in = [f.cpu().pin_memory() for f in fields]
+        host_out = [torch.empty(n_local, dtype=torch.float32).pin_memory() for _ in range(4)]
+        g_nz = step.nzl  # each rank pushes its own slab through the host entry point
+        chunk = 32
+
+        def e2e_call():
+            st = lib.divuq_host_propagate3d_f32(
+                *(t.data_ptr() for t in host_in), nx, ny, g_nz, 1.0, 1.0, 1.0, cfg.t,
+                *(t.data_ptr() for t in host_out), chunk, local)
+            if st != 0:
+                raise RuntimeError(f"host pipeline status {st}")
+
+        e2e_call()
+        if world > 1:
+            dist.barrier()
+        reps = 3
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            e2e_call()
+        e2e_s = (time.perf_counter() - t0) / reps
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        nchunks = -(-g_nz // chunk)
+        w_planes = sum(min(g_nz, (c + 1) * chunk + 1) - max(0, c * chunk - 1) for c in range(nchunks))
+        h2d = 4 * (4 * n_local + 2 * w_planes * nx * ny)
+        e2e = {"value": total_pts / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
+               "d2h_bytes_per_step": 16 * n_local * world, "ms_per_step": e2e_s * 1e3,
+               "path": "divuq_host_propagate3d_f32 (pinned host buffers, 2-stream z-chunk pipeline)"}
+    elif not args.no_e2e and args.config == 1:
+        import numpy as np
+
+        host_mem = members.cpu().pin_memory()
+        host_out = [torch.empty(n_local, dtype=torch.float32).pin_memory() for _ in range(3)]
+
+        def e2e_call():
+            st = lib.divuq_host_ensemble_divergence2d_f32(
+                host_mem.data_ptr(), cfg.members, nx, ny, 1.0, 1.0, cfg.t,
+                *(t.data_ptr() for t in host_out), None, None, None, local)
+            if st != 0:
+                raise RuntimeError(f"host entry status {st}")
+
+        e2e_call()
+        reps = 5
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            e2e_call()
+        e2e_s = (time.perf_counter() - t0) / reps
+        e2e = {"value": total_pts / e2e_s, "unit": UNIT, "h2d_bytes_per_step": host_mem.numel() * 4,
+               "d2h_bytes_per_step": 12 * n_local, "ms_per_step": e2e_s * 1e3}
+        _ = np
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        from oracle import cpu_baseline as cb
+
+        if args.config == 4:
+            v, thr, runs = cb.rate(cb.ensemble3d_thunk(1024, 1024, 2, 16), seconds=10.0)
+            sample = f"fit_gaussian(M=16)+3D propagation+tails on 1024x1024x2 sub-volume, {runs} runs"
+        elif args.config == 1:
+            v, thr, runs = cb.rate(cb.ensemble3d_thunk(1024, 64, 2, 20), seconds=5.0)
+            sample = f"fit_gaussian(M=20)+propagation+tails on 1024x64x2, {runs} runs"
+        else:
+            v, thr, runs = cb.rate(cb.propagate3d_thunk(512, 512, 16), seconds=10.0)
+            sample = f"3D propagation + P(div>0) + P(div<0) on 512x512x16 sub-volume, {runs} runs"
+        cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "port", "sample": sample}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": scaling, "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded on-device generator, BASELINE.json config recipe)",
+        "config": {"workload": workload, "grid_points": total_pts, "t": cfg.t,
+                   "parallelism": f"z-slab x{world}" if args.config != 1 else f"replicas x{world}",
+                   "l2": ("flushed between steps (256 MB write)" if args.config == 1 else
+                          "inputs larger than L2 (126 MB); no flush")},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches, "clocks": clocks.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

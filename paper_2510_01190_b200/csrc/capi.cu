@@ -11,6 +11,7 @@
 
 #include "../../include/divuq_b200.h"
 #include "gen.cuh"
+#include "k2tma.cuh"
 #include "mc.cuh"
 #include "stencil.cuh"
 
@@ -149,6 +150,111 @@ int propagate2d(const T* mu_u, const T* mu_v, const T* s_u, const T* s_v, int64_
   return dispatch_vec<T, false, kMoments>(p, has_sigma, static_cast<cudaStream_t>(stream));
 }
 
+// ---- TMA path for 3D K2 -------------------------------------------------
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+template <typename T>
+bool make_map3d(CUtensorMap* m, const T* base, int64_t nx, int64_t ny, int64_t nz, int bx, int by) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn || !base) return false;
+  const cuuint64_t dims[3] = {cuuint64_t(nx), cuuint64_t(ny), cuuint64_t(nz)};
+  const cuuint64_t strides[2] = {cuuint64_t(nx) * sizeof(T), cuuint64_t(nx * ny) * sizeof(T)};
+  const cuuint32_t box[3] = {cuuint32_t(bx), cuuint32_t(by), 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  const int64_t promo = env_int("DIVUQ_TMA_PROMO", 256);
+  const CUtensorMapL2promotion l2 = promo >= 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                    : promo >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                    : promo >= 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                                   : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  return fn(m, dt, 3, const_cast<T*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, l2, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <typename T, bool HAS_SIGMA>
+int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
+  using C = TmaCfg<T>;
+  *used = false;
+  // tile height: all CTAs own whole tile columns and march the planes in
+  // lockstep, so pick TY minimising (waves of tiles) x (rows per tile)
+  const int64_t sms = sm_count();
+  const int64_t tiles_x = (sp.nx + C::TX - 1) / C::TX;
+  int ty = C::TYMAX;
+  int64_t best = INT64_MAX;
+  for (int cand = C::TYMAX; cand >= 8; --cand) {
+    const int64_t tiles = tiles_x * ((sp.ny + cand - 1) / cand);
+    const int64_t cost = ((tiles + sms - 1) / sms) * cand;
+    if (cost < best) { best = cost; ty = cand; }
+  }
+  if (const int64_t forced = env_int("DIVUQ_TMA_TY", 0)) ty = int(std::max<int64_t>(1, std::min<int64_t>(forced, C::TYMAX)));
+  CUtensorMap tm[6];
+  std::memset(tm, 0, sizeof(tm));
+  const T* arrs[6] = {sp.mu_u, sp.mu_v, sp.mu_w, sp.s_u, sp.s_v, sp.s_w};
+  const int bx[6] = {C::TXP, C::TX, C::TX, C::TXP, C::TX, C::TX};
+  const int by[6] = {ty, ty + 2, ty, ty, ty + 2, ty};
+  for (int a = 0; a < (HAS_SIGMA ? 6 : 3); ++a)
+    if (!make_map3d<T>(&tm[a], arrs[a], sp.nx, sp.ny, sp.nzl, bx[a], by[a])) return DIVUQ_OK;
+  if (!HAS_SIGMA)
+    for (int a = 3; a < 6; ++a) tm[a] = tm[a - 3];
+  TmaParams<T> p;
+  std::memset(&p, 0, sizeof(p));
+  p.mu_w = sp.mu_w; p.s_w = sp.s_w;
+  p.halo_lo_mu_w = sp.halo_lo_mu_w; p.halo_lo_s_w = sp.halo_lo_s_w;
+  p.halo_hi_mu_w = sp.halo_hi_mu_w; p.halo_hi_s_w = sp.halo_hi_s_w;
+  p.nx = int(sp.nx); p.ny = int(sp.ny); p.nzl = sp.nzl; p.z0 = sp.z0; p.nzg = sp.nzg;
+  p.kbeg = sp.kbeg; p.kend = sp.kend;
+  p.ty = ty;
+  p.tiles_x = int(tiles_x);
+  p.n_tiles = int(tiles_x * ((sp.ny + ty - 1) / ty));
+  p.stage_bytes = uint32_t((ty * C::TXP + (ty + 2) * C::TX + ty * C::TX) * sizeof(T)) * (HAS_SIGMA ? 2u : 1u);
+  const int64_t n_work = int64_t(p.n_tiles) * (sp.kend - sp.kbeg);
+  p.cx_in = sp.cx_in; p.cx_bd = sp.cx_bd; p.cy_in = sp.cy_in; p.cy_bd = sp.cy_bd;
+  p.cz_in = sp.cz_in; p.cz_bd = sp.cz_bd; p.theta = sp.theta;
+  p.out_mu = sp.out_mu; p.out_sigma = sp.out_sigma; p.out_psrc = sp.out_psrc; p.out_psnk = sp.out_psnk;
+  p.err = sp.err;
+  if (n_work <= 0) { *used = true; return DIVUQ_OK; }
+  auto kern = k2_tma_kernel<T, HAS_SIGMA>;
+  const size_t smem = sizeof(TmaStage<T>) * C::S + 2 * C::S * sizeof(uint64_t);
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    DIVUQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr_set = true;
+  }
+  const int64_t grid = std::min<int64_t>(p.n_tiles, sms);
+  kern<<<unsigned(grid), C::THREADS, smem, s>>>(tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], p);
+  *used = true;
+  return int(cudaGetLastError());
+}
+
+template <typename T>
+int try_k2_tma(const StencilParams<T>& p, bool has_sigma, cudaStream_t s, bool* used) {
+  *used = false;
+  if (env_int("DIVUQ_NO_TMA", 0)) return DIVUQ_OK;
+  constexpr int VW = TmaCfg<T>::VEC;
+  if (p.nx % VW) return DIVUQ_OK;
+  const void* ptrs[] = {p.mu_u, p.mu_v, p.mu_w, p.s_u, p.s_v, p.s_w, p.halo_lo_mu_w, p.halo_lo_s_w,
+                        p.halo_hi_mu_w, p.halo_hi_s_w, p.out_mu, p.out_sigma, p.out_psrc, p.out_psnk};
+  for (const void* q : ptrs)
+    if (!aligned(q, 16)) return DIVUQ_OK;
+  if (p.nx > (int64_t(1) << 31) || p.ny > (int64_t(1) << 31) || p.nzl > (int64_t(1) << 31)) return DIVUQ_OK;
+  return has_sigma ? launch_k2_tma<T, true>(p, s, used) : launch_k2_tma<T, false>(p, s, used);
+}
+
 template <typename T>
 int propagate3d(const T* mu_u, const T* mu_v, const T* mu_w, const T* s_u, const T* s_v, const T* s_w,
                 const T* hl_mu, const T* hl_s, const T* hh_mu, const T* hh_s, int64_t nx, int64_t ny,
@@ -171,6 +277,9 @@ int propagate3d(const T* mu_u, const T* mu_v, const T* mu_w, const T* s_u, const
   p.theta = T(t);
   p.out_mu = out_mu; p.out_sigma = out_sigma; p.out_psrc = out_ps; p.out_psnk = out_pk;
   p.err = err;
+  bool used = false;
+  if (int r = try_k2_tma<T>(p, has_sigma, static_cast<cudaStream_t>(stream), &used)) return r;
+  if (used) return DIVUQ_OK;
   return dispatch_vec<T, true, kMoments>(p, has_sigma, static_cast<cudaStream_t>(stream));
 }
 

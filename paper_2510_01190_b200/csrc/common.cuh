@@ -38,26 +38,83 @@ template <> struct Arith<float> {
 
 // ---- normal CDF with scipy/cephes ndtr's structure ----------------------
 // The reference evaluates both tails with scipy.special.ndtr (lcp.py:66-67).
-// ndtr scales the argument by sqrt(1/2) with one multiply, uses erf near zero
-// and erfc in the tails, and never forms 1-p for the small tail; keeping that
-// structure keeps us within ~1e-13 relative of scipy even at x ~ -37.
+// Like ndtr we scale the argument by sqrt(1/2) with one multiply and never
+// form 1-p for the small tail: small = erfc(|x|)/2 <= 1/2, large = 1 - small.
+// (ndtr switches to 0.5 + 0.5*erf(x) for |x| < sqrt(1/2), where both tails are
+// ~1/2 and the two forms agree to an ulp; dropping that branch keeps warps
+// convergent.)  Within ~1e-13 relative of scipy even at x ~ -37.
+// erfc(|x|).  fp64: libdevice erfc (~5 ulp), needed for the 1e-12 parity bar.
+// fp32: erfc(a) = exp(-a^2) * h(q) / (a + 2) with q = (a - 2)/(a + 2) and h a
+// degree-9 polynomial fitted offline against scipy's erfcx
+// (tools/fit_erfc.py; max relative error 3.1e-7 ~ 5 ulp in fp32 evaluation,
+// the same class as libdevice erfcf at about half the instructions: one
+// reciprocal, one exp, 9 FMA).  exp(-a^2) is corrected for the rounding of
+// a*a with one FMA so the deep tail keeps its relative accuracy.
+__device__ __forceinline__ double erfc_abs(double x) { return erfc(fabs(x)); }
+
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ float rsqrt_approx(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+__device__ __forceinline__ float erfc_abs(float x) {
+  const float a = fabsf(x);
+  const float r = rcp_approx(a + 2.0f);  // a + 2 in [2, inf]: no special cases
+  const float q = __fmul_rn(a - 2.0f, r);
+  float p = -4.708851338e-05f;
+  p = fmaf(p, q, -5.272014532e-04f);
+  p = fmaf(p, q, -7.228796021e-04f);
+  p = fmaf(p, q, 3.042218974e-03f);
+  p = fmaf(p, q, 6.432665512e-03f);
+  p = fmaf(p, q, -2.150291763e-02f);
+  p = fmaf(p, q, -3.643533960e-02f);
+  p = fmaf(p, q, 2.794715464e-01f);
+  p = fmaf(p, q, -6.871609688e-01f);
+  p = fmaf(p, q, 1.021582723e+00f);
+  const float s = __fmul_rn(a, a);
+  const float lo = fmaf(a, a, -s);  // a*a - s exactly
+  float y = __fmul_rn(__fmul_rn(p, r), expf(-s));
+  y = fmaf(y, -lo, y);              // * exp(-lo) ~ (1 - lo)
+  return a > 10.0546875f ? 0.0f : y;  // fp32 erfc underflows past here (and a = inf)
+}
+
 __device__ __forceinline__ double ndtr_(double a) {
-  const double kSqrtHalf = 0.70710678118654752440;
-  double x = __dmul_rn(a, kSqrtHalf);
-  double z = fabs(x);
-  if (z < kSqrtHalf) return __dadd_rn(0.5, __dmul_rn(0.5, erf(x)));
-  double y = __dmul_rn(0.5, erfc(z));
+  const double x = __dmul_rn(a, 0.70710678118654752440);
+  const double y = __dmul_rn(0.5, erfc_abs(x));
   return x > 0.0 ? __dsub_rn(1.0, y) : y;
 }
 
 __device__ __forceinline__ float ndtr_(float a) {
-  const float kSqrtHalf = 0.70710678118654752440f;
-  float x = __fmul_rn(a, kSqrtHalf);
-  float z = fabsf(x);
-  if (z < kSqrtHalf) return __fadd_rn(0.5f, __fmul_rn(0.5f, erff(x)));
-  float y = __fmul_rn(0.5f, erfcf(z));
+  const float x = __fmul_rn(a, 0.70710678118654752440f);
+  const float y = __fmul_rn(0.5f, erfc_abs(x));
   return x > 0.0f ? __fsub_rn(1.0f, y) : y;
 }
+
+// ---- sigma = sqrt(var) and the tails P(div > t), P(div < -t) -------------
+// fp64: IEEE sqrt and division (sigma bitwise equal to the reference).
+// fp32: branch-free -- one approximate rsqrt gives sigma = var * rsqrt(var)
+// and 1/sigma (|err| <= ~3 ulp, well inside the 1e-5 fp32 bar), so the VEC
+// points of a lane interleave without slow-path branches.
+// Both: reference semantics of _tail_probs (lcp.py:48-68) -- sigma == 0 is a
+// step with mu == theta counted "below"; otherwise both tails evaluated
+// directly; theta = t for the source map, -t for the sink map.
+template <typename T> struct Tails;
+
+template <> struct Tails<double> {
+  static __device__ __forceinline__ void eval(double m, double var, double t, bool t_zero,
+                                              double& sg, double& ps, double& pk);
+};
+template <> struct Tails<float> {
+  static __device__ __forceinline__ void eval(float m, float var, float t, bool t_zero,
+                                              float& sg, float& ps, float& pk);
+};
 
 // P(X > theta) and P(X <= theta) exactly as _tail_probs (lcp.py:48-68):
 // sigma == 0 is a step with mu == theta counted as "below"; otherwise
@@ -74,6 +131,58 @@ __device__ __forceinline__ T prob_below(T mu, T sigma, T theta) {
   if (sigma == T(0)) return mu <= theta ? T(1) : T(0);
   T t = Arith<T>::div(Arith<T>::sub(theta, mu), sigma);
   return ndtr_(t);
+}
+
+// below = P(X <= t_arg quantile) = ndtr(q), above = ndtr(-q) from one erfc
+// (ndtr structure: x = q*sqrt(1/2); small tail erfc(|x|)/2, never 1 - p).
+template <typename T>
+__device__ __forceinline__ void ndtr_pair(T q, T& below, T& above) {
+  using A = Arith<T>;
+  const T x = A::mul(q, T(0.70710678118654752440));
+  const T y = A::mul(T(0.5), erfc_abs(x));
+  const T c = A::sub(T(1), y);
+  below = x > T(0) ? c : y;
+  above = x > T(0) ? y : c;
+}
+
+__device__ __forceinline__ void Tails<double>::eval(double m, double var, double t, bool t_zero,
+                                                    double& sg, double& ps, double& pk) {
+  using A = Arith<double>;
+  sg = A::sqrt_(var);
+  if (sg == 0.0) {
+    ps = m <= t ? 0.0 : 1.0;
+    pk = m <= -t ? 1.0 : 0.0;
+    return;
+  }
+  double b1, a1, b2, a2;
+  ndtr_pair(A::div(A::sub(t, m), sg), b1, a1);
+  if (t_zero) {  // theta = +0 and -0 give the same quotient: one erfc serves both
+    ps = a1;
+    pk = b1;
+  } else {
+    ndtr_pair(A::div(A::sub(-t, m), sg), b2, a2);
+    ps = a1;
+    pk = b2;
+  }
+}
+
+__device__ __forceinline__ void Tails<float>::eval(float m, float var, float t, bool t_zero,
+                                                   float& sg, float& ps, float& pk) {
+  // subnormal variances are scaled into range first (rsqrt.approx flushes them)
+  const bool tiny = var < 1.17549435e-38f;
+  const float vs = tiny ? var * 0x1p64f : var;
+  const float rs = rsqrt_approx(vs);             // inf for var == 0
+  sg = var == 0.0f ? 0.0f : (vs * rs) * (tiny ? 0x1p-32f : 1.0f);
+  const float r = rs * (tiny ? 0x1p32f : 1.0f);
+  float b1, a1, b2, a2;
+  ndtr_pair((t - m) * r, b1, a1);
+  if (t_zero) {
+    b2 = b1;
+  } else {
+    ndtr_pair((-t - m) * r, b2, a2);
+  }
+  ps = var == 0.0f ? (m <= t ? 0.0f : 1.0f) : a1;
+  pk = var == 0.0f ? (m <= -t ? 1.0f : 0.0f) : b2;
 }
 
 // ---- vector types: VEC consecutive x-points per thread ------------------

@@ -1,0 +1,295 @@
+// K2 (3D, TMA pipeline): the HBM-bound hot kernel of BASELINE config 3.
+//
+// Same arithmetic as stencil.cuh (reference op order, stencils.py:54-84;
+// tails lcp.py:48-68) with Blackwell-native data movement:
+//
+//   * warp-specialised persistent CTA (one per SM): 1 producer warp + TY
+//     consumer warps, an S-stage shared-memory ring guarded by mbarriers;
+//   * per plane the producer issues six 3D TMA box loads
+//     (cp.async.bulk.tensor): u / s_u with a 16-byte x-halo on each side,
+//     v / s_v with one halo row above and below, w / s_w of plane k+1.
+//     Out-of-grid box parts are zero-filled by the TMA unit, so the producer
+//     never branches on borders;
+//   * consumers (one grid row per warp, VEC points per lane) take their
+//     operands from the stage (x neighbours by warp shuffle), keep w[k-1],
+//     w[k] in registers (z-march), evaluate mean, sigma and both tails and
+//     stream the four outputs to HBM;
+//   * scheduling: a CTA owns whole tile COLUMNS (all planes of a tile) and
+//     the host picks the tile height TY so #tiles is (close to) a multiple of
+//     the SM count.  All CTAs then march the planes in lockstep, so the halo
+//     rows / columns a CTA reads were fetched by its neighbours moments
+//     earlier and come from L2, not HBM.
+//
+// Slab sharding: planes are slab-local; w at local planes -1 / nzl comes from
+// the halo pointers (exchanged by the caller), read with plain loads.
+#pragma once
+
+#include "common.cuh"
+#include "tma.cuh"
+
+namespace divuq {
+
+template <typename T>
+struct TmaCfg {
+  static constexpr int VEC = 16 / int(sizeof(T));  // 4 x fp32 or 2 x fp64 per lane
+  static constexpr int TX = 32 * VEC;               // tile width (points)
+  static constexpr int PAD = VEC;                    // x-halo (16 bytes) each side
+  static constexpr int TXP = TX + 2 * PAD;
+  static constexpr int TYMAX = 16;                   // consumer warps (tile rows, max)
+  static constexpr int S = 4;                        // pipeline stages
+  static constexpr int THREADS = 32 * (TYMAX + 1);
+};
+
+template <typename T>
+struct alignas(128) TmaStage {
+  using C = TmaCfg<T>;
+  T u[C::TYMAX][C::TXP];
+  T su[C::TYMAX][C::TXP];
+  T v[C::TYMAX + 2][C::TX];
+  T sv[C::TYMAX + 2][C::TX];
+  T w[C::TYMAX][C::TX];
+  T sw[C::TYMAX][C::TX];
+};
+
+template <typename T>
+struct TmaParams {
+  const T* mu_w; const T* s_w;                      // for the z-march restarts
+  const T* halo_lo_mu_w; const T* halo_lo_s_w;
+  const T* halo_hi_mu_w; const T* halo_hi_s_w;
+  int64_t nzl, z0, nzg, kbeg, kend;
+  int nx, ny, ty, tiles_x, n_tiles;
+  uint32_t stage_bytes;                              // TMA bytes per stage (depends on ty)
+  T cx_in, cx_bd, cy_in, cy_bd, cz_in, cz_bd;
+  T theta;
+  T* out_mu; T* out_sigma; T* out_psrc; T* out_psnk;
+  int* err;
+};
+
+template <typename T, bool HAS_SIGMA>
+struct K2Tma {
+  using C = TmaCfg<T>;
+  using V = Vec<T, C::VEC>;
+  using A = Arith<T>;
+  using Stage = TmaStage<T>;
+  static constexpr int VEC = C::VEC, TX = C::TX, S = C::S, PAD = C::PAD;
+
+  static __device__ __forceinline__ V zero() {
+    V r;
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) r.v[e] = T(0);
+    return r;
+  }
+  static __device__ __forceinline__ V lds(const T* p) { return *reinterpret_cast<const V*>(p); }
+
+  // w / s_w of local plane kk at this lane's points by plain loads
+  static __device__ __forceinline__ void load_w(const TmaParams<T>& p, int64_t kk, int64_t off2d,
+                                                bool act, V& w, V& sw) {
+    w = zero(); sw = zero();
+    if (!act) return;
+    const int64_t plane = int64_t(p.nx) * p.ny;
+    const T* bw = nullptr; const T* bs = nullptr;
+    if (kk >= 0 && kk < p.nzl) {
+      bw = p.mu_w + kk * plane; bs = HAS_SIGMA ? p.s_w + kk * plane : nullptr;
+    } else if (kk == -1 && p.z0 > 0) {
+      bw = p.halo_lo_mu_w; bs = p.halo_lo_s_w;
+    } else if (kk == p.nzl && p.z0 + p.nzl < p.nzg) {
+      bw = p.halo_hi_mu_w; bs = p.halo_hi_s_w;
+    }
+    if (bw) {
+      w = ldg_vec<T, VEC>(bw + off2d);
+      if constexpr (HAS_SIGMA) sw = ldg_vec<T, VEC>(bs + off2d);
+    }
+  }
+
+  // mean, sigma and both tails of one point; `B` = boundary-aware variant
+  template <bool B>
+  static __device__ __forceinline__ void point(const TmaParams<T>& p, T ul, T uh, T vl, T vh, T wl,
+                                               T wh, T sl, T sh, T svl, T svh, T swl, T swh,
+                                               T cx, T cy, T cz, bool t_zero, T& m, T& sg, T& ps,
+                                               T& pk) {
+    // ((((u_hi*cx - u_lo*cx) + v_hi*cy) - v_lo*cy) + w_hi*cz) - w_lo*cz
+    m = A::sub(A::add(A::sub(A::mul(uh, cx), A::mul(ul, cx)), A::mul(vh, cy)), A::mul(vl, cy));
+    m = A::sub(A::add(m, A::mul(wh, cz)), A::mul(wl, cz));
+    if constexpr (HAS_SIGMA) {
+      const T a = A::mul(sh, cx), b = A::mul(sl, cx), c = A::mul(svh, cy), d = A::mul(svl, cy);
+      const T f = A::mul(swh, cz), g = A::mul(swl, cz);
+      T var = A::add(A::add(A::add(A::mul(a, a), A::mul(b, b)), A::mul(c, c)), A::mul(d, d));
+      var = A::add(A::add(var, A::mul(f, f)), A::mul(g, g));
+      Tails<T>::eval(m, var, p.theta, t_zero, sg, ps, pk);
+    }
+  }
+
+  static __device__ void run(const TmaParams<T>& p, const CUtensorMap* tu, const CUtensorMap* tv,
+                             const CUtensorMap* tw, const CUtensorMap* tsu, const CUtensorMap* tsv,
+                             const CUtensorMap* tsw, Stage* st, uint64_t* full, uint64_t* empty) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int G = gridDim.x;
+
+    if (warp == C::TYMAX) {
+      // ---------------- producer (one elected lane) ----------------
+      if (lane == 0) {
+        int s = 0;
+        uint32_t ph = 0;
+        for (int tile = blockIdx.x; tile < p.n_tiles; tile += G) {
+          const int x0 = (tile % p.tiles_x) * TX;
+          const int y0 = (tile / p.tiles_x) * p.ty;
+          for (int k = int(p.kbeg); k < int(p.kend); ++k) {
+            mbar_wait(&empty[s], ph ^ 1u);
+            mbar_expect_tx(&full[s], p.stage_bytes);
+            tma_load_3d(&st[s].u[0][0], tu, &full[s], x0 - PAD, y0, k);
+            tma_load_3d(&st[s].v[0][0], tv, &full[s], x0, y0 - 1, k);
+            tma_load_3d(&st[s].w[0][0], tw, &full[s], x0, y0, k + 1);
+            if constexpr (HAS_SIGMA) {
+              tma_load_3d(&st[s].su[0][0], tsu, &full[s], x0 - PAD, y0, k);
+              tma_load_3d(&st[s].sv[0][0], tsv, &full[s], x0, y0 - 1, k);
+              tma_load_3d(&st[s].sw[0][0], tsw, &full[s], x0, y0, k + 1);
+            }
+            if (++s == S) { s = 0; ph ^= 1u; }
+          }
+        }
+      }
+      return;
+    }
+    const int ty = warp;
+    if (ty >= p.ty) return;  // tile shorter than TYMAX: spare warps sit out
+
+    // ---------------- consumers ----------------
+    const int cx0 = lane * VEC;
+    const int64_t plane = int64_t(p.nx) * p.ny;
+    const bool validate = p.err != nullptr;
+    const bool t_zero = (p.theta == T(0));
+    int errbits = 0;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int tile = blockIdx.x; tile < p.n_tiles; tile += G) {
+      const int x0 = (tile % p.tiles_x) * TX;
+      const int j = (tile / p.tiles_x) * p.ty + ty;
+      const int xi = x0 + cx0;
+      const bool act = xi < p.nx && j < p.ny;
+      const int64_t off2d = int64_t(j) * p.nx + xi;
+      const bool xin = xi > 0 && xi + VEC < p.nx;   // no x-boundary point in this lane
+      const bool yin = j > 0 && j < p.ny - 1;
+      const bool jlo = j == 0, jhi = j == p.ny - 1;
+      const T cy = (jlo || jhi) ? p.cy_bd : p.cy_in;
+      V wm, w0, swm, sw0;
+      load_w(p, p.kbeg - 1, off2d, act, wm, swm);
+      load_w(p, p.kbeg, off2d, act, w0, sw0);
+      int64_t o = p.kbeg * plane + off2d;
+      for (int64_t k = p.kbeg; k < p.kend; ++k, o += plane) {
+        mbar_wait(&full[s], ph);
+        const Stage& S_ = st[s];
+        const V u_own = lds(&S_.u[ty][PAD + cx0]);
+        const V v_lo = lds(&S_.v[ty][cx0]);
+        const V v_hi = lds(&S_.v[ty + 2][cx0]);
+        V wp = lds(&S_.w[ty][cx0]);
+        T u_l = __shfl_up_sync(0xffffffffu, u_own.v[VEC - 1], 1);
+        T u_r = __shfl_down_sync(0xffffffffu, u_own.v[0], 1);
+        if (lane == 0) u_l = S_.u[ty][PAD - 1];
+        if (lane == 31) u_r = S_.u[ty][PAD + TX];
+        V su_own = zero(), sv_lo = zero(), sv_hi = zero(), swp = zero();
+        T s_l = T(0), s_r = T(0);
+        if constexpr (HAS_SIGMA) {
+          su_own = lds(&S_.su[ty][PAD + cx0]);
+          sv_lo = lds(&S_.sv[ty][cx0]);
+          sv_hi = lds(&S_.sv[ty + 2][cx0]);
+          swp = lds(&S_.sw[ty][cx0]);
+          s_l = __shfl_up_sync(0xffffffffu, su_own.v[VEC - 1], 1);
+          s_r = __shfl_down_sync(0xffffffffu, su_own.v[0], 1);
+          if (lane == 0) s_l = S_.su[ty][PAD - 1];
+          if (lane == 31) s_r = S_.su[ty][PAD + TX];
+        }
+        // own v / s_v only matter on the y faces (and for validation)
+        V v_own = zero(), sv_own = zero();
+        if (!yin || validate) {
+          v_own = lds(&S_.v[ty + 1][cx0]);
+          if constexpr (HAS_SIGMA) sv_own = lds(&S_.sv[ty + 1][cx0]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);   // stage consumed: the producer may refill it
+        if (++s == S) { s = 0; ph ^= 1u; }
+        if (k + 1 == p.nzl) load_w(p, k + 1, off2d, act, wp, swp);  // past the slab: halo or none
+
+        if (act) {
+          const int64_t kg = p.z0 + k;
+          const bool klo = kg == 0, khi = kg == p.nzg - 1;
+          V omu, osg, ops, opk;
+          if (xin && yin && !klo && !khi) {
+            // interior fast path: central differences on every axis
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+              const T ul = e == 0 ? u_l : u_own.v[e == 0 ? 0 : e - 1];
+              const T uh = e == VEC - 1 ? u_r : u_own.v[e == VEC - 1 ? 0 : e + 1];
+              const T sl = e == 0 ? s_l : su_own.v[e == 0 ? 0 : e - 1];
+              const T sh = e == VEC - 1 ? s_r : su_own.v[e == VEC - 1 ? 0 : e + 1];
+              point<false>(p, ul, uh, v_lo.v[e], v_hi.v[e], wm.v[e], wp.v[e], sl, sh, sv_lo.v[e],
+                           sv_hi.v[e], swm.v[e], swp.v[e], p.cx_in, p.cy_in, p.cz_in, t_zero,
+                           omu.v[e], osg.v[e], ops.v[e], opk.v[e]);
+            }
+          } else {
+            const T cz = (klo || khi) ? p.cz_bd : p.cz_in;
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+              const int i = xi + e;
+              const bool ilo = i == 0, ihi = i == p.nx - 1;
+              const T cx = (ilo || ihi) ? p.cx_bd : p.cx_in;
+              const T uo = u_own.v[e], so = su_own.v[e];
+              const T ul = ilo ? uo : (e == 0 ? u_l : u_own.v[e == 0 ? 0 : e - 1]);
+              const T uh = ihi ? uo : (e == VEC - 1 ? u_r : u_own.v[e == VEC - 1 ? 0 : e + 1]);
+              const T sl = ilo ? so : (e == 0 ? s_l : su_own.v[e == 0 ? 0 : e - 1]);
+              const T sh = ihi ? so : (e == VEC - 1 ? s_r : su_own.v[e == VEC - 1 ? 0 : e + 1]);
+              point<true>(p, ul, uh, jlo ? v_own.v[e] : v_lo.v[e], jhi ? v_own.v[e] : v_hi.v[e],
+                          klo ? w0.v[e] : wm.v[e], khi ? w0.v[e] : wp.v[e], sl, sh,
+                          jlo ? sv_own.v[e] : sv_lo.v[e], jhi ? sv_own.v[e] : sv_hi.v[e],
+                          klo ? sw0.v[e] : swm.v[e], khi ? sw0.v[e] : swp.v[e], cx, cy, cz, t_zero,
+                          omu.v[e], osg.v[e], ops.v[e], opk.v[e]);
+            }
+          }
+          if (validate) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+              errbits |= check_value(u_own.v[e]) | check_value(v_own.v[e]) | check_value(w0.v[e]);
+              if constexpr (HAS_SIGMA)
+                errbits |= check_sigma(su_own.v[e]) | check_sigma(sv_own.v[e]) | check_sigma(sw0.v[e]);
+            }
+          }
+          if (p.out_mu) st_stream<T, VEC>(p.out_mu + o, omu);
+          if constexpr (HAS_SIGMA) {
+            if (p.out_sigma) st_stream<T, VEC>(p.out_sigma + o, osg);
+            if (p.out_psrc) st_stream<T, VEC>(p.out_psrc + o, ops);
+            if (p.out_psnk) st_stream<T, VEC>(p.out_psnk + o, opk);
+          }
+        }
+        wm = w0; w0 = wp;
+        if constexpr (HAS_SIGMA) { swm = sw0; sw0 = swp; }
+      }
+    }
+    if (validate) flush_error(p.err, errbits);
+  }
+};
+
+template <typename T, bool HAS_SIGMA>
+__global__ void __launch_bounds__(TmaCfg<T>::THREADS, 1)
+k2_tma_kernel(const __grid_constant__ CUtensorMap tu, const __grid_constant__ CUtensorMap tv,
+              const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tsu,
+              const __grid_constant__ CUtensorMap tsv, const __grid_constant__ CUtensorMap tsw,
+              const TmaParams<T> p) {
+  using C = TmaCfg<T>;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  auto* st = reinterpret_cast<TmaStage<T>*>(smem_raw);
+  auto* bars = reinterpret_cast<uint64_t*>(smem_raw + sizeof(TmaStage<T>) * C::S);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + C::S;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], uint32_t(p.ty));
+    }
+    mbar_fence_init();
+    tma_prefetch_desc(&tu); tma_prefetch_desc(&tv); tma_prefetch_desc(&tw);
+    if (HAS_SIGMA) { tma_prefetch_desc(&tsu); tma_prefetch_desc(&tsv); tma_prefetch_desc(&tsw); }
+  }
+  __syncthreads();
+  K2Tma<T, HAS_SIGMA>::run(p, &tu, &tv, &tw, &tsu, &tsv, &tsw, st, full, empty);
+}
+
+}  // namespace divuq

@@ -334,10 +334,7 @@ struct StencilKernel {
                 var = A::add(A::add(var, A::mul(f, f)), A::mul(g, g));
                 if constexpr (!ENS) errbits |= check_sigma(sw0.v[e]);
               }
-              const T sg = A::sqrt_(var);
-              osg.v[e] = sg;
-              ops.v[e] = prob_above(m, sg, p.theta);
-              opk.v[e] = prob_below(m, sg, -p.theta);
+              Tails<T>::eval(m, var, p.theta, p.theta == T(0), osg.v[e], ops.v[e], opk.v[e]);
               if constexpr (!ENS) errbits |= check_sigma(own_s) | check_sigma(cur.sv.v[e]);
             }
           }

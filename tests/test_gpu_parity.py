@@ -467,3 +467,18 @@ def test_device_validation_raises(dev, rng):
         dev.ensemble_divergence3d(cu(mem), 16, 8, 4)
     with pytest.raises(ValueError):
         dev.fit_moments(cu(rng.normal(size=(1, 2, 10))))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_tma_pipeline_matches_register_kernel_bitwise(dev, dtype, rng, monkeypatch):
+    """The TMA/mbarrier K2 and the register-prefetch K2 are the same arithmetic."""
+    nx, ny, nz = 256, 40, 21
+    f = _model3d(nx, ny, nz, rng, dtype)
+    ins = [cu(x) for x in f]
+    for t in (0.0, 0.25):
+        a = dev.propagate3d(*ins, nx, ny, nz, 0.5, 1.5, 0.75, t)
+        monkeypatch.setenv("DIVUQ_NO_TMA", "1")
+        b = dev.propagate3d(*ins, nx, ny, nz, 0.5, 1.5, 0.75, t)
+        monkeypatch.delenv("DIVUQ_NO_TMA")
+        for k in a:
+            assert torch.equal(a[k], b[k]), k
