@@ -169,7 +169,8 @@ EncodeTiledFn encode_tiled() {
 }
 
 template <typename T>
-bool make_map3d(CUtensorMap* m, const T* base, int64_t nx, int64_t ny, int64_t nz, int bx, int by) {
+bool make_map3d(CUtensorMap* m, const T* base, int64_t nx, int64_t ny, int64_t nz, int bx, int by,
+                int64_t promo) {
   EncodeTiledFn fn = encode_tiled();
   if (!fn || !base) return false;
   const cuuint64_t dims[3] = {cuuint64_t(nx), cuuint64_t(ny), cuuint64_t(nz)};
@@ -177,7 +178,6 @@ bool make_map3d(CUtensorMap* m, const T* base, int64_t nx, int64_t ny, int64_t n
   const cuuint32_t box[3] = {cuuint32_t(bx), cuuint32_t(by), 1};
   const cuuint32_t es[3] = {1, 1, 1};
   const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
-  const int64_t promo = env_int("DIVUQ_TMA_PROMO", 256);
   const CUtensorMapL2promotion l2 = promo >= 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
                                     : promo >= 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
                                     : promo >= 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
@@ -202,15 +202,24 @@ int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
     if (cost < best) { best = cost; ty = cand; }
   }
   if (const int64_t forced = env_int("DIVUQ_TMA_TY", 0)) ty = int(std::max<int64_t>(1, std::min<int64_t>(forced, C::TYMAX)));
-  CUtensorMap tm[6];
-  std::memset(tm, 0, sizeof(tm));
+  // main boxes: whole 512-byte rows, L2 fill promotion on; halo boxes: 16-byte
+  // columns / single rows, no promotion (they are L2 hits by design)
+  const int64_t promo = env_int("DIVUQ_TMA_PROMO", 256);
+  TmaMaps tm;
+  std::memset(&tm, 0, sizeof(tm));
   const T* arrs[6] = {sp.mu_u, sp.mu_v, sp.mu_w, sp.s_u, sp.s_v, sp.s_w};
-  const int bx[6] = {C::TXP, C::TX, C::TX, C::TXP, C::TX, C::TX};
-  const int by[6] = {ty, ty + 2, ty, ty, ty + 2, ty};
   for (int a = 0; a < (HAS_SIGMA ? 6 : 3); ++a)
-    if (!make_map3d<T>(&tm[a], arrs[a], sp.nx, sp.ny, sp.nzl, bx[a], by[a])) return DIVUQ_OK;
-  if (!HAS_SIGMA)
-    for (int a = 3; a < 6; ++a) tm[a] = tm[a - 3];
+    if (!make_map3d<T>(&tm.m[kMapU + a], arrs[a], sp.nx, sp.ny, sp.nzl, C::TX, ty, promo)) return DIVUQ_OK;
+  if (!make_map3d<T>(&tm.m[kMapUH], sp.mu_u, sp.nx, sp.ny, sp.nzl, C::PAD, ty, 0)) return DIVUQ_OK;
+  if (!make_map3d<T>(&tm.m[kMapVH], sp.mu_v, sp.nx, sp.ny, sp.nzl, C::TX, 1, 0)) return DIVUQ_OK;
+  if (HAS_SIGMA) {
+    if (!make_map3d<T>(&tm.m[kMapSUH], sp.s_u, sp.nx, sp.ny, sp.nzl, C::PAD, ty, 0)) return DIVUQ_OK;
+    if (!make_map3d<T>(&tm.m[kMapSVH], sp.s_v, sp.nx, sp.ny, sp.nzl, C::TX, 1, 0)) return DIVUQ_OK;
+  } else {
+    for (int a = kMapSU; a <= kMapSW; ++a) tm.m[a] = tm.m[a - kMapSU];
+    tm.m[kMapSUH] = tm.m[kMapUH];
+    tm.m[kMapSVH] = tm.m[kMapVH];
+  }
   TmaParams<T> p;
   std::memset(&p, 0, sizeof(p));
   p.mu_w = sp.mu_w; p.s_w = sp.s_w;
@@ -221,7 +230,7 @@ int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
   p.ty = ty;
   p.tiles_x = int(tiles_x);
   p.n_tiles = int(tiles_x * ((sp.ny + ty - 1) / ty));
-  p.stage_bytes = uint32_t((ty * C::TXP + (ty + 2) * C::TX + ty * C::TX) * sizeof(T)) * (HAS_SIGMA ? 2u : 1u);
+  p.stage_bytes = uint32_t((3 * ty * C::TX + 2 * ty * C::PAD + 2 * C::TX) * sizeof(T)) * (HAS_SIGMA ? 2u : 1u);
   const int64_t n_work = int64_t(p.n_tiles) * (sp.kend - sp.kbeg);
   p.cx_in = sp.cx_in; p.cx_bd = sp.cx_bd; p.cy_in = sp.cy_in; p.cy_bd = sp.cy_bd;
   p.cz_in = sp.cz_in; p.cz_bd = sp.cz_bd; p.theta = sp.theta;
@@ -236,7 +245,7 @@ int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
     attr_set = true;
   }
   const int64_t grid = std::min<int64_t>(p.n_tiles, sms);
-  kern<<<unsigned(grid), C::THREADS, smem, s>>>(tm[0], tm[1], tm[2], tm[3], tm[4], tm[5], p);
+  kern<<<unsigned(grid), C::THREADS, smem, s>>>(tm, p);
   *used = true;
   return int(cudaGetLastError());
 }

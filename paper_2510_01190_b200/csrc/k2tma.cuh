@@ -1,24 +1,29 @@
 // K2 (3D, TMA pipeline): the HBM-bound hot kernel of BASELINE config 3.
 //
-// Same arithmetic as stencil.cuh (reference op order, stencils.py:54-84;
-// tails lcp.py:48-68) with Blackwell-native data movement:
+// Same arithmetic as stencil.cuh (StencilMath / Tails in common.cuh: the
+// reference's op order in fp64, stencils.py:54-84, tails lcp.py:48-68) with
+// Blackwell-native data movement:
 //
 //   * warp-specialised persistent CTA (one per SM): 1 producer warp + TY
 //     consumer warps, an S-stage shared-memory ring guarded by mbarriers;
-//   * per plane the producer issues six 3D TMA box loads
-//     (cp.async.bulk.tensor): u / s_u with a 16-byte x-halo on each side,
-//     v / s_v with one halo row above and below, w / s_w of plane k+1.
+//   * per plane the producer issues 3D TMA box loads (cp.async.bulk.tensor):
+//       main boxes  u, v, w(k+1) [and s_u, s_v, s_w]: the tile's own TX x TY
+//                   points, 512-byte aligned rows;
+//       halo boxes  u / s_u: 4 columns left and right of the tile;
+//                   v / s_v: the row above and the row below.
 //     Out-of-grid box parts are zero-filled by the TMA unit, so the producer
 //     never branches on borders;
+//   * the halo boxes of plane k are issued D stages AFTER its main boxes.
+//     Every CTA marches the same planes in lockstep (see scheduling), so by
+//     then the neighbouring CTA has already pulled those halo bytes into L2
+//     with its own main box: halos cost L2 bandwidth, not HBM bandwidth;
 //   * consumers (one grid row per warp, VEC points per lane) take their
 //     operands from the stage (x neighbours by warp shuffle), keep w[k-1],
 //     w[k] in registers (z-march), evaluate mean, sigma and both tails and
 //     stream the four outputs to HBM;
 //   * scheduling: a CTA owns whole tile COLUMNS (all planes of a tile) and
 //     the host picks the tile height TY so #tiles is (close to) a multiple of
-//     the SM count.  All CTAs then march the planes in lockstep, so the halo
-//     rows / columns a CTA reads were fetched by its neighbours moments
-//     earlier and come from L2, not HBM.
+//     the SM count; all CTAs then advance through the planes in lockstep.
 //
 // Slab sharding: planes are slab-local; w at local planes -1 / nzl comes from
 // the halo pointers (exchanged by the caller), read with plain loads.
@@ -33,22 +38,39 @@ template <typename T>
 struct TmaCfg {
   static constexpr int VEC = 16 / int(sizeof(T));  // 4 x fp32 or 2 x fp64 per lane
   static constexpr int TX = 32 * VEC;               // tile width (points)
-  static constexpr int PAD = VEC;                    // x-halo (16 bytes) each side
-  static constexpr int TXP = TX + 2 * PAD;
+  static constexpr int PAD = VEC;                    // x-halo box width (16 bytes)
   static constexpr int TYMAX = 16;                   // consumer warps (tile rows, max)
   static constexpr int S = 4;                        // pipeline stages
+  static constexpr int D = 2;                        // halo boxes trail the main boxes by D stages
   static constexpr int THREADS = 32 * (TYMAX + 1);
 };
 
 template <typename T>
 struct alignas(128) TmaStage {
   using C = TmaCfg<T>;
-  T u[C::TYMAX][C::TXP];
-  T su[C::TYMAX][C::TXP];
-  T v[C::TYMAX + 2][C::TX];
-  T sv[C::TYMAX + 2][C::TX];
+  // main boxes (rows of TX, dense)
+  T u[C::TYMAX][C::TX];
+  T v[C::TYMAX][C::TX];
   T w[C::TYMAX][C::TX];
+  T su[C::TYMAX][C::TX];
+  T sv[C::TYMAX][C::TX];
   T sw[C::TYMAX][C::TX];
+  // halo boxes
+  T v_top[C::TX];
+  T v_bot[C::TX];
+  T sv_top[C::TX];
+  T sv_bot[C::TX];
+  T u_l[C::TYMAX][C::PAD];
+  T u_r[C::TYMAX][C::PAD];
+  T su_l[C::TYMAX][C::PAD];
+  T su_r[C::TYMAX][C::PAD];
+};
+
+// tensor maps, one per (array, box shape)
+enum TmaMap { kMapU, kMapV, kMapW, kMapSU, kMapSV, kMapSW, kMapUH, kMapVH, kMapSUH, kMapSVH, kNumMaps };
+
+struct TmaMaps {
+  CUtensorMap m[kNumMaps];
 };
 
 template <typename T>
@@ -71,7 +93,7 @@ struct K2Tma {
   using V = Vec<T, C::VEC>;
   using A = Arith<T>;
   using Stage = TmaStage<T>;
-  static constexpr int VEC = C::VEC, TX = C::TX, S = C::S, PAD = C::PAD;
+  static constexpr int VEC = C::VEC, TX = C::TX, S = C::S, PAD = C::PAD, D = C::D;
 
   static __device__ __forceinline__ V zero() {
     V r;
@@ -101,67 +123,88 @@ struct K2Tma {
     }
   }
 
-  // mean, sigma and both tails of one point; `B` = boundary-aware variant
   template <bool B>
   static __device__ __forceinline__ void point(const TmaParams<T>& p, T ul, T uh, T vl, T vh, T wl,
                                                T wh, T sl, T sh, T svl, T svh, T swl, T swh,
                                                T cx, T cy, T cz, bool t_zero, T& m, T& sg, T& ps,
                                                T& pk) {
-    // ((((u_hi*cx - u_lo*cx) + v_hi*cy) - v_lo*cy) + w_hi*cz) - w_lo*cz
-    m = A::sub(A::add(A::sub(A::mul(uh, cx), A::mul(ul, cx)), A::mul(vh, cy)), A::mul(vl, cy));
-    m = A::sub(A::add(m, A::mul(wh, cz)), A::mul(wl, cz));
+    using SM = StencilMath<T, true>;
+    m = SM::mean(uh, ul, vh, vl, wh, wl, cx, cy, cz);
+    if constexpr (HAS_SIGMA)
+      Tails<T>::eval(m, SM::var(sh, sl, svh, svl, swh, swl, cx, cy, cz), p.theta, t_zero, sg, ps, pk);
+  }
+
+  struct Pending { int x0, y0, k, s; };
+
+  static __device__ __forceinline__ void issue_main(const TmaMaps& tm, Stage& st, uint64_t* bar,
+                                                    int x0, int y0, int k) {
+    tma_load_3d(&st.u[0][0], &tm.m[kMapU], bar, x0, y0, k);
+    tma_load_3d(&st.v[0][0], &tm.m[kMapV], bar, x0, y0, k);
+    tma_load_3d(&st.w[0][0], &tm.m[kMapW], bar, x0, y0, k + 1);
     if constexpr (HAS_SIGMA) {
-      const T a = A::mul(sh, cx), b = A::mul(sl, cx), c = A::mul(svh, cy), d = A::mul(svl, cy);
-      const T f = A::mul(swh, cz), g = A::mul(swl, cz);
-      T var = A::add(A::add(A::add(A::mul(a, a), A::mul(b, b)), A::mul(c, c)), A::mul(d, d));
-      var = A::add(A::add(var, A::mul(f, f)), A::mul(g, g));
-      Tails<T>::eval(m, var, p.theta, t_zero, sg, ps, pk);
+      tma_load_3d(&st.su[0][0], &tm.m[kMapSU], bar, x0, y0, k);
+      tma_load_3d(&st.sv[0][0], &tm.m[kMapSV], bar, x0, y0, k);
+      tma_load_3d(&st.sw[0][0], &tm.m[kMapSW], bar, x0, y0, k + 1);
     }
   }
 
-  static __device__ void run(const TmaParams<T>& p, const CUtensorMap* tu, const CUtensorMap* tv,
-                             const CUtensorMap* tw, const CUtensorMap* tsu, const CUtensorMap* tsv,
-                             const CUtensorMap* tsw, Stage* st, uint64_t* full, uint64_t* empty) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int G = gridDim.x;
-
-    if (warp == C::TYMAX) {
-      // ---------------- producer (one elected lane) ----------------
-      if (lane == 0) {
-        int s = 0;
-        uint32_t ph = 0;
-        for (int tile = blockIdx.x; tile < p.n_tiles; tile += G) {
-          const int x0 = (tile % p.tiles_x) * TX;
-          const int y0 = (tile / p.tiles_x) * p.ty;
-          for (int k = int(p.kbeg); k < int(p.kend); ++k) {
-            mbar_wait(&empty[s], ph ^ 1u);
-            mbar_expect_tx(&full[s], p.stage_bytes);
-            tma_load_3d(&st[s].u[0][0], tu, &full[s], x0 - PAD, y0, k);
-            tma_load_3d(&st[s].v[0][0], tv, &full[s], x0, y0 - 1, k);
-            tma_load_3d(&st[s].w[0][0], tw, &full[s], x0, y0, k + 1);
-            if constexpr (HAS_SIGMA) {
-              tma_load_3d(&st[s].su[0][0], tsu, &full[s], x0 - PAD, y0, k);
-              tma_load_3d(&st[s].sv[0][0], tsv, &full[s], x0, y0 - 1, k);
-              tma_load_3d(&st[s].sw[0][0], tsw, &full[s], x0, y0, k + 1);
-            }
-            if (++s == S) { s = 0; ph ^= 1u; }
-          }
-        }
-      }
-      return;
+  static __device__ __forceinline__ void issue_halo(const TmaMaps& tm, Stage& st, uint64_t* bar,
+                                                    int x0, int y0, int k, int ty) {
+    tma_load_3d(&st.u_l[0][0], &tm.m[kMapUH], bar, x0 - PAD, y0, k);
+    tma_load_3d(&st.u_r[0][0], &tm.m[kMapUH], bar, x0 + TX, y0, k);
+    tma_load_3d(&st.v_top[0], &tm.m[kMapVH], bar, x0, y0 - 1, k);
+    tma_load_3d(&st.v_bot[0], &tm.m[kMapVH], bar, x0, y0 + ty, k);
+    if constexpr (HAS_SIGMA) {
+      tma_load_3d(&st.su_l[0][0], &tm.m[kMapSUH], bar, x0 - PAD, y0, k);
+      tma_load_3d(&st.su_r[0][0], &tm.m[kMapSUH], bar, x0 + TX, y0, k);
+      tma_load_3d(&st.sv_top[0], &tm.m[kMapSVH], bar, x0, y0 - 1, k);
+      tma_load_3d(&st.sv_bot[0], &tm.m[kMapSVH], bar, x0, y0 + ty, k);
     }
-    const int ty = warp;
-    if (ty >= p.ty) return;  // tile shorter than TYMAX: spare warps sit out
+  }
 
-    // ---------------- consumers ----------------
+  static __device__ void produce(const TmaParams<T>& p, const TmaMaps& tm, Stage* st,
+                                 uint64_t* full, uint64_t* empty) {
+    Pending pend[D];
+    int n_pend = 0, head = 0;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+      const int x0 = (tile % p.tiles_x) * TX;
+      const int y0 = (tile / p.tiles_x) * p.ty;
+      for (int k = int(p.kbeg); k < int(p.kend); ++k) {
+        mbar_wait_backoff(&empty[s], ph ^ 1u);
+        mbar_expect_tx(&full[s], p.stage_bytes);
+        issue_main(tm, st[s], &full[s], x0, y0, k);
+        if (n_pend == D) {  // the oldest pending stage gets its halos now
+          const Pending q = pend[head];
+          issue_halo(tm, st[q.s], &full[q.s], q.x0, q.y0, q.k, p.ty);
+          pend[head] = Pending{x0, y0, k, s};
+          head = (head + 1) % D;
+        } else {
+          pend[(head + n_pend) % D] = Pending{x0, y0, k, s};
+          ++n_pend;
+        }
+        if (++s == S) { s = 0; ph ^= 1u; }
+      }
+    }
+    for (int i = 0; i < n_pend; ++i) {
+      const Pending q = pend[(head + i) % D];
+      issue_halo(tm, st[q.s], &full[q.s], q.x0, q.y0, q.k, p.ty);
+    }
+  }
+
+  static __device__ void consume(const TmaParams<T>& p, Stage* st, uint64_t* full,
+                                 uint64_t* empty) {
+    const int ty = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int cx0 = lane * VEC;
     const int64_t plane = int64_t(p.nx) * p.ny;
     const bool validate = p.err != nullptr;
     const bool t_zero = (p.theta == T(0));
+    const bool top = ty == 0, bot = ty == p.ty - 1;
     int errbits = 0;
     int s = 0;
     uint32_t ph = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += G) {
+    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
       const int x0 = (tile % p.tiles_x) * TX;
       const int j = (tile / p.tiles_x) * p.ty + ty;
       const int xi = x0 + cx0;
@@ -178,31 +221,27 @@ struct K2Tma {
       for (int64_t k = p.kbeg; k < p.kend; ++k, o += plane) {
         mbar_wait(&full[s], ph);
         const Stage& S_ = st[s];
-        const V u_own = lds(&S_.u[ty][PAD + cx0]);
-        const V v_lo = lds(&S_.v[ty][cx0]);
-        const V v_hi = lds(&S_.v[ty + 2][cx0]);
+        const V u_own = lds(&S_.u[ty][cx0]);
+        const V v_own = lds(&S_.v[ty][cx0]);
+        const V v_lo = top ? lds(&S_.v_top[cx0]) : lds(&S_.v[ty > 0 ? ty - 1 : 0][cx0]);
+        const V v_hi = bot ? lds(&S_.v_bot[cx0]) : lds(&S_.v[ty + 1][cx0]);
         V wp = lds(&S_.w[ty][cx0]);
         T u_l = __shfl_up_sync(0xffffffffu, u_own.v[VEC - 1], 1);
         T u_r = __shfl_down_sync(0xffffffffu, u_own.v[0], 1);
-        if (lane == 0) u_l = S_.u[ty][PAD - 1];
-        if (lane == 31) u_r = S_.u[ty][PAD + TX];
-        V su_own = zero(), sv_lo = zero(), sv_hi = zero(), swp = zero();
+        if (lane == 0) u_l = S_.u_l[ty][PAD - 1];
+        if (lane == 31) u_r = S_.u_r[ty][0];
+        V su_own = zero(), sv_own = zero(), sv_lo = zero(), sv_hi = zero(), swp = zero();
         T s_l = T(0), s_r = T(0);
         if constexpr (HAS_SIGMA) {
-          su_own = lds(&S_.su[ty][PAD + cx0]);
-          sv_lo = lds(&S_.sv[ty][cx0]);
-          sv_hi = lds(&S_.sv[ty + 2][cx0]);
+          su_own = lds(&S_.su[ty][cx0]);
+          sv_own = lds(&S_.sv[ty][cx0]);
+          sv_lo = top ? lds(&S_.sv_top[cx0]) : lds(&S_.sv[ty > 0 ? ty - 1 : 0][cx0]);
+          sv_hi = bot ? lds(&S_.sv_bot[cx0]) : lds(&S_.sv[ty + 1][cx0]);
           swp = lds(&S_.sw[ty][cx0]);
           s_l = __shfl_up_sync(0xffffffffu, su_own.v[VEC - 1], 1);
           s_r = __shfl_down_sync(0xffffffffu, su_own.v[0], 1);
-          if (lane == 0) s_l = S_.su[ty][PAD - 1];
-          if (lane == 31) s_r = S_.su[ty][PAD + TX];
-        }
-        // own v / s_v only matter on the y faces (and for validation)
-        V v_own = zero(), sv_own = zero();
-        if (!yin || validate) {
-          v_own = lds(&S_.v[ty + 1][cx0]);
-          if constexpr (HAS_SIGMA) sv_own = lds(&S_.sv[ty + 1][cx0]);
+          if (lane == 0) s_l = S_.su_l[ty][PAD - 1];
+          if (lane == 31) s_r = S_.su_r[ty][0];
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);   // stage consumed: the producer may refill it
@@ -269,27 +308,29 @@ struct K2Tma {
 
 template <typename T, bool HAS_SIGMA>
 __global__ void __launch_bounds__(TmaCfg<T>::THREADS, 1)
-k2_tma_kernel(const __grid_constant__ CUtensorMap tu, const __grid_constant__ CUtensorMap tv,
-              const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tsu,
-              const __grid_constant__ CUtensorMap tsv, const __grid_constant__ CUtensorMap tsw,
-              const TmaParams<T> p) {
+k2_tma_kernel(const __grid_constant__ TmaMaps tm, const TmaParams<T> p) {
   using C = TmaCfg<T>;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   auto* st = reinterpret_cast<TmaStage<T>*>(smem_raw);
   auto* bars = reinterpret_cast<uint64_t*>(smem_raw + sizeof(TmaStage<T>) * C::S);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::S;
+  const int warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], uint32_t(p.ty));
     }
     mbar_fence_init();
-    tma_prefetch_desc(&tu); tma_prefetch_desc(&tv); tma_prefetch_desc(&tw);
-    if (HAS_SIGMA) { tma_prefetch_desc(&tsu); tma_prefetch_desc(&tsv); tma_prefetch_desc(&tsw); }
   }
+  if (warp == C::TYMAX && (threadIdx.x & 31) < kNumMaps) tma_prefetch_desc(&tm.m[threadIdx.x & 31]);
   __syncthreads();
-  K2Tma<T, HAS_SIGMA>::run(p, &tu, &tv, &tw, &tsu, &tsv, &tsw, st, full, empty);
+  if (warp == C::TYMAX) {
+    if ((threadIdx.x & 31) == 0) K2Tma<T, HAS_SIGMA>::produce(p, tm, st, full, empty);
+    return;
+  }
+  if (warp >= p.ty) return;  // tile shorter than TYMAX: spare warps sit out
+  K2Tma<T, HAS_SIGMA>::consume(p, st, full, empty);
 }
 
 }  // namespace divuq

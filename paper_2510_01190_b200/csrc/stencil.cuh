@@ -305,14 +305,10 @@ struct StencilKernel {
             const T u_hi = ihi ? own_u : (e < VEC - 1 ? cur.u.v[e < VEC - 1 ? e + 1 : 0] : uRight);
             const T v_lo = jlo ? cur.v.v[e] : vlo.v[e];
             const T v_hi = jhi ? cur.v.v[e] : vhi.v[e];
-            // ((u_hi*cx - u_lo*cx) + v_hi*cy) - v_lo*cy  [+ w_hi*cz - w_lo*cz]
-            T m = A::sub(A::add(A::sub(A::mul(u_hi, cx), A::mul(u_lo, cx)), A::mul(v_hi, cy)),
-                         A::mul(v_lo, cy));
-            if constexpr (HAS_W) {
-              const T w_lo = klo ? w0.v[e] : wm.v[e];
-              const T w_hi = khi ? w0.v[e] : wp.v[e];
-              m = A::sub(A::add(m, A::mul(w_hi, cz)), A::mul(w_lo, cz));
-            }
+            const T w_lo = HAS_W ? (klo ? w0.v[e] : wm.v[e]) : T(0);
+            const T w_hi = HAS_W ? (khi ? w0.v[e] : wp.v[e]) : T(0);
+            using SM = StencilMath<T, HAS_W>;
+            const T m = SM::mean(u_hi, u_lo, v_hi, v_lo, w_hi, w_lo, cx, cy, cz);
             omu.v[e] = m;
             if constexpr (!ENS) {
               errbits |= check_value(own_u) | check_value(cur.v.v[e]);
@@ -324,16 +320,10 @@ struct StencilKernel {
               const T s_hi = ihi ? own_s : (e < VEC - 1 ? cur.su.v[e < VEC - 1 ? e + 1 : 0] : sRight);
               const T sv_lo = jlo ? cur.sv.v[e] : svlo.v[e];
               const T sv_hi = jhi ? cur.sv.v[e] : svhi.v[e];
-              const T a = A::mul(s_hi, cx), b = A::mul(s_lo, cx);
-              const T c = A::mul(sv_hi, cy), d = A::mul(sv_lo, cy);
-              T var = A::add(A::add(A::add(A::mul(a, a), A::mul(b, b)), A::mul(c, c)), A::mul(d, d));
-              if constexpr (HAS_W) {
-                const T sw_lo = klo ? sw0.v[e] : swm.v[e];
-                const T sw_hi = khi ? sw0.v[e] : swp.v[e];
-                const T f = A::mul(sw_hi, cz), g = A::mul(sw_lo, cz);
-                var = A::add(A::add(var, A::mul(f, f)), A::mul(g, g));
-                if constexpr (!ENS) errbits |= check_sigma(sw0.v[e]);
-              }
+              const T sw_lo = HAS_W ? (klo ? sw0.v[e] : swm.v[e]) : T(0);
+              const T sw_hi = HAS_W ? (khi ? sw0.v[e] : swp.v[e]) : T(0);
+              if constexpr (HAS_W && !ENS) errbits |= check_sigma(sw0.v[e]);
+              const T var = SM::var(s_hi, s_lo, sv_hi, sv_lo, sw_hi, sw_lo, cx, cy, cz);
               Tails<T>::eval(m, var, p.theta, p.theta == T(0), osg.v[e], ops.v[e], opk.v[e]);
               if constexpr (!ENS) errbits |= check_sigma(own_s) | check_sigma(cur.sv.v[e]);
             }
