@@ -12,6 +12,7 @@
 #include "../../include/divuq_b200.h"
 #include "gen.cuh"
 #include "k2tma.cuh"
+#include "k3tma.cuh"
 #include "mc.cuh"
 #include "stencil.cuh"
 
@@ -247,6 +248,82 @@ int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
   const int64_t grid = std::min<int64_t>(p.n_tiles, sms);
   kern<<<unsigned(grid), C::THREADS, smem, s>>>(tm, p);
   *used = true;
+  return int(cudaGetLastError());
+}
+
+// ---- TMA path for the fused 3D ensemble kernel (K3) ---------------------
+bool make_map5d_members(CUtensorMap* m, const float* base, int64_t nx, int64_t ny, int64_t nzl,
+                        int64_t members, int bx, int by, int bm, int64_t promo) {
+  // view of the (M, 3, nzl, ny, nx) member slab as (x, y, plane, component, member)
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn || !base) return false;
+  const cuuint64_t nl = cuuint64_t(nx * ny * nzl);
+  const cuuint64_t dims[5] = {cuuint64_t(nx), cuuint64_t(ny), cuuint64_t(nzl), 3, cuuint64_t(members)};
+  const cuuint64_t strides[4] = {cuuint64_t(nx) * 4, cuuint64_t(nx * ny) * 4, nl * 4, 3 * nl * 4};
+  const cuuint32_t box[5] = {cuuint32_t(bx), cuuint32_t(by), 1, 1, cuuint32_t(bm)};
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  const CUtensorMapL2promotion l2 = promo >= 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+                                                 : CU_TENSOR_MAP_L2_PROMOTION_NONE;
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, l2,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int try_k3_tma(const StencilParams<float>& sp, cudaStream_t s, bool* used) {
+  using C = K3Cfg;
+  *used = false;
+  if (env_int("DIVUQ_NO_TMA", 0)) return DIVUQ_OK;
+  if (sp.nx % 4 || sp.n_members < 2) return DIVUQ_OK;
+  const void* ptrs[] = {sp.members, sp.halo_lo_mu_w, sp.halo_lo_s_w, sp.halo_hi_mu_w, sp.halo_hi_s_w,
+                        sp.out_mu, sp.out_sigma, sp.out_psrc, sp.out_psnk, sp.out_mom_mu, sp.out_mom_sigma};
+  for (const void* q : ptrs)
+    if (!aligned(q, 16)) return DIVUQ_OK;
+  if (sp.nx > (int64_t(1) << 30) || sp.ny > (int64_t(1) << 30) || sp.nzl > (int64_t(1) << 30)) return DIVUQ_OK;
+  const int64_t sms = sm_count();
+  const int64_t tiles_x = (sp.nx + C::TX - 1) / C::TX;
+  int ty = C::TYMAX;
+  int64_t best = INT64_MAX;
+  for (int cand = C::TYMAX; cand >= 8; --cand) {
+    const int64_t tiles = tiles_x * ((sp.ny + cand - 1) / cand);
+    const int64_t cost = ((tiles + sms - 1) / sms) * cand;
+    if (cost < best) { best = cost; ty = cand; }
+  }
+  if (const int64_t forced = env_int("DIVUQ_TMA_TY", 0)) ty = int(std::max<int64_t>(1, std::min<int64_t>(forced, C::TYMAX)));
+  K3Maps tm;
+  std::memset(&tm, 0, sizeof(tm));
+  const int64_t promo = env_int("DIVUQ_TMA_PROMO", 256);
+  const int64_t M = sp.n_members;
+  if (!make_map5d_members(&tm.m[kK3Main], sp.members, sp.nx, sp.ny, sp.nzl, M, C::TX, ty, C::MB, promo) ||
+      !make_map5d_members(&tm.m[kK3HaloX], sp.members, sp.nx, sp.ny, sp.nzl, M, C::PAD, ty, C::MB, 0) ||
+      !make_map5d_members(&tm.m[kK3HaloY], sp.members, sp.nx, sp.ny, sp.nzl, M, C::TX, 1, C::MB, 0))
+    return DIVUQ_OK;
+  K3Params p;
+  std::memset(&p, 0, sizeof(p));
+  p.halo_lo_mu_w = sp.halo_lo_mu_w; p.halo_lo_s_w = sp.halo_lo_s_w;
+  p.halo_hi_mu_w = sp.halo_hi_mu_w; p.halo_hi_s_w = sp.halo_hi_s_w;
+  p.nzl = sp.nzl; p.z0 = sp.z0; p.nzg = sp.nzg; p.kbeg = sp.kbeg; p.kend = sp.kend;
+  p.comp_stride = sp.comp_stride;
+  p.nx = int(sp.nx); p.ny = int(sp.ny); p.ty = ty; p.tiles_x = int(tiles_x);
+  p.n_tiles = int(tiles_x * ((sp.ny + ty - 1) / ty));
+  p.M = int(sp.n_members);
+  p.bytes_u = uint32_t((C::TX * ty + 2 * C::PAD * ty) * 4 * C::MB);
+  p.bytes_v = uint32_t((C::TX * ty + 2 * C::TX) * 4 * C::MB);
+  p.bytes_w = uint32_t(C::TX * ty * 4 * C::MB);
+  p.cx_in = sp.cx_in; p.cx_bd = sp.cx_bd; p.cy_in = sp.cy_in; p.cy_bd = sp.cy_bd;
+  p.cz_in = sp.cz_in; p.cz_bd = sp.cz_bd; p.theta = sp.theta;
+  p.out_mu = sp.out_mu; p.out_sigma = sp.out_sigma; p.out_psrc = sp.out_psrc; p.out_psnk = sp.out_psnk;
+  p.out_mom_mu = sp.out_mom_mu; p.out_mom_sigma = sp.out_mom_sigma;
+  p.err = sp.err;
+  *used = true;
+  if (sp.kend <= sp.kbeg) return DIVUQ_OK;
+  const size_t smem = sizeof(K3Stage) * C::S + sizeof(K3Xchg) + 2 * C::S * sizeof(uint64_t);
+  static bool attr_set = false;
+  if (!attr_set) {
+    DIVUQ_CUDA(cudaFuncSetAttribute(k3_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr_set = true;
+  }
+  const int64_t grid = std::min<int64_t>(p.n_tiles, sms);
+  k3_tma_kernel<<<unsigned(grid), C::THREADS, smem, s>>>(tm, p);
   return int(cudaGetLastError());
 }
 
@@ -504,6 +581,9 @@ int divuq_ensemble_divergence3d_f32(const float* members, int64_t M, const float
   p.out_mu = out_mu; p.out_sigma = out_sigma; p.out_psrc = out_p_src; p.out_psnk = out_p_snk;
   p.out_mom_mu = out_mom_mu; p.out_mom_sigma = out_mom_sigma;
   p.err = err;
+  bool used = false;
+  if (int r = try_k3_tma(p, static_cast<cudaStream_t>(stream), &used)) return r;
+  if (used) return DIVUQ_OK;
   return dispatch_vec<float, true, kEnsemble>(p, true, static_cast<cudaStream_t>(stream));
 }
 

@@ -97,6 +97,41 @@ __device__ __forceinline__ float ndtr_(float a) {
   return x > 0.0f ? __fsub_rn(1.0f, y) : y;
 }
 
+// ---- fp32 ensemble moments: one pass, shifted by the first member ----------
+// d_m = x_m - x_0; s = sum d, q = sum d^2 (FMA);  mu = x_0 + s/M;
+// var = (q - s*s/M) / (M-1) clamped at 0 (ddof = 1, gaussian.py:41-44).
+// Shifting by a member keeps the cancellation benign (|mu - x_0| ~ sigma), and
+// a single pass lets the streaming kernels consume each member once without
+// holding M values per point.  Every fp32 moment in the library goes through
+// this one routine, so the fused, unfused and sharded paths agree bitwise.
+template <int VEC>
+struct ShiftedMoments {
+  float x0[VEC], s[VEC], q[VEC];
+  __device__ __forceinline__ void add(int m, const float* x) {
+    if (m == 0) {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) { x0[e] = x[e]; s[e] = 0.0f; q[e] = 0.0f; }
+    } else {
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        const float d = x[e] - x0[e];
+        s[e] += d;
+        q[e] = fmaf(d, d, q[e]);
+      }
+    }
+  }
+  __device__ __forceinline__ void finish(int M, float* mu, float* sg) const {
+    const float inv_m = __fdiv_rn(1.0f, float(M));
+    const float inv_m1 = __fdiv_rn(1.0f, float(M - 1));
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      mu[e] = fmaf(s[e], inv_m, x0[e]);
+      const float var = fmaxf(0.0f, fmaf(-s[e], s[e] * inv_m, q[e])) * inv_m1;
+      sg[e] = __fsqrt_rn(var);
+    }
+  }
+};
+
 // ---- the stencil: mean and variance of one point ---------------------------
 // fp64: the reference's evaluation order bit for bit (stencils.py:64-66,
 // 79-84): ((u_hi*c - u_lo*c) + v_hi*c) - v_lo*c [+ w terms], every product

@@ -39,7 +39,7 @@ struct TmaCfg {
   static constexpr int VEC = 16 / int(sizeof(T));  // 4 x fp32 or 2 x fp64 per lane
   static constexpr int TX = 32 * VEC;               // tile width (points)
   static constexpr int PAD = VEC;                    // x-halo box width (16 bytes)
-  static constexpr int TYMAX = 16;                   // consumer warps (tile rows, max)
+  static constexpr int TYMAX = 15;  // consumer warps (tile rows, max): 16 warps/CTA -> 128 regs
   static constexpr int S = 4;                        // pipeline stages
   static constexpr int D = 2;                        // halo boxes trail the main boxes by D stages
   static constexpr int THREADS = 32 * (TYMAX + 1);
@@ -48,22 +48,23 @@ struct TmaCfg {
 template <typename T>
 struct alignas(128) TmaStage {
   using C = TmaCfg<T>;
+  // every TMA destination must be 128-byte aligned
   // main boxes (rows of TX, dense)
-  T u[C::TYMAX][C::TX];
-  T v[C::TYMAX][C::TX];
-  T w[C::TYMAX][C::TX];
-  T su[C::TYMAX][C::TX];
-  T sv[C::TYMAX][C::TX];
-  T sw[C::TYMAX][C::TX];
+  alignas(128) T u[C::TYMAX][C::TX];
+  alignas(128) T v[C::TYMAX][C::TX];
+  alignas(128) T w[C::TYMAX][C::TX];
+  alignas(128) T su[C::TYMAX][C::TX];
+  alignas(128) T sv[C::TYMAX][C::TX];
+  alignas(128) T sw[C::TYMAX][C::TX];
   // halo boxes
-  T v_top[C::TX];
-  T v_bot[C::TX];
-  T sv_top[C::TX];
-  T sv_bot[C::TX];
-  T u_l[C::TYMAX][C::PAD];
-  T u_r[C::TYMAX][C::PAD];
-  T su_l[C::TYMAX][C::PAD];
-  T su_r[C::TYMAX][C::PAD];
+  alignas(128) T v_top[C::TX];
+  alignas(128) T v_bot[C::TX];
+  alignas(128) T sv_top[C::TX];
+  alignas(128) T sv_bot[C::TX];
+  alignas(128) T u_l[C::TYMAX][C::PAD];
+  alignas(128) T u_r[C::TYMAX][C::PAD];
+  alignas(128) T su_l[C::TYMAX][C::PAD];
+  alignas(128) T su_r[C::TYMAX][C::PAD];
 };
 
 // tensor maps, one per (array, box shape)

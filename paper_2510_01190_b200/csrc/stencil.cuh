@@ -57,12 +57,39 @@ struct StencilParams {
 
 constexpr int kStencilTY = 8;  // warps (rows) per CTA
 
-// --- ensemble moments: sequential sum / M, two-pass ddof=1 (gaussian.py:41-44)
-// The MR member values stay in registers between the passes (fully unrolled
-// and predicated on k < M); M > MR falls back to re-reading the members.
+// --- ensemble moments ------------------------------------------------------
+// fp64: numpy's algorithm bit for bit (gaussian.py:41-44) -- sequential sum /
+//   M, then the two-pass ddof=1 variance.  The MR member values stay in
+//   registers between the passes (fully unrolled and predicated on k < M);
+//   M > MR falls back to re-reading the members.
+// fp32: single pass shifted by the first member (ShiftedMoments in
+//   common.cuh), the formula every fp32 kernel (K1, the register K3 and the
+//   TMA K3) shares, so fused == K1 + K2 and sharded == whole bit for bit.
+template <typename T, int VEC, int MR>
+__device__ __forceinline__ void member_moments_2pass(const T* base, int64_t mstride, int M,
+                                                     Vec<T, VEC>& mu, Vec<T, VEC>& sg, int& err);
+
 template <typename T, int VEC, int MR>
 __device__ __noinline__ void member_moments(const T* base, int64_t mstride, int M,
                                                Vec<T, VEC>& mu, Vec<T, VEC>& sg, int& err) {
+  if constexpr (sizeof(T) == 4) {
+    ShiftedMoments<VEC> acc;
+#pragma unroll 8
+    for (int k = 0; k < M; ++k) {
+      const Vec<T, VEC> x = ld_stream<T, VEC>(base + k * mstride);
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) err |= check_value(x.v[e]);
+      acc.add(k, x.v);
+    }
+    acc.finish(M, mu.v, sg.v);
+    return;
+  }
+  member_moments_2pass<T, VEC, MR>(base, mstride, M, mu, sg, err);
+}
+
+template <typename T, int VEC, int MR>
+__device__ __forceinline__ void member_moments_2pass(const T* base, int64_t mstride, int M,
+                                                     Vec<T, VEC>& mu, Vec<T, VEC>& sg, int& err) {
   using A = Arith<T>;
   using V = Vec<T, VEC>;
   V s, q;
