@@ -170,7 +170,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", type=int, default=3, choices=(1, 3, 4))
+    ap.add_argument("--config", type=int, default=3, choices=(0, 1, 2, 3, 4))
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -274,6 +274,47 @@ def main():
         workload = (f"config4 slab: fused ensemble (M=16) -> moments -> divergence -> P(div>0.1), "
                     f"P(div<-0.1), fp32, 1024x1024x{args.planes_per_gpu} per GPU "
                     f"(N=8 -> the full 1024^3 config 4)")
+    elif args.config == 0:  # 2D analytic fp64 128^2 (L2-resident, launch-bound): replicas only
+        nx, ny = cfg.nx, cfg.ny
+        host_model = configs.config0_model()
+        model = [torch.from_numpy(a).cuda() for a in host_model]
+        n_local = nx * ny
+        out = {k: torch.empty(n_local, dtype=torch.float64, device="cuda") for k in dev.ALL_OUTPUTS}
+        total_pts = nx * ny * world
+        scaling = "weak"
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+        def one_step(timed):
+            if timed:
+                flush.zero_()  # L2 flush between steps; outside the kernel events
+            e0 = ev() if timed else None
+            dev.propagate2d(*model, nx, ny, 1.0, 1.0, cfg.t, out=out, check=False)
+            if timed:
+                kernel_events.append((e0, ev(), nx * ny))
+            return 1
+
+        bpp = cfg.bytes_per_point
+        workload = "config0: 2D analytic divergence mean+sigma+P(div>0)+P(div<0), fp64, 128^2"
+    elif args.config == 2:  # Monte Carlo fp64 256^2 x 2000 samples: replicas only
+        nx, ny = cfg.nx, cfg.ny
+        host_model = configs.config2_model()
+        model = [torch.from_numpy(a).cuda() for a in host_model]
+        n_local = nx * ny
+        mean = torch.empty(n_local, dtype=torch.float64, device="cuda")
+        std = torch.empty_like(mean)
+        total_pts = nx * ny * cfg.n_samples * world
+        scaling = "weak"
+
+        def one_step(timed):
+            e0 = ev() if timed else None
+            dev.mc_divergence2d(*model, nx, ny, 1.0, 1.0, cfg.n_samples, 2024, out=(mean, std),
+                                check=False)
+            if timed:
+                kernel_events.append((e0, ev(), nx * ny))
+            return 2
+
+        bpp = cfg.bytes_per_point
+        workload = "config2: 2D Monte Carlo divergence mean/std, fp64, 256^2, N=2000, Philox4x32-10"
     else:  # config 1: 2D fused ensemble, replicas only
         nx, ny = cfg.nx, cfg.ny
         members = configs.config1_members(nx, ny, cfg.members, cfg.seed)
@@ -317,7 +358,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     elapsed_ms = t_start.elapsed_time(t_end)
-    if args.config == 1:  # flushes excluded: sum of kernel intervals
+    if args.config in (0, 1):  # flushes excluded: sum of kernel intervals
         elapsed_ms = sum(a.elapsed_time(b) for a, b, _ in kernel_events)
     if world > 1:
         t = torch.tensor([elapsed_ms], dtype=torch.float64, device="cuda")
@@ -337,6 +378,13 @@ def main():
                 "frac": achieved / peak, "traffic": traffic,
                 "bytes_per_point": bpp, "points_per_launch": k_pts,
                 "avg_launch_ms": avg_k_s * 1e3, "peak_source": peak_src}
+    if args.config == 2:  # fp64-ALU bound: the HBM fraction is not the bound that matters
+        roofline = {"bound": "fp64 (CUDA cores; no tensor-core work)", "achieved": None, "peak": None,
+                    "unit": None, "frac": None, "traffic": traffic,
+                    "note": "Philox + Box-Muller per vertex-sample; HBM traffic is ~48 B/vertex",
+                    "avg_launch_ms": avg_k_s * 1e3}
+    elif args.config == 0:
+        roofline["note"] = "0.9 MB working set: launch/latency-bound, L2 flushed between steps"
 
     # e2e through the host-buffer C ABI (pinned host buffers, copies timed)
     e2e = None
@@ -371,6 +419,31 @@ def main():
         e2e = {"value": total_pts / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
                "d2h_bytes_per_step": 16 * n_local * world, "ms_per_step": e2e_s * 1e3,
                "path": "divuq_host_propagate3d_f32 (pinned host buffers, 2-stream z-chunk pipeline)"}
+    elif not args.no_e2e and args.config in (0, 2):
+        host_in = [torch.from_numpy(a).pin_memory() for a in host_model]
+        nouts = 4 if args.config == 0 else 2
+        host_out = [torch.empty(n_local, dtype=torch.float64).pin_memory() for _ in range(nouts)]
+
+        def e2e_call():
+            if args.config == 0:
+                st = lib.divuq_host_propagate2d_f64(*(t.data_ptr() for t in host_in), nx, ny, 1.0, 1.0,
+                                                    cfg.t, *(t.data_ptr() for t in host_out), local)
+            else:
+                st = lib.divuq_host_mc_divergence2d_f64(*(t.data_ptr() for t in host_in), nx, ny, 1.0,
+                                                        1.0, cfg.n_samples, 2024,
+                                                        *(t.data_ptr() for t in host_out), local)
+            if st != 0:
+                raise RuntimeError(f"host entry status {st}")
+
+        e2e_call()
+        reps = 20 if args.config == 0 else 5
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            e2e_call()
+        e2e_s = (time.perf_counter() - t0) / reps
+        e2e = {"value": total_pts / e2e_s, "unit": UNIT if args.config == 0 else "vertex-samples/s",
+               "h2d_bytes_per_step": 32 * n_local, "d2h_bytes_per_step": 8 * nouts * n_local,
+               "ms_per_step": e2e_s * 1e3}
     elif not args.no_e2e and args.config == 1:
         import numpy as np
 
@@ -404,20 +477,31 @@ def main():
         elif args.config == 1:
             v, thr, runs = cb.rate(cb.ensemble3d_thunk(1024, 64, 2, 20), seconds=5.0)
             sample = f"fit_gaussian(M=20)+propagation+tails on 1024x64x2, {runs} runs"
+        elif args.config == 0:
+            v, thr, runs = cb.rate(cb.propagate2d_thunk(host_model, nx, ny, cfg.t), seconds=5.0)
+            sample = f"reference-order 2D propagation + both tails, 128^2 fp64, serial, {runs} runs"
+        elif args.config == 2:
+            v, thr, runs = cb.rate(cb.mc_thunk(host_model, nx, ny, 8), seconds=10.0)
+            sample = f"Philox MC estimator restated in numpy, 256^2 x 8 samples, {runs} runs"
         else:
             v, thr, runs = cb.rate(cb.propagate3d_thunk(512, 512, 16), seconds=10.0)
             sample = f"3D propagation + P(div>0) + P(div<0) on 512x512x16 sub-volume, {runs} runs"
         cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "port", "sample": sample}
 
+    unit = "vertex-samples/s" if args.config == 2 else UNIT
+    if cpu is not None:
+        cpu["unit"] = unit
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC if args.config != 2 else "vertex-samples/sec (Monte Carlo divergence mean+std)",
+        "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": scaling, "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded on-device generator, BASELINE.json config recipe)",
+        "scaling": scaling, "vs_baseline": None, "dtype": "f64" if args.config in (0, 2) else "f32",
+        "data": "synthetic (seeded generator, BASELINE.json config recipe)",
         "config": {"workload": workload, "grid_points": total_pts, "t": cfg.t,
-                   "parallelism": f"z-slab x{world}" if args.config != 1 else f"replicas x{world}",
-                   "l2": ("flushed between steps (256 MB write)" if args.config == 1 else
-                          "inputs larger than L2 (126 MB); no flush")},
+                   "parallelism": f"z-slab x{world}" if args.config in (3, 4) else f"replicas x{world}",
+                   "l2": ("flushed between steps (256 MB write)" if args.config in (0, 1) else
+                          "inputs larger than L2 (126 MB); no flush" if args.config in (3, 4) else
+                          "compute-bound; 2 MB model stays in L2")},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": clocks.summary(),
     }

@@ -84,3 +84,26 @@ def rate(thunk_n_threads, seconds=10.0):
         if el >= seconds:
             break
     return runs * n / el, threads, runs
+
+
+def propagate2d_thunk(model, nx, ny, t):
+    """Serial reference-order 2D propagation + both tails (config 0; the
+    reference runs it serially when no ParallelConfig is given)."""
+    mu_u, mu_v, s_u, s_v = model
+
+    def work():
+        mu, sg = ref2d.propagate2d(mu_u, mu_v, s_u, s_v, nx, ny, 1.0, 1.0)
+        ref2d.source_probability(mu, sg, t)
+        ref2d.sink_probability(mu, sg, t)
+
+    return work, nx * ny, 1
+
+
+def mc_thunk(model, nx, ny, n_samples):
+    """The GPU's Philox estimator restated in numpy on `n_samples` samples
+    (vertex-samples per call = nx*ny*n_samples)."""
+    from . import philox
+
+    mu_u, mu_v, s_u, s_v = model
+    return (lambda: philox.mc_divergence(mu_u, mu_v, s_u, s_v, nx, ny, 1.0, 1.0, n_samples, 7),
+            nx * ny * n_samples, 1)
