@@ -1,0 +1,160 @@
+"""Parity at BASELINE.json's full sizes (GPU).
+
+The oracle cannot evaluate 134 M points in seconds, so full-size runs are
+checked through (1) exact oracle comparisons on z-slabs cut from the full
+field -- full x/y extent, so every x and y face is covered -- at the global
+z faces and in the interior, using the slab restatement with ghost planes;
+(2) size-independent properties: TMA kernel == register kernel bitwise,
+sharded == whole bitwise, P(div>0) + P(div<0) == 1, sigma scale covariance.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import random_model_arrays  # noqa: F401
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import ref2d, ref3d  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def dev():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+
+    __graft_entry__.build()
+    from paper_2510_01190_b200 import device
+
+    return device
+
+
+@pytest.fixture(scope="module")
+def config3(dev):
+    from paper_2510_01190_b200 import configs
+
+    n = 512
+    f = configs.config3_slab(0, n)
+    out = dev.propagate3d(*f, n, n, n, 1.0, 1.0, 1.0, 0.0)
+    torch.cuda.synchronize()
+    return n, f, out
+
+
+def _slab_oracle(host_f, n, z0, z1, t):
+    plane = n * n
+    sl = [a[z0 * plane:z1 * plane].astype(np.float64) for a in host_f]
+    lo = (host_f[2][(z0 - 1) * plane:z0 * plane], host_f[5][(z0 - 1) * plane:z0 * plane]) if z0 else None
+    hi = (host_f[2][z1 * plane:(z1 + 1) * plane], host_f[5][z1 * plane:(z1 + 1) * plane]) if z1 < n else None
+    mu, sg = ref3d.propagate3d_slab(sl, lo, hi, n, n, z0, n, 1.0, 1.0, 1.0)
+    return mu, sg, ref2d.source_probability(mu, sg, t), ref2d.sink_probability(mu, sg, t)
+
+
+def test_config3_full_size_slabs_vs_oracle(config3):
+    n, f, out = config3
+    plane = n * n
+    host_f = [x.cpu().numpy() for x in f]
+    got = {k: v.cpu().numpy() for k, v in out.items()}
+    for z0, z1 in ((0, 3), (255, 258), (509, 512)):
+        mu, sg, ps, pk = _slab_oracle(host_f, n, z0, z1, 0.0)
+        sl = slice(z0 * plane, z1 * plane)
+        scale_mu, scale_sg = np.abs(mu).max(), np.abs(sg).max()
+        assert np.abs(got["mu"][sl] - mu).max() / scale_mu <= 1e-5
+        assert np.abs(got["sigma"][sl] - sg).max() / scale_sg <= 1e-5
+        assert np.all(np.abs(got["p_src"][sl] - ps) <= 1e-5 * ps + 1e-6)
+        assert np.all(np.abs(got["p_snk"][sl] - pk) <= 1e-5 * pk + 1e-6)
+
+
+def test_config3_full_size_properties(dev, config3, monkeypatch):
+    n, f, out = config3
+    # P(div > 0) + P(div < 0) == 1 wherever sigma > 0 (both tails from one erfc)
+    s = out["p_src"] + out["p_snk"]
+    assert float((s - 1).abs().max()) <= 2.4e-7
+    # TMA pipeline == register-prefetch kernel, bit for bit, at full size
+    monkeypatch.setenv("DIVUQ_NO_TMA", "1")
+    ref = dev.propagate3d(*f, n, n, n, 1.0, 1.0, 1.0, 0.0)
+    monkeypatch.delenv("DIVUQ_NO_TMA")
+    for k in out:
+        assert torch.equal(out[k], ref[k]), k
+    # 4-way z-slab sharding with ghost planes == whole grid, bit for bit
+    plane = n * n
+    for z0, z1 in ((0, 128), (128, 256), (256, 384), (384, 512)):
+        sl = [x[z0 * plane:z1 * plane] for x in f]
+        lo = (f[2][(z0 - 1) * plane:z0 * plane], f[5][(z0 - 1) * plane:z0 * plane]) if z0 else None
+        hi = (f[2][z1 * plane:(z1 + 1) * plane], f[5][z1 * plane:(z1 + 1) * plane]) if z1 < n else None
+        o = dev.propagate3d(*sl, n, n, z1 - z0, 1.0, 1.0, 1.0, 0.0, z0=z0, nz_global=n,
+                            halo_lo=lo, halo_hi=hi)
+        for k in o:
+            assert torch.equal(o[k], out[k][z0 * plane:z1 * plane]), (z0, k)
+
+
+def test_config3_sigma_scale_covariance(dev, config3):
+    n, f, out = config3
+    c = 2.0  # power of two: the scaled run is exact in fp32
+    scaled = f[:3] + [x * c for x in f[3:]]
+    o = dev.propagate3d(*scaled, n, n, n, 1.0, 1.0, 1.0, 0.0, outputs=("mu", "sigma"))
+    assert torch.equal(o["mu"], out["mu"])
+    assert float(((o["sigma"] - c * out["sigma"]).abs() / (c * out["sigma"]).clamp_min(1e-30)).max()) <= 1e-6
+
+
+def test_config4_full_width_slab_vs_oracle(dev):
+    """The fused kernel at config 4's plane size (1024^2, M = 16) on a
+    4-plane slab with reduced-moment halos, checked plane by plane."""
+    from paper_2510_01190_b200 import configs
+
+    nx = ny = 1024
+    nzl, z0, nz = 4, 500, 1024
+    plane = nx * ny
+    mem = configs.config4_slab(z0 - 1, nzl + 2, nx, ny, nz)  # the slab plus one ghost plane each side
+    slab = mem[:, :, plane:(nzl + 1) * plane].contiguous()
+    lo = dev.w_moments_plane(mem, nx, ny, nzl + 2, 0)
+    hi = dev.w_moments_plane(mem, nx, ny, nzl + 2, nzl + 1)
+    o = dev.ensemble_divergence3d(slab, nx, ny, nzl, 1.0, 1.0, 1.0, 0.1, z0=z0, nz_global=nz,
+                                  halo_lo=lo, halo_hi=hi, moments=True)
+    host = mem.cpu().numpy().astype(np.float64)
+    mu_r, sg_r = ref2d.fit_moments(host)                       # (3, (nzl+2)*plane)
+    assert np.abs(o["mom_mu"].cpu().numpy() - mu_r[:, plane:(nzl + 1) * plane]).max() <= 1e-5 * np.abs(mu_r).max()
+    fields = [mu_r[c, plane:(nzl + 1) * plane] for c in range(3)] + \
+             [sg_r[c, plane:(nzl + 1) * plane] for c in range(3)]
+    g_lo = (mu_r[2, :plane], sg_r[2, :plane])
+    g_hi = (mu_r[2, (nzl + 1) * plane:], sg_r[2, (nzl + 1) * plane:])
+    mu, sg = ref3d.propagate3d_slab(fields, g_lo, g_hi, nx, ny, z0, nz, 1.0, 1.0, 1.0)
+    assert np.abs(o["mu"].cpu().numpy() - mu).max() <= 1e-5 * np.abs(mu).max()
+    assert np.abs(o["sigma"].cpu().numpy() - sg).max() <= 1e-5 * np.abs(sg).max()
+    ps = ref2d.source_probability(mu, sg, 0.1)
+    pk = ref2d.sink_probability(mu, sg, 0.1)
+    assert np.all(np.abs(o["p_src"].cpu().numpy() - ps) <= 1e-5 * ps + 1e-6)
+    assert np.all(np.abs(o["p_snk"].cpu().numpy() - pk) <= 1e-5 * pk + 1e-6)
+
+
+def test_config2_mc_full_size_statistics(dev):
+    from paper_2510_01190_b200 import configs
+
+    model = configs.config2_model()
+    nx = ny = 256
+    n = 2000
+    mean, std = dev.mc_divergence2d(*(torch.from_numpy(a).cuda() for a in model), nx, ny, 1.0, 1.0,
+                                    n, 2024)
+    mu, sg = ref2d.propagate2d(*model, nx, ny, 1.0, 1.0)
+    mean, std = mean.cpu().numpy(), std.cpu().numpy()
+    # BASELINE gate: within 4 sigma / sqrt(N) (mean) and 4 sigma / sqrt(2N) (std) for >= 99.9 %
+    assert np.mean(np.abs(mean - mu) <= 4 * sg / np.sqrt(n)) >= 0.999
+    assert np.mean(np.abs(std - sg) <= 4 * sg / np.sqrt(2 * n)) >= 0.999
+    z = (mean - mu) / (sg / np.sqrt(n))
+    assert abs(z.mean()) < 0.05 and 0.9 < z.var() < 1.1
+
+
+def test_config1_full_size_vs_oracle(dev):
+    from paper_2510_01190_b200 import configs
+
+    nx = ny = 1024
+    mem = configs.config1_members(nx, ny, 20)
+    o = dev.ensemble_divergence2d(mem, nx, ny, 1.0, 1.0, 0.0, moments=True)
+    host = mem.cpu().numpy()
+    mu_r, sg_r = ref2d.fit_moments(host)
+    dmu, dsg = ref2d.propagate2d(mu_r[0], mu_r[1], sg_r[0], sg_r[1], nx, ny, 1.0, 1.0)
+    assert np.abs(o["mu"].cpu().numpy() - dmu).max() <= 1e-5 * np.abs(dmu).max()
+    assert np.abs(o["sigma"].cpu().numpy() - dsg).max() <= 1e-5 * np.abs(dsg).max()
+    ps = ref2d.source_probability(dmu, dsg, 0.0)
+    assert np.all(np.abs(o["p_src"].cpu().numpy() - ps) <= 1e-5 * ps + 1e-6)
