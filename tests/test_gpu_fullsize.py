@@ -156,5 +156,15 @@ def test_config1_full_size_vs_oracle(dev):
     dmu, dsg = ref2d.propagate2d(mu_r[0], mu_r[1], sg_r[0], sg_r[1], nx, ny, 1.0, 1.0)
     assert np.abs(o["mu"].cpu().numpy() - dmu).max() <= 1e-5 * np.abs(dmu).max()
     assert np.abs(o["sigma"].cpu().numpy() - dsg).max() <= 1e-5 * np.abs(dsg).max()
+    # P is ill-conditioned in fp32 here: sigma(x) goes down to 0.02 while the
+    # fields reach ~5, so dP ~ phi(t) * dmu / sigma.  Check (a) the tail map
+    # against the oracle evaluated at the kernel's own fp32 mu / sigma (the
+    # kernel's job), and (b) the end-to-end deviation, which is fp32 mu
+    # rounding amplified by 1/sigma.
+    gmu = o["mu"].cpu().numpy().astype(np.float64)
+    gsg = o["sigma"].cpu().numpy().astype(np.float64)
+    ps_own = ref2d.source_probability(gmu, gsg, 0.0)
+    p = o["p_src"].cpu().numpy()
+    assert np.all(np.abs(p - ps_own) <= 1e-5 * ps_own + 1e-6)
     ps = ref2d.source_probability(dmu, dsg, 0.0)
-    assert np.all(np.abs(o["p_src"].cpu().numpy() - ps) <= 1e-5 * ps + 1e-6)
+    assert np.abs(p - ps).max() <= 1e-3
