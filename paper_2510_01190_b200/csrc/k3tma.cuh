@@ -67,6 +67,8 @@ struct K3Xchg {
   float uh_mu[2][2][K3Cfg::TYMAX];
   float uh_sg[2][2][K3Cfg::TYMAX];
   K3Pending pend[K3Cfg::D];  // producer-private halo queue
+  // each consumer lane's w moments of plane k-1 (kept out of registers)
+  Vec<float, 4> wm[K3Cfg::TYMAX][2][32];
 };
 
 enum K3Map { kK3Main, kK3HaloX, kK3HaloY, kK3NumMaps };
@@ -265,19 +267,17 @@ struct K3 {
 #pragma unroll 1
           for (int b = 0; b < nb; ++b) {
             const K3Stage& t = r.wait();
-            V4 a[MB], c[MB];
-#pragma unroll
-            for (int mb = 0; mb < MB; ++mb) {
-              a[mb] = *reinterpret_cast<const V4*>(&t.top[mb * TX + cx0]);
-              c[mb] = *reinterpret_cast<const V4*>(&t.bot[mb * TX + cx0]);
-            }
-            r.release(lane);
+            // accumulate straight from the stage (holding MB rows in registers
+            // on top of two accumulator sets spills); release afterwards
 #pragma unroll
             for (int mb = 0; mb < MB; ++mb)
               if (b * MB + mb < p.M) {
-                at.add(b * MB + mb, a[mb].v);
-                ab.add(b * MB + mb, c[mb].v);
+                const V4 a = *reinterpret_cast<const V4*>(&t.top[mb * TX + cx0]);
+                const V4 c = *reinterpret_cast<const V4*>(&t.bot[mb * TX + cx0]);
+                at.add(b * MB + mb, a.v);
+                ab.add(b * MB + mb, c.v);
               }
+            r.release(lane);
           }
           V4 mu, sg;
           at.finish(p.M, mu.v, sg.v);
@@ -316,9 +316,14 @@ struct K3 {
       const bool jlo = j == 0, jhi = j == p.ny - 1;
       const float cy = (jlo || jhi) ? p.cy_bd : p.cy_in;
       const int kb = int(p.kbeg);
-      V4 wm_mu, wm_sg, w0_mu, w0_sg;
-      if (kb - 1 >= 0) row_moments(p, r, ty, cx0, lane, false, err, wm_mu, wm_sg);
-      else halo_w(p, -1, off2d, act, wm_mu, wm_sg);
+      V4 w0_mu, w0_sg;
+      {
+        V4 wm_mu, wm_sg;
+        if (kb - 1 >= 0) row_moments(p, r, ty, cx0, lane, false, err, wm_mu, wm_sg);
+        else halo_w(p, -1, off2d, act, wm_mu, wm_sg);
+        xb.wm[ty][0][lane] = wm_mu;
+        xb.wm[ty][1][lane] = wm_sg;
+      }
       row_moments(p, r, ty, cx0, lane, validate, err, w0_mu, w0_sg);
       int64_t o = int64_t(kb) * plane + off2d;
       for (int k = kb; k < int(p.kend); ++k, o += plane) {
@@ -331,10 +336,12 @@ struct K3 {
         else halo_w(p, k + 1, off2d, act, wp_mu, wp_sg);
 
         named_sync(1, 32 * (p.ty + 1));  // every row's v moments + the halo moments visible
-        const V4 vlo_mu = *reinterpret_cast<const V4*>(&xb.mu[xbuf][ty][cx0]);
-        const V4 vlo_sg = *reinterpret_cast<const V4*>(&xb.sg[xbuf][ty][cx0]);
-        const V4 vhi_mu = *reinterpret_cast<const V4*>(&xb.mu[xbuf][ty + 2][cx0]);
-        const V4 vhi_sg = *reinterpret_cast<const V4*>(&xb.sg[xbuf][ty + 2][cx0]);
+        // v neighbours are read per point from shared memory below (holding
+        // four more float4 here pushes the epilogue into local memory)
+        const float* vlo_mu = &xb.mu[xbuf][ty][cx0];
+        const float* vlo_sg = &xb.sg[xbuf][ty][cx0];
+        const float* vhi_mu = &xb.mu[xbuf][ty + 2][cx0];
+        const float* vhi_sg = &xb.sg[xbuf][ty + 2][cx0];
         float ul_mu = __shfl_up_sync(0xffffffffu, u_mu.v[3], 1);
         float ul_sg = __shfl_up_sync(0xffffffffu, u_sg.v[3], 1);
         float ur_mu = __shfl_down_sync(0xffffffffu, u_mu.v[0], 1);
@@ -350,6 +357,8 @@ struct K3 {
           const float cz = (klo || khi) ? p.cz_bd : p.cz_in;
           V4 omu, osg, ops, opk;
           using SM = StencilMath<float, true>;
+          const float* wm_mu = xb.wm[ty][0][lane].v;
+          const float* wm_sg = xb.wm[ty][1][lane].v;
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int i = xi + e;
@@ -360,13 +369,13 @@ struct K3 {
             const float uh = ihi ? uo : (e == 3 ? ur_mu : u_mu.v[e == 3 ? 0 : e + 1]);
             const float sl = ilo ? so : (e == 0 ? ul_sg : u_sg.v[e == 0 ? 0 : e - 1]);
             const float sh = ihi ? so : (e == 3 ? ur_sg : u_sg.v[e == 3 ? 0 : e + 1]);
-            const float vl = jlo ? v_mu.v[e] : vlo_mu.v[e];
-            const float vh = jhi ? v_mu.v[e] : vhi_mu.v[e];
-            const float svl = jlo ? v_sg.v[e] : vlo_sg.v[e];
-            const float svh = jhi ? v_sg.v[e] : vhi_sg.v[e];
-            const float wl = klo ? w0_mu.v[e] : wm_mu.v[e];
+            const float vl = jlo ? v_mu.v[e] : vlo_mu[e];
+            const float vh = jhi ? v_mu.v[e] : vhi_mu[e];
+            const float svl = jlo ? v_sg.v[e] : vlo_sg[e];
+            const float svh = jhi ? v_sg.v[e] : vhi_sg[e];
+            const float wl = klo ? w0_mu.v[e] : wm_mu[e];
             const float wh = khi ? w0_mu.v[e] : wp_mu.v[e];
-            const float swl = klo ? w0_sg.v[e] : wm_sg.v[e];
+            const float swl = klo ? w0_sg.v[e] : wm_sg[e];
             const float swh = khi ? w0_sg.v[e] : wp_sg.v[e];
             const float m = SM::mean(uh, ul, vh, vl, wh, wl, cx, cy, cz);
             omu.v[e] = m;
@@ -387,7 +396,8 @@ struct K3 {
             st_stream<float, 4>(p.out_mom_sigma + 2 * nl + o, w0_sg);
           }
         }
-        wm_mu = w0_mu; wm_sg = w0_sg;
+        xb.wm[ty][0][lane] = w0_mu;  // plane k becomes k-1 (own slot: no sync needed)
+        xb.wm[ty][1][lane] = w0_sg;
         w0_mu = wp_mu; w0_sg = wp_sg;
       }
     }
