@@ -253,13 +253,15 @@ int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
 
 // ---- TMA path for the fused 3D ensemble kernel (K3) ---------------------
 bool make_map5d_members(CUtensorMap* m, const float* base, int64_t nx, int64_t ny, int64_t nzl,
-                        int64_t members, int bx, int by, int bm, int64_t promo) {
+                        int64_t comps, int64_t members, int bx, int by, int bm, int64_t promo) {
   // view of the (M, 3, nzl, ny, nx) member slab as (x, y, plane, component, member)
   EncodeTiledFn fn = encode_tiled();
   if (!fn || !base) return false;
   const cuuint64_t nl = cuuint64_t(nx * ny * nzl);
-  const cuuint64_t dims[5] = {cuuint64_t(nx), cuuint64_t(ny), cuuint64_t(nzl), 3, cuuint64_t(members)};
-  const cuuint64_t strides[4] = {cuuint64_t(nx) * 4, cuuint64_t(nx * ny) * 4, nl * 4, 3 * nl * 4};
+  const cuuint64_t dims[5] = {cuuint64_t(nx), cuuint64_t(ny), cuuint64_t(nzl), cuuint64_t(comps),
+                              cuuint64_t(members)};
+  const cuuint64_t strides[4] = {cuuint64_t(nx) * 4, cuuint64_t(nx * ny) * 4, nl * 4,
+                                 cuuint64_t(comps) * nl * 4};
   const cuuint32_t box[5] = {cuuint32_t(bx), cuuint32_t(by), 1, 1, cuuint32_t(bm)};
   const cuuint32_t es[5] = {1, 1, 1, 1, 1};
   const CUtensorMapL2promotion l2 = promo >= 256 ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B
@@ -269,7 +271,7 @@ bool make_map5d_members(CUtensorMap* m, const float* base, int64_t nx, int64_t n
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int try_k3_tma(const StencilParams<float>& sp, cudaStream_t s, bool* used) {
+int try_k3_tma(const StencilParams<float>& sp, int comps, cudaStream_t s, bool* used) {
   using C = K3Cfg;
   *used = false;
   if (env_int("DIVUQ_NO_TMA", 0)) return DIVUQ_OK;
@@ -293,9 +295,9 @@ int try_k3_tma(const StencilParams<float>& sp, cudaStream_t s, bool* used) {
   std::memset(&tm, 0, sizeof(tm));
   const int64_t promo = env_int("DIVUQ_TMA_PROMO", 256);
   const int64_t M = sp.n_members;
-  if (!make_map5d_members(&tm.m[kK3Main], sp.members, sp.nx, sp.ny, sp.nzl, M, C::TX, ty, C::MB, promo) ||
-      !make_map5d_members(&tm.m[kK3HaloX], sp.members, sp.nx, sp.ny, sp.nzl, M, C::PAD, ty, C::MB, 0) ||
-      !make_map5d_members(&tm.m[kK3HaloY], sp.members, sp.nx, sp.ny, sp.nzl, M, C::TX, 1, C::MB, 0))
+  if (!make_map5d_members(&tm.m[kK3Main], sp.members, sp.nx, sp.ny, sp.nzl, comps, M, C::TX, ty, C::MB, promo) ||
+      !make_map5d_members(&tm.m[kK3HaloX], sp.members, sp.nx, sp.ny, sp.nzl, comps, M, C::PAD, ty, C::MB, 0) ||
+      !make_map5d_members(&tm.m[kK3HaloY], sp.members, sp.nx, sp.ny, sp.nzl, comps, M, C::TX, 1, C::MB, 0))
     return DIVUQ_OK;
   K3Params p;
   std::memset(&p, 0, sizeof(p));
@@ -306,6 +308,7 @@ int try_k3_tma(const StencilParams<float>& sp, cudaStream_t s, bool* used) {
   p.nx = int(sp.nx); p.ny = int(sp.ny); p.ty = ty; p.tiles_x = int(tiles_x);
   p.n_tiles = int(tiles_x * ((sp.ny + ty - 1) / ty));
   p.M = int(sp.n_members);
+  p.has_w = comps == 3;
   p.bytes_u = uint32_t((C::TX * ty + 2 * C::PAD * ty) * 4 * C::MB);
   p.bytes_v = uint32_t((C::TX * ty + 2 * C::TX) * 4 * C::MB);
   p.bytes_w = uint32_t(C::TX * ty * 4 * C::MB);
@@ -553,6 +556,9 @@ int divuq_ensemble_divergence2d_f32(const float* members, int64_t M, int64_t nx,
   p.out_mu = out_mu; p.out_sigma = out_sigma; p.out_psrc = out_p_src; p.out_psnk = out_p_snk;
   p.out_mom_mu = out_mom_mu; p.out_mom_sigma = out_mom_sigma;
   p.err = err;
+  bool used = false;
+  if (int r = try_k3_tma(p, 2, static_cast<cudaStream_t>(stream), &used)) return r;
+  if (used) return DIVUQ_OK;
   return dispatch_vec<float, false, kEnsemble>(p, true, static_cast<cudaStream_t>(stream));
 }
 
@@ -582,7 +588,7 @@ int divuq_ensemble_divergence3d_f32(const float* members, int64_t M, const float
   p.out_mom_mu = out_mom_mu; p.out_mom_sigma = out_mom_sigma;
   p.err = err;
   bool used = false;
-  if (int r = try_k3_tma(p, static_cast<cudaStream_t>(stream), &used)) return r;
+  if (int r = try_k3_tma(p, 3, static_cast<cudaStream_t>(stream), &used)) return r;
   if (used) return DIVUQ_OK;
   return dispatch_vec<float, true, kEnsemble>(p, true, static_cast<cudaStream_t>(stream));
 }

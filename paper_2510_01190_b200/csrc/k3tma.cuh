@@ -82,6 +82,7 @@ struct K3Params {
   int64_t nzl, z0, nzg, kbeg, kend;
   int64_t comp_stride;                                   // Nl = nx*ny*nzl
   int nx, ny, ty, tiles_x, n_tiles, M;
+  int has_w;                                             // 0: 2D ensemble (u, v only)
   uint32_t bytes_u, bytes_v, bytes_w;
   float cx_in, cx_bd, cy_in, cy_bd, cz_in, cz_bd;
   float theta;
@@ -143,13 +144,15 @@ struct K3 {
       const int y0 = (tile / p.tiles_x) * p.ty;
       const int kb = int(p.kbeg);
       const int nb = n_blocks(p);
-      if (kb - 1 >= 0)
-        for (int b = 0; b < nb; ++b) item(kW, x0, y0, kb - 1, b);
-      for (int b = 0; b < nb; ++b) item(kW, x0, y0, kb, b);
+      if (p.has_w) {
+        if (kb - 1 >= 0)
+          for (int b = 0; b < nb; ++b) item(kW, x0, y0, kb - 1, b);
+        for (int b = 0; b < nb; ++b) item(kW, x0, y0, kb, b);
+      }
       for (int k = kb; k < int(p.kend); ++k) {
         for (int b = 0; b < nb; ++b) item(kU, x0, y0, k, b);
         for (int b = 0; b < nb; ++b) item(kV, x0, y0, k, b);
-        if (k + 1 < p.nzl)
+        if (p.has_w && k + 1 < p.nzl)
           for (int b = 0; b < nb; ++b) item(kW, x0, y0, k + 1, b);
       }
     }
@@ -239,7 +242,7 @@ struct K3 {
     const int nb = n_blocks(p);
     for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
       const int kb = int(p.kbeg);
-      r.skip((kb - 1 >= 0 ? nb : 0) + nb, lane);
+      if (p.has_w) r.skip((kb - 1 >= 0 ? nb : 0) + nb, lane);
       for (int k = kb; k < int(p.kend); ++k) {
         {  // u: the 2*TY x-halo points
           ShiftedMoments<1> acc;
@@ -287,7 +290,7 @@ struct K3 {
           *reinterpret_cast<V4*>(&xb.mu[xbuf][p.ty + 1][cx0]) = mu;
           *reinterpret_cast<V4*>(&xb.sg[xbuf][p.ty + 1][cx0]) = sg;
         }
-        if (k + 1 < p.nzl) r.skip(nb, lane);
+        if (p.has_w && k + 1 < p.nzl) r.skip(nb, lane);
         named_sync(1, 32 * (p.ty + 1));
         xbuf ^= 1;
       }
@@ -316,15 +319,17 @@ struct K3 {
       const bool jlo = j == 0, jhi = j == p.ny - 1;
       const float cy = (jlo || jhi) ? p.cy_bd : p.cy_in;
       const int kb = int(p.kbeg);
-      V4 w0_mu, w0_sg;
+      V4 w0_mu = V4{{0.f, 0.f, 0.f, 0.f}}, w0_sg = w0_mu;
       {
-        V4 wm_mu, wm_sg;
-        if (kb - 1 >= 0) row_moments(p, r, ty, cx0, lane, false, err, wm_mu, wm_sg);
-        else halo_w(p, -1, off2d, act, wm_mu, wm_sg);
+        V4 wm_mu = w0_mu, wm_sg = w0_mu;
+        if (p.has_w) {
+          if (kb - 1 >= 0) row_moments(p, r, ty, cx0, lane, false, err, wm_mu, wm_sg);
+          else halo_w(p, -1, off2d, act, wm_mu, wm_sg);
+        }
         xb.wm[ty][0][lane] = wm_mu;
         xb.wm[ty][1][lane] = wm_sg;
       }
-      row_moments(p, r, ty, cx0, lane, validate, err, w0_mu, w0_sg);
+      if (p.has_w) row_moments(p, r, ty, cx0, lane, validate, err, w0_mu, w0_sg);
       int64_t o = int64_t(kb) * plane + off2d;
       for (int k = kb; k < int(p.kend); ++k, o += plane) {
         V4 u_mu, u_sg, v_mu, v_sg, wp_mu, wp_sg;
@@ -332,7 +337,8 @@ struct K3 {
         row_moments(p, r, ty, cx0, lane, validate, err, v_mu, v_sg);
         *reinterpret_cast<V4*>(&xb.mu[xbuf][ty + 1][cx0]) = v_mu;
         *reinterpret_cast<V4*>(&xb.sg[xbuf][ty + 1][cx0]) = v_sg;
-        if (k + 1 < p.nzl) row_moments(p, r, ty, cx0, lane, validate && k + 1 < p.kend, err, wp_mu, wp_sg);
+        if (!p.has_w) wp_mu = wp_sg = V4{{0.f, 0.f, 0.f, 0.f}};
+        else if (k + 1 < p.nzl) row_moments(p, r, ty, cx0, lane, validate && k + 1 < p.kend, err, wp_mu, wp_sg);
         else halo_w(p, k + 1, off2d, act, wp_mu, wp_sg);
 
         named_sync(1, 32 * (p.ty + 1));  // every row's v moments + the halo moments visible
@@ -352,7 +358,8 @@ struct K3 {
 
         if (act) {
           const int64_t kg = p.z0 + k;
-          const bool klo = kg == 0, khi = kg == p.nzg - 1;
+          // 2D: no z terms (w moments are zero, so c*(0-0) adds exactly 0)
+          const bool klo = p.has_w && kg == 0, khi = p.has_w && kg == p.nzg - 1;
           const bool interior = xin && yin && !klo && !khi;
           const float cz = (klo || khi) ? p.cz_bd : p.cz_in;
           V4 omu, osg, ops, opk;
@@ -390,10 +397,10 @@ struct K3 {
             const int64_t nl = p.comp_stride;
             st_stream<float, 4>(p.out_mom_mu + o, u_mu);
             st_stream<float, 4>(p.out_mom_mu + nl + o, v_mu);
-            st_stream<float, 4>(p.out_mom_mu + 2 * nl + o, w0_mu);
+            if (p.has_w) st_stream<float, 4>(p.out_mom_mu + 2 * nl + o, w0_mu);
             st_stream<float, 4>(p.out_mom_sigma + o, u_sg);
             st_stream<float, 4>(p.out_mom_sigma + nl + o, v_sg);
-            st_stream<float, 4>(p.out_mom_sigma + 2 * nl + o, w0_sg);
+            if (p.has_w) st_stream<float, 4>(p.out_mom_sigma + 2 * nl + o, w0_sg);
           }
         }
         xb.wm[ty][0][lane] = w0_mu;  // plane k becomes k-1 (own slot: no sync needed)

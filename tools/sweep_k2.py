@@ -11,10 +11,10 @@ from paper_2510_01190_b200 import configs, device as dev  # noqa: E402
 n = 512
 f = configs.config3_slab(0, n)
 out = {k: torch.empty(n**3, device="cuda") for k in dev.ALL_OUTPUTS}
-knobs = {
-    "DIVUQ_TMA_PROMO": os.environ.get("SWEEP_PROMO", "256,64,0").split(","),
-    "DIVUQ_TMA_TY": os.environ.get("SWEEP_TY", "0,16,12,8").split(","),
-}
+knobs = {}
+for spec in os.environ.get("SWEEP", "DIVUQ_PHASE=0,1,2,4").split(";"):
+    k, v = spec.split("=")
+    knobs[k] = v.split(",")
 for combo in itertools.product(*knobs.values()):
     for k, v in zip(knobs, combo):
         os.environ[k] = v
