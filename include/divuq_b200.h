@@ -112,6 +112,19 @@ int divuq_tail_probs_f64(const double* mu, const double* sigma, int64_t n, doubl
 int divuq_tail_probs_f32(const float* mu, const float* sigma, int64_t n, double theta,
                          float* out_below, float* out_above, int32_t* err_word, void* stream);
 
+/* ---- level-crossing probability ----------------------
+ * Replaces lcp() / cell_crossing_probability (lcp.py:71-100).  lcp2d: one
+ * value per cell, cell index cj*(nx-1)+ci, corners v00, v00+1, v00+nx,
+ * v00+nx+1; LCP = clip(1 - (prod below + prod above), 0, 1) with the
+ * _tail_probs tails (lcp.py:48-68).  cell_crossing: stacked (n, 4) corner
+ * arrays, same formula. */
+int divuq_lcp2d_f64(const double* mu, const double* sigma, int64_t nx, int64_t ny, double isovalue,
+                    double* out_cells, int32_t* err_word, void* stream);
+int divuq_lcp2d_f32(const float* mu, const float* sigma, int64_t nx, int64_t ny, double isovalue,
+                    float* out_cells, int32_t* err_word, void* stream);
+int divuq_cell_crossing_f64(const double* mu4, const double* sigma4, int64_t n_cells,
+                            double isovalue, double* out, int32_t* err_word, void* stream);
+
 /* ---- K1: ensemble moments ---------------------------------------------
  * Replaces fit_gaussian (gaussian.py:35-45): mean = sequential sum / M,
  * sigma = sqrt(two-pass sum of squared deviations / (M-1)); fp64 is
@@ -195,6 +208,10 @@ int divuq_host_propagate3d_f32(const float* mu_u, const float* mu_v, const float
                                int64_t chunk_planes, int device);
 int divuq_host_tail_probs_f64(const double* mu, const double* sigma, int64_t n, double theta,
                               double* out_below, double* out_above, int device);
+int divuq_host_lcp2d_f64(const double* mu, const double* sigma, int64_t nx, int64_t ny,
+                         double isovalue, double* out_cells, int device);
+int divuq_host_cell_crossing_f64(const double* mu4, const double* sigma4, int64_t n_cells,
+                                 double isovalue, double* out, int device);
 int divuq_host_fit_gaussian_f64(const double* members, int64_t n_members, int64_t n_components,
                                 int64_t n_points, double* out_mu, double* out_sigma, int device);
 int divuq_host_ensemble_divergence2d_f32(const float* members, int64_t n_members,

@@ -153,3 +153,22 @@ def error_metrics(est_mean, est_std, mu, sigma):
         float(np.abs(ds).mean()),
         float(np.sum(dm**2) + np.sum(ds**2)),
     )
+
+
+def cell_crossing_probability(mu, sigma, isovalue):
+    """LCP for stacked cells (..., 4) (lcp.py:71-77): sequential products of
+    the four corners' tails, 1 - (prod below + prod above), clipped."""
+    below, above = tail_probs(np.asarray(mu, float), np.asarray(sigma, float), isovalue)
+    pb = below[..., 0] * below[..., 1] * below[..., 2] * below[..., 3]
+    pa = above[..., 0] * above[..., 1] * above[..., 2] * above[..., 3]
+    return np.clip(1.0 - (pb + pa), 0.0, 1.0)
+
+
+def lcp(mu, sigma, nx, ny, isovalue):
+    """Per-cell LCP, cell index cj*(nx-1)+ci (lcp.py:80-100)."""
+    ci, cj = np.meshgrid(np.arange(nx - 1), np.arange(ny - 1))
+    v00 = (cj * nx + ci).ravel()
+    corners = np.stack([v00, v00 + 1, v00 + nx, v00 + nx + 1], axis=-1)
+    mu = np.asarray(mu, float)
+    sigma = np.asarray(sigma, float)
+    return cell_crossing_probability(mu[corners], sigma[corners], isovalue)

@@ -16,6 +16,8 @@ there is no CPU fallback.
 from . import _lib  # noqa: F401  (fails loudly without the CUDA library)
 from .api import (
     EnsembleDivergence,
+    cell_crossing_probability,
+    lcp,
     Propagation,
     divergence_deterministic,
     ensemble_divergence,
@@ -37,6 +39,7 @@ from .types import (
     GaussianScalarField3,
     GaussianVectorField,
     GaussianVectorField3,
+    LcpField,
     McConfig,
     McDivergenceEstimate,
     ParallelConfig,
@@ -51,10 +54,10 @@ __version__ = "0.1.0"
 
 __all__ = [
     "Ensemble2", "EnsembleDivergence", "GaussianScalarField", "GaussianScalarField3",
-    "GaussianVectorField", "GaussianVectorField3", "McConfig", "McDivergenceEstimate",
+    "GaussianVectorField", "GaussianVectorField3", "LcpField", "McConfig", "McDivergenceEstimate",
     "ParallelConfig", "Propagation", "ScalarField2", "UniformGrid2", "UniformGrid3",
-    "VectorField2", "divergence_deterministic", "ensemble_divergence", "error_metrics",
-    "fit_gaussian", "mc_divergence", "propagate_divergence", "propagate_with_probabilities",
+    "VectorField2", "cell_crossing_probability", "divergence_deterministic", "ensemble_divergence", "error_metrics",
+    "fit_gaussian", "lcp", "mc_divergence", "propagate_divergence", "propagate_with_probabilities",
     "propagate_with_probabilities3d", "set_device", "sink_probability", "source_probability",
     "stencil_distribution", "tail_probs", "vertex_index",
 ]

@@ -23,6 +23,7 @@ from .types import (
     GaussianScalarField3,
     GaussianVectorField,
     GaussianVectorField3,
+    LcpField,
     McConfig,
     McDivergenceEstimate,
     ParallelConfig,
@@ -232,3 +233,24 @@ def ensemble_divergence(ensemble: Ensemble2, t: float = 0.0) -> EnsembleDivergen
     model = GaussianVectorField(g, mom_mu[0], mom_mu[1], mom_sg[0], mom_sg[1])
     return EnsembleDivergence(model, GaussianScalarField(g, o[0], o[1]), o[2].astype(np.float64),
                               o[3].astype(np.float64))
+
+
+def cell_crossing_probability(mu, sigma, isovalue: float) -> np.ndarray:
+    """LCP for stacked cells: mu, sigma of shape (..., 4) (lcp.py:71-77)."""
+    mu = _c64(mu)
+    sigma = _c64(sigma)
+    if mu.shape != sigma.shape or mu.shape[-1:] != (4,):
+        raise ValueError("mu and sigma must have the same shape (..., 4)")
+    out = np.empty(mu.shape[:-1])
+    _check(lib.divuq_host_cell_crossing_f64(_p(mu), _p(sigma), out.size, float(isovalue), _p(out),
+                                            _DEVICE))
+    return out
+
+
+def lcp(fld: GaussianScalarField, isovalue: float, config: ParallelConfig | None = None) -> LcpField:
+    """Crossing probability of the isovalue for every grid cell (lcp.py:80-100)."""
+    g = fld.grid
+    out = np.empty(g.n_cells)
+    _check(lib.divuq_host_lcp2d_f64(_p(fld.mu), _p(fld.sigma), g.nx, g.ny, float(isovalue), _p(out),
+                                    _DEVICE))
+    return LcpField(g, isovalue, out)

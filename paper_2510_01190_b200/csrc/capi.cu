@@ -13,6 +13,7 @@
 #include "gen.cuh"
 #include "k2tma.cuh"
 #include "k3tma.cuh"
+#include "lcp.cuh"
 #include "mc.cuh"
 #include "stencil.cuh"
 
@@ -603,6 +604,36 @@ int divuq_tail_probs_f32(const float* mu, const float* sigma, int64_t n, double 
   return tail_probs<float>(mu, sigma, n, theta, out_below, out_above, err, stream);
 }
 
+int divuq_lcp2d_f64(const double* mu, const double* sigma, int64_t nx, int64_t ny, double isovalue,
+                    double* out, int32_t* err, void* stream) {
+  if (nx < 2 || ny < 2) return DIVUQ_EGRID;
+  if (!mu || !sigma || !out) return DIVUQ_EINVAL;
+  dim3 grid(unsigned((nx - 1 + kLcpTX - 1) / kLcpTX), unsigned((ny - 1 + kLcpTY - 1) / kLcpTY));
+  lcp2d_kernel<double><<<grid, dim3(kLcpTX, kLcpTY), 0, static_cast<cudaStream_t>(stream)>>>(
+      mu, sigma, nx, ny, isovalue, out, err);
+  return int(cudaGetLastError());
+}
+
+int divuq_lcp2d_f32(const float* mu, const float* sigma, int64_t nx, int64_t ny, double isovalue,
+                    float* out, int32_t* err, void* stream) {
+  if (nx < 2 || ny < 2) return DIVUQ_EGRID;
+  if (!mu || !sigma || !out) return DIVUQ_EINVAL;
+  dim3 grid(unsigned((nx - 1 + kLcpTX - 1) / kLcpTX), unsigned((ny - 1 + kLcpTY - 1) / kLcpTY));
+  lcp2d_kernel<float><<<grid, dim3(kLcpTX, kLcpTY), 0, static_cast<cudaStream_t>(stream)>>>(
+      mu, sigma, nx, ny, float(isovalue), out, err);
+  return int(cudaGetLastError());
+}
+
+int divuq_cell_crossing_f64(const double* mu4, const double* sigma4, int64_t n_cells, double isovalue,
+                            double* out, int32_t* err, void* stream) {
+  if (n_cells < 0 || (n_cells && (!mu4 || !sigma4 || !out))) return DIVUQ_EINVAL;
+  if (n_cells == 0) return DIVUQ_OK;
+  const int64_t grid = std::min<int64_t>((n_cells + 255) / 256, int64_t(sm_count()) * 8);
+  cell_crossing_kernel<double><<<unsigned(grid), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      mu4, sigma4, n_cells, isovalue, out, err);
+  return int(cudaGetLastError());
+}
+
 int64_t divuq_mc_scratch_bytes(int64_t nx, int64_t row_begin, int64_t row_end, int64_t n_samples) {
   if (nx < 1 || row_end <= row_begin || n_samples < 1) return 0;
   const int64_t chunks = (n_samples + kMcChunk - 1) / kMcChunk;
@@ -733,6 +764,53 @@ int divuq_host_tail_probs_f64(const double* mu, const double* sigma, int64_t n, 
     return r;
   if (out_below) DIVUQ_CUDA(cudaMemcpyAsync(out_below, base + 2 * n, b, cudaMemcpyDeviceToHost, sg.s));
   if (out_above) DIVUQ_CUDA(cudaMemcpyAsync(out_above, base + 3 * n, b, cudaMemcpyDeviceToHost, sg.s));
+  int status = 0;
+  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  return status;
+}
+
+int divuq_host_lcp2d_f64(const double* mu, const double* sigma, int64_t nx, int64_t ny,
+                         double isovalue, double* out, int device) {
+  if (nx < 2 || ny < 2) return DIVUQ_EGRID;
+  if (!mu || !sigma || !out) return DIVUQ_EINVAL;
+  DIVUQ_CUDA(cudaSetDevice(device));
+  StreamGuard sg;
+  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  const int64_t n = nx * ny, nc = (nx - 1) * (ny - 1);
+  DevBuf d;
+  DIVUQ_CUDA(d.alloc(size_t(2 * n + nc) * sizeof(double) + 256, sg.s));
+  double* dmu = d.as<double>();
+  double* dsg = dmu + n;
+  double* dout = dsg + n;
+  int32_t* derr = reinterpret_cast<int32_t*>(dout + nc);
+  DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
+  DIVUQ_CUDA(cudaMemcpyAsync(dmu, mu, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, sg.s));
+  DIVUQ_CUDA(cudaMemcpyAsync(dsg, sigma, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, sg.s));
+  if (int r = divuq_lcp2d_f64(dmu, dsg, nx, ny, isovalue, dout, derr, sg.s)) return r;
+  DIVUQ_CUDA(cudaMemcpyAsync(out, dout, size_t(nc) * sizeof(double), cudaMemcpyDeviceToHost, sg.s));
+  int status = 0;
+  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  return status;
+}
+
+int divuq_host_cell_crossing_f64(const double* mu4, const double* sigma4, int64_t n_cells,
+                                 double isovalue, double* out, int device) {
+  if (n_cells < 0 || (n_cells && (!mu4 || !sigma4 || !out))) return DIVUQ_EINVAL;
+  if (n_cells == 0) return DIVUQ_OK;
+  DIVUQ_CUDA(cudaSetDevice(device));
+  StreamGuard sg;
+  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  DevBuf d;
+  DIVUQ_CUDA(d.alloc(size_t(9 * n_cells) * sizeof(double) + 256, sg.s));
+  double* dmu = d.as<double>();
+  double* dsg = dmu + 4 * n_cells;
+  double* dout = dsg + 4 * n_cells;
+  int32_t* derr = reinterpret_cast<int32_t*>(dout + n_cells);
+  DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
+  DIVUQ_CUDA(cudaMemcpyAsync(dmu, mu4, size_t(4 * n_cells) * sizeof(double), cudaMemcpyHostToDevice, sg.s));
+  DIVUQ_CUDA(cudaMemcpyAsync(dsg, sigma4, size_t(4 * n_cells) * sizeof(double), cudaMemcpyHostToDevice, sg.s));
+  if (int r = divuq_cell_crossing_f64(dmu, dsg, n_cells, isovalue, dout, derr, sg.s)) return r;
+  DIVUQ_CUDA(cudaMemcpyAsync(out, dout, size_t(n_cells) * sizeof(double), cudaMemcpyDeviceToHost, sg.s));
   int status = 0;
   DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
   return status;

@@ -147,6 +147,19 @@ def tail_probs(mu, sigma, theta, *, check=True):
     return below, above
 
 
+def lcp2d(mu, sigma, nx, ny, isovalue, *, check=True):
+    """Per-cell level-crossing probability ((ny-1)*(nx-1),) (lcp.py:80-100)."""
+    dt = mu.dtype
+    _req(mu, "mu", dt, nx * ny)
+    _req(sigma, "sigma", dt, nx * ny)
+    out = torch.empty((nx - 1) * (ny - 1), dtype=dt, device=mu.device)
+    err = _ErrWord(mu.device, check)
+    fn = getattr(lib, f"divuq_lcp2d_{_FP[dt]}")
+    _check(fn(_ptr(mu), _ptr(sigma), nx, ny, float(isovalue), _ptr(out), err.ptr, _stream()))
+    err.raise_if_set()
+    return out
+
+
 def fit_moments(members, *, out=None, check=True):
     """K1: (M, C, N) members -> mu (C, N), sigma (C, N) (gaussian.py:35-45)."""
     _req(members, "members")
@@ -254,7 +267,7 @@ def mc_divergence2d(mu_u, mu_v, s_u, s_v, nx, ny, dx, dy, n_samples, seed, *, ro
 
 
 __all__ = [
-    "ALL_OUTPUTS", "propagate2d", "propagate3d", "tail_probs", "fit_moments",
+    "ALL_OUTPUTS", "propagate2d", "propagate3d", "tail_probs", "lcp2d", "fit_moments",
     "ensemble_divergence2d", "ensemble_divergence3d", "w_moments_plane", "mc_divergence2d",
 ]
 _ = _lib  # re-export guard

@@ -205,6 +205,25 @@ class GaussianScalarField:
 
 
 @dataclass(frozen=True)
+class LcpField:
+    """Per-cell crossing probability, cell-major j*(nx-1) + i (lcp.py:26-45)."""
+
+    grid: UniformGrid2
+    isovalue: float
+    probabilities: np.ndarray = field(repr=False)
+
+    def __post_init__(self):
+        object.__setattr__(self, "probabilities",
+                           _frozen_array(self.probabilities, self.grid.n_cells, "probabilities"))
+        p = self.probabilities
+        if np.any(p < 0) or np.any(p > 1):
+            raise ValueError("probabilities must lie in [0, 1]")
+
+    def as_2d(self) -> np.ndarray:
+        return self.probabilities.reshape(self.grid.ny - 1, self.grid.nx - 1)
+
+
+@dataclass(frozen=True)
 class GaussianVectorField3:
     """Independent N(mu, sigma^2) per vertex and component on a 3D grid."""
 

@@ -83,6 +83,25 @@ def main():
     prop["n_grids"] = np.array(len(grids))
     np.savez_compressed(os.path.join(OUT, "propagate2d.npz"), **prop)
 
+    # ---- lcp (lcp.py:71-100): per-cell crossing probability --------------
+    lc = {}
+    for gi, (nx, ny, iso) in enumerate([(9, 6, 0.2), (5, 4, -0.1), (33, 17, 0.0), (2, 2, 0.5)]):
+        g = divuq.UniformGrid2(nx, ny)
+        mu = rng.normal(size=g.n_vertices)
+        sg = rng.uniform(0.01, 1.0, g.n_vertices)
+        sg[::5] = 0.0
+        fld = divuq.GaussianScalarField(g, mu, sg)
+        lc[f"l{gi}_grid"] = np.array([nx, ny, iso])
+        lc[f"l{gi}_mu"], lc[f"l{gi}_sigma"] = mu, sg
+        lc[f"l{gi}_lcp"] = divuq.lcp(fld, iso).probabilities
+    cm = rng.normal(0.0, 1.0, (300, 4))
+    cs = rng.uniform(0.05, 1.5, (300, 4))
+    cs[::7, 2] = 0.0
+    lc["cells_mu"], lc["cells_sigma"] = cm, cs
+    lc["cells_lcp"] = divuq.cell_crossing_probability(cm, cs, 0.3)
+    lc["n_grids"] = np.array(4)
+    np.savez_compressed(os.path.join(OUT, "lcp.npz"), **lc)
+
     # ---- Fig. 1 golden (test_divergence.py:16-21) -------------------------
     fig1 = ((5.98, 0.96), (6.40, 0.38), (6.50, 0.94), (4.30, 0.65))
     mu, sd = divuq.stencil_distribution(fig1, (1.0, 1.0))

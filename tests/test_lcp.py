@@ -1,0 +1,101 @@
+"""Level-crossing probability (lcp.py:71-100).
+
+CPU part: the oracle restatement is pinned BITWISE to the reference's own
+lcp() / cell_crossing_probability outputs (tests/golden/lcp.npz).
+GPU part: the kernel vs those golden values at |dP| <= 1e-12 (the tails come
+from a different erfc than scipy's), plus the reference suite's own LCP
+properties (pkg/tests/test_lcp.py): range, exact negation symmetry, sigma -> 0
+indicator, finite extreme tails, the cell formula on a field.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import ref2d
+
+
+def test_oracle_lcp_bitwise_vs_reference_golden():
+    g = golden("lcp.npz")
+    for gi in range(int(g["n_grids"])):
+        nx, ny, iso = g[f"l{gi}_grid"]
+        got = ref2d.lcp(g[f"l{gi}_mu"], g[f"l{gi}_sigma"], int(nx), int(ny), float(iso))
+        assert np.array_equal(got, g[f"l{gi}_lcp"]), gi
+    got = ref2d.cell_crossing_probability(g["cells_mu"], g["cells_sigma"], 0.3)
+    assert np.array_equal(got, g["cells_lcp"])
+
+
+@pytest.fixture(scope="module")
+def gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+
+    __graft_entry__.build()
+    import paper_2510_01190_b200 as d
+
+    return d
+
+
+def _cell(d, mus, sigmas, theta):
+    return float(d.cell_crossing_probability(np.array([mus], float), np.array([sigmas], float), theta)[0])
+
+
+@pytest.mark.gpu
+def test_lcp_gpu_vs_reference_golden(gpu):
+    d = gpu
+    g = golden("lcp.npz")
+    for gi in range(int(g["n_grids"])):
+        nx, ny, iso = g[f"l{gi}_grid"]
+        grid = d.UniformGrid2(int(nx), int(ny))
+        fld = d.GaussianScalarField(grid, g[f"l{gi}_mu"], g[f"l{gi}_sigma"])
+        out = d.lcp(fld, float(iso))
+        assert isinstance(out, d.LcpField) and out.probabilities.shape == (grid.n_cells,)
+        assert np.abs(out.probabilities - g[f"l{gi}_lcp"]).max() <= 1e-12
+    got = d.cell_crossing_probability(g["cells_mu"], g["cells_sigma"], 0.3)
+    assert np.abs(got - g["cells_lcp"]).max() <= 1e-12
+
+
+@pytest.mark.gpu
+def test_lcp_reference_suite_properties(gpu, rng):
+    d = gpu
+    assert _cell(d, [1, 2, 3, 4], [0, 0, 0, 0], 0.5) == 0.0
+    assert _cell(d, [-1, 2, 3, 4], [0, 0, 0, 0], 0.5) == 1.0
+    assert abs(_cell(d, [0.7] * 4, [0.3] * 4, 0.7) - 0.875) <= 1e-15
+    assert _cell(d, [1e8] * 4, [1e-8] * 4, 0.0) == 0.0
+    assert _cell(d, [0.0, 0.0, 1e8, -1e8], [1e-8] * 4, 0.5) == 1.0
+    # exact negation symmetry and range on random cells
+    mus = rng.uniform(-100, 100, (5000, 4))
+    sgs = rng.uniform(0.001, 10, (5000, 4))
+    th = 0.37
+    a = d.cell_crossing_probability(mus, sgs, th)
+    b = d.cell_crossing_probability(-mus, sgs, -th)
+    assert np.array_equal(a, b)
+    assert np.all((a >= 0) & (a <= 1))
+    # sigma -> 0: the deterministic crossing indicator
+    mus = rng.normal(size=(500, 4))
+    theta = 0.1
+    crossing = ~(np.all(mus < theta, axis=1) | np.all(mus > theta, axis=1))
+    assert np.array_equal(d.cell_crossing_probability(mus, np.zeros_like(mus), theta), crossing.astype(float))
+    shrunk = d.cell_crossing_probability(mus, np.full_like(mus, 1e-300), theta)
+    assert np.abs(shrunk - crossing).max() <= 1e-12
+
+
+@pytest.mark.gpu
+def test_lcp_field_matches_cell_formula_and_device_api(gpu, rng):
+    d = gpu
+    import torch
+
+    from paper_2510_01190_b200 import device as dev
+
+    for nx, ny in ((5, 4), (70, 33), (2, 2)):
+        grid = d.UniformGrid2(nx, ny)
+        mu = rng.normal(size=grid.n_vertices)
+        sg = rng.uniform(0.05, 0.5, grid.n_vertices)
+        out = d.lcp(d.GaussianScalarField(grid, mu, sg), -0.1)
+        assert np.abs(out.probabilities - ref2d.lcp(mu, sg, nx, ny, -0.1)).max() <= 1e-12
+        o32 = dev.lcp2d(torch.from_numpy(mu.astype(np.float32)).cuda(),
+                        torch.from_numpy(sg.astype(np.float32)).cuda(), nx, ny, -0.1).cpu().numpy()
+        ref32 = ref2d.lcp(mu.astype(np.float32), sg.astype(np.float32), nx, ny, -0.1)
+        assert np.abs(o32 - ref32).max() <= 2e-5
