@@ -125,6 +125,24 @@ int divuq_lcp2d_f32(const float* mu, const float* sigma, int64_t nx, int64_t ny,
 int divuq_cell_crossing_f64(const double* mu4, const double* sigma4, int64_t n_cells,
                             double isovalue, double* out, int32_t* err_word, void* stream);
 
+/* ---- velocity-magnitude-gradient prologue ---------------
+ * velocity_magnitude (gaussian.py:48-50) = hypot(u, v); gradient
+ * (gaussian.py:53-58, stencils.py:87-96) = (f[hi]*cx - f[lo]*cx,
+ * f[hi]*cy - f[lo]*cy) with the divergence's one-sided boundary rule, output
+ * (2, n); gradient_ensemble (gaussian.py:61-66): every member of (M, 2, n)
+ * mapped through both, fused (magnitudes recomputed per neighbour, never
+ * stored), output (M, 2, n). */
+int divuq_velocity_magnitude_f64(const double* u, const double* v, int64_t n, double* out,
+                                 int32_t* err_word, void* stream);
+int divuq_gradient2d_f64(const double* values, int64_t nx, int64_t ny, double dx, double dy,
+                         double* out_gx_gy, int32_t* err_word, void* stream);
+int divuq_gradient_ensemble2d_f64(const double* members, int64_t n_members, int64_t nx, int64_t ny,
+                                  double dx, double dy, double* out_members, int32_t* err_word,
+                                  void* stream);
+int divuq_gradient_ensemble2d_f32(const float* members, int64_t n_members, int64_t nx, int64_t ny,
+                                  double dx, double dy, float* out_members, int32_t* err_word,
+                                  void* stream);
+
 /* ---- K1: ensemble moments ---------------------------------------------
  * Replaces fit_gaussian (gaussian.py:35-45): mean = sequential sum / M,
  * sigma = sqrt(two-pass sum of squared deviations / (M-1)); fp64 is
@@ -212,6 +230,13 @@ int divuq_host_lcp2d_f64(const double* mu, const double* sigma, int64_t nx, int6
                          double isovalue, double* out_cells, int device);
 int divuq_host_cell_crossing_f64(const double* mu4, const double* sigma4, int64_t n_cells,
                                  double isovalue, double* out, int device);
+int divuq_host_velocity_magnitude_f64(const double* u, const double* v, int64_t n, double* out,
+                                      int device);
+int divuq_host_gradient2d_f64(const double* values, int64_t nx, int64_t ny, double dx, double dy,
+                              double* out_gx_gy, int device);
+int divuq_host_gradient_ensemble2d_f64(const double* members, int64_t n_members, int64_t nx,
+                                       int64_t ny, double dx, double dy, double* out_members,
+                                       int device);
 int divuq_host_fit_gaussian_f64(const double* members, int64_t n_members, int64_t n_components,
                                 int64_t n_points, double* out_mu, double* out_sigma, int device);
 int divuq_host_ensemble_divergence2d_f32(const float* members, int64_t n_members,

@@ -17,7 +17,10 @@ from . import _lib  # noqa: F401  (fails loudly without the CUDA library)
 from .api import (
     EnsembleDivergence,
     cell_crossing_probability,
+    gradient,
+    gradient_ensemble,
     lcp,
+    velocity_magnitude,
     Propagation,
     divergence_deterministic,
     ensemble_divergence,
@@ -57,7 +60,8 @@ __all__ = [
     "GaussianVectorField", "GaussianVectorField3", "LcpField", "McConfig", "McDivergenceEstimate",
     "ParallelConfig", "Propagation", "ScalarField2", "UniformGrid2", "UniformGrid3",
     "VectorField2", "cell_crossing_probability", "divergence_deterministic", "ensemble_divergence", "error_metrics",
-    "fit_gaussian", "lcp", "mc_divergence", "propagate_divergence", "propagate_with_probabilities",
+    "fit_gaussian", "gradient", "gradient_ensemble", "lcp", "mc_divergence",
+    "velocity_magnitude", "propagate_divergence", "propagate_with_probabilities",
     "propagate_with_probabilities3d", "set_device", "sink_probability", "source_probability",
     "stencil_distribution", "tail_probs", "vertex_index",
 ]

@@ -235,6 +235,35 @@ def ensemble_divergence(ensemble: Ensemble2, t: float = 0.0) -> EnsembleDivergen
                               o[3].astype(np.float64))
 
 
+def velocity_magnitude(member: VectorField2) -> ScalarField2:
+    """hypot(u, v) per vertex (gaussian.py:48-50)."""
+    g = member.grid
+    out = np.empty(g.n_vertices)
+    _check(lib.divuq_host_velocity_magnitude_f64(_p(member.u), _p(member.v), g.n_vertices, _p(out),
+                                                 _DEVICE))
+    return ScalarField2(g, out)
+
+
+def gradient(fld: ScalarField2) -> VectorField2:
+    """Central-difference gradient, one-sided on the boundary (gaussian.py:53-58)."""
+    g = fld.grid
+    out = np.empty((2, g.n_vertices))
+    _check(lib.divuq_host_gradient2d_f64(_p(fld.values), g.nx, g.ny, float(g.dx), float(g.dy),
+                                         _p(out), _DEVICE))
+    return VectorField2(g, out[0], out[1])
+
+
+def gradient_ensemble(ensemble: Ensemble2) -> Ensemble2:
+    """Each member through velocity_magnitude then gradient (gaussian.py:61-66),
+    fused on the GPU: the magnitude field is never materialised."""
+    g = ensemble.grid
+    stacked = _c64(ensemble.stacked())
+    out = np.empty_like(stacked)
+    _check(lib.divuq_host_gradient_ensemble2d_f64(_p(stacked), stacked.shape[0], g.nx, g.ny,
+                                                  float(g.dx), float(g.dy), _p(out), _DEVICE))
+    return Ensemble2(g, tuple(VectorField2(g, o[0], o[1]) for o in out))
+
+
 def cell_crossing_probability(mu, sigma, isovalue: float) -> np.ndarray:
     """LCP for stacked cells: mu, sigma of shape (..., 4) (lcp.py:71-77)."""
     mu = _c64(mu)

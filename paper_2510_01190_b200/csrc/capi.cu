@@ -13,6 +13,7 @@
 #include "gen.cuh"
 #include "k2tma.cuh"
 #include "k3tma.cuh"
+#include "gradient.cuh"
 #include "lcp.cuh"
 #include "mc.cuh"
 #include "stencil.cuh"
@@ -472,6 +473,120 @@ struct StreamGuard {
   cudaStream_t s = nullptr;
   ~StreamGuard() { if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); } }
 };
+
+// ---- velocity-magnitude-gradient prologue ----------
+template <typename T>
+int launch_gradient(const T* in, int64_t members, int64_t in_mstride, int64_t nx, int64_t ny,
+                    double dx, double dy, T* out, int64_t out_mstride, bool mag, int32_t* err,
+                    void* stream) {
+  if (int r = grid_ok(nx, ny, dx, dy)) return r;
+  if (!in || !out || members < 1) return DIVUQ_EINVAL;
+  const int64_t total = members * nx * ny;
+  const int64_t grid = std::min<int64_t>((total + 255) / 256, int64_t(sm_count()) * 16);
+  const T cxi = T(1.0 / (2.0 * dx)), cxb = T(1.0 / dx), cyi = T(1.0 / (2.0 * dy)), cyb = T(1.0 / dy);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (mag)
+    gradient2d_kernel<T, true><<<unsigned(grid), 256, 0, s>>>(in, members, in_mstride, nx, ny, cxi, cxb,
+                                                              cyi, cyb, out, out_mstride, err);
+  else
+    gradient2d_kernel<T, false><<<unsigned(grid), 256, 0, s>>>(in, members, in_mstride, nx, ny, cxi, cxb,
+                                                               cyi, cyb, out, out_mstride, err);
+  return int(cudaGetLastError());
+}
+
+}  // namespace (reopened below)
+
+extern "C" {
+
+int divuq_velocity_magnitude_f64(const double* u, const double* v, int64_t n, double* out,
+                                 int32_t* err, void* stream) {
+  if (n < 0 || (n && (!u || !v || !out))) return DIVUQ_EINVAL;
+  if (n == 0) return DIVUQ_OK;
+  const int64_t grid = std::min<int64_t>((n + 255) / 256, int64_t(sm_count()) * 8);
+  vmag_kernel<double><<<unsigned(grid), 256, 0, static_cast<cudaStream_t>(stream)>>>(u, v, n, out, err);
+  return int(cudaGetLastError());
+}
+
+int divuq_gradient2d_f64(const double* values, int64_t nx, int64_t ny, double dx, double dy,
+                         double* out_gx_gy, int32_t* err, void* stream) {
+  return launch_gradient<double>(values, 1, 0, nx, ny, dx, dy, out_gx_gy, 0, false, err, stream);
+}
+
+int divuq_gradient_ensemble2d_f64(const double* members, int64_t n_members, int64_t nx, int64_t ny,
+                                  double dx, double dy, double* out_members, int32_t* err,
+                                  void* stream) {
+  if (n_members < 1) return DIVUQ_EMEMBERS;
+  return launch_gradient<double>(members, n_members, 2 * nx * ny, nx, ny, dx, dy, out_members,
+                                 2 * nx * ny, true, err, stream);
+}
+
+int divuq_gradient_ensemble2d_f32(const float* members, int64_t n_members, int64_t nx, int64_t ny,
+                                  double dx, double dy, float* out_members, int32_t* err,
+                                  void* stream) {
+  if (n_members < 1) return DIVUQ_EMEMBERS;
+  return launch_gradient<float>(members, n_members, 2 * nx * ny, nx, ny, dx, dy, out_members,
+                                2 * nx * ny, true, err, stream);
+}
+
+// host-buffer variants: kind 0 = velocity magnitude (n = nx*ny), 1 = gradient
+// of a scalar field, 2 = gradient_ensemble of (M, 2, nx*ny) members
+static int host_gradient_common(int kind, const double* a, const double* b, int64_t M, int64_t nx,
+                                int64_t ny, double dx, double dy, double* out, int device) {
+  DIVUQ_CUDA(cudaSetDevice(device));
+  StreamGuard sg;
+  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  const int64_t n = nx * ny;
+  const int64_t in_elems = kind == 0 ? 2 * n : kind == 1 ? n : 2 * M * n;
+  const int64_t out_elems = kind == 0 ? n : kind == 1 ? 2 * n : 2 * M * n;
+  DevBuf d;
+  DIVUQ_CUDA(d.alloc(size_t(in_elems + out_elems) * sizeof(double) + 256, sg.s));
+  double* din = d.as<double>();
+  double* dout = din + in_elems;
+  int32_t* derr = reinterpret_cast<int32_t*>(dout + out_elems);
+  DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
+  if (kind == 0) {
+    DIVUQ_CUDA(cudaMemcpyAsync(din, a, size_t(n) * 8, cudaMemcpyHostToDevice, sg.s));
+    DIVUQ_CUDA(cudaMemcpyAsync(din + n, b, size_t(n) * 8, cudaMemcpyHostToDevice, sg.s));
+    if (int r = divuq_velocity_magnitude_f64(din, din + n, n, dout, derr, sg.s)) return r;
+  } else {
+    DIVUQ_CUDA(cudaMemcpyAsync(din, a, size_t(in_elems) * 8, cudaMemcpyHostToDevice, sg.s));
+    const int r = kind == 1 ? divuq_gradient2d_f64(din, nx, ny, dx, dy, dout, derr, sg.s)
+                            : divuq_gradient_ensemble2d_f64(din, M, nx, ny, dx, dy, dout, derr, sg.s);
+    if (r) return r;
+  }
+  DIVUQ_CUDA(cudaMemcpyAsync(out, dout, size_t(out_elems) * 8, cudaMemcpyDeviceToHost, sg.s));
+  int status = 0;
+  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  return status;
+}
+
+int divuq_host_velocity_magnitude_f64(const double* u, const double* v, int64_t n, double* out,
+                                      int device) {
+  if (n < 0 || (n && (!u || !v || !out))) return DIVUQ_EINVAL;
+  if (n == 0) return DIVUQ_OK;
+  return host_gradient_common(0, u, v, 1, n, 1, 1.0, 1.0, out, device);
+}
+
+int divuq_host_gradient2d_f64(const double* values, int64_t nx, int64_t ny, double dx, double dy,
+                              double* out_gx_gy, int device) {
+  if (int r = grid_ok(nx, ny, dx, dy)) return r;
+  if (!values || !out_gx_gy) return DIVUQ_EINVAL;
+  return host_gradient_common(1, values, nullptr, 1, nx, ny, dx, dy, out_gx_gy, device);
+}
+
+int divuq_host_gradient_ensemble2d_f64(const double* members, int64_t n_members, int64_t nx,
+                                       int64_t ny, double dx, double dy, double* out_members,
+                                       int device) {
+  if (int r = grid_ok(nx, ny, dx, dy)) return r;
+  if (!members || !out_members) return DIVUQ_EINVAL;
+  if (n_members < 1) return DIVUQ_EMEMBERS;
+  return host_gradient_common(2, members, nullptr, n_members, nx, ny, dx, dy, out_members, device);
+}
+
+}  // extern "C"
+
+namespace {
+
 
 }  // namespace
 

@@ -160,6 +160,20 @@ def lcp2d(mu, sigma, nx, ny, isovalue, *, check=True):
     return out
 
 
+def gradient_ensemble2d(members, nx, ny, dx=1.0, dy=1.0, *, out=None, check=True):
+    """(M, 2, nx*ny) members -> (M, 2, nx*ny) gradients of |(u, v)| (gaussian.py:61-66)."""
+    _req(members, "members")
+    if members.dim() != 3 or members.shape[1:] != (2, nx * ny):
+        raise ValueError("members must have shape (M, 2, nx*ny)")
+    out = torch.empty_like(members) if out is None else _req(out, "out", members.dtype, members.numel())
+    err = _ErrWord(members.device, check)
+    fn = getattr(lib, f"divuq_gradient_ensemble2d_{_FP[members.dtype]}")
+    _check(fn(_ptr(members), members.shape[0], nx, ny, float(dx), float(dy), _ptr(out), err.ptr,
+              _stream()))
+    err.raise_if_set()
+    return out
+
+
 def fit_moments(members, *, out=None, check=True):
     """K1: (M, C, N) members -> mu (C, N), sigma (C, N) (gaussian.py:35-45)."""
     _req(members, "members")

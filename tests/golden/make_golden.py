@@ -171,6 +171,20 @@ def main():
         s_v=m.sigma_v, n_samples=np.array(4000), mean=est.mean, std=est.std,
         an_mu=an.mu, an_sigma=an.sigma,
     )
+    # ---- gradient prologue (gaussian.py:48-66) -- appended last so the
+    # earlier fixtures' random draws are unchanged
+    gr = {}
+    g = divuq.UniformGrid2(19, 13, 0.3, 0.7)
+    members = tuple(
+        divuq.VectorField2(g, rng.normal(size=g.n_vertices), rng.normal(size=g.n_vertices))
+        for _ in range(4)
+    )
+    out = divuq.gradient_ensemble(divuq.Ensemble2(g, members))
+    gr["members"] = np.stack([np.stack([m.u, m.v]) for m in members])
+    gr["out"] = np.stack([np.stack([m.u, m.v]) for m in out.members])
+    gr["vmag0"] = divuq.velocity_magnitude(members[0]).values
+    gr["grid"] = np.array([19, 13, 0.3, 0.7])
+    np.savez_compressed(os.path.join(OUT, "gradient.npz"), **gr)
     print("golden fixtures written to", OUT)
 
 
