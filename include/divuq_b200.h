@@ -51,6 +51,10 @@ extern "C" {
 #define DIVUQ_ESAMPLES (-4)        /* fewer than 2 Monte Carlo samples */
 #define DIVUQ_ENONFINITE (-10)     /* an input value is NaN / inf */
 #define DIVUQ_ENEGSIGMA (-11)      /* a sigma input is negative */
+#define DIVUQ_EFORMAT (-20)        /* DIVUQ1: bad magic / malformed header (io.FormatError) */
+#define DIVUQ_ELENGTH (-21)        /* DIVUQ1: payload length mismatch (io.LengthError) */
+#define DIVUQ_EOS (-22)            /* DIVUQ1: file cannot be read / written (OSError) */
+#define DIVUQ_EDATA (-23)          /* DIVUQ1: non-finite payload (io.DataError) */
 
 #define DIVUQ_ERRBIT_NONFINITE 1
 #define DIVUQ_ERRBIT_NEGSIGMA 2
@@ -206,6 +210,20 @@ int divuq_gen_field_f32(const float* bumps, int n_bumps, int dims,
                         double shear_amp, uint64_t seed, double sig_lo, double sig_hi,
                         int sigma_mode, int64_t n_members, float* const* out, float* members,
                         void* stream);
+
+/* ---- DIVUQ1 container (io.py:43-134) ---------------------
+ * Header "DIVUQ1 nx ny dx dy M\n" then M blocks of (u-plane, v-plane) LE fp32:
+ * exactly the (M, 2, N) layout the ensemble kernels read.  ingest_f32 streams
+ * the payload disk -> pinned staging (double-buffered) -> device memory;
+ * write_f32 is byte-identical to the reference writer (Python-repr header
+ * reals, io.py:38-55). */
+int divuq_divuq1_read_header(const char* path, int64_t* nx, int64_t* ny, double* dx, double* dy,
+                             int64_t* n_members);
+int divuq_divuq1_read_f32(const char* path, float* out, int64_t count, int check_finite);
+int divuq_divuq1_ingest_f32(const char* path, float* dev_out, int64_t count, int device);
+int divuq_divuq1_write_f32(const char* path, int64_t nx, int64_t ny, double dx, double dy,
+                           int64_t n_members, const float* data);
+int divuq_divuq1_format_real(double x, char* out, int64_t cap);
 
 /* ---- host-buffer entry points (the reference-facing path) ----------------
  * Same semantics as the device versions; synchronous; `device` = CUDA

@@ -14,6 +14,7 @@ there is no CPU fallback.
 """
 
 from . import _lib  # noqa: F401  (fails loudly without the CUDA library)
+from . import io  # noqa: F401  (DIVUQ1 container, reference divuq.io)
 from .api import (
     EnsembleDivergence,
     cell_crossing_probability,

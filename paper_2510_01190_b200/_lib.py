@@ -59,6 +59,11 @@ SIGNATURES = {
     "divuq_host_velocity_magnitude_f64": (_int, [_p, _p, _i64, _p, _int]),
     "divuq_host_gradient2d_f64": (_int, [_p, _i64, _i64, _f64, _f64, _p, _int]),
     "divuq_host_gradient_ensemble2d_f64": (_int, [_p, _i64, _i64, _i64, _f64, _f64, _p, _int]),
+    "divuq_divuq1_read_header": (_int, [ctypes.c_char_p, _p, _p, _p, _p, _p]),
+    "divuq_divuq1_read_f32": (_int, [ctypes.c_char_p, _p, _i64, _int]),
+    "divuq_divuq1_ingest_f32": (_int, [ctypes.c_char_p, _p, _i64, _int]),
+    "divuq_divuq1_write_f32": (_int, [ctypes.c_char_p, _i64, _i64, _f64, _f64, _i64, _p]),
+    "divuq_divuq1_format_real": (_int, [_f64, ctypes.c_char_p, _i64]),
     "divuq_mc_scratch_bytes": (_i64, [_i64, _i64, _i64, _i64]),
     "divuq_mc_divergence2d_f64": (
         _int, [_p] * 4 + [_i64, _i64, _f64, _f64, _i64, _u64, _i64, _i64] + [_p] * 3 + [_p, _p]),
@@ -87,6 +92,7 @@ if ABI_VERSION != 1:
 
 # status codes (include/divuq_b200.h)
 OK, EINVAL, EGRID, EMEMBERS, ESAMPLES, ENONFINITE, ENEGSIGMA = 0, -1, -2, -3, -4, -10, -11
+EFORMAT, ELENGTH, EOS, EDATA = -20, -21, -22, -23
 
 
 class DivuqError(RuntimeError):

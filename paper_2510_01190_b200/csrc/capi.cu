@@ -13,6 +13,7 @@
 #include "gen.cuh"
 #include "k2tma.cuh"
 #include "k3tma.cuh"
+#include "divuq1.cuh"
 #include "gradient.cuh"
 #include "lcp.cuh"
 #include "mc.cuh"
@@ -604,6 +605,10 @@ const char* divuq_status_string(int status) {
     case DIVUQ_ESAMPLES: return "mc_divergence needs n_samples >= 2";
     case DIVUQ_ENONFINITE: return "non-finite values are not allowed";
     case DIVUQ_ENEGSIGMA: return "sigma must be non-negative";
+    case DIVUQ_EFORMAT: return "not a DIVUQ1 file or malformed header";
+    case DIVUQ_ELENGTH: return "payload length differs from what the header promises";
+    case DIVUQ_EOS: return "cannot read or write the file";
+    case DIVUQ_EDATA: return "payload contains non-finite values";
     default: return status > 0 ? cudaGetErrorString(cudaError_t(status)) : "unknown status";
   }
 }
@@ -1090,6 +1095,105 @@ int divuq_host_propagate3d_f32(const float* mu_u, const float* mu_v, const float
   int status = 0;
   DIVUQ_CUDA(check_err_word(derr, sg[0].s, &status));
   return status;
+}
+
+// ---------------------------------------------------------------------
+// DIVUQ1 container (io.py:43-134)
+// ---------------------------------------------------------------------
+
+int divuq_divuq1_read_header(const char* path, int64_t* nx, int64_t* ny, double* dx, double* dy,
+                             int64_t* n_members) {
+  if (!path || !nx || !ny || !dx || !dy || !n_members) return DIVUQ_EINVAL;
+  io::Header h;
+  if (int r = io::read_header(path, &h)) return r;
+  *nx = h.nx; *ny = h.ny; *dx = h.dx; *dy = h.dy; *n_members = h.members;
+  return DIVUQ_OK;
+}
+
+// payload -> host buffer (pinned or pageable); check_finite mirrors the
+// reference's DataError (io.py:89-90)
+int divuq_divuq1_read_f32(const char* path, float* out, int64_t count, int check_finite) {
+  if (!path || !out || count < 0) return DIVUQ_EINVAL;
+  io::Header h;
+  if (int r = io::read_header(path, &h)) return r;
+  if (count != h.members * 2 * h.nx * h.ny) return DIVUQ_EINVAL;
+  FILE* f = std::fopen(path, "rb");
+  if (!f) return io::kOsError;
+  const bool ok = std::fseek(f, long(h.offset), SEEK_SET) == 0 &&
+                  std::fread(out, sizeof(float), size_t(count), f) == size_t(count);
+  std::fclose(f);
+  if (!ok) return io::kOsError;
+  if (check_finite)
+    for (int64_t i = 0; i < count; ++i)
+      if (!std::isfinite(out[i])) return io::kDataError;
+  return DIVUQ_OK;
+}
+
+// payload -> HBM (M, 2, N) fp32: disk reads into two pinned staging buffers
+// alternate with async host->device copies, so the read of chunk i+1
+// overlaps the copy of chunk i.
+int divuq_divuq1_ingest_f32(const char* path, float* dev_out, int64_t count, int device) {
+  if (!path || !dev_out || count < 0) return DIVUQ_EINVAL;
+  io::Header h;
+  if (int r = io::read_header(path, &h)) return r;
+  if (count != h.members * 2 * h.nx * h.ny) return DIVUQ_EINVAL;
+  DIVUQ_CUDA(cudaSetDevice(device));
+  const int64_t chunk = int64_t(16) << 20;  // floats per chunk (64 MiB)
+  float* stage[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  StreamGuard sg;
+  int status = DIVUQ_OK;
+  FILE* f = nullptr;
+  do {
+    if ((status = int(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking)))) break;
+    if ((status = int(cudaMallocHost(&stage[0], size_t(chunk) * 4)))) break;
+    if ((status = int(cudaMallocHost(&stage[1], size_t(chunk) * 4)))) break;
+    if ((status = int(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming)))) break;
+    if ((status = int(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming)))) break;
+    f = std::fopen(path, "rb");
+    if (!f || std::fseek(f, long(h.offset), SEEK_SET) != 0) { status = io::kOsError; break; }
+    int b = 0;
+    for (int64_t off = 0; off < count; off += chunk, b ^= 1) {
+      const int64_t nfl = std::min(chunk, count - off);
+      if ((status = int(cudaEventSynchronize(done[b])))) break;  // staging buffer b free again
+      if (std::fread(stage[b], sizeof(float), size_t(nfl), f) != size_t(nfl)) { status = io::kOsError; break; }
+      if ((status = int(cudaMemcpyAsync(dev_out + off, stage[b], size_t(nfl) * 4,
+                                        cudaMemcpyHostToDevice, sg.s)))) break;
+      if ((status = int(cudaEventRecord(done[b], sg.s)))) break;
+    }
+    if (!status) status = int(cudaStreamSynchronize(sg.s));
+  } while (false);
+  if (f) std::fclose(f);
+  if (sg.s) cudaStreamSynchronize(sg.s);
+  for (int i = 0; i < 2; ++i) {
+    if (done[i]) cudaEventDestroy(done[i]);
+    if (stage[i]) cudaFreeHost(stage[i]);
+  }
+  return status;
+}
+
+// byte-identical to the reference's write_members (io.py:43-55)
+int divuq_divuq1_write_f32(const char* path, int64_t nx, int64_t ny, double dx, double dy,
+                           int64_t n_members, const float* data) {
+  if (!path || (!data && n_members > 0) || n_members < 0) return DIVUQ_EINVAL;
+  const std::string header = "DIVUQ1 " + std::to_string(nx) + " " + std::to_string(ny) + " " +
+                             io::py_repr(dx) + " " + io::py_repr(dy) + " " +
+                             std::to_string(n_members) + "\n";
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return io::kOsError;
+  const size_t count = size_t(n_members * 2 * nx * ny);
+  const bool ok = std::fwrite(header.data(), 1, header.size(), f) == header.size() &&
+                  std::fwrite(data, sizeof(float), count, f) == count;
+  return (std::fclose(f) == 0 && ok) ? DIVUQ_OK : io::kOsError;
+}
+
+// Python repr of a header real (exposed for the format tests)
+int divuq_divuq1_format_real(double x, char* out, int64_t cap) {
+  if (!out || cap < 2) return DIVUQ_EINVAL;
+  const std::string s = io::py_repr(x);
+  if (int64_t(s.size()) + 1 > cap) return DIVUQ_EINVAL;
+  std::memcpy(out, s.c_str(), s.size() + 1);
+  return DIVUQ_OK;
 }
 
 }  // extern "C"

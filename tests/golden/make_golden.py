@@ -185,6 +185,21 @@ def main():
     gr["vmag0"] = divuq.velocity_magnitude(members[0]).values
     gr["grid"] = np.array([19, 13, 0.3, 0.7])
     np.savez_compressed(os.path.join(OUT, "gradient.npz"), **gr)
+
+    # ---- DIVUQ1 container (io.py:43-55): files written by the reference's
+    # own writer, for byte-identity of ours and parsing of theirs
+    from divuq import io as ref_io
+
+    for name, (nx, ny, dx, dy, m) in {
+        "ens_a": (6, 5, 0.5, 2.0, 4), "ens_b": (7, 3, 0.1, 1e-3, 3),
+        "ens_c": (3, 4, 123456.789, 3.0e-7, 2), "ens_d": (2, 2, 1e16, 0.3333333333333333, 5),
+    }.items():
+        g = divuq.UniformGrid2(nx, ny, dx, dy)
+        members = tuple(
+            divuq.VectorField2(g, rng.normal(size=g.n_vertices), rng.normal(size=g.n_vertices))
+            for _ in range(m)
+        )
+        ref_io.write_members(g, members, os.path.join(OUT, f"divuq1_{name}.duq"))
     print("golden fixtures written to", OUT)
 
 
