@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Benchmark of the divergence-uncertainty hot path on B200 (driver contract).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config {1,3,4}] [--impl {ours,reference}]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config {0..4}] [--impl {ours,reference}]
+    python bench.py --workload {lcp,gradient,ingest}     # SURVEY 8f rows, 1 GPU
 
 Default workload = BASELINE.json config 3 (the metric's "1/2/4/8 B200" config):
 3D analytic divergence mean + sigma + P(div>0) + P(div<0) on a 512^3 fp32
@@ -162,6 +163,206 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+# SURVEY 8f "next" rows: LCP, gradient prologue, DIVUQ1 ingest (1 GPU lines)
+# ---------------------------------------------------------------------------
+
+def run_next(args):
+    """One JSON line for a widened row (not a BASELINE config; same keys)."""
+    import torch
+
+    import __graft_entry__
+
+    __graft_entry__.build()
+    from paper_2510_01190_b200 import configs, device as dev, io as dio
+    from paper_2510_01190_b200._lib import lib
+
+    torch.cuda.set_device(0)
+    stream = torch.cuda.current_stream()
+    peak, peak_src = measured_peak()
+    ev_pairs = []
+
+    def ev():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        return e
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    wl = args.workload
+    if wl == "lcp":
+        nx = ny = 4096
+        model = configs.host_model2d(nx, ny, 24, 105)
+        dm = [torch.from_numpy(a).cuda() for a in model]
+        o = dev.propagate2d(*dm, nx, ny, 1.0, 1.0, 0.0, outputs=("mu", "sigma"))
+        mu, sg = o["mu"], o["sigma"]
+        units = (nx - 1) * (ny - 1)
+        bpu = 8 * 2 * nx * ny / units + 8  # mu, sigma read once per vertex + one fp64 out per cell
+        unit = "cells/s"
+        metric = "level-crossing probability cells/sec (lcp.py:80-100), fp64"
+        workload = "lcp: per-cell P(div field crosses 0) on a 4096^2 fp64 divergence (mu, sigma) field"
+
+        def step():
+            dev.lcp2d(mu, sg, nx, ny, 0.0, check=False)
+
+        hm, hs = mu.cpu().pin_memory(), sg.cpu().pin_memory()
+        hout = torch.empty(units, dtype=torch.float64).pin_memory()
+
+        def e2e_call():
+            st = lib.divuq_host_lcp2d_f64(hm.data_ptr(), hs.data_ptr(), nx, ny, 0.0,
+                                          hout.data_ptr(), 0)
+            assert st == 0, st
+
+        h2d, d2h = 16 * nx * ny, 8 * units
+        mu_h, sg_h = hm.numpy()[: 1024 * 1024], hs.numpy()[: 1024 * 1024]
+        from oracle import ref2d
+
+        cpu_thunk = (lambda: ref2d.lcp(mu_h, sg_h, 1024, 1024, 0.0), 1023 * 1023, 1)
+        cpu_sample = "numpy restatement of lcp() on a 1024x1024 corner of the field, 1 thread"
+        dtype = "f64"
+    elif wl == "gradient":
+        nx = ny = 1024
+        m = 20
+        mem = configs.config1_members(nx, ny, m, 101).double()
+        out = torch.empty_like(mem)
+        units = m * nx * ny
+        bpu = 32  # u, v in + gx, gy out, fp64, per member-vertex
+        unit = "member-vertices/s"
+        metric = "velocity-magnitude-gradient member-vertices/sec (gaussian.py:48-66), fp64"
+        workload = "gradient: gradient_ensemble of the config-1 ensemble (M=20, 1024^2), fp64"
+
+        def step():
+            dev.gradient_ensemble2d(mem, nx, ny, 1.0, 1.0, out=out, check=False)
+
+        hin = mem.cpu().pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+
+        def e2e_call():
+            st = lib.divuq_host_gradient_ensemble2d_f64(hin.data_ptr(), m, nx, ny, 1.0, 1.0,
+                                                        hout.data_ptr(), 0)
+            assert st == 0, st
+
+        h2d = d2h = 16 * units
+        sub = hin.numpy()[:4, :, : 256 * 1024]
+        from oracle import ref2d
+
+        cpu_thunk = (lambda: ref2d.gradient_ensemble(sub, 1024, 256, 1.0, 1.0), 4 * 256 * 1024, 1)
+        cpu_sample = "numpy restatement (hypot + reference stencil), 4 members x 1024x256, 1 thread"
+        dtype = "f64"
+    else:  # ingest: DIVUQ1 file -> HBM -> fused fit/propagate/tails (the CLI's pipeline)
+        import tempfile
+
+        nx = ny = 1024
+        m = 20
+        mem = configs.config1_members(nx, ny, m, 101)
+        host = mem.cpu().numpy()
+        tmpdir = tempfile.mkdtemp(prefix="divuq_bench_")
+        path = os.path.join(tmpdir, "config1.duq")
+        st = lib.divuq_divuq1_write_f32(os.fsencode(path), nx, ny, 1.0, 1.0, m, host.ctypes.data)
+        assert st == 0, st
+        units = nx * ny
+        file_bytes = host.nbytes
+        unit = "grid points/s"
+        metric = "DIVUQ1 file -> P(div>0) maps grid points/sec (io.py:58-93 + config 1 pipeline)"
+        workload = ("ingest: DIVUQ1 file (config-1 ensemble M=20 1024^2, 168 MB, page-cache "
+                    "resident) -> pinned staging -> HBM -> fused fit/propagate/tails, fp32")
+        outs = {k: torch.empty(units, dtype=torch.float32, device="cuda") for k in ("mu", "sigma", "p_src")}
+
+        def step():
+            _, x = dio.load_ensemble_device(path)
+            dev.ensemble_divergence2d(x, nx, ny, 1.0, 1.0, 0.0, outputs=("mu", "sigma", "p_src"),
+                                      out=outs, check=False)
+
+        e2e_call = None
+        h2d, d2h = file_bytes, 0
+        from oracle import divuq1, ref2d
+
+        def cpu_work():
+            (_, _, _, _), planes = divuq1.read_members(path)
+            mu_f, sg_f = ref2d.fit_moments(planes)
+            mu_d, sg_d = ref2d.propagate2d(mu_f[0], mu_f[1], sg_f[0], sg_f[1], nx, ny, 1.0, 1.0)
+            ref2d.source_probability(mu_d, sg_d, 0.0)
+
+        cpu_thunk = (cpu_work, units, 1)
+        cpu_sample = "oracle reader + fit_gaussian + propagate + P(div>0) on the same file, fp64, 1 thread"
+        dtype = "f32"
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches_per_step = 1 if wl != "ingest" else 1
+    with ClockSampler(0) as clocks:
+        if wl == "ingest":  # host work inside the step: wall clock around synchronized steps
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                step()
+            torch.cuda.synchronize()
+            ms = (time.perf_counter() - t0) * 1e3 / args.steps
+            ev_ms = None
+        else:
+            for _ in range(args.steps):
+                flush.zero_()  # L2 flush; outside the kernel events
+                a = ev()
+                step()
+                ev_pairs.append((a, ev()))
+            torch.cuda.synchronize()
+            ev_ms = [a.elapsed_time(b) for a, b in ev_pairs]
+            ms = sum(ev_ms) / len(ev_ms)
+    value = units / (ms * 1e-3)
+    if wl == "ingest":
+        # the bound is the host->device link: measure pinned H2D of the same bytes
+        src = torch.from_numpy(host).pin_memory()
+        dst = torch.empty_like(mem)
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        a = ev()
+        for _ in range(5):
+            dst.copy_(src, non_blocking=True)
+        b = ev()
+        torch.cuda.synchronize()
+        h2d_gbs = file_bytes * 5 / (a.elapsed_time(b) * 1e-3) / 1e9
+        achieved = file_bytes / (ms * 1e-3) / 1e9
+        roofline = {"bound": "pcie (host->device)", "achieved": achieved, "peak": h2d_gbs,
+                    "unit": "GB/s", "frac": achieved / h2d_gbs, "traffic": None,
+                    "peak_source": "pinned cudaMemcpy H2D of the same 168 MB, measured in this run",
+                    "bytes_per_step": file_bytes}
+        e2e = {"value": value, "unit": unit, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": ms, "path": "io.load_ensemble_device (divuq_divuq1_ingest_f32) + K3 2D"}
+    else:
+        achieved = bpu * units / (ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": committed_traffic(wl),
+                    "bytes_per_unit": bpu, "units_per_launch": units, "avg_launch_ms": ms,
+                    "peak_source": peak_src}
+        e2e_call()
+        reps = 3
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            e2e_call()
+        e2e_s = (time.perf_counter() - t0) / reps
+        e2e = {"value": units / e2e_s, "unit": unit, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3}
+    cpu = None
+    if not args.no_cpu:
+        from oracle import cpu_baseline as cb
+
+        v, thr, runs = cb.rate(cpu_thunk, seconds=8.0)
+        cpu = {"value": v, "unit": unit, "cores": thr, "kind": "port",
+               "sample": cpu_sample + f", {runs} runs"}
+    if wl == "ingest":
+        os.remove(path)
+        os.rmdir(tmpdir)
+    line = {
+        "metric": metric, "value": value, "unit": unit, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": dtype, "data": "synthetic (seeded generator)",
+        "config": {"workload": workload, "parallelism": "replicas x1",
+                   "l2": "flushed between steps (256 MB write)" if wl != "ingest" else "n/a (host-bound)"},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches_per_step * args.steps, "clocks": clocks.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
 
@@ -175,8 +376,15 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--planes-per-gpu", type=int, default=128, help="config 4 slab depth")
+    ap.add_argument("--workload", default=None, choices=("lcp", "gradient", "ingest"),
+                    help="a SURVEY 8f row instead of a BASELINE config (1 GPU, ours only)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.workload is not None:
+        if args.impl == "reference" or int(os.environ.get("RANK", "0")) != 0:
+            return
+        run_next(args)
+        return
 
     if args.impl == "reference":
         run_reference(args)

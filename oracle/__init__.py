@@ -20,6 +20,8 @@ Contents
            kernel (the north star mandates it instead of the reference's
            splitmix64 + AS241), pinned by the Random123 known-answer vectors,
            and the MC estimator restated with the GPU's exact chunk/merge order.
+``divuq1`` the DIVUQ1 container reader / header formatter (io.py:38-93),
+           pinned against files the reference's own writer produced.
 """
 
-from . import ref2d, ref3d, philox  # noqa: F401
+from . import ref2d, ref3d, philox, divuq1  # noqa: F401

@@ -172,3 +172,26 @@ def lcp(mu, sigma, nx, ny, isovalue):
     mu = np.asarray(mu, float)
     sigma = np.asarray(sigma, float)
     return cell_crossing_probability(mu[corners], sigma[corners], isovalue)
+
+
+def velocity_magnitude(u, v):
+    """hypot(u, v) per vertex (gaussian.py:48-50)."""
+    return np.hypot(np.asarray(u, float), np.asarray(v, float))
+
+
+def gradient2d(values, nx, ny, dx, dy):
+    """(gx, gy) = (f[hx]*cx - f[lx]*cx, f[hy]*cy - f[ly]*cy) (gaussian.py:53-58,
+    stencils.py:87-96), the divergence's per-axis rule (axis_rule)."""
+    f2 = np.asarray(values, float).reshape(ny, nx)
+    xh, xl = _x_terms(f2, dx)
+    yh, yl = _y_terms(f2, dy)
+    return (xh - xl).ravel(), (yh - yl).ravel()
+
+
+def gradient_ensemble(members, nx, ny, dx, dy):
+    """(M, 2, N) members -> (M, 2, N) gradients of |(u, v)| (gaussian.py:61-66)."""
+    members = np.asarray(members, float)
+    out = np.empty_like(members)
+    for k, m in enumerate(members):
+        out[k, 0], out[k, 1] = gradient2d(velocity_magnitude(m[0], m[1]), nx, ny, dx, dy)
+    return out

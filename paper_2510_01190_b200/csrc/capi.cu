@@ -435,8 +435,10 @@ __global__ void tail_probs_kernel(const T* __restrict__ mu, const T* __restrict_
        i += int64_t(gridDim.x) * blockDim.x) {
     const T m = mu[i], s = sigma[i];
     errbits |= check_value(m) | check_sigma(s);
-    if (below) below[i] = prob_below(m, s, theta);
-    if (above) above[i] = prob_above(m, s, theta);
+    T b, a;
+    tail_pair(m, s, theta, b, a);
+    if (below) below[i] = b;
+    if (above) above[i] = a;
   }
   flush_error(err, errbits);
 }
@@ -482,15 +484,16 @@ int launch_gradient(const T* in, int64_t members, int64_t in_mstride, int64_t nx
                     void* stream) {
   if (int r = grid_ok(nx, ny, dx, dy)) return r;
   if (!in || !out || members < 1) return DIVUQ_EINVAL;
-  const int64_t total = members * nx * ny;
-  const int64_t grid = std::min<int64_t>((total + 255) / 256, int64_t(sm_count()) * 16);
+  const dim3 grid(unsigned((nx + kGrTX - 1) / kGrTX), unsigned((ny + kGrTY - 1) / kGrTY),
+                  unsigned(std::min<int64_t>(members, 65535)));
+  if ((nx + kGrTX - 1) / kGrTX > INT32_MAX || (ny + kGrTY - 1) / kGrTY > 65535) return DIVUQ_EGRID;
   const T cxi = T(1.0 / (2.0 * dx)), cxb = T(1.0 / dx), cyi = T(1.0 / (2.0 * dy)), cyb = T(1.0 / dy);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (mag)
-    gradient2d_kernel<T, true><<<unsigned(grid), 256, 0, s>>>(in, members, in_mstride, nx, ny, cxi, cxb,
+    gradient2d_kernel<T, true><<<grid, dim3(kGrBX, kGrBY), 0, s>>>(in, members, in_mstride, nx, ny, cxi, cxb,
                                                               cyi, cyb, out, out_mstride, err);
   else
-    gradient2d_kernel<T, false><<<unsigned(grid), 256, 0, s>>>(in, members, in_mstride, nx, ny, cxi, cxb,
+    gradient2d_kernel<T, false><<<grid, dim3(kGrBX, kGrBY), 0, s>>>(in, members, in_mstride, nx, ny, cxi, cxb,
                                                                cyi, cyb, out, out_mstride, err);
   return int(cudaGetLastError());
 }
@@ -729,7 +732,7 @@ int divuq_lcp2d_f64(const double* mu, const double* sigma, int64_t nx, int64_t n
   if (nx < 2 || ny < 2) return DIVUQ_EGRID;
   if (!mu || !sigma || !out) return DIVUQ_EINVAL;
   dim3 grid(unsigned((nx - 1 + kLcpTX - 1) / kLcpTX), unsigned((ny - 1 + kLcpTY - 1) / kLcpTY));
-  lcp2d_kernel<double><<<grid, dim3(kLcpTX, kLcpTY), 0, static_cast<cudaStream_t>(stream)>>>(
+  lcp2d_kernel<double><<<grid, dim3(kLcpBX, kLcpBY), 0, static_cast<cudaStream_t>(stream)>>>(
       mu, sigma, nx, ny, isovalue, out, err);
   return int(cudaGetLastError());
 }
@@ -739,7 +742,7 @@ int divuq_lcp2d_f32(const float* mu, const float* sigma, int64_t nx, int64_t ny,
   if (nx < 2 || ny < 2) return DIVUQ_EGRID;
   if (!mu || !sigma || !out) return DIVUQ_EINVAL;
   dim3 grid(unsigned((nx - 1 + kLcpTX - 1) / kLcpTX), unsigned((ny - 1 + kLcpTY - 1) / kLcpTY));
-  lcp2d_kernel<float><<<grid, dim3(kLcpTX, kLcpTY), 0, static_cast<cudaStream_t>(stream)>>>(
+  lcp2d_kernel<float><<<grid, dim3(kLcpBX, kLcpBY), 0, static_cast<cudaStream_t>(stream)>>>(
       mu, sigma, nx, ny, float(isovalue), out, err);
   return int(cudaGetLastError());
 }
@@ -1129,46 +1132,49 @@ int divuq_divuq1_read_f32(const char* path, float* out, int64_t count, int check
   return DIVUQ_OK;
 }
 
-// payload -> HBM (M, 2, N) fp32: disk reads into two pinned staging buffers
-// alternate with async host->device copies, so the read of chunk i+1
-// overlaps the copy of chunk i.
+// payload -> HBM (M, 2, N) fp32.  The file is read with parallel pread()s
+// into a persistent ring of pinned staging buffers (allocated once per
+// process: pinning 100+ MB costs more than the copy), and each filled buffer
+// is sent to the device with an async H2D copy, so the reads of chunk i+1
+// overlap the PCIe transfer of chunk i.  Bound: min(page-cache/disk read
+// bandwidth, host->device link).
 int divuq_divuq1_ingest_f32(const char* path, float* dev_out, int64_t count, int device) {
   if (!path || !dev_out || count < 0) return DIVUQ_EINVAL;
   io::Header h;
   if (int r = io::read_header(path, &h)) return r;
   if (count != h.members * 2 * h.nx * h.ny) return DIVUQ_EINVAL;
+  if (count == 0) return DIVUQ_OK;
   DIVUQ_CUDA(cudaSetDevice(device));
-  const int64_t chunk = int64_t(16) << 20;  // floats per chunk (64 MiB)
-  float* stage[2] = {nullptr, nullptr};
-  cudaEvent_t done[2] = {nullptr, nullptr};
+  io::Staging& st = io::staging();
+  std::lock_guard<std::mutex> lock(st.mu);
+  if (int r = st.ensure()) return r;
+  const int fd = ::open(path, O_RDONLY | O_CLOEXEC);
+  if (fd < 0) return io::kOsError;
+  ::posix_fadvise(fd, 0, 0, POSIX_FADV_SEQUENTIAL);
   StreamGuard sg;
+  cudaEvent_t done[io::Staging::kBuffers] = {};
   int status = DIVUQ_OK;
-  FILE* f = nullptr;
   do {
     if ((status = int(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking)))) break;
-    if ((status = int(cudaMallocHost(&stage[0], size_t(chunk) * 4)))) break;
-    if ((status = int(cudaMallocHost(&stage[1], size_t(chunk) * 4)))) break;
-    if ((status = int(cudaEventCreateWithFlags(&done[0], cudaEventDisableTiming)))) break;
-    if ((status = int(cudaEventCreateWithFlags(&done[1], cudaEventDisableTiming)))) break;
-    f = std::fopen(path, "rb");
-    if (!f || std::fseek(f, long(h.offset), SEEK_SET) != 0) { status = io::kOsError; break; }
+    for (auto& e : done)
+      if ((status = int(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)))) break;
+    if (status) break;
+    const int64_t total = count * int64_t(sizeof(float));
     int b = 0;
-    for (int64_t off = 0; off < count; off += chunk, b ^= 1) {
-      const int64_t nfl = std::min(chunk, count - off);
-      if ((status = int(cudaEventSynchronize(done[b])))) break;  // staging buffer b free again
-      if (std::fread(stage[b], sizeof(float), size_t(nfl), f) != size_t(nfl)) { status = io::kOsError; break; }
-      if ((status = int(cudaMemcpyAsync(dev_out + off, stage[b], size_t(nfl) * 4,
+    for (int64_t off = 0; off < total; off += io::Staging::kChunk, b = (b + 1) % io::Staging::kBuffers) {
+      const int64_t len = std::min<int64_t>(io::Staging::kChunk, total - off);
+      if ((status = int(cudaEventSynchronize(done[b])))) break;  // buffer b's last copy finished
+      if (!io::pread_parallel(fd, st.buf[b], len, h.offset + off)) { status = io::kOsError; break; }
+      if ((status = int(cudaMemcpyAsync(reinterpret_cast<char*>(dev_out) + off, st.buf[b], size_t(len),
                                         cudaMemcpyHostToDevice, sg.s)))) break;
       if ((status = int(cudaEventRecord(done[b], sg.s)))) break;
     }
     if (!status) status = int(cudaStreamSynchronize(sg.s));
   } while (false);
-  if (f) std::fclose(f);
+  ::close(fd);
   if (sg.s) cudaStreamSynchronize(sg.s);
-  for (int i = 0; i < 2; ++i) {
-    if (done[i]) cudaEventDestroy(done[i]);
-    if (stage[i]) cudaFreeHost(stage[i]);
-  }
+  for (auto& e : done)
+    if (e) cudaEventDestroy(e);
   return status;
 }
 

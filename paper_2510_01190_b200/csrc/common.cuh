@@ -224,6 +224,19 @@ __device__ __forceinline__ void ndtr_pair(T q, T& below, T& above) {
   above = x > T(0) ? y : c;
 }
 
+// (below, above) of one point from ONE erfc: bitwise equal to
+// (prob_below, prob_above) -- ndtr(-t) negates ndtr(t)'s scaled argument
+// exactly, so both evaluate the same erfc(|x|) (lcp.py:48-68).
+template <typename T>
+__device__ __forceinline__ void tail_pair(T mu, T sigma, T theta, T& below, T& above) {
+  if (sigma == T(0)) {
+    below = mu <= theta ? T(1) : T(0);
+    above = T(1) - below;
+    return;
+  }
+  ndtr_pair(Arith<T>::div(Arith<T>::sub(theta, mu), sigma), below, above);
+}
+
 __device__ __forceinline__ void Tails<double>::eval(double m, double var, double t, bool t_zero,
                                                     double& sg, double& ps, double& pk) {
   using A = Arith<double>;

@@ -12,6 +12,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <fcntl.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cctype>
@@ -20,7 +22,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace divuq {
@@ -153,6 +157,60 @@ inline int read_header(const char* path, Header* h) {
       __builtin_mul_overflow(expected, 8LL, &expected) || total - h->offset != expected)
     return kLengthError;
   return 0;
+}
+
+// Process-wide ring of pinned staging buffers for the HBM ingest (portable
+// across devices).  Pinning is paid once, not per file.
+struct Staging {
+  static constexpr int kBuffers = 3;
+  static constexpr int64_t kChunk = int64_t(32) << 20;  // bytes per buffer
+  std::mutex mu;
+  char* buf[kBuffers] = {};
+  int ensure() {
+    for (auto& p : buf)
+      if (!p) {
+        const cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&p), size_t(kChunk),
+                                            cudaHostAllocPortable);
+        if (e != cudaSuccess) { p = nullptr; return int(e); }
+      }
+    return 0;
+  }
+};
+inline Staging& staging() {
+  static Staging* s = new Staging();  // never destroyed: no CUDA calls at static teardown
+  return *s;
+}
+
+// read len bytes at file offset off into dst with up to 16 concurrent
+// pread()s, one per host core (page-cache copies are per-thread memcpy-bound)
+inline bool pread_span(int fd, char* dst, int64_t len, int64_t off) {
+  while (len > 0) {
+    const ssize_t r = ::pread(fd, dst, size_t(len), off_t(off));
+    if (r <= 0) {
+      if (r < 0 && errno == EINTR) continue;
+      return false;
+    }
+    dst += r; off += r; len -= r;
+  }
+  return true;
+}
+
+inline bool pread_parallel(int fd, char* dst, int64_t len, int64_t off) {
+  constexpr int kMaxThreads = 16;
+  const int64_t kSlice = int64_t(1) << 20;
+  const int64_t hw = std::max(1u, std::thread::hardware_concurrency());
+  const int nt = int(std::min<int64_t>(std::min<int64_t>(kMaxThreads, hw), (len + kSlice - 1) / kSlice));
+  if (nt <= 1) return pread_span(fd, dst, len, off);
+  const int64_t per = (len + nt - 1) / nt;
+  bool ok[kMaxThreads];
+  std::thread th[kMaxThreads];
+  for (int t = 0; t < nt; ++t) {
+    const int64_t a = t * per, n = std::min(per, len - a);
+    th[t] = std::thread([=, &ok] { ok[t] = n <= 0 || pread_span(fd, dst + a, n, off + a); });
+  }
+  bool all = true;
+  for (int t = 0; t < nt; ++t) { th[t].join(); all = all && ok[t]; }
+  return all;
 }
 
 }  // namespace io

@@ -98,3 +98,26 @@ def test_vortex_magnitude_gradient_pipeline_to_divergence(d):
     grad = d.gradient(d.velocity_magnitude(m))
     centre = g.vertex_index(20, 20)
     assert d.divergence_deterministic(grad).values[centre] > 0
+
+
+@pytest.mark.parametrize("shape", [(2, 2, 1.0, 1.0), (3, 70, 0.5, 0.25), (33, 9, 0.1, 0.3),
+                                   (65, 17, 1.0, 2.0), (130, 41, 0.01, 0.07)])
+def test_gradient_ensemble_tiles_vs_oracle(d, shape):
+    # tile edges (32 x 8) at every offset, 2-wide axes, partial tiles
+    import torch
+
+    from oracle import ref2d
+    from paper_2510_01190_b200 import device
+
+    nx, ny, dx, dy = shape
+    rng = np.random.default_rng(nx * 1000 + ny)
+    mem = rng.normal(size=(3, 2, nx * ny))
+    want = ref2d.gradient_ensemble(mem, nx, ny, dx, dy)
+    got = device.gradient_ensemble2d(torch.from_numpy(mem).cuda(), nx, ny, dx, dy).cpu().numpy()
+    # GPU hypot within 1 ulp of glibc's: |d(gx)| <= (ulp(a) + ulp(b)) * c <= 4.4e-16 * max|f| / h
+    fmax = np.hypot(mem[:, 0], mem[:, 1]).max()
+    assert np.abs(got - want).max() <= 5e-16 * fmax / min(dx, dy)
+    got32 = device.gradient_ensemble2d(torch.from_numpy(mem.astype(np.float32)).cuda(), nx, ny,
+                                       dx, dy).cpu().numpy()
+    want32 = ref2d.gradient_ensemble(mem.astype(np.float32), nx, ny, dx, dy)
+    assert np.abs(got32 - want32).max() <= 1e-5 * np.abs(want32).max()

@@ -162,3 +162,28 @@ def test_philox_mc_oracle_statistics_and_zero_sigma(rng):
     m0, s0 = philox.mc_divergence(g["mu_u"], g["mu_v"], z, z, nx, ny, dx, dy, 300, 9)
     assert np.array_equal(m0, ref2d.divergence2d(g["mu_u"], g["mu_v"], nx, ny, dx, dy))
     assert np.all(s0 == 0.0)
+
+
+def test_gradient_oracle_pinned_to_reference():
+    from oracle import ref2d
+
+    gd = golden("gradient.npz")
+    nx, ny, dx, dy = gd["grid"]
+    out = ref2d.gradient_ensemble(gd["members"], int(nx), int(ny), float(dx), float(dy))
+    assert np.array_equal(out, gd["out"])
+    m0 = gd["members"][0]
+    assert np.array_equal(ref2d.velocity_magnitude(m0[0], m0[1]), gd["vmag0"])
+
+
+@pytest.mark.parametrize("name", ["ens_a", "ens_b", "ens_c", "ens_d"])
+def test_divuq1_oracle_pinned_to_reference_files(name):
+    import os
+
+    from conftest import GOLDEN
+    from oracle import divuq1
+
+    path = os.path.join(GOLDEN, f"divuq1_{name}.duq")
+    (nx, ny, dx, dy), planes = divuq1.read_members(path)
+    raw = open(path, "rb").read()
+    hdr = divuq1.header(nx, ny, dx, dy, planes.shape[0])
+    assert raw == hdr + planes.astype("<f4").tobytes()
