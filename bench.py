@@ -113,6 +113,24 @@ class ClockSampler:
                 "reasons": names, "n_samples": len(self.samples)}
 
 
+class L2Flush:
+    """Between timed launches: write a 256 MB buffer (> the 126 MB L2), then
+    read a second one, so the inputs are evicted AND the flush's own dirty
+    lines are written back before the timed kernel starts (otherwise their
+    write-back would steal HBM bandwidth inside the timed region)."""
+
+    NOTE = "flushed between steps (256 MB write, then 256 MB read to drain dirty lines)"
+
+    def __init__(self, torch):
+        self.w = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        self.r = torch.ones(256 << 20, dtype=torch.uint8, device="cuda")
+        self.i64 = torch.int64
+
+    def __call__(self):
+        self.w.zero_()
+        return self.r.sum(dtype=self.i64)
+
+
 # ---------------------------------------------------------------------------
 # reference arm
 # ---------------------------------------------------------------------------
@@ -186,7 +204,7 @@ def run_next(args):
         e.record(stream)
         return e
 
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush(torch)
     wl = args.workload
     if wl == "lcp":
         nx = ny = 4096
@@ -299,7 +317,7 @@ def run_next(args):
             ev_ms = None
         else:
             for _ in range(args.steps):
-                flush.zero_()  # L2 flush; outside the kernel events
+                flush()  # L2 flush; outside the kernel events
                 a = ev()
                 step()
                 ev_pairs.append((a, ev()))
@@ -355,7 +373,7 @@ def run_next(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": dtype, "data": "synthetic (seeded generator)",
         "config": {"workload": workload, "parallelism": "replicas x1",
-                   "l2": "flushed between steps (256 MB write)" if wl != "ingest" else "n/a (host-bound)"},
+                   "l2": L2Flush.NOTE if wl != "ingest" else "n/a (host-bound)"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps, "clocks": clocks.summary(),
     }
@@ -490,11 +508,11 @@ def main():
         out = {k: torch.empty(n_local, dtype=torch.float64, device="cuda") for k in dev.ALL_OUTPUTS}
         total_pts = nx * ny * world
         scaling = "weak"
-        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        flush = L2Flush(torch)
 
         def one_step(timed):
             if timed:
-                flush.zero_()  # L2 flush between steps; outside the kernel events
+                flush()  # L2 flush between steps; outside the kernel events
             e0 = ev() if timed else None
             dev.propagate2d(*model, nx, ny, 1.0, 1.0, cfg.t, out=out, check=False)
             if timed:
@@ -531,11 +549,11 @@ def main():
                for k in ("mu", "sigma", "p_src")}
         total_pts = nx * ny * world
         scaling = "weak"
-        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        flush = L2Flush(torch)
 
         def one_step(timed):
             if timed:
-                flush.zero_()  # L2 flush (inputs 168 MB are ~L2-sized); outside the kernel events
+                flush()  # L2 flush (inputs 168 MB are ~L2-sized); outside the kernel events
             e0 = ev() if timed else None
             dev.ensemble_divergence2d(members, nx, ny, 1.0, 1.0, cfg.t, outputs=("mu", "sigma", "p_src"),
                                       out=out, check=False)
@@ -707,7 +725,7 @@ def main():
         "data": "synthetic (seeded generator, BASELINE.json config recipe)",
         "config": {"workload": workload, "grid_points": total_pts, "t": cfg.t,
                    "parallelism": f"z-slab x{world}" if args.config in (3, 4) else f"replicas x{world}",
-                   "l2": ("flushed between steps (256 MB write)" if args.config in (0, 1) else
+                   "l2": (L2Flush.NOTE if args.config in (0, 1) else
                           "inputs larger than L2 (126 MB); no flush" if args.config in (3, 4) else
                           "compute-bound; 2 MB model stays in L2")},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,

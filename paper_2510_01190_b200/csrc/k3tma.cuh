@@ -66,7 +66,7 @@ struct K3Xchg {
   // u moments at the x-halo columns: [buf][left/right][row]
   float uh_mu[2][2][K3Cfg::TYMAX];
   float uh_sg[2][2][K3Cfg::TYMAX];
-  K3Pending pend[K3Cfg::D];  // producer-private halo queue
+  K3Pending pend[K3Cfg::D + 1];  // producer-private halo queue
   // each consumer lane's w moments of plane k-1 (kept out of registers)
   Vec<float, 4> wm[K3Cfg::TYMAX][2][32];
 };
@@ -83,6 +83,7 @@ struct K3Params {
   int64_t comp_stride;                                   // Nl = nx*ny*nzl
   int nx, ny, ty, tiles_x, n_tiles, M;
   int has_w;                                             // 0: 2D ensemble (u, v only)
+  int hdelay;                                            // halo boxes trail by this many items (<= D)
   uint32_t bytes_u, bytes_v, bytes_w;
   float cx_in, cx_bd, cy_in, cy_bd, cz_in, cz_bd;
   float theta;
@@ -126,15 +127,15 @@ struct K3 {
       mbar_expect_tx(&full[s], comp == kU ? p.bytes_u : comp == kV ? p.bytes_v : p.bytes_w);
       const int m0 = b * MB;
       tma_load_5d(&st[s].main[0], &tm.m[kK3Main], &full[s], x0, y0, k, comp, m0);
-      while (qn > 0 && q[qh].idx <= idx - D) {  // halos of the item D stages back
-        halo(q[qh]);
-        qh = qh + 1 == D ? 0 : qh + 1;
-        --qn;
-      }
       if (comp != kW) {
-        const int slot = (qh + qn) % D;
+        const int slot = (qh + qn) % (D + 1);
         q[slot] = K3Pending{idx, x0, y0, k, m0, s, comp, 0};
         ++qn;
+      }
+      while (qn > 0 && q[qh].idx <= idx - p.hdelay) {  // halos of the item hdelay stages back
+        halo(q[qh]);
+        qh = qh + 1 == D + 1 ? 0 : qh + 1;
+        --qn;
       }
       ++idx;
       if (++s == S) { s = 0; ph ^= 1u; }
@@ -158,7 +159,7 @@ struct K3 {
     }
     while (qn > 0) {
       halo(q[qh]);
-      qh = qh + 1 == D ? 0 : qh + 1;
+      qh = qh + 1 == D + 1 ? 0 : qh + 1;
       --qn;
     }
   }
