@@ -315,7 +315,7 @@ int try_k3_tma(const StencilParams<float>& sp, int comps, cudaStream_t s, bool* 
   // 3D: halo boxes trail D items so the neighbour CTA (lockstep z-march) has
   // pulled them into L2; 2D tiles are short, and a trailing halo only delays
   // the stage it completes
-  p.hdelay = int(std::max<int64_t>(0, std::min<int64_t>(C::D, env_int("DIVUQ_K3_HDELAY", comps == 3 ? C::D : 1))));
+  p.hdelay = int(std::max<int64_t>(0, std::min<int64_t>(C::D, env_int("DIVUQ_K3_HDELAY", comps == 3 ? C::D : 0))));
   p.bytes_u = uint32_t((C::TX * ty + 2 * C::PAD * ty) * 4 * C::MB);
   p.bytes_v = uint32_t((C::TX * ty + 2 * C::TX) * 4 * C::MB);
   p.bytes_w = uint32_t(C::TX * ty * 4 * C::MB);

@@ -6,10 +6,8 @@ little-endian fp32, io.py:1-14).  Header parsing, the payload read and the
 byte-deterministic writer are native (``divuq_divuq1_*`` in the C ABI); the
 payload is already the (M, 2, N) member-major fp32 block the ensemble kernels
 read, so ``load_ensemble_device`` streams it disk -> pinned -> HBM with no
-host-side reshaping, ready for ``device.ensemble_divergence2d``.
-
-CSV helpers (io.py:137-148) belong to the reference's CLI and are out of
-scope (DESIGN.md).
+host-side reshaping, ready for ``device.ensemble_divergence2d``.  The CSV
+helpers (io.py:137-148) serve the CLI routing (``cli.py``).
 """
 
 from __future__ import annotations
@@ -143,7 +141,7 @@ def read_model(mu_path, sigma_path) -> GaussianVectorField:
 
 def load_ensemble_device(path, device=None):
     """DIVUQ1 ensemble -> (grid, (M, 2, N) fp32 CUDA tensor), streamed through
-    double-buffered pinned staging.  Non-finite payload values are not scanned
+    a ring of pinned staging buffers (parallel pread, async H2D).  Non-finite payload values are not scanned
     here: the consuming kernels reject them (device.* ``check=True`` raises
     ValueError, the DataError condition) inside the same pass that reads them."""
     import torch
@@ -157,3 +155,16 @@ def load_ensemble_device(path, device=None):
     _raise(lib.divuq_divuq1_ingest_f32(os.fsencode(path), out.data_ptr(), out.numel(),
                                        dev.index if dev.index is not None else 0), path, "read")
     return grid, out
+
+
+def csv_float(x: float) -> str:
+    """Full round-trip precision for CSV cells (io.py:137-139)."""
+    return repr(float(x))
+
+
+def write_csv(path, header: str, rows) -> None:
+    """Header row + comma-joined rows, \\n line endings (io.py:142-148)."""
+    with open(path, "w", encoding="ascii", newline="\n") as fh:
+        fh.write(header + "\n")
+        for row in rows:
+            fh.write(",".join(str(c) for c in row) + "\n")

@@ -200,6 +200,26 @@ def main():
             for _ in range(m)
         )
         ref_io.write_members(g, members, os.path.join(OUT, f"divuq1_{name}.duq"))
+
+    # ---- CLI routing (cli.py:58-107,152-155): the reference CLI's own outputs
+    # for the wind-scale pipeline of pkg/tests/test_cli.py:14-40
+    from divuq.cli import cli_main
+
+    def p(name):
+        return os.path.join(OUT, f"cli_{name}")
+
+    ens = divuq.generate_synthetic("source-sink", divuq.UniformGrid2(24, 24), 15, 0.3, seed=7)
+    ref_io.write_ensemble(ens, p("wind.duq"))
+    steps = [
+        ["fit", "--in", p("wind.duq"), "--out-mu", p("mu.duq"), "--out-sigma", p("sg.duq")],
+        ["div", "--in-mu", p("mu.duq"), "--in-sigma", p("sg.duq"), "--out-mu", p("dmu.duq"),
+         "--out-sigma", p("dsg.duq")],
+        ["lcp", "--in-mu", p("dmu.duq"), "--in-sigma", p("dsg.duq"), "--iso", "-2.525",
+         "--out", p("lcp.csv")],
+        ["gradmag", "--in", p("wind.duq"), "--out", p("gm.duq")],
+    ]
+    for argv in steps:
+        assert cli_main(argv) == 0, argv
     print("golden fixtures written to", OUT)
 
 
