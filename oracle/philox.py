@@ -38,7 +38,7 @@ from .ref2d import divergence2d
 
 M0, M1 = np.uint64(0xD2511F53), np.uint64(0xCD9E8D57)
 W0, W1 = np.uint32(0x9E3779B9), np.uint32(0xBB67AE85)
-CHUNK = 256
+CHUNK = 128
 _MASK32 = np.uint64(0xFFFFFFFF)
 
 

@@ -782,6 +782,10 @@ int divuq_mc_divergence2d_f64(const double* mu_u, const double* mu_v, const doub
   p.nx = nx; p.ny = ny; p.row_begin = row_begin; p.row_end = row_end;
   p.n_samples = n_samples; p.n_chunks = (n_samples + kMcChunk - 1) / kMcChunk;
   p.seed = seed;
+  for (int r = 0; r < 10; ++r) {  // Philox round keys: key + r * (W0, W1) mod 2^32
+    p.k0[r] = uint32_t(seed) + uint32_t(r) * 0x9E3779B9u;
+    p.k1[r] = uint32_t(seed >> 32) + uint32_t(r) * 0xBB67AE85u;
+  }
   p.cx_in = 1.0 / (2.0 * dx); p.cx_bd = 1.0 / dx; p.cy_in = 1.0 / (2.0 * dy); p.cy_bd = 1.0 / dy;
   const int64_t nv = (row_end - row_begin) * nx;
   p.part_mean = static_cast<double*>(scratch);
@@ -790,7 +794,9 @@ int divuq_mc_divergence2d_f64(const double* mu_u, const double* mu_v, const doub
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   dim3 grid(unsigned((nx + kMcTX - 1) / kMcTX), unsigned((row_end - row_begin + kMcTY - 1) / kMcTY),
             unsigned(p.n_chunks));
-  mc_chunk_kernel<<<grid, dim3(kMcTX, kMcTY), 0, s>>>(p);
+  DIVUQ_CUDA(cudaFuncSetAttribute(mc_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(sizeof(McSmem))));
+  mc_chunk_kernel<<<grid, dim3(kMcTX, kMcTY), sizeof(McSmem), s>>>(p);
   DIVUQ_CUDA(cudaGetLastError());
   const int64_t threads = 256;
   mc_merge_kernel<<<unsigned((nv * 32 + threads - 1) / threads), unsigned(threads), 0, s>>>(p);

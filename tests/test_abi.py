@@ -57,7 +57,7 @@ def test_argument_validation_before_any_launch(pkg):
     assert lib.divuq_fit_gaussian_f64(1, 1, 2, 10, 1, 1, None, None) == -3
     assert lib.divuq_mc_divergence2d_f64(1, 1, 1, 1, 4, 4, 1.0, 1.0, 1, 0, 0, 4,
                                          1, 1, 1, None, None) == -4
-    assert lib.divuq_mc_scratch_bytes(256, 0, 256, 2000) == 2 * 8 * 256 * 256 * 8
+    assert lib.divuq_mc_scratch_bytes(256, 0, 256, 2000) == 2 * 16 * 256 * 256 * 8  # 16 chunks of 128
 
 
 def test_reference_type_validation(pkg):
