@@ -25,9 +25,12 @@ sample axis over thread blocks):
     fixed shuffle tree (offsets 16, 8, 4, 2, 1) merges the 32 lanes;
     std = sqrt(M2 / (n - 1)).
 The chunking depends on n only, so results are invariant to launch shape and
-GPU count.  The GPU uses libdevice log/sincospi, which differ from numpy's in
-the last ulp, so GPU-vs-oracle agreement is tolerance-based (tests state it);
-the Philox words and the uniforms are bit-exact.
+GPU count.  The GPU evaluates log (table + log1p series, <= 1.6 ulp), sqrt and
+sin/cos(2 pi u) (quadrant reduction + Taylor, more accurate than numpy's
+cos(2*pi*u)) with its own in-range routines and fuses the draw mu + sigma*z and
+the Welford updates into fmas, so GPU-vs-oracle agreement is tolerance-based
+(tests state it); the Philox words and the uniforms are bit-exact, and
+sigma = 0 still reproduces the deterministic divergence exactly.
 """
 
 from __future__ import annotations
