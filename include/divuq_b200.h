@@ -252,6 +252,33 @@ int divuq_host_velocity_magnitude_f64(const double* u, const double* v, int64_t 
                                       int device);
 int divuq_host_gradient2d_f64(const double* values, int64_t nx, int64_t ny, double dx, double dy,
                               double* out_gx_gy, int device);
+
+/* ---- K4 parity mode: the reference's own stream ---------------------------
+ * splitmix64 + AS241 (rng.py:23-92), counters (2s) n + v / (2s+1) n + v
+ * (mc.py:80-91), one Welford pass per vertex in strict sample order with
+ * mean += delta / count (mc.py:106-117): replaces mc_divergence draw for draw.
+ * No scratch (no chunk split). */
+int divuq_mc_divergence2d_ref_f64(const double* mu_u, const double* mu_v,
+                                  const double* s_u, const double* s_v,
+                                  int64_t nx, int64_t ny, double dx, double dy,
+                                  int64_t n_samples, uint64_t seed,
+                                  int64_t row_begin, int64_t row_end,
+                                  double* out_mean, double* out_std,
+                                  int32_t* err_word, void* stream);
+/* sample_divergence_1d (mc.py:142-156): neighbors = host array of 8 doubles
+ * (mu, sigma) x (u_{i-1}, u_{i+1}, v_{j-1}, v_{j+1}); out = device array. */
+int divuq_sample_divergence1d_f64(const double* neighbors, double dx, double dy,
+                                  int64_t n_samples, uint64_t seed, double* out, void* stream);
+/* min / max of a device array -> out_minmax[2] (device); scratch16: 16 bytes. */
+int divuq_minmax_f64(const double* values, int64_t n, double* out_minmax, void* scratch16,
+                     void* stream);
+/* np.histogram(values, bins=n_bins, range=(lo, hi)) (numpy's uniform-bin rule,
+ * linspace edges): edges_dev n_bins+1 doubles, counts_dev n_bins int64.
+ * Synchronises the stream (the edges are staged from the host). */
+int divuq_histogram_uniform_f64(const double* values, int64_t n, double lo, double hi,
+                                int64_t n_bins, double* edges_dev, int64_t* counts_dev,
+                                void* stream);
+
 int divuq_host_gradient_ensemble2d_f64(const double* members, int64_t n_members, int64_t nx,
                                        int64_t ny, double dx, double dy, double* out_members,
                                        int device);
@@ -267,6 +294,20 @@ int divuq_host_mc_divergence2d_f64(const double* mu_u, const double* mu_v,
                                    int64_t nx, int64_t ny, double dx, double dy,
                                    int64_t n_samples, uint64_t seed,
                                    double* out_mean, double* out_std, int device);
+
+/* host twins of the parity mode (mc.py:94-156) */
+int divuq_host_mc_divergence2d_ref_f64(const double* mu_u, const double* mu_v,
+                                       const double* s_u, const double* s_v,
+                                       int64_t nx, int64_t ny, double dx, double dy,
+                                       int64_t n_samples, uint64_t seed,
+                                       double* out_mean, double* out_std, int device);
+/* mc_histogram_1d (mc.py:120-139): out_edges n_bins+1, out_counts n_bins,
+ * *out_nbins = bins used (1 for the all-identical degenerate case),
+ * out_values (nullable) = the raw samples. */
+int divuq_host_mc_histogram1d_f64(const double* neighbors, double dx, double dy,
+                                  int64_t n_samples, uint64_t seed, int64_t n_bins,
+                                  double* out_edges, int64_t* out_counts, int64_t* out_nbins,
+                                  double* out_values, int device);
 
 #ifdef __cplusplus
 }

@@ -20,6 +20,10 @@ Contents
            kernel (the north star mandates it instead of the reference's
            splitmix64 + AS241), pinned by the Random123 known-answer vectors,
            and the MC estimator restated with the GPU's exact chunk/merge order.
+``refstream`` the reference's own MC stream (splitmix64 + AS241, rng.py) and
+           its estimator / single-vertex sampler / histogram (mc.py:94-156),
+           pinned bitwise against vectors the reference produced
+           (``tests/golden/make_golden_refstream.py``).
 ``divuq1`` the DIVUQ1 container reader / header formatter (io.py:38-93),
            pinned against files the reference's own writer produced.
 """

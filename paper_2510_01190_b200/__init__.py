@@ -28,12 +28,14 @@ from .api import (
     error_metrics,
     fit_gaussian,
     mc_divergence,
+    mc_histogram_1d,
     propagate_divergence,
     propagate_with_probabilities,
     propagate_with_probabilities3d,
     set_device,
     sink_probability,
     source_probability,
+    sample_divergence_1d,
     stencil_distribution,
     tail_probs,
 )
@@ -46,6 +48,7 @@ from .types import (
     LcpField,
     McConfig,
     McDivergenceEstimate,
+    McHistogram,
     ParallelConfig,
     ScalarField2,
     UniformGrid2,
@@ -58,10 +61,11 @@ __version__ = "0.1.0"
 
 __all__ = [
     "Ensemble2", "EnsembleDivergence", "GaussianScalarField", "GaussianScalarField3",
-    "GaussianVectorField", "GaussianVectorField3", "LcpField", "McConfig", "McDivergenceEstimate",
+    "GaussianVectorField", "GaussianVectorField3", "LcpField", "McConfig", "McDivergenceEstimate", "McHistogram",
     "ParallelConfig", "Propagation", "ScalarField2", "UniformGrid2", "UniformGrid3",
     "VectorField2", "cell_crossing_probability", "divergence_deterministic", "ensemble_divergence", "error_metrics",
-    "fit_gaussian", "gradient", "gradient_ensemble", "lcp", "mc_divergence",
+    "fit_gaussian", "gradient", "gradient_ensemble", "lcp", "mc_divergence", "mc_histogram_1d",
+    "sample_divergence_1d",
     "velocity_magnitude", "propagate_divergence", "propagate_with_probabilities",
     "propagate_with_probabilities3d", "set_device", "sink_probability", "source_probability",
     "stencil_distribution", "tail_probs", "vertex_index",

@@ -79,6 +79,15 @@ SIGNATURES = {
         _int, [_p, _i64, _i64, _i64, _f64, _f64, _f64] + [_p] * 6 + [_int]),
     "divuq_host_mc_divergence2d_f64": (
         _int, [_p] * 4 + [_i64, _i64, _f64, _f64, _i64, _u64, _p, _p, _int]),
+    "divuq_mc_divergence2d_ref_f64": (
+        _int, [_p] * 4 + [_i64, _i64, _f64, _f64, _i64, _u64, _i64, _i64] + [_p] * 2 + [_p, _p]),
+    "divuq_sample_divergence1d_f64": (_int, [_p, _f64, _f64, _i64, _u64, _p, _p]),
+    "divuq_minmax_f64": (_int, [_p, _i64, _p, _p, _p]),
+    "divuq_histogram_uniform_f64": (_int, [_p, _i64, _f64, _f64, _i64, _p, _p, _p]),
+    "divuq_host_mc_divergence2d_ref_f64": (
+        _int, [_p] * 4 + [_i64, _i64, _f64, _f64, _i64, _u64, _p, _p, _int]),
+    "divuq_host_mc_histogram1d_f64": (
+        _int, [_p, _f64, _f64, _i64, _u64, _i64, _p, _p, _p, _p, _int]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():

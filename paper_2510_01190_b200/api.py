@@ -26,6 +26,7 @@ from .types import (
     LcpField,
     McConfig,
     McDivergenceEstimate,
+    McHistogram,
     ParallelConfig,
     ScalarField2,
     VectorField2,
@@ -177,24 +178,80 @@ def sink_probability(fld: GaussianScalarField, t: float = 0.0) -> np.ndarray:
     return tail_probs(fld.mu, fld.sigma, -t)[0]
 
 
-def mc_divergence(model: GaussianVectorField, config: McConfig) -> McDivergenceEstimate:
-    """Per-vertex empirical divergence mean/std (mc.py:94-117), Philox stream.
+def mc_divergence(model: GaussianVectorField, config: McConfig, *,
+                  stream: str = "philox") -> McDivergenceEstimate:
+    """Per-vertex empirical divergence mean/std (mc.py:94-117).
 
-    Statistically equivalent to the reference (its splitmix64 + AS241 draws
-    are replaced by Philox4x32-10 + Box-Muller as the north star mandates);
-    deterministic in (model, seed, n) and invariant to launch shape.
+    ``stream="philox"`` (default, the north star's kernel): Philox4x32-10 +
+    Box-Muller draws, statistically equivalent to the reference; deterministic
+    in (model, seed, n) and invariant to launch shape.
+    ``stream="reference"``: the reference's own splitmix64 + AS241 stream,
+    counters and single-pass Welford, so the estimate reproduces the
+    reference's ``mc_divergence`` draw for draw (golden-tested).
     """
     if config.n_samples < 2:
         raise ValueError("mc_divergence needs n_samples >= 2")
+    if stream not in ("philox", "reference"):
+        raise ValueError("stream must be 'philox' or 'reference'")
     g = model.grid
     n = g.n_vertices
     mean = np.empty(n)
     std = np.empty(n)
-    _check(lib.divuq_host_mc_divergence2d_f64(
+    fn = (lib.divuq_host_mc_divergence2d_f64 if stream == "philox"
+          else lib.divuq_host_mc_divergence2d_ref_f64)
+    _check(fn(
         _p(model.mu_u), _p(model.mu_v), _p(model.sigma_u), _p(model.sigma_v), g.nx, g.ny,
         float(g.dx), float(g.dy), int(config.n_samples), int(config.seed), _p(mean), _p(std),
         _DEVICE))
     return McDivergenceEstimate(g, mean, std, config.n_samples)
+
+
+def _neighbors8(neighbors) -> np.ndarray:
+    nb = np.ascontiguousarray(np.asarray(neighbors, dtype=np.float64).reshape(4, 2)).ravel()
+    if np.any(nb[1::2] < 0):
+        raise ValueError("sigmas must be non-negative")   # mc.py:147-149
+    return nb
+
+
+def sample_divergence_1d(neighbors, spacing: tuple[float, float], config: McConfig) -> np.ndarray:
+    """Raw single-vertex divergence samples (mc.py:142-156), reference stream.
+
+    neighbors: four (mu, sigma) pairs in stencil order -- u at i-1, u at i+1,
+    v at j-1, v at j+1.  Draw k uses counters 4k..4k+3 of the reference's
+    splitmix64 + AS241 stream, so the samples equal the reference's.
+    """
+    nb = _neighbors8(neighbors)
+    dx, dy = spacing
+    n = int(config.n_samples)
+    values = np.empty(n)
+    edges = np.empty(2)
+    counts = np.empty(1, dtype=np.int64)
+    used = np.zeros(1, dtype=np.int64)
+    _check(lib.divuq_host_mc_histogram1d_f64(
+        _p(nb), float(dx), float(dy), n, int(config.seed), 1, _p(edges), _p(counts), _p(used),
+        _p(values), _DEVICE))
+    return values
+
+
+def mc_histogram_1d(neighbors, spacing: tuple[float, float], config: McConfig,
+                    n_bins: int) -> McHistogram:
+    """Histogram of sampled single-vertex divergence (mc.py:120-139).
+
+    Samples, [min, max] and np.histogram's uniform-bin rule all run on the
+    GPU; all-identical draws give the reference's one-bin histogram.
+    """
+    if n_bins < 1:
+        raise ValueError("n_bins must be >= 1")
+    nb = _neighbors8(neighbors)
+    dx, dy = spacing
+    edges = np.empty(n_bins + 1)
+    counts = np.empty(n_bins, dtype=np.int64)
+    used = np.zeros(1, dtype=np.int64)
+    _check(lib.divuq_host_mc_histogram1d_f64(
+        _p(nb), float(dx), float(dy), int(config.n_samples), int(config.seed), int(n_bins),
+        _p(edges), _p(counts), _p(used), None, _DEVICE))
+    k = int(used[0])
+    return McHistogram(edges[: k + 1].copy(), counts[:k].copy(), int(config.n_samples))
 
 
 def error_metrics(estimate: McDivergenceEstimate, analytic: GaussianScalarField):

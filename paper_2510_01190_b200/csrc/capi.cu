@@ -803,6 +803,82 @@ int divuq_mc_divergence2d_f64(const double* mu_u, const double* mu_v, const doub
   return int(cudaGetLastError());
 }
 
+int divuq_mc_divergence2d_ref_f64(const double* mu_u, const double* mu_v, const double* s_u,
+                                  const double* s_v, int64_t nx, int64_t ny, double dx, double dy,
+                                  int64_t n_samples, uint64_t seed, int64_t row_begin,
+                                  int64_t row_end, double* out_mean, double* out_std, int32_t* err,
+                                  void* stream) {
+  if (int r = grid_ok(nx, ny, dx, dy)) return r;
+  if (n_samples < 2) return DIVUQ_ESAMPLES;
+  if (!mu_u || !mu_v || !s_u || !s_v || !out_mean || !out_std) return DIVUQ_EINVAL;
+  if (row_begin < 0 || row_end > ny || row_begin >= row_end) return DIVUQ_EINVAL;
+  McRefParams p;
+  p.mu_u = mu_u; p.mu_v = mu_v; p.s_u = s_u; p.s_v = s_v;
+  p.nx = nx; p.ny = ny; p.row_begin = row_begin; p.row_end = row_end;
+  p.n_samples = n_samples; p.seed = seed;
+  p.cx_in = 1.0 / (2.0 * dx); p.cx_bd = 1.0 / dx; p.cy_in = 1.0 / (2.0 * dy); p.cy_bd = 1.0 / dy;
+  p.out_mean = out_mean; p.out_std = out_std; p.err = err;
+  dim3 grid(unsigned((nx + kMrTX - 1) / kMrTX), unsigned((row_end - row_begin + kMrTY - 1) / kMrTY));
+  mc_ref_kernel<<<grid, dim3(kMrTX, kMrTY), 0, static_cast<cudaStream_t>(stream)>>>(p);
+  return int(cudaGetLastError());
+}
+
+int divuq_sample_divergence1d_f64(const double* neighbors, double dx, double dy, int64_t n_samples,
+                                  uint64_t seed, double* out, void* stream) {
+  if (!neighbors || n_samples < 0 || (n_samples && !out)) return DIVUQ_EINVAL;
+  for (int k = 1; k < 8; k += 2)
+    if (neighbors[k] < 0.0) return DIVUQ_ENEGSIGMA;   // mc.py:147-149
+  if (n_samples == 0) return DIVUQ_OK;
+  const int64_t grid = std::min<int64_t>((n_samples + 255) / 256, int64_t(sm_count()) * 8);
+  sample_1d_kernel<<<unsigned(grid), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      neighbors[0], neighbors[1], neighbors[2], neighbors[3], neighbors[4], neighbors[5],
+      neighbors[6], neighbors[7], 2.0 * dx, 2.0 * dy, n_samples, seed, out);
+  return int(cudaGetLastError());
+}
+
+int divuq_minmax_f64(const double* values, int64_t n, double* out_minmax, void* scratch16,
+                     void* stream) {
+  if (!values || n < 1 || !out_minmax || !scratch16) return DIVUQ_EINVAL;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long long init[2] = {0x7fffffffffffffffll, (long long)0x8000000000000000ull};
+  DIVUQ_CUDA(cudaMemcpyAsync(scratch16, init, sizeof(init), cudaMemcpyHostToDevice, s));
+  const int64_t grid = std::min<int64_t>((n + 255) / 256, int64_t(sm_count()) * 8);
+  minmax_kernel<<<unsigned(grid), 256, 0, s>>>(values, n, static_cast<long long*>(scratch16));
+  DIVUQ_CUDA(cudaGetLastError());
+  minmax_finish_kernel<<<1, 1, 0, s>>>(static_cast<long long*>(scratch16), out_minmax);
+  return int(cudaGetLastError());
+}
+
+// np.linspace(lo, hi, nbins + 1) (numpy 2.3 function_base: step = (hi - lo) / nbins,
+// edge_i = i * step + lo, last = hi) -- host arithmetic, no contraction
+static void linspace_edges(double lo, double hi, int64_t nbins, double* edges) {
+  volatile double step = (hi - lo) / double(nbins);
+  for (int64_t i = 0; i <= nbins; ++i) {
+    volatile double y = double(i) * step;
+    edges[i] = y + lo;
+  }
+  edges[nbins] = hi;
+}
+
+int divuq_histogram_uniform_f64(const double* values, int64_t n, double lo, double hi,
+                                int64_t n_bins, double* edges_dev, int64_t* counts_dev,
+                                void* stream) {
+  if (!values || n < 0 || n_bins < 1 || !edges_dev || !counts_dev || !(lo < hi)) return DIVUQ_EINVAL;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<double> e(size_t(n_bins) + 1);
+  linspace_edges(lo, hi, n_bins, e.data());
+  DIVUQ_CUDA(cudaMemcpyAsync(edges_dev, e.data(), e.size() * sizeof(double), cudaMemcpyHostToDevice, s));
+  DIVUQ_CUDA(cudaMemsetAsync(counts_dev, 0, size_t(n_bins) * sizeof(int64_t), s));
+  if (n) {
+    const int64_t grid = std::min<int64_t>((n + 255) / 256, int64_t(sm_count()) * 8);
+    histogram_kernel<<<unsigned(grid), 256, 0, s>>>(values, n, edges_dev, n_bins,
+                                                    reinterpret_cast<unsigned long long*>(counts_dev));
+  }
+  // the host edge vector must outlive the async copy
+  DIVUQ_CUDA(cudaStreamSynchronize(s));
+  return int(cudaGetLastError());
+}
+
 int divuq_gen_field_f32(const float* bumps, int n_bumps, int dims, int64_t nx, int64_t ny, int64_t nzl,
                         int64_t z0, double dx, double dy, double dz, double vortex_amp,
                         double vortex_cx, double vortex_cy, double vortex_r, double shear_amp,
@@ -1051,6 +1127,83 @@ int divuq_host_mc_divergence2d_f64(const double* mu_u, const double* mu_v, const
 // 3D host pipeline: z-chunks of `chunk_planes` planes; chunk c uses buffer
 // set c % 2 and stream c % 2, so chunk c+1's host->device copies overlap
 // chunk c's kernel and device->host copies (two copy engines + SMs busy).
+int divuq_host_mc_divergence2d_ref_f64(const double* mu_u, const double* mu_v, const double* s_u,
+                                       const double* s_v, int64_t nx, int64_t ny, double dx,
+                                       double dy, int64_t n_samples, uint64_t seed,
+                                       double* out_mean, double* out_std, int device) {
+  if (int r = grid_ok(nx, ny, dx, dy)) return r;
+  if (n_samples < 2) return DIVUQ_ESAMPLES;
+  if (!mu_u || !mu_v || !s_u || !s_v || !out_mean || !out_std) return DIVUQ_EINVAL;
+  DIVUQ_CUDA(cudaSetDevice(device));
+  StreamGuard sg;
+  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  const int64_t n = nx * ny;
+  const size_t b = size_t(n) * sizeof(double);
+  DevBuf d;
+  DIVUQ_CUDA(d.alloc(6 * b + 256, sg.s));
+  double* base = d.as<double>();
+  int32_t* derr = reinterpret_cast<int32_t*>(base + 6 * n);
+  DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
+  const double* src[4] = {mu_u, mu_v, s_u, s_v};
+  for (int q = 0; q < 4; ++q)
+    DIVUQ_CUDA(cudaMemcpyAsync(base + q * n, src[q], b, cudaMemcpyHostToDevice, sg.s));
+  int r = divuq_mc_divergence2d_ref_f64(base, base + n, base + 2 * n, base + 3 * n, nx, ny, dx, dy,
+                                        n_samples, seed, 0, ny, base + 4 * n, base + 5 * n, derr, sg.s);
+  if (r) return r;
+  DIVUQ_CUDA(cudaMemcpyAsync(out_mean, base + 4 * n, b, cudaMemcpyDeviceToHost, sg.s));
+  DIVUQ_CUDA(cudaMemcpyAsync(out_std, base + 5 * n, b, cudaMemcpyDeviceToHost, sg.s));
+  int status = 0;
+  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  return status;
+}
+
+// mc_histogram_1d (mc.py:120-139): samples, [min, max], then np.histogram's
+// uniform bins; the all-identical case is the reference's one-bin histogram
+// [lo - 0.5, hi + 0.5].  out_edges: n_bins + 1 doubles, out_counts: n_bins
+// int64; *out_nbins receives the bin count actually used (1 when degenerate).
+// out_values (nullable) receives the raw samples (sample_divergence_1d).
+int divuq_host_mc_histogram1d_f64(const double* neighbors, double dx, double dy,
+                                  int64_t n_samples, uint64_t seed, int64_t n_bins,
+                                  double* out_edges, int64_t* out_counts, int64_t* out_nbins,
+                                  double* out_values, int device) {
+  if (n_bins < 1) return DIVUQ_EINVAL;   // mc.py:131-132
+  if (!neighbors || n_samples < 1 || !out_edges || !out_counts || !out_nbins) return DIVUQ_EINVAL;
+  DIVUQ_CUDA(cudaSetDevice(device));
+  StreamGuard sg;
+  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  const size_t vb = size_t(n_samples) * sizeof(double);
+  DevBuf d;
+  DIVUQ_CUDA(d.alloc(vb + size_t(n_bins + 1) * 16 + 64, sg.s));
+  double* vals = d.as<double>();
+  double* edges = vals + n_samples;
+  int64_t* counts = reinterpret_cast<int64_t*>(edges + n_bins + 1);
+  double* mm = reinterpret_cast<double*>(counts + n_bins);
+  void* scratch = mm + 2;
+  if (int r = divuq_sample_divergence1d_f64(neighbors, dx, dy, n_samples, seed, vals, sg.s)) return r;
+  if (int r = divuq_minmax_f64(vals, n_samples, mm, scratch, sg.s)) return r;
+  double lohi[2];
+  DIVUQ_CUDA(cudaMemcpyAsync(lohi, mm, sizeof(lohi), cudaMemcpyDeviceToHost, sg.s));
+  DIVUQ_CUDA(cudaStreamSynchronize(sg.s));
+  if (out_values) DIVUQ_CUDA(cudaMemcpyAsync(out_values, vals, vb, cudaMemcpyDeviceToHost, sg.s));
+  if (lohi[0] == lohi[1]) {   // all draws identical: one-bin degenerate histogram (mc.py:135-137)
+    out_edges[0] = lohi[0] - 0.5;
+    out_edges[1] = lohi[1] + 0.5;
+    out_counts[0] = n_samples;
+    *out_nbins = 1;
+    DIVUQ_CUDA(cudaStreamSynchronize(sg.s));
+    return DIVUQ_OK;
+  }
+  if (int r = divuq_histogram_uniform_f64(vals, n_samples, lohi[0], lohi[1], n_bins, edges, counts, sg.s))
+    return r;
+  DIVUQ_CUDA(cudaMemcpyAsync(out_edges, edges, size_t(n_bins + 1) * sizeof(double),
+                             cudaMemcpyDeviceToHost, sg.s));
+  DIVUQ_CUDA(cudaMemcpyAsync(out_counts, counts, size_t(n_bins) * sizeof(int64_t),
+                             cudaMemcpyDeviceToHost, sg.s));
+  DIVUQ_CUDA(cudaStreamSynchronize(sg.s));
+  *out_nbins = n_bins;
+  return DIVUQ_OK;
+}
+
 int divuq_host_propagate3d_f32(const float* mu_u, const float* mu_v, const float* mu_w,
                                const float* s_u, const float* s_v, const float* s_w, int64_t nx,
                                int64_t ny, int64_t nz, double dx, double dy, double dz, double t,

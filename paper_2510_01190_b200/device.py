@@ -256,8 +256,15 @@ def w_moments_plane(members, nx, ny, nz_local, k, *, check=True):
 
 
 def mc_divergence2d(mu_u, mu_v, s_u, s_v, nx, ny, dx, dy, n_samples, seed, *, rows=None,
-                    out=None, check=True):
-    """K4: Philox Monte Carlo estimate for rows [r0, r1) (default all)."""
+                    out=None, check=True, stream="philox"):
+    """K4: Monte Carlo estimate for rows [r0, r1) (default all).
+
+    stream="philox": the north star's Philox4x32-10 + Box-Muller kernel;
+    stream="reference": the reference's splitmix64 + AS241 stream and
+    single-pass Welford (draw-for-draw parity with mc.py:94-117).
+    """
+    if stream not in ("philox", "reference"):
+        raise ValueError("stream must be 'philox' or 'reference'")
     n = nx * ny
     for name, x in (("mu_u", mu_u), ("mu_v", mu_v), ("s_u", s_u), ("s_v", s_v)):
         _req(x, name, torch.float64, n)
@@ -270,9 +277,15 @@ def mc_divergence2d(mu_u, mu_v, s_u, s_v, nx, ny, dx, dy, n_samples, seed, *, ro
     mean, std = out if out is not None else (
         torch.empty(nv, dtype=torch.float64, device=mu_u.device),
         torch.empty(nv, dtype=torch.float64, device=mu_u.device))
+    err = _ErrWord(mu_u.device, check)
+    if stream == "reference":
+        _check(lib.divuq_mc_divergence2d_ref_f64(
+            _ptr(mu_u), _ptr(mu_v), _ptr(s_u), _ptr(s_v), nx, ny, float(dx), float(dy),
+            n_samples, int(seed), r0, r1, _ptr(mean), _ptr(std), err.ptr, _stream()))
+        err.raise_if_set()
+        return mean, std
     scratch = torch.empty(max(1, lib.divuq_mc_scratch_bytes(nx, r0, r1, n_samples)),
                           dtype=torch.uint8, device=mu_u.device)
-    err = _ErrWord(mu_u.device, check)
     _check(lib.divuq_mc_divergence2d_f64(
         _ptr(mu_u), _ptr(mu_v), _ptr(s_u), _ptr(s_v), nx, ny, float(dx), float(dy), n_samples,
         int(seed), r0, r1, _ptr(mean), _ptr(std), _ptr(scratch), err.ptr, _stream()))

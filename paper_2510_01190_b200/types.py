@@ -292,6 +292,31 @@ class McDivergenceEstimate:
 
 
 @dataclass(frozen=True)
+class McHistogram:
+    """mc.py:56-77: bin edges, counts, sample count (same invariants)."""
+
+    bin_edges: np.ndarray
+    counts: np.ndarray
+    n_samples: int
+
+    def __post_init__(self):
+        edges = np.asarray(self.bin_edges, dtype=np.float64)
+        counts = np.asarray(self.counts, dtype=np.int64)
+        if edges.ndim != 1 or np.any(np.diff(edges) <= 0):
+            raise ValueError("bin_edges must be strictly increasing")
+        if counts.shape != (edges.size - 1,) or np.any(counts < 0):
+            raise ValueError("counts must be non-negative with length len(edges)-1")
+        if int(counts.sum()) != self.n_samples:
+            raise ValueError("counts must sum to n_samples")
+        object.__setattr__(self, "bin_edges", edges)
+        object.__setattr__(self, "counts", counts)
+
+    def normalized_density(self) -> np.ndarray:
+        """counts scaled so the histogram integrates to 1."""
+        return self.counts / (self.n_samples * np.diff(self.bin_edges))
+
+
+@dataclass(frozen=True)
 class ParallelConfig:
     """threads and chunk may be a positive int or 'auto' (parallel.py:19-41)."""
 

@@ -187,3 +187,39 @@ def test_divuq1_oracle_pinned_to_reference_files(name):
     raw = open(path, "rb").read()
     hdr = divuq1.header(nx, ny, dx, dy, planes.shape[0])
     assert raw == hdr + planes.astype("<f4").tobytes()
+
+
+# --------------------------------------------------------------------------
+# the reference's own MC stream (oracle/refstream.py) vs the reference itself
+# --------------------------------------------------------------------------
+
+def test_refstream_oracle_bitwise_vs_reference_golden():
+    from oracle import refstream
+
+    g = golden("mc_refstream.npz")
+    for i, seed in enumerate(g["seeds"]):
+        assert np.array_equal(refstream.normal_stream(int(seed), g["counters"]), g["normals"][i])
+    for c in "abc":
+        nx, ny, dx, dy, n, seed = g[f"mc_{c}_grid"]
+        m = g[f"mc_{c}_model"]
+        mean, std = refstream.mc_divergence(m[0], m[1], m[2], m[3], int(nx), int(ny), dx, dy,
+                                            int(n), int(seed))
+        assert np.array_equal(mean, g[f"mc_{c}_mean"]) and np.array_equal(std, g[f"mc_{c}_std"])
+    fig1 = ((5.98, 0.96), (6.40, 0.38), (6.50, 0.94), (4.30, 0.65))
+    assert np.array_equal(refstream.sample_divergence_1d(fig1, (1.0, 1.0), 5000, 7), g["s1d_values"])
+    e, c = refstream.mc_histogram_1d(fig1, (1.0, 1.0), 20000, 7, 50)
+    assert np.array_equal(e, g["hist_edges"]) and np.array_equal(c, g["hist_counts"])
+    e, c = refstream.mc_histogram_1d(((1.0, 0.0), (2.0, 0.0), (3.0, 0.0), (4.0, 0.0)),
+                                     (1.0, 1.0), 500, 0, 10)
+    assert np.array_equal(e, g["hist0_edges"]) and np.array_equal(c, g["hist0_counts"])
+
+
+def test_mc_histogram_type_invariants():
+    import paper_2510_01190_b200 as d
+
+    with pytest.raises(ValueError):
+        d.McHistogram(np.array([0.0, 0.0, 1.0]), np.array([1, 1]), 2)
+    with pytest.raises(ValueError):
+        d.McHistogram(np.array([0.0, 1.0]), np.array([3]), 2)
+    h = d.McHistogram(np.array([0.0, 1.0, 3.0]), np.array([1, 1]), 2)
+    assert np.allclose(h.normalized_density(), [0.5, 0.25])
