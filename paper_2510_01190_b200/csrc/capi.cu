@@ -234,7 +234,32 @@ int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
   p.ty = ty;
   p.tiles_x = int(tiles_x);
   p.n_tiles = int(tiles_x * ((sp.ny + ty - 1) / ty));
-  p.stage_bytes = uint32_t((3 * ty * C::TX + 2 * ty * C::PAD + 2 * C::TX) * sizeof(T)) * (HAS_SIGMA ? 2u : 1u);
+  p.hdelay = int(std::max<int64_t>(0, std::min<int64_t>(C::D, env_int("DIVUQ_K2_HDELAY", 2))));
+  p.halo_off = int(env_int("DIVUQ_K2_HALO_OFF", 0));   // diagnostics only (wrong edge points)
+  p.sync_w = int(env_int("DIVUQ_K2_SYNC_W", 8));
+  p.sync_spin = int(env_int("DIVUQ_K2_SYNC_SPIN", 256));
+  p.sync_sleep = int(env_int("DIVUQ_K2_SYNC_SLEEP", 1000));
+  p.pf_dist = int(env_int("DIVUQ_K2_PF", 0));
+  p.diag_null = HAS_SIGMA && sp.out_mu && sp.out_sigma && sp.out_psrc && sp.out_psnk
+                    ? int(env_int("DIVUQ_K2_NULL", 0)) : 0;   // diagnostics only
+  p.progress = nullptr;
+  if (p.sync_w > 0 && p.n_tiles <= 4096) {
+    static unsigned long long* flags[64] = {};        // per device, allocated once, never reset
+    static unsigned long long epoch = 0;
+    int dev = 0;
+    DIVUQ_CUDA(cudaGetDevice(&dev));
+    if (dev < 64) {
+      if (!flags[dev]) {
+        const size_t bytes = 4096 * kFlagStride * sizeof(unsigned long long);
+        DIVUQ_CUDA(cudaMalloc(&flags[dev], bytes));
+        DIVUQ_CUDA(cudaMemset(flags[dev], 0, bytes));
+      }
+      p.progress = flags[dev];
+      p.epoch = ++epoch;
+    }
+  }
+  p.stage_bytes = uint32_t((3 * ty * C::TX + (p.halo_off ? 0 : 2 * ty * C::PAD + 2 * C::TX)) *
+                           sizeof(T)) * (HAS_SIGMA ? 2u : 1u);
   const int64_t n_work = int64_t(p.n_tiles) * (sp.kend - sp.kbeg);
   p.cx_in = sp.cx_in; p.cx_bd = sp.cx_bd; p.cy_in = sp.cy_in; p.cy_bd = sp.cy_bd;
   p.cz_in = sp.cz_in; p.cz_bd = sp.cz_bd; p.theta = sp.theta;

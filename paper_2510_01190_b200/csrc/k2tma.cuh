@@ -41,8 +41,8 @@ struct TmaCfg {
   static constexpr int PAD = VEC;                    // x-halo box width (16 bytes)
   static constexpr int TYMAX = 15;  // consumer warps (tile rows, max): 16 warps/CTA -> 128 regs
   static constexpr int S = 4;                        // pipeline stages
-  static constexpr int D = 2;                        // halo boxes trail the main boxes by D stages
-  static constexpr int THREADS = 32 * (TYMAX + 1);
+  static constexpr int D = 3;                        // max stages the halo boxes may trail (runtime hdelay)
+  static constexpr int THREADS = 32 * (TYMAX + 2);  // + producer warp + pacer warp
 };
 
 template <typename T>
@@ -74,6 +74,11 @@ struct TmaMaps {
   CUtensorMap m[kNumMaps];
 };
 
+// progress flags sit 512 B apart so they hash to different L2 slices: all
+// pacers polling a handful of lines would turn those slices into hot spots
+// that stall everyone's DRAM traffic
+constexpr size_t kFlagStride = 64;
+
 template <typename T>
 struct TmaParams {
   const T* mu_w; const T* s_w;                      // for the z-march restarts
@@ -82,6 +87,15 @@ struct TmaParams {
   int64_t nzl, z0, nzg, kbeg, kend;
   int nx, ny, ty, tiles_x, n_tiles;
   uint32_t stage_bytes;                              // TMA bytes per stage (depends on ty)
+  int hdelay;                                        // halo boxes trail the main boxes by this many stages (<= D)
+  int halo_off;                                      // diagnostics only: skip halo boxes (wrong edges; traffic attribution)
+  unsigned long long* progress;                      // per-tile progress flags (nullptr: no lockstep)
+  unsigned long long epoch;                          // launch tag in the flags' high word
+  int sync_w;                                        // max planes ahead of a neighbour tile
+  int sync_spin;                                     // bounded wait: polls before giving up
+  int sync_sleep;                                    // ns between polls
+  int pf_dist;                                       // L2 prefetch distance in planes (0: off)
+  int diag_null;                                     // diagnostics only: skip the math
   T cx_in, cx_bd, cy_in, cy_bd, cz_in, cz_bd;
   T theta;
   T* out_mu; T* out_sigma; T* out_psrc; T* out_psnk;
@@ -149,6 +163,17 @@ struct K2Tma {
     }
   }
 
+  static __device__ __forceinline__ void prefetch_main(const TmaMaps& tm, int x0, int y0, int k) {
+    tma_prefetch_l2_3d(&tm.m[kMapU], x0, y0, k);
+    tma_prefetch_l2_3d(&tm.m[kMapV], x0, y0, k);
+    tma_prefetch_l2_3d(&tm.m[kMapW], x0, y0, k + 1);
+    if constexpr (HAS_SIGMA) {
+      tma_prefetch_l2_3d(&tm.m[kMapSU], x0, y0, k);
+      tma_prefetch_l2_3d(&tm.m[kMapSV], x0, y0, k);
+      tma_prefetch_l2_3d(&tm.m[kMapSW], x0, y0, k + 1);
+    }
+  }
+
   static __device__ __forceinline__ void issue_halo(const TmaMaps& tm, Stage& st, uint64_t* bar,
                                                     int x0, int y0, int k, int ty) {
     tma_load_3d(&st.u_l[0][0], &tm.m[kMapUH], bar, x0 - PAD, y0, k);
@@ -164,33 +189,76 @@ struct K2Tma {
   }
 
   static __device__ void produce(const TmaParams<T>& p, const TmaMaps& tm, Stage* st,
-                                 uint64_t* full, uint64_t* empty) {
-    Pending pend[D];
+                                 uint64_t* full, uint64_t* empty, volatile int* permit) {
+    Pending pend[D + 1];
     int n_pend = 0, head = 0;
     int s = 0;
     uint32_t ph = 0;
+    const int hd = p.hdelay;
+    // loose lockstep: only when every tile has its own resident CTA
+    const bool sync = p.progress != nullptr && p.n_tiles <= int(gridDim.x);
     for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
       const int x0 = (tile % p.tiles_x) * TX;
       const int y0 = (tile / p.tiles_x) * p.ty;
       for (int k = int(p.kbeg); k < int(p.kend); ++k) {
+        if (sync)   // the pacer warp grants planes (neighbour-progress window)
+          while (int(k - p.kbeg) >= *permit) __nanosleep(32);
+        if (p.pf_dist > 0) {   // keep pf_dist planes of this tile on their way into L2
+          if (k == int(p.kbeg))
+            for (int q = 1; q < p.pf_dist && k + q < int(p.kend); ++q) prefetch_main(tm, x0, y0, k + q);
+          if (k + p.pf_dist < int(p.kend)) prefetch_main(tm, x0, y0, k + p.pf_dist);
+        }
         mbar_wait_backoff(&empty[s], ph ^ 1u);
         mbar_expect_tx(&full[s], p.stage_bytes);
         issue_main(tm, st[s], &full[s], x0, y0, k);
-        if (n_pend == D) {  // the oldest pending stage gets its halos now
+        pend[(head + n_pend) % (D + 1)] = Pending{x0, y0, k, s};
+        ++n_pend;
+        if (n_pend > hd) {  // the oldest pending stage gets its halos now (hd stages late)
           const Pending q = pend[head];
-          issue_halo(tm, st[q.s], &full[q.s], q.x0, q.y0, q.k, p.ty);
-          pend[head] = Pending{x0, y0, k, s};
-          head = (head + 1) % D;
-        } else {
-          pend[(head + n_pend) % D] = Pending{x0, y0, k, s};
-          ++n_pend;
+          if (!p.halo_off) issue_halo(tm, st[q.s], &full[q.s], q.x0, q.y0, q.k, p.ty);
+          head = (head + 1) % (D + 1);
+          --n_pend;
         }
         if (++s == S) { s = 0; ph ^= 1u; }
       }
     }
     for (int i = 0; i < n_pend; ++i) {
-      const Pending q = pend[(head + i) % D];
-      issue_halo(tm, st[q.s], &full[q.s], q.x0, q.y0, q.k, p.ty);
+      const Pending q = pend[(head + i) % (D + 1)];
+      if (!p.halo_off) issue_halo(tm, st[q.s], &full[q.s], q.x0, q.y0, q.k, p.ty);
+    }
+  }
+
+  // Pacer warp (lane 0): polls the neighbour tiles' progress flags (planes
+  // their consumers have finished; published by consumer warp 0 -- a store
+  // from the producer thread would queue behind its bulk copies) and grants
+  // the producer planes up to (slowest neighbour + W).  Kept off the producer
+  // thread: a global load there would wait behind its outstanding bulk copies.
+  // Bounded: after sync_spin polls without a change it grants everything.
+  static __device__ void pace(const TmaParams<T>& p, volatile int* permit) {
+    const int tile = blockIdx.x;
+    const int nplanes = int(p.kend - p.kbeg);
+    const int tcol = tile % p.tiles_x;
+    int nb[4], n_nb = 0;
+    if (tcol > 0) nb[n_nb++] = tile - 1;
+    if (tcol + 1 < p.tiles_x && tile + 1 < p.n_tiles) nb[n_nb++] = tile + 1;
+    if (tile >= p.tiles_x) nb[n_nb++] = tile - p.tiles_x;
+    if (tile + p.tiles_x < p.n_tiles) nb[n_nb++] = tile + p.tiles_x;
+    int granted = p.sync_w + 1, idle = 0;
+    *permit = granted;
+    while (granted < nplanes) {
+      unsigned long long f[4];
+      // weak L2-only loads (ld.global.cg): a .gpu-scope strong load here measurably
+      // stalls the SM's memory pipeline (sweep in DESIGN.md); L2 is the coherence point
+      for (int q = 0; q < 4; ++q) f[q] = q < n_nb ? __ldcg(p.progress + size_t(nb[q]) * kFlagStride) : 0ull;
+      int lo = nplanes;
+      for (int q = 0; q < n_nb; ++q) {
+        const int c = (f[q] >> 32) == (p.epoch & 0xffffffffull) ? int(f[q] & 0xffffffffull) : 0;
+        lo = min(lo, c);
+      }
+      const int g = min(nplanes, lo + p.sync_w + 1);
+      if (g > granted) { granted = g; *permit = granted; idle = 0; }
+      else if (++idle >= p.sync_spin) { granted = nplanes; *permit = granted; }
+      __nanosleep(p.sync_sleep);
     }
   }
 
@@ -202,6 +270,7 @@ struct K2Tma {
     const bool validate = p.err != nullptr;
     const bool t_zero = (p.theta == T(0));
     const bool top = ty == 0, bot = ty == p.ty - 1;
+    const bool sync = p.progress != nullptr && p.n_tiles <= int(gridDim.x);
     int errbits = 0;
     int s = 0;
     uint32_t ph = 0;
@@ -211,10 +280,33 @@ struct K2Tma {
       const int xi = x0 + cx0;
       const bool act = xi < p.nx && j < p.ny;
       const int64_t off2d = int64_t(j) * p.nx + xi;
-      const bool xin = xi > 0 && xi + VEC < p.nx;   // no x-boundary point in this lane
-      const bool yin = j > 0 && j < p.ny - 1;
+      // Boundary handling is folded into ONE branch-free path (no divergent
+      // slow path): the one-sided rule of stencils.py:46-51 is "lo or hi is the
+      // point itself, c = 1/h".  With nx % VEC == 0 only element 0 of the lane
+      // holding x = 0 and element VEC-1 of the lane holding x = nx-1 can be x
+      // boundaries: they get their own coefficient and the shuffled neighbour
+      // is replaced by the point itself.  Row / plane boundaries are
+      // warp- / plane-uniform: the neighbour row / plane is replaced the same way.
+      const bool x_lo_edge = xi == 0, x_hi_edge = xi + VEC == p.nx;
+      const T cx_first = x_lo_edge ? p.cx_bd : p.cx_in;
+      const T cx_last = x_hi_edge ? p.cx_bd : p.cx_in;
       const bool jlo = j == 0, jhi = j == p.ny - 1;
       const T cy = (jlo || jhi) ? p.cy_bd : p.cy_in;
+      // byte offsets (within a stage) of this lane's v / s_v rows below and above
+      const char* const sb0 = reinterpret_cast<const char*>(&st[0]);
+      const uint32_t off_own = uint32_t(reinterpret_cast<const char*>(&st[0].v[ty][cx0]) - sb0);
+      const uint32_t off_vlo = jlo ? off_own
+                               : top ? uint32_t(reinterpret_cast<const char*>(&st[0].v_top[cx0]) - sb0)
+                                     : off_own - uint32_t(sizeof(T) * TX);
+      const uint32_t off_vhi = jhi ? off_own
+                               : bot ? uint32_t(reinterpret_cast<const char*>(&st[0].v_bot[cx0]) - sb0)
+                                     : off_own + uint32_t(sizeof(T) * TX);
+      const uint32_t d_sv = uint32_t(reinterpret_cast<const char*>(&st[0].sv[0][0]) -
+                                     reinterpret_cast<const char*>(&st[0].v[0][0]));
+      const uint32_t d_svhalo = uint32_t(reinterpret_cast<const char*>(&st[0].sv_top[0]) -
+                                         reinterpret_cast<const char*>(&st[0].v_top[0]));
+      const uint32_t off_svlo = (!jlo && top) ? off_vlo + d_svhalo : off_vlo + d_sv;
+      const uint32_t off_svhi = (!jhi && bot) ? off_vhi + d_svhalo : off_vhi + d_sv;
       V wm, w0, swm, sw0;
       load_w(p, p.kbeg - 1, off2d, act, wm, swm);
       load_w(p, p.kbeg, off2d, act, w0, sw0);
@@ -222,10 +314,11 @@ struct K2Tma {
       for (int64_t k = p.kbeg; k < p.kend; ++k, o += plane) {
         mbar_wait(&full[s], ph);
         const Stage& S_ = st[s];
+        const char* sb = reinterpret_cast<const char*>(&S_);
         const V u_own = lds(&S_.u[ty][cx0]);
-        const V v_own = lds(&S_.v[ty][cx0]);
-        const V v_lo = top ? lds(&S_.v_top[cx0]) : lds(&S_.v[ty > 0 ? ty - 1 : 0][cx0]);
-        const V v_hi = bot ? lds(&S_.v_bot[cx0]) : lds(&S_.v[ty + 1][cx0]);
+        const V v_own = validate ? lds(&S_.v[ty][cx0]) : zero();   // validation only
+        const V v_lo = lds(reinterpret_cast<const T*>(sb + off_vlo));
+        const V v_hi = lds(reinterpret_cast<const T*>(sb + off_vhi));
         V wp = lds(&S_.w[ty][cx0]);
         T u_l = __shfl_up_sync(0xffffffffu, u_own.v[VEC - 1], 1);
         T u_r = __shfl_down_sync(0xffffffffu, u_own.v[0], 1);
@@ -235,9 +328,9 @@ struct K2Tma {
         T s_l = T(0), s_r = T(0);
         if constexpr (HAS_SIGMA) {
           su_own = lds(&S_.su[ty][cx0]);
-          sv_own = lds(&S_.sv[ty][cx0]);
-          sv_lo = top ? lds(&S_.sv_top[cx0]) : lds(&S_.sv[ty > 0 ? ty - 1 : 0][cx0]);
-          sv_hi = bot ? lds(&S_.sv_bot[cx0]) : lds(&S_.sv[ty + 1][cx0]);
+          if (validate) sv_own = lds(&S_.sv[ty][cx0]);
+          sv_lo = lds(reinterpret_cast<const T*>(sb + off_svlo));
+          sv_hi = lds(reinterpret_cast<const T*>(sb + off_svhi));
           swp = lds(&S_.sw[ty][cx0]);
           s_l = __shfl_up_sync(0xffffffffu, su_own.v[VEC - 1], 1);
           s_r = __shfl_down_sync(0xffffffffu, su_own.v[0], 1);
@@ -246,43 +339,42 @@ struct K2Tma {
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);   // stage consumed: the producer may refill it
+        if (ty == 0 && lane == 0 && sync)        // publish progress (planes consumed) for the pacers
+          st_relaxed_u64(p.progress + size_t(tile) * kFlagStride,
+                         ((p.epoch & 0xffffffffull) << 32) | (unsigned long long)(k - p.kbeg + 1));
         if (++s == S) { s = 0; ph ^= 1u; }
         if (k + 1 == p.nzl) load_w(p, k + 1, off2d, act, wp, swp);  // past the slab: halo or none
 
-        if (act) {
+        if (act && p.diag_null) {   // diagnostics: pipeline + stores only, no math
+          V z;
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) z.v[e] = u_own.v[e] + v_lo.v[e] + wp.v[e] + su_own.v[e];
+          st_stream<T, VEC>(p.out_mu + o, z);
+          st_stream<T, VEC>(p.out_sigma + o, z);
+          st_stream<T, VEC>(p.out_psrc + o, z);
+          st_stream<T, VEC>(p.out_psnk + o, z);
+        } else if (act) {
           const int64_t kg = p.z0 + k;
           const bool klo = kg == 0, khi = kg == p.nzg - 1;
+          const T cz = (klo || khi) ? p.cz_bd : p.cz_in;
+          // one-sided substitutions (lane / plane uniform)
+          if (x_lo_edge) { u_l = u_own.v[0]; s_l = su_own.v[0]; }
+          if (x_hi_edge) { u_r = u_own.v[VEC - 1]; s_r = su_own.v[VEC - 1]; }
+          const V& wl = klo ? w0 : wm;
+          const V& wh = khi ? w0 : wp;
+          const V& swl = klo ? sw0 : swm;
+          const V& swh = khi ? sw0 : swp;
           V omu, osg, ops, opk;
-          if (xin && yin && !klo && !khi) {
-            // interior fast path: central differences on every axis
 #pragma unroll
-            for (int e = 0; e < VEC; ++e) {
-              const T ul = e == 0 ? u_l : u_own.v[e == 0 ? 0 : e - 1];
-              const T uh = e == VEC - 1 ? u_r : u_own.v[e == VEC - 1 ? 0 : e + 1];
-              const T sl = e == 0 ? s_l : su_own.v[e == 0 ? 0 : e - 1];
-              const T sh = e == VEC - 1 ? s_r : su_own.v[e == VEC - 1 ? 0 : e + 1];
-              point<false>(p, ul, uh, v_lo.v[e], v_hi.v[e], wm.v[e], wp.v[e], sl, sh, sv_lo.v[e],
-                           sv_hi.v[e], swm.v[e], swp.v[e], p.cx_in, p.cy_in, p.cz_in, t_zero,
-                           omu.v[e], osg.v[e], ops.v[e], opk.v[e]);
-            }
-          } else {
-            const T cz = (klo || khi) ? p.cz_bd : p.cz_in;
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) {
-              const int i = xi + e;
-              const bool ilo = i == 0, ihi = i == p.nx - 1;
-              const T cx = (ilo || ihi) ? p.cx_bd : p.cx_in;
-              const T uo = u_own.v[e], so = su_own.v[e];
-              const T ul = ilo ? uo : (e == 0 ? u_l : u_own.v[e == 0 ? 0 : e - 1]);
-              const T uh = ihi ? uo : (e == VEC - 1 ? u_r : u_own.v[e == VEC - 1 ? 0 : e + 1]);
-              const T sl = ilo ? so : (e == 0 ? s_l : su_own.v[e == 0 ? 0 : e - 1]);
-              const T sh = ihi ? so : (e == VEC - 1 ? s_r : su_own.v[e == VEC - 1 ? 0 : e + 1]);
-              point<true>(p, ul, uh, jlo ? v_own.v[e] : v_lo.v[e], jhi ? v_own.v[e] : v_hi.v[e],
-                          klo ? w0.v[e] : wm.v[e], khi ? w0.v[e] : wp.v[e], sl, sh,
-                          jlo ? sv_own.v[e] : sv_lo.v[e], jhi ? sv_own.v[e] : sv_hi.v[e],
-                          klo ? sw0.v[e] : swm.v[e], khi ? sw0.v[e] : swp.v[e], cx, cy, cz, t_zero,
-                          omu.v[e], osg.v[e], ops.v[e], opk.v[e]);
-            }
+          for (int e = 0; e < VEC; ++e) {
+            const T cx = e == 0 ? cx_first : (e == VEC - 1 ? cx_last : p.cx_in);
+            const T ul = e == 0 ? u_l : u_own.v[e == 0 ? 0 : e - 1];
+            const T uh = e == VEC - 1 ? u_r : u_own.v[e == VEC - 1 ? 0 : e + 1];
+            const T sl = e == 0 ? s_l : su_own.v[e == 0 ? 0 : e - 1];
+            const T sh = e == VEC - 1 ? s_r : su_own.v[e == VEC - 1 ? 0 : e + 1];
+            point<false>(p, ul, uh, v_lo.v[e], v_hi.v[e], wl.v[e], wh.v[e], sl, sh, sv_lo.v[e],
+                         sv_hi.v[e], swl.v[e], swh.v[e], cx, cy, cz, t_zero, omu.v[e], osg.v[e],
+                         ops.v[e], opk.v[e]);
           }
           if (validate) {
 #pragma unroll
@@ -326,8 +418,16 @@ k2_tma_kernel(const __grid_constant__ TmaMaps tm, const TmaParams<T> p) {
   }
   if (warp == C::TYMAX && (threadIdx.x & 31) < kNumMaps) tma_prefetch_desc(&tm.m[threadIdx.x & 31]);
   __syncthreads();
+  __shared__ int permit;
+  const bool sync = p.progress != nullptr && p.n_tiles <= int(gridDim.x);
+  if (threadIdx.x == 0) permit = sync ? 0 : 0x7fffffff;
+  __syncthreads();
   if (warp == C::TYMAX) {
-    if ((threadIdx.x & 31) == 0) K2Tma<T, HAS_SIGMA>::produce(p, tm, st, full, empty);
+    if ((threadIdx.x & 31) == 0) K2Tma<T, HAS_SIGMA>::produce(p, tm, st, full, empty, &permit);
+    return;
+  }
+  if (warp == C::TYMAX + 1) {
+    if ((threadIdx.x & 31) == 0 && sync) K2Tma<T, HAS_SIGMA>::pace(p, &permit);
     return;
   }
   if (warp >= p.ty) return;  // tile shorter than TYMAX: spare warps sit out

@@ -103,8 +103,32 @@ __device__ __forceinline__ void named_sync(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
+// bulk tensor prefetch of a 3D box into L2 (no shared memory, no barrier):
+// lets a streaming kernel keep more DRAM traffic in flight than its
+// shared-memory ring can hold
+__device__ __forceinline__ void tma_prefetch_l2_3d(const CUtensorMap* map, int x, int y, int z) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(z)
+               : "memory");
+}
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// ---- loose inter-CTA lockstep (neighbour progress flags) -------------------
+// A persistent CTA publishes (epoch << 32 | plane + 1) after issuing a plane's
+// main boxes; before running more than W planes ahead of a neighbour it polls
+// that neighbour's flag.  The wait is bounded (never a correctness
+// dependency: a CTA that is not co-resident only costs the timeout), and the
+// epoch tag makes a per-launch reset unnecessary.
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 }  // namespace divuq

@@ -18,13 +18,14 @@ for spec in os.environ.get("SWEEP", "DIVUQ_PHASE=0,1,2,4").split(";"):
 for combo in itertools.product(*knobs.values()):
     for k, v in zip(knobs, combo):
         os.environ[k] = v
-    for _ in range(3):
+    reps = 1 if os.environ.get("NCU") else 20
+    for _ in range(1 if reps == 1 else 3):
         dev.propagate3d(*f, n, n, n, out=out, check=False)
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
-    for _ in range(20):
+    for _ in range(reps):
         dev.propagate3d(*f, n, n, n, out=out, check=False)
     e.record()
     torch.cuda.synchronize()
-    ms = s.elapsed_time(e) / 20
+    ms = s.elapsed_time(e) / reps
     print(dict(zip(knobs, combo)), f"{ms:.3f} ms  {40 * n**3 / ms / 1e6:.0f} GB/s", flush=True)
