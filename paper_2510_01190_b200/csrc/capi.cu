@@ -190,6 +190,28 @@ bool make_map3d(CUtensorMap* m, const T* base, int64_t nx, int64_t ny, int64_t n
             CU_TENSOR_MAP_SWIZZLE_NONE, l2, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Per-device progress flags for the loose inter-CTA lockstep of the TMA
+// kernels (k2tma.cuh / k3tma.cuh): allocated once, never reset -- every launch
+// gets a fresh epoch tag, so stale flags from earlier launches are ignored.
+constexpr int kMaxFlagTiles = 4096;
+cudaError_t progress_flags(unsigned long long** flags_out, unsigned long long* epoch_out) {
+  static unsigned long long* flags[64] = {};
+  static unsigned long long epoch = 0;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  if (dev >= 64) { *flags_out = nullptr; return cudaSuccess; }
+  if (!flags[dev]) {
+    const size_t bytes = size_t(kMaxFlagTiles) * kFlagStride * sizeof(unsigned long long);
+    if (cudaError_t e = cudaMalloc(&flags[dev], bytes)) return e;
+    if (cudaError_t e = cudaMemset(flags[dev], 0, bytes)) return e;
+  }
+  *flags_out = flags[dev];
+  *epoch_out = ++epoch;
+  return cudaSuccess;
+}
+
 template <typename T, bool HAS_SIGMA>
 int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
   using C = TmaCfg<T>;
@@ -243,21 +265,8 @@ int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
   p.diag_null = HAS_SIGMA && sp.out_mu && sp.out_sigma && sp.out_psrc && sp.out_psnk
                     ? int(env_int("DIVUQ_K2_NULL", 0)) : 0;   // diagnostics only
   p.progress = nullptr;
-  if (p.sync_w > 0 && p.n_tiles <= 4096) {
-    static unsigned long long* flags[64] = {};        // per device, allocated once, never reset
-    static unsigned long long epoch = 0;
-    int dev = 0;
-    DIVUQ_CUDA(cudaGetDevice(&dev));
-    if (dev < 64) {
-      if (!flags[dev]) {
-        const size_t bytes = 4096 * kFlagStride * sizeof(unsigned long long);
-        DIVUQ_CUDA(cudaMalloc(&flags[dev], bytes));
-        DIVUQ_CUDA(cudaMemset(flags[dev], 0, bytes));
-      }
-      p.progress = flags[dev];
-      p.epoch = ++epoch;
-    }
-  }
+  if (p.sync_w > 0 && p.n_tiles <= kMaxFlagTiles)
+    DIVUQ_CUDA(progress_flags(&p.progress, &p.epoch));
   p.stage_bytes = uint32_t((3 * ty * C::TX + (p.halo_off ? 0 : 2 * ty * C::PAD + 2 * C::TX)) *
                            sizeof(T)) * (HAS_SIGMA ? 2u : 1u);
   const int64_t n_work = int64_t(p.n_tiles) * (sp.kend - sp.kbeg);
@@ -337,10 +346,17 @@ int try_k3_tma(const StencilParams<float>& sp, int comps, cudaStream_t s, bool* 
   p.n_tiles = int(tiles_x * ((sp.ny + ty - 1) / ty));
   p.M = int(sp.n_members);
   p.has_w = comps == 3;
-  // 3D: halo boxes trail D items so the neighbour CTA (lockstep z-march) has
-  // pulled them into L2; 2D tiles are short, and a trailing halo only delays
-  // the stage it completes
-  p.hdelay = int(std::max<int64_t>(0, std::min<int64_t>(C::D, env_int("DIVUQ_K3_HDELAY", comps == 3 ? C::D : 0))));
+  // halo boxes go out with their main box (hdelay 0): a trailing halo delays
+  // the stage it completes, and the 5-stage ring's depth is worth more than
+  // the neighbour's L2 lines (measured: config-4 slab 5.11 ms at hdelay 3,
+  // 4.26 ms at 0 -- DRAM reads stay within 1 % of algorithmic either way)
+  p.hdelay = int(std::max<int64_t>(0, std::min<int64_t>(C::D, env_int("DIVUQ_K3_HDELAY", 0))));
+  p.sync_w = int(env_int("DIVUQ_K3_SYNC_W", 0));   // lockstep off: no gain measured for K3
+  p.sync_spin = int(env_int("DIVUQ_K3_SYNC_SPIN", 256));
+  p.sync_sleep = int(env_int("DIVUQ_K3_SYNC_SLEEP", 500));
+  p.progress = nullptr;
+  if (p.sync_w > 0 && p.n_tiles <= kMaxFlagTiles && p.has_w)
+    DIVUQ_CUDA(progress_flags(&p.progress, &p.epoch));
   p.bytes_u = uint32_t((C::TX * ty + 2 * C::PAD * ty) * 4 * C::MB);
   p.bytes_v = uint32_t((C::TX * ty + 2 * C::TX) * 4 * C::MB);
   p.bytes_w = uint32_t(C::TX * ty * 4 * C::MB);

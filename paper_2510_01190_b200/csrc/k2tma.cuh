@@ -74,11 +74,6 @@ struct TmaMaps {
   CUtensorMap m[kNumMaps];
 };
 
-// progress flags sit 512 B apart so they hash to different L2 slices: all
-// pacers polling a handful of lines would turn those slices into hot spots
-// that stall everyone's DRAM traffic
-constexpr size_t kFlagStride = 64;
-
 template <typename T>
 struct TmaParams {
   const T* mu_w; const T* s_w;                      // for the z-march restarts

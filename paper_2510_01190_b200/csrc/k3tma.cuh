@@ -84,6 +84,9 @@ struct K3Params {
   int nx, ny, ty, tiles_x, n_tiles, M;
   int has_w;                                             // 0: 2D ensemble (u, v only)
   int hdelay;                                            // halo boxes trail by this many items (<= D)
+  unsigned long long* progress;                          // per-tile progress flags (nullptr: no lockstep)
+  unsigned long long epoch;                              // launch tag in the flags' high word
+  int sync_w, sync_spin, sync_sleep;                     // window (planes), bounded polls, ns per poll
   uint32_t bytes_u, bytes_v, bytes_w;
   float cx_in, cx_bd, cy_in, cy_bd, cz_in, cz_bd;
   float theta;
@@ -150,7 +153,30 @@ struct K3 {
           for (int b = 0; b < nb; ++b) item(kW, x0, y0, kb - 1, b);
         for (int b = 0; b < nb; ++b) item(kW, x0, y0, kb, b);
       }
+      // loose inter-CTA lockstep (as K2): before plane k, wait (bounded) until
+      // every neighbour tile has consumed plane k - W, so the delayed halo
+      // boxes find the neighbour's bytes in L2
+      const bool sync = p.progress != nullptr && p.n_tiles <= int(gridDim.x);
+      const int tcol = tile % p.tiles_x;
+      int nbr[4], n_nbr = 0;
+      if (tcol > 0) nbr[n_nbr++] = tile - 1;
+      if (tcol + 1 < p.tiles_x && tile + 1 < p.n_tiles) nbr[n_nbr++] = tile + 1;
+      if (tile >= p.tiles_x) nbr[n_nbr++] = tile - p.tiles_x;
+      if (tile + p.tiles_x < p.n_tiles) nbr[n_nbr++] = tile + p.tiles_x;
+      int seen = -1;   // min consumed planes over the neighbours, as last observed
       for (int k = kb; k < int(p.kend); ++k) {
+        const int need = (k - kb) - p.sync_w;
+        for (int spin = 0; sync && seen < need && spin < p.sync_spin; ++spin) {
+          unsigned long long f[4];
+          for (int q = 0; q < 4; ++q)
+            f[q] = q < n_nbr ? __ldcg(p.progress + size_t(nbr[q]) * kFlagStride) : 0ull;
+          int lo = 1 << 30;
+          for (int q = 0; q < n_nbr; ++q)
+            lo = min(lo, (f[q] >> 32) == (p.epoch & 0xffffffffull) ? int(f[q] & 0xffffffffull) : 0);
+          seen = lo;
+          if (seen < need) __nanosleep(p.sync_sleep);
+        }
+        if (seen < need) seen = need;   // gave up (bounded): never a correctness dependency
         for (int b = 0; b < nb; ++b) item(kU, x0, y0, k, b);
         for (int b = 0; b < nb; ++b) item(kV, x0, y0, k, b);
         if (p.has_w && k + 1 < p.nzl)
@@ -404,6 +430,9 @@ struct K3 {
             if (p.has_w) st_stream<float, 4>(p.out_mom_sigma + 2 * nl + o, w0_sg);
           }
         }
+        if (ty == 0 && lane == 0 && p.progress != nullptr && p.n_tiles <= int(gridDim.x))
+          st_relaxed_u64(p.progress + size_t(tile) * kFlagStride,   // planes consumed, for the pacing
+                         ((p.epoch & 0xffffffffull) << 32) | (unsigned long long)(k - kb + 1));
         xb.wm[ty][0][lane] = w0_mu;  // plane k becomes k-1 (own slot: no sync needed)
         xb.wm[ty][1][lane] = w0_sg;
         w0_mu = wp_mu; w0_sg = wp_sg;

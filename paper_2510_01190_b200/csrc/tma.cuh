@@ -122,6 +122,11 @@ __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
 // that neighbour's flag.  The wait is bounded (never a correctness
 // dependency: a CTA that is not co-resident only costs the timeout), and the
 // epoch tag makes a per-launch reset unnecessary.
+// progress flags sit 512 B apart so they hash to different L2 slices: all
+// pacers polling a handful of lines would turn those slices into hot spots
+// that stall everyone's DRAM traffic
+constexpr size_t kFlagStride = 64;   // in u64 elements
+
 __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
