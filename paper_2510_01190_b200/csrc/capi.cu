@@ -553,7 +553,9 @@ int launch_gradient(const T* in, int64_t members, int64_t in_mstride, int64_t nx
   if (int r = grid_ok(nx, ny, dx, dy)) return r;
   if (!in || !out || members < 1) return DIVUQ_EINVAL;
   const dim3 grid(unsigned((nx + kGrTX - 1) / kGrTX), unsigned((ny + kGrTY - 1) / kGrTY),
-                  unsigned(std::min<int64_t>(members, 65535)));
+                  unsigned(std::max<int64_t>(1, std::min<int64_t>(
+                      (members + env_int("DIVUQ_GR_MPC", kGrMembersPerCta) - 1) /
+                          std::max<int64_t>(1, env_int("DIVUQ_GR_MPC", kGrMembersPerCta)), 65535))));
   if ((nx + kGrTX - 1) / kGrTX > INT32_MAX || (ny + kGrTY - 1) / kGrTY > 65535) return DIVUQ_EGRID;
   const T cxi = T(1.0 / (2.0 * dx)), cxb = T(1.0 / dx), cyi = T(1.0 / (2.0 * dy)), cyb = T(1.0 / dy);
   cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -32,16 +32,19 @@ __global__ void vmag_kernel(const T* __restrict__ u, const T* __restrict__ v, in
 }
 
 // gradient of a scalar field, or (MAG) of |(u, v)| computed on the fly.
-// A CTA of 32 x 8 threads owns a 64 x 16 tile of one member (2 x 2 points per
-// thread): it loads the tile plus a one-point halo with all of a thread's
-// loads in flight at once (coalesced row segments; halo re-reads, 16 %, hit
-// L2), evaluates the field (the magnitude, for MAG) ONCE per loaded point into
-// shared memory, then every thread forms its points' one-axis differences.
+// A CTA of 32 x 8 threads owns a 64 x 16 tile (2 x 2 points per thread) and
+// walks several members of it: every index (the clamped tile + one-point halo
+// load offsets, the output offsets, coefficients and neighbour slots) is
+// member-invariant and computed once, so the member loop is loads, one
+// magnitude per loaded point into shared memory (halo re-reads, 16 %, hit
+// L2), then the one-axis differences and two stores per point.
 // planes: `members` blocks of (u[, v]) with stride in_mstride; outputs
 // (gx, gy) per member.
 constexpr int kGrTX = 64, kGrTY = 16, kGrBX = 32, kGrBY = 8;
 constexpr int kGrV = (kGrTX + 2) * (kGrTY + 2);
 constexpr int kGrNQ = (kGrV + kGrBX * kGrBY - 1) / (kGrBX * kGrBY);
+constexpr int kGrPY = kGrTY / kGrBY, kGrPX = kGrTX / kGrBX;   // points per thread
+constexpr int64_t kGrMembersPerCta = 4;                         // members a CTA walks
 
 template <typename T, bool MAG>
 __global__ void __launch_bounds__(kGrBX * kGrBY, 3)
@@ -50,58 +53,67 @@ gradient2d_kernel(const T* __restrict__ in, int64_t members, int64_t in_mstride,
                   int64_t out_mstride, int* err) {
   using A = Arith<T>;
   __shared__ T f[kGrTY + 2][kGrTX + 2];
+  T* const fl = &f[0][0];
   const int64_t n = nx * ny;
   const int tid = threadIdx.y * kGrBX + threadIdx.x;
   const int64_t i0 = int64_t(blockIdx.x) * kGrTX, j0 = int64_t(blockIdx.y) * kGrTY;
+  // (tile + halo) load slots with clamped coordinates: a clamped slot is only
+  // read as the one-sided boundary neighbour, which IS the clamped point
+  int64_t ld_off[kGrNQ];
+  bool ld_st[kGrNQ];
+#pragma unroll
+  for (int k = 0; k < kGrNQ; ++k) {
+    const int q = min(tid + k * kGrBX * kGrBY, kGrV - 1);
+    const int qy = q / (kGrTX + 2), qx = q - qy * (kGrTX + 2);
+    const int64_t gi = min(max(i0 + qx - 1, int64_t(0)), nx - 1);
+    const int64_t gj = min(max(j0 + qy - 1, int64_t(0)), ny - 1);
+    ld_off[k] = gj * nx + gi;
+    ld_st[k] = tid + k * kGrBX * kGrBY < kGrV;
+  }
+  // this thread's points: output offset (-1: outside), coefficients, slots
+  int64_t o_off[kGrPY * kGrPX];
+  T o_cx[kGrPY * kGrPX], o_cy[kGrPY * kGrPX];
+  int o_xh[kGrPY * kGrPX], o_xl[kGrPY * kGrPX], o_yh[kGrPY * kGrPX], o_yl[kGrPY * kGrPX];
+#pragma unroll
+  for (int py = 0; py < kGrPY; ++py)
+#pragma unroll
+    for (int px = 0; px < kGrPX; ++px) {
+      const int e = py * kGrPX + px;
+      const int64_t i = i0 + threadIdx.x + px * kGrBX, j = j0 + threadIdx.y + py * kGrBY;
+      const int x = threadIdx.x + px * kGrBX + 1, y = threadIdx.y + py * kGrBY + 1;
+      const bool bx = i == 0 || i == nx - 1, by = j == 0 || j == ny - 1;
+      o_off[e] = (i < nx && j < ny) ? j * nx + i : -1;
+      o_cx[e] = bx ? cx_bd : cx_in;
+      o_cy[e] = by ? cy_bd : cy_in;
+      const int w = kGrTX + 2;
+      o_xh[e] = y * w + (i < nx - 1 ? x + 1 : x);
+      o_xl[e] = y * w + (i > 0 ? x - 1 : x);
+      o_yh[e] = (j < ny - 1 ? y + 1 : y) * w + x;
+      o_yl[e] = (j > 0 ? y - 1 : y) * w + x;
+    }
   int errbits = 0;
   for (int64_t m = blockIdx.z; m < members; m += gridDim.z) {
     const T* src = in + m * in_mstride;
-    // (tile + halo) with clamped coordinates: a clamped slot is only read as
-    // the one-sided boundary neighbour, which IS the clamped point
     T a[kGrNQ], b[kGrNQ];
 #pragma unroll
-    for (int k = 0; k < kGrNQ; ++k) {
-      const int q = min(tid + k * kGrBX * kGrBY, kGrV - 1);
-      const int qy = q / (kGrTX + 2), qx = q % (kGrTX + 2);
-      const int64_t gi = min(max(i0 + qx - 1, int64_t(0)), nx - 1);
-      const int64_t gj = min(max(j0 + qy - 1, int64_t(0)), ny - 1);
-      const int64_t p = gj * nx + gi;
-      a[k] = src[p];
-      if constexpr (MAG) b[k] = src[n + p];
+    for (int k = 0; k < kGrNQ; ++k) {   // all of a thread's loads in flight at once
+      a[k] = src[ld_off[k]];
+      if constexpr (MAG) b[k] = src[n + ld_off[k]];
     }
 #pragma unroll
     for (int k = 0; k < kGrNQ; ++k) {
-      const int q = tid + k * kGrBX * kGrBY;
-      if (q < kGrV) {
-        if constexpr (MAG) f[q / (kGrTX + 2)][q % (kGrTX + 2)] = hypot_(a[k], b[k]);
-        else f[q / (kGrTX + 2)][q % (kGrTX + 2)] = a[k];
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int ry = 0; ry < kGrTY; ry += kGrBY) {
-#pragma unroll
-      for (int rx = 0; rx < kGrTX; rx += kGrBX) {
-        const int64_t i = i0 + threadIdx.x + rx, j = j0 + threadIdx.y + ry;
-        if (i < nx && j < ny) {
-          const int x = threadIdx.x + rx + 1, y = threadIdx.y + ry + 1;
-          const bool bx = i == 0 || i == nx - 1, by = j == 0 || j == ny - 1;
-          const T cx = bx ? cx_bd : cx_in, cy = by ? cy_bd : cy_in;
-          const int xh = i < nx - 1 ? x + 1 : x, xl = i > 0 ? x - 1 : x;
-          const int yh = j < ny - 1 ? y + 1 : y, yl = j > 0 ? y - 1 : y;
-          const T gx = A::sub(A::mul(f[y][xh], cx), A::mul(f[y][xl], cx));
-          const T gy = A::sub(A::mul(f[yh][x], cy), A::mul(f[yl][x], cy));
-          const int64_t p = j * nx + i;
-          out[m * out_mstride + p] = gx;
-          out[m * out_mstride + n + p] = gy;
-        }
-      }
-    }
-    // validation word: every loaded interior slot is some point's own value
-#pragma unroll
-    for (int k = 0; k < kGrNQ; ++k) {
+      if (ld_st[k]) fl[tid + k * kGrBX * kGrBY] = MAG ? hypot_(a[k], b[k]) : a[k];
       errbits |= check_value(a[k]);
       if constexpr (MAG) errbits |= check_value(b[k]);
+    }
+    __syncthreads();
+    T* dst = out + m * out_mstride;
+#pragma unroll
+    for (int e = 0; e < kGrPY * kGrPX; ++e) {
+      if (o_off[e] < 0) continue;
+      // stencils.py:87-96: f[hi]*c - f[lo]*c per axis, each product rounded
+      dst[o_off[e]] = A::sub(A::mul(fl[o_xh[e]], o_cx[e]), A::mul(fl[o_xl[e]], o_cx[e]));
+      dst[n + o_off[e]] = A::sub(A::mul(fl[o_yh[e]], o_cy[e]), A::mul(fl[o_yl[e]], o_cy[e]));
     }
     __syncthreads();
   }
