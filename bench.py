@@ -394,6 +394,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--planes-per-gpu", type=int, default=128, help="config 4 slab depth")
+    ap.add_argument("--exchange", default="p2p", choices=("p2p", "nccl"),
+                    help="z-slab halo exchange for configs 3/4 at N>1: peer memory read in "
+                         "place by the kernels (p2p) or NCCL send/recv overlapped with the interior")
     ap.add_argument("--workload", default=None, choices=("lcp", "gradient", "ingest"),
                     help="a SURVEY 8f row instead of a BASELINE config (1 GPU, ours only)")
     args = ap.parse_args()
@@ -426,6 +429,7 @@ def main():
         dist.barrier()
     from paper_2510_01190_b200 import configs, device as dev
     from paper_2510_01190_b200._lib import lib
+    from paper_2510_01190_b200 import shard
     from paper_2510_01190_b200.shard import SlabStep
 
     cfg = configs.CONFIGS[args.config]
@@ -439,7 +443,7 @@ def main():
 
     if args.config == 3:
         nx, ny, nz = cfg.nx, cfg.ny, cfg.nz
-        step = SlabStep(nx, ny, nz, rank, world, device="cuda")
+        step = SlabStep(nx, ny, nz, rank, world, device="cuda", exchange=args.exchange)
         fields = configs.config3_slab(step.z0, step.nzl, nx, ny, nz, seed=cfg.seed)
         n_local = nx * ny * step.nzl
         out = {k: torch.empty(n_local, dtype=torch.float32, device="cuda") for k in dev.ALL_OUTPUTS}
@@ -462,6 +466,12 @@ def main():
             return 1
 
         def one_step(timed):
+            if step.exchange == "p2p" and world > 1:   # one launch, halos read over NVLink
+                e0 = ev() if timed else None
+                n = shard.propagate3d_step(step, fields, out, 1.0, 1.0, 1.0, cfg.t)
+                if timed:
+                    kernel_events.append((e0, ev(), step.nzl * plane))
+                return n
             return step.run(edges, lambda kr, lo, hi: compute(kr, lo, hi, timed))
 
         bpp = cfg.bytes_per_point
@@ -470,7 +480,7 @@ def main():
     elif args.config == 4:
         nx, ny = cfg.nx, cfg.ny
         nz = args.planes_per_gpu * world
-        step = SlabStep(nx, ny, nz, rank, world, device="cuda")
+        step = SlabStep(nx, ny, nz, rank, world, device="cuda", exchange=args.exchange)
         members = configs.config4_slab(step.z0, step.nzl, nx, ny, nz, cfg.members, cfg.seed)
         n_local = nx * ny * step.nzl
         out = {k: torch.empty(n_local, dtype=torch.float32, device="cuda") for k in dev.ALL_OUTPUTS}
@@ -493,8 +503,14 @@ def main():
             return 1
 
         def one_step(timed):
+            if step.exchange == "p2p" and world > 1:   # neighbours' edge moments read over NVLink
+                e0 = ev() if timed else None           # (whole step timed: conservative roofline)
+                n = shard.ensemble3d_step(step, members, out, 1.0, 1.0, 1.0, cfg.t)
+                if timed:
+                    kernel_events.append((e0, ev(), step.nzl * nx * ny))
+                return n
             n = step.run(edges, lambda kr, lo, hi: compute(kr, lo, hi, timed))
-            return n + (4 if world > 1 else 0)
+            return n + (2 if world > 1 else 0)
 
         bpp = cfg.bytes_per_point
         workload = (f"config4 slab: fused ensemble (M=16) -> moments -> divergence -> P(div>0.1), "
@@ -566,6 +582,8 @@ def main():
 
     # correctness guard on the real inputs before timing (validation word)
     torch.cuda.synchronize()
+    if world > 1:   # every slab is written before any peer reads it in place (p2p)
+        dist.barrier()
 
     for _ in range(args.warmup):
         one_step(False)
@@ -725,6 +743,9 @@ def main():
         "data": "synthetic (seeded generator, BASELINE.json config recipe)",
         "config": {"workload": workload, "grid_points": total_pts, "t": cfg.t,
                    "parallelism": f"z-slab x{world}" if args.config in (3, 4) else f"replicas x{world}",
+                   "exchange": (("peer memory (CUDA IPC over NVLink), read in place by the kernels"
+                                 if args.exchange == "p2p" else "NCCL send/recv overlapped with the interior")
+                                if args.config in (3, 4) and world > 1 else None),
                    "l2": (L2Flush.NOTE if args.config in (0, 1) else
                           "inputs larger than L2 (126 MB); no flush" if args.config in (3, 4) else
                           "compute-bound; 2 MB model stays in L2")},

@@ -295,6 +295,22 @@ int divuq_host_mc_divergence2d_f64(const double* mu_u, const double* mu_v,
                                    int64_t n_samples, uint64_t seed,
                                    double* out_mean, double* out_std, int device);
 
+/* K1 on a member-strided view: member m's N values start at members + m*member_stride
+ * (e.g. the w plane of a z-slab: stride 3*n_local) -- the reduced halo a slab
+ * neighbour needs, read in place (also through peer memory). */
+int divuq_fit_gaussian_strided_f32(const float* members, int64_t n_members, int64_t member_stride,
+                                   int64_t n_points, float* out_mu, float* out_sigma,
+                                   int32_t* err_word, void* stream);
+
+/* Peer memory (CUDA IPC) for the z-slab exchange over NVLink: export the
+ * allocation holding `ptr` (handle: divuq_ipc_handle_bytes() bytes, plus the
+ * offset of ptr inside it); import maps a neighbour's export (peer access
+ * enabled lazily) and returns the mapping base (for close) and the pointer. */
+int64_t divuq_ipc_handle_bytes(void);
+int divuq_ipc_export(const void* ptr, void* handle_out, int64_t* offset_out);
+int divuq_ipc_import(const void* handle, int64_t offset, void** base_out, void** ptr_out);
+int divuq_ipc_close(void* base);
+
 /* host twins of the parity mode (mc.py:94-156) */
 int divuq_host_mc_divergence2d_ref_f64(const double* mu_u, const double* mu_v,
                                        const double* s_u, const double* s_v,

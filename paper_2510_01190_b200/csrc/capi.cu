@@ -423,7 +423,7 @@ int propagate3d(const T* mu_u, const T* mu_v, const T* mu_w, const T* s_u, const
 // ---- K1: per-point moments over members, all components ----------------
 template <typename T, int VEC, int MR>
 __global__ void __launch_bounds__(256) fit_kernel(const T* __restrict__ members, int64_t M, int64_t C,
-                                                  int64_t N, T* __restrict__ out_mu,
+                                                  int64_t N, int64_t mstride, T* __restrict__ out_mu,
                                                   T* __restrict__ out_sigma, int* err) {
   const int64_t groups = N / VEC;
   int errbits = 0;
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(256) fit_kernel(const T* __restrict__ members,
        g += int64_t(gridDim.x) * blockDim.x) {
     for (int64_t c = 0; c < C; ++c) {
       Vec<T, VEC> mu, sg;
-      member_moments<T, VEC, MR>(members + c * N + g * VEC, C * N, int(M), mu, sg, errbits);
+      member_moments<T, VEC, MR>(members + c * N + g * VEC, mstride, int(M), mu, sg, errbits);
       st_stream<T, VEC>(out_mu + c * N + g * VEC, mu);
       st_stream<T, VEC>(out_sigma + c * N + g * VEC, sg);
     }
@@ -440,35 +440,39 @@ __global__ void __launch_bounds__(256) fit_kernel(const T* __restrict__ members,
 }
 
 template <typename T, int VEC, int MR>
-int launch_fit(const T* m, int64_t M, int64_t C, int64_t N, T* mu, T* sg, int32_t* err, cudaStream_t s) {
+int launch_fit(const T* m, int64_t M, int64_t C, int64_t N, int64_t ms, T* mu, T* sg, int32_t* err,
+               cudaStream_t s) {
   auto kern = fit_kernel<T, VEC, MR>;
   const int64_t groups = N / VEC;
   const int64_t cap = int64_t(blocks_per_sm(kern, 256, 0)) * sm_count();
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((groups + 255) / 256, cap));
-  kern<<<unsigned(grid), 256, 0, s>>>(m, M, C, N, mu, sg, err);
+  kern<<<unsigned(grid), 256, 0, s>>>(m, M, C, N, ms, mu, sg, err);
   return int(cudaGetLastError());
 }
 
 template <typename T, int VEC>
-int fit_mr(const T* m, int64_t M, int64_t C, int64_t N, T* mu, T* sg, int32_t* err, cudaStream_t s) {
-  if (M <= 8) return launch_fit<T, VEC, 8>(m, M, C, N, mu, sg, err, s);
-  if (M <= 16) return launch_fit<T, VEC, 16>(m, M, C, N, mu, sg, err, s);
-  if (M <= 24) return launch_fit<T, VEC, 24>(m, M, C, N, mu, sg, err, s);
-  return launch_fit<T, VEC, 32>(m, M, C, N, mu, sg, err, s);
+int fit_mr(const T* m, int64_t M, int64_t C, int64_t N, int64_t ms, T* mu, T* sg, int32_t* err,
+           cudaStream_t s) {
+  if (M <= 8) return launch_fit<T, VEC, 8>(m, M, C, N, ms, mu, sg, err, s);
+  if (M <= 16) return launch_fit<T, VEC, 16>(m, M, C, N, ms, mu, sg, err, s);
+  if (M <= 24) return launch_fit<T, VEC, 24>(m, M, C, N, ms, mu, sg, err, s);
+  return launch_fit<T, VEC, 32>(m, M, C, N, ms, mu, sg, err, s);
 }
 
 template <typename T>
 int fit_gaussian(const T* members, int64_t M, int64_t C, int64_t N, T* out_mu, T* out_sigma,
-                 int32_t* err, void* stream) {
+                 int32_t* err, void* stream, int64_t mstride = -1) {
   if (!members || !out_mu || !out_sigma || C < 1 || N < 1) return DIVUQ_EINVAL;
   if (M < 2) return DIVUQ_EMEMBERS;
+  if (mstride < 0) mstride = C * N;
+  if (mstride < C * N) return DIVUQ_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   constexpr int VW = (sizeof(T) == 4) ? 4 : 2;
   // wide vectors only while the M register-resident values stay small
-  const bool vec = M <= 16 && (N % VW) == 0 && aligned(members, 16) && aligned(out_mu, 16) &&
-                   aligned(out_sigma, 16);
-  if (vec) return fit_mr<T, VW>(members, M, C, N, out_mu, out_sigma, err, s);
-  return fit_mr<T, 1>(members, M, C, N, out_mu, out_sigma, err, s);
+  const bool vec = M <= 16 && (N % VW) == 0 && (mstride % VW) == 0 && aligned(members, 16) &&
+                   aligned(out_mu, 16) && aligned(out_sigma, 16);
+  if (vec) return fit_mr<T, VW>(members, M, C, N, mstride, out_mu, out_sigma, err, s);
+  return fit_mr<T, 1>(members, M, C, N, mstride, out_mu, out_sigma, err, s);
 }
 
 // ---- probability map on an existing Gaussian scalar field (lcp.py:48-68)
@@ -733,6 +737,57 @@ int divuq_fit_gaussian_f32(const float* members, int64_t M, int64_t C, int64_t N
                            float* out_sigma, int32_t* err, void* stream) {
   return fit_gaussian<float>(members, M, C, N, out_mu, out_sigma, err, stream);
 }
+
+int divuq_fit_gaussian_strided_f32(const float* members, int64_t M, int64_t member_stride,
+                                   int64_t N, float* out_mu, float* out_sigma, int32_t* err,
+                                   void* stream) {
+  return fit_gaussian<float>(members, M, 1, N, out_mu, out_sigma, err, stream, member_stride);
+}
+
+// ---- peer memory (CUDA IPC) for the z-slab exchange over NVLink ----------
+// A rank exports the allocation holding a tensor (handle + the tensor's offset
+// in it); a neighbour imports it and its kernels read the halo planes straight
+// from the owner's HBM -- no separate exchange step.
+using GetAddressRangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+int divuq_ipc_export(const void* ptr, void* handle_out, int64_t* offset_out) {
+  if (!ptr || !handle_out || !offset_out) return DIVUQ_EINVAL;
+  static GetAddressRangeFn range = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<GetAddressRangeFn>(p);
+  }();
+  if (!range) return int(cudaErrorNotSupported);
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS) return int(cudaErrorInvalidValue);
+  cudaIpcMemHandle_t h;
+  DIVUQ_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+  std::memcpy(handle_out, &h, sizeof(h));
+  *offset_out = int64_t(reinterpret_cast<CUdeviceptr>(ptr) - base);
+  return DIVUQ_OK;
+}
+
+int divuq_ipc_import(const void* handle, int64_t offset, void** base_out, void** ptr_out) {
+  if (!handle || !base_out || !ptr_out || offset < 0) return DIVUQ_EINVAL;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  void* base = nullptr;
+  DIVUQ_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  *base_out = base;
+  *ptr_out = static_cast<char*>(base) + offset;
+  return DIVUQ_OK;
+}
+
+int divuq_ipc_close(void* base) {
+  if (!base) return DIVUQ_EINVAL;
+  return int(cudaIpcCloseMemHandle(base));
+}
+
+int64_t divuq_ipc_handle_bytes(void) { return int64_t(sizeof(cudaIpcMemHandle_t)); }
 
 int divuq_ensemble_divergence2d_f32(const float* members, int64_t M, int64_t nx, int64_t ny, double dx,
                                     double dy, double t, float* out_mu, float* out_sigma,

@@ -20,7 +20,11 @@ _FP = {torch.float64: "f64", torch.float32: "f32"}
 
 
 def _ptr(t):
-    return None if t is None else t.data_ptr()
+    """Device address of a tensor; an int is taken as a raw device address
+    (e.g. a neighbour's peer-mapped halo plane, peer.py)."""
+    if t is None or isinstance(t, int):
+        return t
+    return t.data_ptr()
 
 
 def _stream():
@@ -118,7 +122,7 @@ def propagate3d(mu_u, mu_v, mu_w, s_u, s_v, s_w, nx, ny, nz_local, dx=1.0, dy=1.
     hl = halo_lo or (None, None)
     hh = halo_hi or (None, None)
     for h in (*hl, *hh):
-        if h is not None:
+        if h is not None and not isinstance(h, int):
             _req(h, "halo", dt, plane)
     kb, ke = (0, nz_local) if k_range is None else k_range
     o = _outs(mu_u, n, outputs, out)
@@ -241,18 +245,36 @@ def ensemble_divergence3d(members, nx, ny, nz_local, dx=1.0, dy=1.0, dz=1.0, t=0
     return o
 
 
-def w_moments_plane(members, nx, ny, nz_local, k, *, check=True):
+def w_moments_plane(members, nx, ny, nz_local, k, *, out=None, check=True):
     """(mu_w, s_w) of local plane k of a 3D member slab -- the reduced halo
     a z-slab neighbour needs.  Same K1 arithmetic as the fused kernel, so the
-    sharded result stays bit-identical to the single-GPU one."""
+    sharded result stays bit-identical to the single-GPU one.  Read in place
+    (member-strided), no gather copy."""
+    _req(members, "members", torch.float32)
+    m = members.shape[0]
+    plane = nx * ny
+    if members.numel() != m * 3 * plane * nz_local:
+        raise ValueError("members: expected (M, 3, nx*ny*nz_local)")
+    return w_moments_plane_ptr(members.data_ptr(), m, nx, ny, nz_local, k, device=members.device,
+                               out=out, check=check)
+
+
+def w_moments_plane_ptr(members_ptr: int, m, nx, ny, nz_local, k, *, device, out=None, check=True):
+    """``w_moments_plane`` on a raw (M, 3, nx*ny*nz_local) fp32 slab address --
+    typically a neighbour's slab mapped through peer memory (peer.py): the
+    fit kernel then reads the neighbour's member planes over NVLink."""
     plane = nx * ny
     n = plane * nz_local
-    m = members.shape[0]
-    # (M, 1, plane) strided view of component w, plane k -> contiguous copy is
-    # M*plane floats (64 MiB at 1024^2, M=16): gather it with one strided copy
-    sub = members.view(m, 3, n)[:, 2:3, k * plane:(k + 1) * plane].contiguous()
-    mu, sg = fit_moments(sub, check=check)
-    return mu.view(plane), sg.view(plane)
+    if not (0 <= k < nz_local):
+        raise ValueError("plane index outside the slab")
+    mu, sg = out if out is not None else (torch.empty(plane, dtype=torch.float32, device=device),
+                                          torch.empty(plane, dtype=torch.float32, device=device))
+    err = _ErrWord(device, check)
+    base = int(members_ptr) + (2 * n + k * plane) * 4   # component w, plane k, member 0
+    _check(lib.divuq_fit_gaussian_strided_f32(base, m, 3 * n, plane, _ptr(mu), _ptr(sg), err.ptr,
+                                              _stream()))
+    err.raise_if_set()
+    return mu, sg
 
 
 def mc_divergence2d(mu_u, mu_v, s_u, s_v, nx, ny, dx, dy, n_samples, seed, *, rows=None,
@@ -295,6 +317,7 @@ def mc_divergence2d(mu_u, mu_v, s_u, s_v, nx, ny, dx, dy, n_samples, seed, *, ro
 
 __all__ = [
     "ALL_OUTPUTS", "propagate2d", "propagate3d", "tail_probs", "lcp2d", "fit_moments",
-    "ensemble_divergence2d", "ensemble_divergence3d", "w_moments_plane", "mc_divergence2d",
+    "ensemble_divergence2d", "ensemble_divergence3d", "w_moments_plane", "w_moments_plane_ptr",
+    "mc_divergence2d",
 ]
 _ = _lib  # re-export guard

@@ -10,9 +10,20 @@ is ONE plane per neighbour per array:
   (2 planes instead of 2*M), computed by the owner with the same moment
   arithmetic, so sharded results are bit-identical to the 1-GPU run.
 
-Schedule per step (``SlabStep.run``):
-  1. post the neighbour sends/receives (``batch_isend_irecv``; NCCL runs them on
-     its own stream over NVLink),
+Two exchange modes (``SlabStep(exchange=...)``):
+
+* ``"p2p"`` (default on GPUs): no exchange step at all.  Each rank maps its
+  z-neighbours' slabs once through CUDA IPC (peer.py) and its kernels read the
+  halo planes straight from the neighbour's HBM over NVLink while they
+  compute: K2 is ONE launch over the whole slab with the halo pointers aimed
+  at the neighbours' edge planes; K3 reduces the neighbours' edge-plane w
+  moments with a strided K1 reading their member planes in place (side
+  stream), overlapped with the interior planes, then the two edge planes.
+  Inputs are read in place, so a producer that rewrites them must finish
+  (e.g. ``dist.barrier()``) before the step -- ``sync_inputs=True`` does it.
+* ``"nccl"``: the classic schedule (``SlabStep.run``) --
+  1. post the neighbour sends/receives (``batch_isend_irecv``; NCCL runs them
+     on its own stream over NVLink),
   2. launch the interior planes [1, nzl-1) on the compute stream -- they need
      no halo, so the exchange overlaps them,
   3. wait for the exchange, launch the two edge planes.
@@ -59,8 +70,14 @@ class SlabStep:
     dtype: torch.dtype = torch.float32
     device: str | torch.device = "cuda"
     group: object = None
+    exchange: str = "nccl"     # "nccl" | "p2p" (peer memory, see module docstring)
 
     def __post_init__(self):
+        if self.exchange not in ("nccl", "p2p"):
+            raise ValueError("exchange must be 'nccl' or 'p2p'")
+        self.peers = None
+        self._attached = None
+        self._side = None
         self.z0, self.z1 = slab_bounds(self.nz_global, self.world, self.rank)
         self.nzl = self.z1 - self.z0
         plane = self.nx * self.ny
@@ -69,6 +86,30 @@ class SlabStep:
         self.halo_lo = mk() if self.rank > 0 else None
         self.halo_hi = mk() if self.rank < self.world - 1 else None
         self.launches = 0
+
+    def neighbour_nzl(self, r: int) -> int:
+        z0, z1 = slab_bounds(self.nz_global, self.world, r)
+        return z1 - z0
+
+    def attach(self, arrays: dict) -> None:
+        """p2p: export ``arrays`` and map the neighbours' (collective, once per
+        set of buffers; re-attaching the same buffers is free)."""
+        from . import peer
+
+        key = tuple((k, v.data_ptr()) for k, v in sorted(arrays.items()))
+        if self._attached == key:
+            return
+        if self.peers:
+            for arrs in self.peers.values():
+                for a in arrs.values():
+                    a.close()
+        self.peers = peer.exchange_handles(arrays, self.rank, self.world, self.group)
+        self._attached = key
+
+    def side_stream(self):
+        if self._side is None:
+            self._side = torch.cuda.Stream(device=self.device)
+        return self._side
 
     def _exchange_ops(self, first, last):
         ops = []
@@ -103,12 +144,34 @@ class SlabStep:
         return launches
 
 
-def propagate3d_step(step: SlabStep, fields, out, dx, dy, dz, t, check=False):
+def _sync_inputs(step: SlabStep):
+    torch.cuda.current_stream().synchronize()
+    dist.barrier(group=step.group)
+
+
+def propagate3d_step(step: SlabStep, fields, out, dx, dy, dz, t, check=False, sync_inputs=False):
     """K2 sharded step on this rank's slab tensors (fields = 6 slab tensors)."""
     from . import device as dev
 
     plane = step.nx * step.ny
     mu_w, s_w = fields[2], fields[5]
+    if step.exchange == "p2p" and step.world > 1:
+        # ONE launch: the halo planes are read from the neighbours' HBM in place
+        step.attach({"mu_w": mu_w, "s_w": s_w})
+        if sync_inputs:
+            _sync_inputs(step)
+        es = mu_w.element_size()
+        lo = hi = None
+        if step.rank > 0:
+            nb, off = step.peers[step.rank - 1], (step.neighbour_nzl(step.rank - 1) - 1) * plane * es
+            lo = (nb["mu_w"].at(off), nb["s_w"].at(off))
+        if step.rank < step.world - 1:
+            nb = step.peers[step.rank + 1]
+            hi = (nb["mu_w"].at(0), nb["s_w"].at(0))
+        dev.propagate3d(*fields, step.nx, step.ny, step.nzl, dx, dy, dz, t, z0=step.z0,
+                        nz_global=step.nz_global, halo_lo=lo, halo_hi=hi, out=out, check=check)
+        step.launches = 1
+        return 1
 
     def edges():
         return ((mu_w[:plane], s_w[:plane]), (mu_w[-plane:], s_w[-plane:]))
@@ -122,10 +185,48 @@ def propagate3d_step(step: SlabStep, fields, out, dx, dy, dz, t, check=False):
     return step.run(edges, compute)
 
 
-def ensemble3d_step(step: SlabStep, members, out, dx, dy, dz, t, check=False):
-    """K3 sharded step: the owner reduces its edge planes' w moments, the
-    neighbours receive 2 planes each instead of 2*M raw member planes."""
+def ensemble3d_step(step: SlabStep, members, out, dx, dy, dz, t, check=False, sync_inputs=False):
+    """K3 sharded step.  nccl: the owner reduces its edge planes' w moments and
+    the neighbours receive 2 planes each instead of 2*M raw member planes.
+    p2p: each rank reduces its neighbours' edge planes itself, reading their
+    member planes in place over NVLink on a side stream, overlapped with its
+    interior planes."""
     from . import device as dev
+
+    if step.exchange == "p2p" and step.world > 1:
+        step.attach({"members": members})
+        if sync_inputs:
+            _sync_inputs(step)
+        m = members.shape[0]
+        main = torch.cuda.current_stream()
+        side = step.side_stream()
+        side.wait_stream(main)
+        with torch.cuda.stream(side):   # neighbours' edge-plane moments, read over NVLink
+            if step.rank > 0:
+                r = step.rank - 1
+                dev.w_moments_plane_ptr(step.peers[r]["members"].ptr, m, step.nx, step.ny,
+                                        step.neighbour_nzl(r), step.neighbour_nzl(r) - 1,
+                                        device=members.device, out=step.halo_lo, check=check)
+            if step.rank < step.world - 1:
+                r = step.rank + 1
+                dev.w_moments_plane_ptr(step.peers[r]["members"].ptr, m, step.nx, step.ny,
+                                        step.neighbour_nzl(r), 0, device=members.device,
+                                        out=step.halo_hi, check=check)
+        n = 2
+        # the interior planes never read the halo buffers (still being filled)
+        common = dict(z0=step.z0, nz_global=step.nz_global, halo_lo=step.halo_lo,
+                      halo_hi=step.halo_hi, out=out, check=check)
+        if step.nzl > 2:   # interior: overlaps the peer reads
+            dev.ensemble_divergence3d(members, step.nx, step.ny, step.nzl, dx, dy, dz, t,
+                                      k_range=(1, step.nzl - 1), **common)
+            n += 1
+        main.wait_stream(side)
+        for kr in ((0, 1), (step.nzl - 1, step.nzl)):
+            dev.ensemble_divergence3d(members, step.nx, step.ny, step.nzl, dx, dy, dz, t,
+                                      k_range=kr, **common)
+        n += 2
+        step.launches = n
+        return n
 
     def edges():
         first = dev.w_moments_plane(members, step.nx, step.ny, step.nzl, 0, check=check)
@@ -139,4 +240,4 @@ def ensemble3d_step(step: SlabStep, members, out, dx, dy, dz, t, check=False):
         return 1
 
     n = step.run(edges, compute)
-    return n + (4 if step.world > 1 else 0)  # 2 gathers + 2 fits for the edge moments
+    return n + (2 if step.world > 1 else 0)  # 2 strided fits for the edge moments

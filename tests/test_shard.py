@@ -141,3 +141,17 @@ def test_slab_bounds():
     assert b == [(0, 4), (4, 8), (8, 13)]
     with pytest.raises(ValueError):
         slab_bounds(3, 2, 0)
+
+
+def test_exchange_modes_and_neighbour_extents():
+    from paper_2510_01190_b200.shard import SlabStep
+
+    with pytest.raises(ValueError):
+        SlabStep(4, 4, 8, 0, 2, device="cpu", exchange="mpi")
+    s = SlabStep(4, 4, 13, 1, 3, device="cpu", exchange="p2p")
+    assert (s.z0, s.z1) == (4, 8)
+    assert [s.neighbour_nzl(r) for r in range(3)] == [4, 4, 5]
+    # the halo planes a p2p rank reads in place: the last plane of rank-1 and
+    # the first plane of rank+1 (byte offsets into their slabs)
+    plane, es = 16, 4
+    assert (s.neighbour_nzl(0) - 1) * plane * es == 192
