@@ -265,7 +265,11 @@ int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
   p.diag_null = HAS_SIGMA && sp.out_mu && sp.out_sigma && sp.out_psrc && sp.out_psnk
                     ? int(env_int("DIVUQ_K2_NULL", 0)) : 0;   // diagnostics only
   p.progress = nullptr;
-  if (p.sync_w > 0 && p.n_tiles <= kMaxFlagTiles)
+  // lockstep pays off only on long z-marches (drift grows with the march);
+  // short launches -- e.g. the host pipeline's 32-plane chunks, two of which
+  // run concurrently and so are never fully co-resident -- skip it
+  const int64_t min_planes = env_int("DIVUQ_K2_SYNC_MIN_PLANES", 64);
+  if (p.sync_w > 0 && p.n_tiles <= kMaxFlagTiles && sp.kend - sp.kbeg >= min_planes)
     DIVUQ_CUDA(progress_flags(&p.progress, &p.epoch));
   p.stage_bytes = uint32_t((3 * ty * C::TX + (p.halo_off ? 0 : 2 * ty * C::PAD + 2 * C::TX)) *
                            sizeof(T)) * (HAS_SIGMA ? 2u : 1u);
