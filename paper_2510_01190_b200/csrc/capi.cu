@@ -125,6 +125,12 @@ int dispatch_vec(const StencilParams<T>& p, bool has_sigma, cudaStream_t s) {
                         p.out_mu, p.out_sigma, p.out_psrc, p.out_psnk, p.out_mom_mu, p.out_mom_sigma};
   for (const void* q : ptrs) vec = vec && aligned(q, 16);
   if (SRC == kEnsemble) vec = vec && ((p.comp_stride % VW) == 0);
+  // latency-bound small grids (config 0: 128^2 fp64): one point per lane
+  // doubles the CTAs and halves each lane's dependent erfc chain
+  if (vec && SRC != kEnsemble) {
+    const int64_t tiles_vec = ((p.nx + 32 * VW - 1) / (32 * VW)) * ((p.ny + kStencilTY - 1) / kStencilTY);
+    if (tiles_vec * (p.kend - p.kbeg) < sm_count()) vec = false;
+  }
   if (vec) return dispatch_sigma<T, VW, HAS_W, SRC>(p, has_sigma, s);
   return dispatch_sigma<T, 1, HAS_W, SRC>(p, has_sigma, s);
 }
