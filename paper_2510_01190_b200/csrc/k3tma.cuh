@@ -40,8 +40,14 @@ struct K3Cfg {
   static constexpr int TYMAX = 14;   // consumer warps; + halo warp + producer = 16 -> 128 regs
   static constexpr int HALO_WARP = TYMAX;
   static constexpr int PROD_WARP = TYMAX + 1;
-  static constexpr int MB = 4;       // members per stage (one 5D TMA box)
-  static constexpr int S = 5;        // stages of MB member boxes
+#ifndef DIVUQ_K3_MB
+#define DIVUQ_K3_MB 4
+#endif
+#ifndef DIVUQ_K3_S
+#define DIVUQ_K3_S 5
+#endif
+  static constexpr int MB = DIVUQ_K3_MB;   // members per stage (one 5D TMA box)
+  static constexpr int S = DIVUQ_K3_S;     // stages of MB member boxes
   static constexpr int D = 3;        // halo boxes trail their main box by D stages
   static constexpr int THREADS = 32 * (TYMAX + 2);
 };
