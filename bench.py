@@ -417,9 +417,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # DIVUQ_BENCH_ONE_DEVICE=1: dry run of the sharded orchestration with every
+    # rank on cuda:0 over gloo (the p2p slab path never makes a rank wait on
+    # another's kernels, so this is safe); its numbers are NOT multi-GPU numbers
+    one_device = os.environ.get("DIVUQ_BENCH_ONE_DEVICE") == "1"
+    if one_device:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_device:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import __graft_entry__
 
@@ -746,6 +755,9 @@ def main():
                    "exchange": (("peer memory (CUDA IPC over NVLink), read in place by the kernels"
                                  if args.exchange == "p2p" else "NCCL send/recv overlapped with the interior")
                                 if args.config in (3, 4) and world > 1 else None),
+                   **({"dry_run": "DIVUQ_BENCH_ONE_DEVICE=1: every rank on cuda:0 over gloo "
+                                  "(orchestration check, not a multi-GPU number)"}
+                      if one_device and world > 1 else {}),
                    "l2": (L2Flush.NOTE if args.config in (0, 1) else
                           "inputs larger than L2 (126 MB); no flush" if args.config in (3, 4) else
                           "compute-bound; 2 MB model stays in L2")},
