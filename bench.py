@@ -632,8 +632,16 @@ def main():
                 "bytes_per_point": bpp, "points_per_launch": k_pts,
                 "avg_launch_ms": avg_k_s * 1e3, "peak_source": peak_src}
     if args.config == 2:  # fp64-ALU bound: the HBM fraction is not the bound that matters
-        roofline = {"bound": "fp64 (CUDA cores; no tensor-core work)", "achieved": None, "peak": None,
-                    "unit": None, "frac": None, "traffic": traffic,
+        # fp64 flops per vertex-sample of mc_chunk_kernel, counted from the ncu
+        # SASS profile (predicated-on DFMA x2 + DMUL + DADD; profiles/r01/mc_chunk_config2*)
+        flops_vs = 108.7
+        fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12   # vector fp64 FMA pipe, TFLOP/s at max clock
+        vs_launch = cfg.n_samples * nx * ny
+        achieved_tf = flops_vs * vs_launch / avg_k_s / 1e12
+        roofline = {"bound": "fp64 (CUDA-core FMA pipe; no tensor-core work)", "achieved": achieved_tf,
+                    "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved_tf / fp64_peak,
+                    "traffic": traffic, "flops_per_vertex_sample": flops_vs,
+                    "peak_source": "148 SMs x 64 fp64 FMA/clk x 2 x 1.965 GHz (nominal; ncu: fp64 pipe ~49 % busy)",
                     "note": "Philox + Box-Muller per vertex-sample; HBM traffic is ~48 B/vertex",
                     "avg_launch_ms": avg_k_s * 1e3}
     elif args.config == 0:
