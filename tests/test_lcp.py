@@ -3,7 +3,7 @@
 CPU part: the oracle restatement is pinned BITWISE to the reference's own
 lcp() / cell_crossing_probability outputs (tests/golden/lcp.npz).
 GPU part: the kernel vs those golden values at |dP| <= 1e-12 (the tails come
-from a different erfc than scipy's), plus the reference suite's own LCP
+from a branch-free fitted fp64 erfc, max 3.8e-15 relative; not scipy's), plus the reference suite's own LCP
 properties (pkg/tests/test_lcp.py): range, exact negation symmetry, sigma -> 0
 indicator, finite extreme tails, the cell formula on a field.
 """

