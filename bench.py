@@ -265,6 +265,37 @@ def run_next(args):
         cpu_thunk = (lambda: ref2d.gradient_ensemble(sub, 1024, 256, 1.0, 1.0), 4 * 256 * 1024, 1)
         cpu_sample = "numpy restatement (hypot + reference stencil), 4 members x 1024x256, 1 thread"
         dtype = "f64"
+    elif wl == "fit":   # K1: the drop-in fit_gaussian (gaussian.py:35-45), fp64 bitwise
+        nx = ny = 1024
+        m = 20
+        mem = configs.config1_members(nx, ny, m, 101).double()
+        mu_o = torch.empty((2, nx * ny), dtype=torch.float64, device="cuda")
+        sg_o = torch.empty_like(mu_o)
+        units = nx * ny
+        bpu = 2 * m * 8 + 2 * 2 * 8   # M members x (u, v) in, (mu, sigma) x (u, v) out, fp64
+        unit = "grid points/s"
+        metric = "ensemble fit_gaussian grid points/sec (gaussian.py:35-45), fp64 (numpy bitwise)"
+        workload = "fit: fit_gaussian of the config-1 ensemble (M=20, 1024^2) in fp64"
+
+        def step():
+            dev.fit_moments(mem, out=(mu_o, sg_o), check=False)
+
+        hin = mem.cpu().pin_memory()
+        hmu = torch.empty((2, nx * ny), dtype=torch.float64).pin_memory()
+        hsg = torch.empty_like(hmu).pin_memory()
+
+        def e2e_call():
+            st = lib.divuq_host_fit_gaussian_f64(hin.data_ptr(), m, 2, nx * ny, hmu.data_ptr(),
+                                                 hsg.data_ptr(), 0)
+            assert st == 0, st
+
+        h2d, d2h = m * 2 * 8 * units, 4 * 8 * units
+        sub = hin.numpy()[:, :, : 1024 * 64]
+        from oracle import ref2d
+
+        cpu_thunk = (lambda: ref2d.fit_moments(sub), 1024 * 64, 1)
+        cpu_sample = "numpy restatement of fit_gaussian (the reference's numpy calls), 1024x64, 1 thread"
+        dtype = "f64"
     else:  # ingest: DIVUQ1 file -> HBM -> fused fit/propagate/tails (the CLI's pipeline)
         import tempfile
 
@@ -397,7 +428,7 @@ def main():
     ap.add_argument("--exchange", default="p2p", choices=("p2p", "nccl"),
                     help="z-slab halo exchange for configs 3/4 at N>1: peer memory read in "
                          "place by the kernels (p2p) or NCCL send/recv overlapped with the interior")
-    ap.add_argument("--workload", default=None, choices=("lcp", "gradient", "ingest"),
+    ap.add_argument("--workload", default=None, choices=("lcp", "gradient", "ingest", "fit"),
                     help="a SURVEY 8f row instead of a BASELINE config (1 GPU, ours only)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

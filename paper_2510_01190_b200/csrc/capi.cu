@@ -469,6 +469,148 @@ int fit_mr(const T* m, int64_t M, int64_t C, int64_t N, int64_t ms, T* mu, T* sg
   return launch_fit<T, VEC, 32>(m, M, C, N, ms, mu, sg, err, s);
 }
 
+// K1 streaming form: one thread per (component, VEC points), a handful of
+// registers, U member loads (16 B each) in flight per thread and every SM full
+// of threads.  fp64 keeps numpy's two-pass algorithm bit for bit (sequential
+// sum / M, then the sequential sum of squared deviations, gaussian.py:41-44)
+// by re-reading the members for the second pass -- the first pass just
+// pulled them into L2, so HBM sees each member once.  fp32: ShiftedMoments,
+// one pass.
+template <typename T, int VEC, int U, int MINB, bool REREAD>
+__global__ void __launch_bounds__(256, MINB) fit_stream_kernel(const T* __restrict__ members, int64_t M,
+                                                            int64_t C, int64_t N, int64_t mstride,
+                                                            T* __restrict__ out_mu,
+                                                            T* __restrict__ out_sigma, int* err) {
+  using A = Arith<T>;
+  using V = Vec<T, VEC>;
+  int errbits = 0;
+  const int64_t groups = N / VEC, total = C * groups;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t c = i / groups;
+    const int64_t off = c * N + (i - c * groups) * VEC;
+    const T* base = members + off;
+    V mu, sg;
+    if constexpr (sizeof(T) == 8) {
+      V s, q;
+      if constexpr (!REREAD) {   // requires M <= U
+        // all M values of the point in registers (running pointer: one live
+        // address), both passes from registers
+        V x[U];
+        const T* pm = base;
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          if (j < M) x[j] = ld_stream<T, VEC>(pm);
+          pm += mstride;
+        }
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) s.v[e] = x[0].v[e];
+#pragma unroll
+        for (int j = 1; j < U; ++j)
+          if (j < M) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) s.v[e] = A::add(s.v[e], x[j].v[e]);
+          }
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) mu.v[e] = A::div(s.v[e], T(M));
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          if (j < M) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) {
+              errbits |= check_value(x[j].v[e]);
+              const T d = A::sub(x[j].v[e], mu.v[e]);
+              q.v[e] = j == 0 ? A::mul(d, d) : A::add(q.v[e], A::mul(d, d));
+            }
+          }
+      } else {
+        for (int64_t k0 = 0; k0 < M; k0 += U) {   // pass 1: sum in member order
+          V x[U];
+#pragma unroll
+          for (int j = 0; j < U; ++j)   // plain loads: the lines must stay in L2 for pass 2
+            if (k0 + j < M) x[j] = ldg_vec<T, VEC>(base + (k0 + j) * mstride);
+#pragma unroll
+          for (int j = 0; j < U; ++j)
+            if (k0 + j < M) {
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) {
+                errbits |= check_value(x[j].v[e]);
+                s.v[e] = (k0 + j == 0) ? x[j].v[e] : A::add(s.v[e], x[j].v[e]);
+              }
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) mu.v[e] = A::div(s.v[e], T(M));
+        for (int64_t k0 = 0; k0 < M; k0 += U) {   // pass 2: L2-resident re-read
+          V x[U];
+#pragma unroll
+          for (int j = 0; j < U; ++j)
+            if (k0 + j < M) x[j] = ld_stream<T, VEC>(base + (k0 + j) * mstride);
+#pragma unroll
+          for (int j = 0; j < U; ++j)
+            if (k0 + j < M) {
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) {
+                const T d = A::sub(x[j].v[e], mu.v[e]);
+                q.v[e] = (k0 + j == 0) ? A::mul(d, d) : A::add(q.v[e], A::mul(d, d));
+              }
+            }
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) sg.v[e] = A::sqrt_(A::div(q.v[e], T(M - 1)));
+    } else {
+      ShiftedMoments<VEC> acc;
+      for (int64_t k0 = 0; k0 < M; k0 += U) {
+        V x[U];
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          if (k0 + j < M) x[j] = ld_stream<T, VEC>(base + (k0 + j) * mstride);
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+          if (k0 + j < M) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) errbits |= check_value(x[j].v[e]);
+            acc.add(int(k0 + j), x[j].v);
+          }
+      }
+      acc.finish(int(M), mu.v, sg.v);
+    }
+    st_stream<T, VEC>(out_mu + off, mu);
+    st_stream<T, VEC>(out_sigma + off, sg);
+  }
+  flush_error(err, errbits);
+}
+
+template <typename T, int VEC, int U, int MINB, bool REREAD = true>
+int launch_fit_stream(const T* m, int64_t M, int64_t C, int64_t N, int64_t ms, T* mu, T* sg,
+                      int32_t* err, cudaStream_t s) {
+  auto kern = fit_stream_kernel<T, VEC, U, MINB, REREAD>;
+  const int64_t cap = int64_t(blocks_per_sm(kern, 256, 0)) * sm_count();
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((C * (N / VEC) + 255) / 256, cap));
+  kern<<<unsigned(grid), 256, 0, s>>>(m, M, C, N, ms, mu, sg, err);
+  return int(cudaGetLastError());
+}
+
+// measured on B200 (tools/fit_probe.py, M=20, C=2, 1024^2): fp32 float4 lanes,
+// 4 loads in flight, 4 CTAs/SM: 33 us (86 % of HBM, was 113 us); fp64 one
+// point per lane, 8 loads in flight, second pass re-read from L2: 113 us
+// (50 %, was 194 us) -- the two passes serialise per thread
+template <typename T>
+int fit_stream(const T* m, int64_t M, int64_t C, int64_t N, int64_t ms, T* mu, T* sg, int32_t* err,
+               cudaStream_t s) {
+  const bool v16 = (N % (16 / int(sizeof(T)))) == 0 && (ms % (16 / int(sizeof(T)))) == 0 &&
+                   aligned(m, 16) && aligned(mu, 16) && aligned(sg, 16);
+  if constexpr (sizeof(T) == 4) {
+    if (v16) return launch_fit_stream<T, 4, 4, 4>(m, M, C, N, ms, mu, sg, err, s);
+    return launch_fit_stream<T, 1, 8, 4>(m, M, C, N, ms, mu, sg, err, s);
+  } else {
+    // holding all M doubles for both passes spills at these register caps;
+    // the L2 re-read of the second pass is the faster trade (measured)
+    return launch_fit_stream<T, 1, 8, 4, true>(m, M, C, N, ms, mu, sg, err, s);
+  }
+}
+
 template <typename T>
 int fit_gaussian(const T* members, int64_t M, int64_t C, int64_t N, T* out_mu, T* out_sigma,
                  int32_t* err, void* stream, int64_t mstride = -1) {
@@ -477,12 +619,14 @@ int fit_gaussian(const T* members, int64_t M, int64_t C, int64_t N, T* out_mu, T
   if (mstride < 0) mstride = C * N;
   if (mstride < C * N) return DIVUQ_EINVAL;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  constexpr int VW = (sizeof(T) == 4) ? 4 : 2;
-  // wide vectors only while the M register-resident values stay small
-  const bool vec = M <= 16 && (N % VW) == 0 && (mstride % VW) == 0 && aligned(members, 16) &&
-                   aligned(out_mu, 16) && aligned(out_sigma, 16);
-  if (vec) return fit_mr<T, VW>(members, M, C, N, mstride, out_mu, out_sigma, err, s);
-  return fit_mr<T, 1>(members, M, C, N, mstride, out_mu, out_sigma, err, s);
+  if (env_int("DIVUQ_FIT_LEGACY", 0)) {   // the register-array K1 (kept for comparison)
+    constexpr int VW = (sizeof(T) == 4) ? 4 : 2;
+    const bool vec = M <= 16 && (N % VW) == 0 && (mstride % VW) == 0 && aligned(members, 16) &&
+                     aligned(out_mu, 16) && aligned(out_sigma, 16);
+    if (vec) return fit_mr<T, VW>(members, M, C, N, mstride, out_mu, out_sigma, err, s);
+    return fit_mr<T, 1>(members, M, C, N, mstride, out_mu, out_sigma, err, s);
+  }
+  return fit_stream<T>(members, M, C, N, mstride, out_mu, out_sigma, err, s);
 }
 
 // ---- probability map on an existing Gaussian scalar field (lcp.py:48-68)

@@ -70,16 +70,30 @@ __device__ __forceinline__ void member_moments_2pass(const T* base, int64_t mstr
                                                      Vec<T, VEC>& mu, Vec<T, VEC>& sg, int& err);
 
 template <typename T, int VEC, int MR>
-__device__ __noinline__ void member_moments(const T* base, int64_t mstride, int M,
+__device__ __forceinline__ void member_moments(const T* base, int64_t mstride, int M,
                                                Vec<T, VEC>& mu, Vec<T, VEC>& sg, int& err) {
   if constexpr (sizeof(T) == 4) {
     ShiftedMoments<VEC> acc;
-#pragma unroll 8
-    for (int k = 0; k < M; ++k) {
-      const Vec<T, VEC> x = ld_stream<T, VEC>(base + k * mstride);
+    if (M <= MR) {   // all M loads in flight before the first use
+      Vec<T, VEC> x[MR];
 #pragma unroll
-      for (int e = 0; e < VEC; ++e) err |= check_value(x.v[e]);
-      acc.add(k, x.v);
+      for (int k = 0; k < MR; ++k)
+        if (k < M) x[k] = ld_stream<T, VEC>(base + k * mstride);
+#pragma unroll
+      for (int k = 0; k < MR; ++k)
+        if (k < M) {
+#pragma unroll
+          for (int e = 0; e < VEC; ++e) err |= check_value(x[k].v[e]);
+          acc.add(k, x[k].v);
+        }
+    } else {
+#pragma unroll 8
+      for (int k = 0; k < M; ++k) {
+        const Vec<T, VEC> x = ld_stream<T, VEC>(base + k * mstride);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) err |= check_value(x.v[e]);
+        acc.add(k, x.v);
+      }
     }
     acc.finish(M, mu.v, sg.v);
     return;
