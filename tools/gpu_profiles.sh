@@ -1,4 +1,5 @@
 # Round profiles: launch lists of the default bench + one --set full capture per hot kernel.
+# Summaries are written on the box; only the K2 / K3 reports are kept (gpurun_out <= 64 MiB).
 set -x
 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/plain.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_config3.csv \
@@ -6,11 +7,18 @@ python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/plain.log 2>
 python bench.py --config 4 --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/plain4.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_config4.csv \
   python bench.py --config 4 --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_launch4.log 2>&1
-bash tools/gpu_prof.sh k2 k2_tma --config 3 --steps 5 --warmup 3 --no-e2e --no-cpu
-bash tools/gpu_prof.sh k3 k3_tma --config 4 --steps 3 --warmup 3 --no-e2e --no-cpu
-bash tools/gpu_prof.sh c1 k3_tma --config 1 --steps 5 --warmup 3 --no-e2e --no-cpu
-bash tools/gpu_prof.sh mc mc_chunk --config 2 --steps 3 --warmup 3 --no-e2e --no-cpu
-bash tools/gpu_prof.sh lcp lcp2d --workload lcp --steps 3 --no-cpu --no-e2e
-bash tools/gpu_prof.sh gradient gradient2d --workload gradient --steps 3 --no-cpu --no-e2e
-bash tools/gpu_prof.sh fit fit_stream --workload fit --steps 3 --no-cpu --no-e2e
-ls -la gpurun_out/*.ncu-rep
+prof() {  # name kernel-regex bench-args...
+  name=$1; shift; kre=$1; shift
+  bash tools/gpu_prof.sh $name $kre "$@"
+  python tools/ncu_summary.py gpurun_out/prof_$name.ncu-rep > gpurun_out/sum_$name.txt
+}
+prof k2 k2_tma --config 3 --steps 5 --warmup 3 --no-e2e --no-cpu
+prof k3 k3_tma --config 4 --steps 3 --warmup 3 --no-e2e --no-cpu
+prof c1 k3_tma --config 1 --steps 5 --warmup 3 --no-e2e --no-cpu
+prof mc mc_chunk --config 2 --steps 3 --warmup 3 --no-e2e --no-cpu
+prof lcp lcp2d --workload lcp --steps 3 --no-cpu --no-e2e
+prof gradient gradient2d --workload gradient --steps 3 --no-cpu --no-e2e
+prof fit fit_stream --workload fit --steps 3 --no-cpu --no-e2e
+rm -f gpurun_out/prof_c1.ncu-rep gpurun_out/prof_mc.ncu-rep gpurun_out/prof_lcp.ncu-rep \
+      gpurun_out/prof_gradient.ncu-rep gpurun_out/prof_fit.ncu-rep
+du -sh gpurun_out
