@@ -15,6 +15,7 @@ there is no CPU fallback.
 
 from . import _lib  # noqa: F401  (fails loudly without the CUDA library)
 from . import io  # noqa: F401  (DIVUQ1 container, reference divuq.io)
+from .parallel import BenchReport, bench, parallel_map
 from .api import (
     EnsembleDivergence,
     cell_crossing_probability,
@@ -60,7 +61,7 @@ from .types import (
 __version__ = "0.1.0"
 
 __all__ = [
-    "Ensemble2", "EnsembleDivergence", "GaussianScalarField", "GaussianScalarField3",
+    "BenchReport", "bench", "parallel_map", "Ensemble2", "EnsembleDivergence", "GaussianScalarField", "GaussianScalarField3",
     "GaussianVectorField", "GaussianVectorField3", "LcpField", "McConfig", "McDivergenceEstimate", "McHistogram",
     "ParallelConfig", "Propagation", "ScalarField2", "UniformGrid2", "UniformGrid3",
     "VectorField2", "cell_crossing_probability", "divergence_deterministic", "ensemble_divergence", "error_metrics",

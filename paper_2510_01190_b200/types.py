@@ -331,3 +331,7 @@ class ParallelConfig:
 
     def resolve_threads(self) -> int:
         return (os.cpu_count() or 1) if self.threads == "auto" else self.threads
+
+    def resolve_chunk(self, n: int, threads: int) -> int:
+        """'auto': ceil(n / (4 * threads)) -- a few static chunks per thread."""
+        return max(1, -(-n // (threads * 4))) if self.chunk == "auto" else self.chunk
