@@ -4,8 +4,9 @@
 // reference's op order in fp64, stencils.py:54-84, tails lcp.py:48-68) with
 // Blackwell-native data movement:
 //
-//   * warp-specialised persistent CTA (one per SM): 1 producer warp + TY
-//     consumer warps, an S-stage shared-memory ring guarded by mbarriers;
+//   * warp-specialised persistent CTA (one per SM): TY consumer warps, one
+//     producer warp and one pacer warp; an S-stage shared-memory ring guarded
+//     by mbarriers;
 //   * per plane the producer issues 3D TMA box loads (cp.async.bulk.tensor):
 //       main boxes  u, v, w(k+1) [and s_u, s_v, s_w]: the tile's own TX x TY
 //                   points, 512-byte aligned rows;
@@ -13,20 +14,25 @@
 //                   v / s_v: the row above and the row below.
 //     Out-of-grid box parts are zero-filled by the TMA unit, so the producer
 //     never branches on borders;
-//   * the halo boxes of plane k are issued D stages AFTER its main boxes.
-//     Every CTA marches the same planes in lockstep (see scheduling), so by
-//     then the neighbouring CTA has already pulled those halo bytes into L2
-//     with its own main box: halos cost L2 bandwidth, not HBM bandwidth;
+//   * the halo boxes of plane k are issued hdelay (2) stages after its main
+//     boxes, and the pacer keeps every CTA within W planes of its four
+//     neighbour tiles (consumer warp 0 publishes "planes consumed"; bounded
+//     wait, never a correctness dependency).  So the neighbour has just pulled
+//     the halo bytes into L2 with its own main box: halos cost L2 bandwidth,
+//     not HBM bandwidth (without the pacer CTAs drift tens of planes apart
+//     over a long march and every halo byte came from DRAM, +10 % reads);
 //   * consumers (one grid row per warp, VEC points per lane) take their
 //     operands from the stage (x neighbours by warp shuffle), keep w[k-1],
-//     w[k] in registers (z-march), evaluate mean, sigma and both tails and
-//     stream the four outputs to HBM;
+//     w[k] in registers (z-march), evaluate mean, sigma and both tails on ONE
+//     branch-free path (boundary points by operand substitution) and stream
+//     the four outputs to HBM;
 //   * scheduling: a CTA owns whole tile COLUMNS (all planes of a tile) and
 //     the host picks the tile height TY so #tiles is (close to) a multiple of
-//     the SM count; all CTAs then advance through the planes in lockstep.
+//     the SM count.
 //
 // Slab sharding: planes are slab-local; w at local planes -1 / nzl comes from
-// the halo pointers (exchanged by the caller), read with plain loads.
+// the halo pointers (a neighbour's edge plane: exchanged, or read in place
+// through a peer mapping), read with plain loads.
 #pragma once
 
 #include "common.cuh"
