@@ -10,10 +10,11 @@
 //     stage carries ONE member's box of ONE component of one plane (TX x TY
 //     fp32 + halos, ~8 KB), ~150 KB of member data in flight per SM;
 //   * per plane the producer streams u(k) x M, v(k) x M, w(k+1) x M boxes
-//     (4D TMA on the (x, y, plane, member*3 + component) view); the u boxes'
+//     (5D TMA on the (x, y, plane, component, member) view); the u boxes'
 //     4-column x-halos and the v boxes' halo rows are separate small boxes
-//     issued D stages later -- the neighbouring CTA, marching the same
-//     sequence in lockstep, has already pulled those bytes into L2;
+//     issued with their main box (hdelay 0: a trailing halo would delay the
+//     stage it completes, and the ring depth is worth more -- measured; the
+//     delay and a K2-style lockstep pacer remain as knobs);
 //   * consumers fold each member into per-point shifted single-pass moment
 //     accumulators (ShiftedMoments, common.cuh) and release the stage at
 //     once; the halo warp does the same for the tile's halo points (2*TY
