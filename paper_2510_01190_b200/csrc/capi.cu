@@ -13,6 +13,7 @@
 #include "gen.cuh"
 #include "k2tma.cuh"
 #include "k3tma.cuh"
+#include "k3row.cuh"
 #include "divuq1.cuh"
 #include "gradient.cuh"
 #include "lcp.cuh"
@@ -943,6 +944,53 @@ int divuq_ipc_close(void* base) {
 
 int64_t divuq_ipc_handle_bytes(void) { return int64_t(sizeof(cudaIpcMemHandle_t)); }
 
+// 2D fused ensemble as a row march (k3row.cuh); *used = false when not eligible
+int try_k3_rowmarch(const StencilParams<float>& sp, cudaStream_t s, bool* used) {
+  using C = RmCfg;
+  *used = false;
+  if (env_int("DIVUQ_NO_TMA", 0) || env_int("DIVUQ_NO_ROWMARCH", 0)) return DIVUQ_OK;
+  if (sp.nx % 4 || sp.n_members < 2 || sp.n_members > 256) return DIVUQ_OK;   // TMA rows: 16 B units
+  const void* ptrs[] = {sp.members, sp.out_mu, sp.out_sigma, sp.out_psrc, sp.out_psnk,
+                        sp.out_mom_mu, sp.out_mom_sigma};
+  for (const void* q : ptrs)
+    if (!aligned(q, 16)) return DIVUQ_OK;
+  if (sp.nx > (int64_t(1) << 30) || sp.ny > (int64_t(1) << 30)) return DIVUQ_OK;
+  const int64_t M = sp.n_members;
+  RmParams p;
+  std::memset(&p, 0, sizeof(p));
+  const uint32_t u_bytes = uint32_t(M * C::TXP * 4), v_bytes = uint32_t(M * C::TX * 4);
+  p.v_off = (u_bytes + 127) / 128 * 128;
+  p.stage_stride = (p.v_off + v_bytes + 127) / 128 * 128;
+  p.stage_bytes = u_bytes + v_bytes;
+  const size_t ring = (sizeof(RmRing) + 1023) / 1024 * 1024;
+  const size_t budget = 227 * 1024 - ring - 2 * C::SMAX * sizeof(uint64_t) - 1024;
+  p.S = int(std::min<size_t>(C::SMAX, budget / p.stage_stride));
+  // every consumer warp of a group waits on its own stage: S >= NW, or two
+  // rows one phase apart would share a stage (parity aliasing)
+  if (p.S < C::NW) return DIVUQ_OK;
+  RmMaps tm;
+  std::memset(&tm, 0, sizeof(tm));
+  if (!make_map5d_members(&tm.u, sp.members, sp.nx, sp.ny, 1, 2, M, C::TXP, 1, int(M), 256) ||
+      !make_map5d_members(&tm.v, sp.members, sp.nx, sp.ny, 1, 2, M, C::TX, 1, int(M), 256))
+    return DIVUQ_OK;
+  p.nx = int(sp.nx); p.ny = int(sp.ny); p.M = int(M);
+  p.strips = int((sp.nx + C::TX - 1) / C::TX);
+  const int64_t sms = sm_count();
+  const int64_t segs_wanted = std::max<int64_t>(1, sms / p.strips);
+  p.seg_rows = int(std::max<int64_t>(C::NW, (sp.ny + segs_wanted - 1) / segs_wanted));
+  const int64_t segs = (sp.ny + p.seg_rows - 1) / p.seg_rows;
+  p.cx_in = sp.cx_in; p.cx_bd = sp.cx_bd; p.cy_in = sp.cy_in; p.cy_bd = sp.cy_bd; p.theta = sp.theta;
+  p.out_mu = sp.out_mu; p.out_sigma = sp.out_sigma; p.out_psrc = sp.out_psrc; p.out_psnk = sp.out_psnk;
+  p.out_mom_mu = sp.out_mom_mu; p.out_mom_sigma = sp.out_mom_sigma;
+  p.err = sp.err;
+  const size_t smem = ring + size_t(p.S) * p.stage_stride + 2 * C::SMAX * sizeof(uint64_t);
+  DIVUQ_CUDA(cudaFuncSetAttribute(k3_rowmarch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(smem)));
+  k3_rowmarch_kernel<<<unsigned(int64_t(p.strips) * segs), C::THREADS, smem, s>>>(tm, p);
+  *used = true;
+  return int(cudaGetLastError());
+}
+
 int divuq_ensemble_divergence2d_f32(const float* members, int64_t M, int64_t nx, int64_t ny, double dx,
                                     double dy, double t, float* out_mu, float* out_sigma,
                                     float* out_p_src, float* out_p_snk, float* out_mom_mu,
@@ -960,6 +1008,8 @@ int divuq_ensemble_divergence2d_f32(const float* members, int64_t M, int64_t nx,
   p.out_mom_mu = out_mom_mu; p.out_mom_sigma = out_mom_sigma;
   p.err = err;
   bool used = false;
+  if (int r = try_k3_rowmarch(p, static_cast<cudaStream_t>(stream), &used)) return r;
+  if (used) return DIVUQ_OK;
   if (int r = try_k3_tma(p, 2, static_cast<cudaStream_t>(stream), &used)) return r;
   if (used) return DIVUQ_OK;
   return dispatch_vec<float, false, kEnsemble>(p, true, static_cast<cudaStream_t>(stream));
