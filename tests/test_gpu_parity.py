@@ -311,7 +311,11 @@ def test_propagate3d_slabs_and_k_ranges_bitwise(dev, dtype, rng):
 # fused ensemble kernels (K3)
 # --------------------------------------------------------------------------
 
-@pytest.mark.parametrize("m,shape", [(20, (256, 40)), (2, (33, 7)), (16, (128, 17)), (40, (64, 9))])
+@pytest.mark.parametrize("m,shape", [(20, (256, 40)), (2, (33, 7)), (16, (128, 17)), (40, (64, 9)),
+                                     # row-march edges: partial strips, both x edges in one
+                                     # lane, 2-3 row runs, segment boundaries, many members
+                                     (3, (4, 2)), (20, (68, 5)), (5, (100, 200)), (20, (132, 3)),
+                                     (20, (1024, 64)), (30, (192, 130))])
 def test_ensemble_divergence2d(dev, m, shape, rng):
     nx, ny = shape
     n = nx * ny
