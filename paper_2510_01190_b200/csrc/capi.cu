@@ -699,9 +699,23 @@ struct DevBuf {
   template <typename T> T* as() const { return static_cast<T*>(p); }
 };
 
+// The host entry points run on a per-(thread, device) pair of non-blocking
+// streams created once: creating and destroying a stream per call cost more
+// than a small call's copies and kernel.  The guard only drains the stream.
+cudaError_t cached_stream(int slot, cudaStream_t* out) {
+  thread_local cudaStream_t streams[64][2] = {};
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev)) return e;
+  if (dev >= 64 || slot < 0 || slot > 1) return cudaStreamCreateWithFlags(out, cudaStreamNonBlocking);
+  if (!streams[dev][slot])
+    if (cudaError_t e = cudaStreamCreateWithFlags(&streams[dev][slot], cudaStreamNonBlocking)) return e;
+  *out = streams[dev][slot];
+  return cudaSuccess;
+}
+
 struct StreamGuard {
   cudaStream_t s = nullptr;
-  ~StreamGuard() { if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); } }
+  ~StreamGuard() { if (s) cudaStreamSynchronize(s); }
 };
 
 // ---- velocity-magnitude-gradient prologue ----------
@@ -767,7 +781,7 @@ static int host_gradient_common(int kind, const double* a, const double* b, int6
                                 int64_t ny, double dx, double dy, double* out, int device) {
   DIVUQ_CUDA(cudaSetDevice(device));
   StreamGuard sg;
-  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  DIVUQ_CUDA(cached_stream(0, &sg.s));
   const int64_t n = nx * ny;
   const int64_t in_elems = kind == 0 ? 2 * n : kind == 1 ? n : 2 * M * n;
   const int64_t out_elems = kind == 0 ? n : kind == 1 ? 2 * n : 2 * M * n;
@@ -1249,7 +1263,7 @@ int divuq_host_propagate2d_f64(const double* mu_u, const double* mu_v, const dou
   if (has_sigma && (!s_u || !s_v)) return DIVUQ_EINVAL;
   DIVUQ_CUDA(cudaSetDevice(device));
   StreamGuard sg;
-  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  DIVUQ_CUDA(cached_stream(0, &sg.s));
   const int64_t n = nx * ny;
   const size_t b = size_t(n) * sizeof(double);
   DevBuf d;
@@ -1284,7 +1298,7 @@ int divuq_host_tail_probs_f64(const double* mu, const double* sigma, int64_t n, 
   if (n == 0) return DIVUQ_OK;
   DIVUQ_CUDA(cudaSetDevice(device));
   StreamGuard sg;
-  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  DIVUQ_CUDA(cached_stream(0, &sg.s));
   const size_t b = size_t(n) * sizeof(double);
   DevBuf d;
   DIVUQ_CUDA(d.alloc(4 * b + 256, sg.s));
@@ -1309,7 +1323,7 @@ int divuq_host_lcp2d_f64(const double* mu, const double* sigma, int64_t nx, int6
   if (!mu || !sigma || !out) return DIVUQ_EINVAL;
   DIVUQ_CUDA(cudaSetDevice(device));
   StreamGuard sg;
-  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  DIVUQ_CUDA(cached_stream(0, &sg.s));
   const int64_t n = nx * ny, nc = (nx - 1) * (ny - 1);
   DevBuf d;
   DIVUQ_CUDA(d.alloc(size_t(2 * n + nc) * sizeof(double) + 256, sg.s));
@@ -1333,7 +1347,7 @@ int divuq_host_cell_crossing_f64(const double* mu4, const double* sigma4, int64_
   if (n_cells == 0) return DIVUQ_OK;
   DIVUQ_CUDA(cudaSetDevice(device));
   StreamGuard sg;
-  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  DIVUQ_CUDA(cached_stream(0, &sg.s));
   DevBuf d;
   DIVUQ_CUDA(d.alloc(size_t(9 * n_cells) * sizeof(double) + 256, sg.s));
   double* dmu = d.as<double>();
@@ -1356,7 +1370,7 @@ int divuq_host_fit_gaussian_f64(const double* members, int64_t M, int64_t C, int
   if (M < 2) return DIVUQ_EMEMBERS;
   DIVUQ_CUDA(cudaSetDevice(device));
   StreamGuard sg;
-  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  DIVUQ_CUDA(cached_stream(0, &sg.s));
   const size_t in_b = size_t(M * C * N) * sizeof(double), out_b = size_t(C * N) * sizeof(double);
   DevBuf d;
   DIVUQ_CUDA(d.alloc(in_b + 2 * out_b + 256, sg.s));
@@ -1384,7 +1398,7 @@ int divuq_host_ensemble_divergence2d_f32(const float* members, int64_t M, int64_
   if ((out_mom_mu == nullptr) != (out_mom_sigma == nullptr)) return DIVUQ_EINVAL;
   DIVUQ_CUDA(cudaSetDevice(device));
   StreamGuard sg;
-  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  DIVUQ_CUDA(cached_stream(0, &sg.s));
   const int64_t n = nx * ny;
   const size_t in_b = size_t(M * 2 * n) * sizeof(float), b = size_t(n) * sizeof(float);
   DevBuf d;
@@ -1423,7 +1437,7 @@ int divuq_host_mc_divergence2d_f64(const double* mu_u, const double* mu_v, const
   if (!mu_u || !mu_v || !s_u || !s_v || !out_mean || !out_std) return DIVUQ_EINVAL;
   DIVUQ_CUDA(cudaSetDevice(device));
   StreamGuard sg;
-  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  DIVUQ_CUDA(cached_stream(0, &sg.s));
   const int64_t n = nx * ny;
   const size_t b = size_t(n) * sizeof(double);
   const int64_t scratch = divuq_mc_scratch_bytes(nx, 0, ny, n_samples);
@@ -1461,7 +1475,7 @@ int divuq_host_mc_divergence2d_ref_f64(const double* mu_u, const double* mu_v, c
   if (!mu_u || !mu_v || !s_u || !s_v || !out_mean || !out_std) return DIVUQ_EINVAL;
   DIVUQ_CUDA(cudaSetDevice(device));
   StreamGuard sg;
-  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  DIVUQ_CUDA(cached_stream(0, &sg.s));
   const int64_t n = nx * ny;
   const size_t b = size_t(n) * sizeof(double);
   DevBuf d;
@@ -1495,7 +1509,7 @@ int divuq_host_mc_histogram1d_f64(const double* neighbors, double dx, double dy,
   if (!neighbors || n_samples < 1 || !out_edges || !out_counts || !out_nbins) return DIVUQ_EINVAL;
   DIVUQ_CUDA(cudaSetDevice(device));
   StreamGuard sg;
-  DIVUQ_CUDA(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking));
+  DIVUQ_CUDA(cached_stream(0, &sg.s));
   const size_t vb = size_t(n_samples) * sizeof(double);
   DevBuf d;
   DIVUQ_CUDA(d.alloc(vb + size_t(n_bins + 1) * 16 + 64, sg.s));
@@ -1545,7 +1559,7 @@ int divuq_host_propagate3d_f32(const float* mu_u, const float* mu_v, const float
   const int64_t cz = std::max<int64_t>(1, std::min<int64_t>(chunk_planes > 0 ? chunk_planes : 32, nz));
   const int64_t nchunks = (nz + cz - 1) / cz;
   StreamGuard sg[2];
-  for (auto& g : sg) DIVUQ_CUDA(cudaStreamCreateWithFlags(&g.s, cudaStreamNonBlocking));
+  for (int q = 0; q < 2; ++q) DIVUQ_CUDA(cached_stream(q, &sg[q].s));
   // per buffer set: u, v, su, sv: cz planes; w, sw: cz + 2 planes; 4 outputs: cz planes
   const int64_t set_elems = 4 * cz * plane + 2 * (cz + 2) * plane + 4 * cz * plane;
   DevBuf d;
@@ -1643,7 +1657,7 @@ int divuq_divuq1_ingest_f32(const char* path, float* dev_out, int64_t count, int
   cudaEvent_t done[io::Staging::kBuffers] = {};
   int status = DIVUQ_OK;
   do {
-    if ((status = int(cudaStreamCreateWithFlags(&sg.s, cudaStreamNonBlocking)))) break;
+    if ((status = int(cached_stream(0, &sg.s)))) break;
     for (auto& e : done)
       if ((status = int(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)))) break;
     if (status) break;
