@@ -699,6 +699,97 @@ struct DevBuf {
   template <typename T> T* as() const { return static_cast<T*>(p); }
 };
 
+// Pageable host memory (plain numpy arrays through the drop-in API) moves at a
+// fraction of PCIe speed.  Large pageable copies go through the pinned staging
+// ring instead: all host cores memcpy a chunk into a pinned buffer while the
+// previous chunk's DMA runs.  Pinned / registered memory and small copies go
+// straight to cudaMemcpyAsync.  Both helpers leave the stream drained.
+// below these the driver's own pageable path wins (measured on B200 with the
+// drop-in probe, tools/dropin_probe.py): pageable D2H is the slower direction
+constexpr size_t kStageMinH2D = size_t(64) << 20, kStageMinD2H = size_t(12) << 20;
+
+static void memcpy_parallel(char* dst, const char* src, int64_t len) {
+  constexpr int kMaxThreads = 16;
+  const int64_t kSlice = int64_t(2) << 20;
+  const int64_t hw = std::max(1u, std::thread::hardware_concurrency());
+  const int nt = int(std::min<int64_t>(std::min<int64_t>(kMaxThreads, hw), (len + kSlice - 1) / kSlice));
+  if (nt <= 1) { std::memcpy(dst, src, size_t(len)); return; }
+  const int64_t per = (len + nt - 1) / nt;
+  std::thread th[kMaxThreads];
+  for (int t = 0; t < nt; ++t) {
+    const int64_t a = t * per, n = std::min(per, len - a);
+    th[t] = std::thread([=] { if (n > 0) std::memcpy(dst + a, src + a, size_t(n)); });
+  }
+  for (int t = 0; t < nt; ++t) th[t].join();
+}
+
+static bool pageable(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) { cudaGetLastError(); return true; }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+int h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes < kStageMinH2D || !pageable(src))
+    return int(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+  io::Staging& st = io::staging();
+  std::lock_guard<std::mutex> lock(st.mu);
+  if (int r = st.ensure()) return r;
+  cudaEvent_t done[io::Staging::kBuffers] = {};
+  int status = 0;
+  for (auto& e : done)
+    if (!status) status = int(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  const char* in = static_cast<const char*>(src);
+  char* out = static_cast<char*>(dst);
+  int b = 0;
+  for (size_t off = 0; !status && off < bytes; off += io::Staging::kChunk, b = (b + 1) % io::Staging::kBuffers) {
+    const int64_t len = int64_t(std::min<size_t>(io::Staging::kChunk, bytes - off));
+    if ((status = int(cudaEventSynchronize(done[b])))) break;   // buffer b's last DMA finished
+    memcpy_parallel(st.buf[b], in + off, len);
+    if ((status = int(cudaMemcpyAsync(out + off, st.buf[b], size_t(len), cudaMemcpyHostToDevice, s)))) break;
+    status = int(cudaEventRecord(done[b], s));
+  }
+  if (!status) status = int(cudaStreamSynchronize(s));   // the staging ring is released below
+  for (auto& e : done)
+    if (e) cudaEventDestroy(e);
+  return status;
+}
+
+int d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes < kStageMinD2H || !pageable(dst))
+    return int(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+  io::Staging& st = io::staging();
+  std::lock_guard<std::mutex> lock(st.mu);
+  if (int r = st.ensure()) return r;
+  const char* in = static_cast<const char*>(src);
+  char* out = static_cast<char*>(dst);
+  const int nb = io::Staging::kBuffers;
+  cudaEvent_t done[io::Staging::kBuffers] = {};
+  int status = 0;
+  for (auto& e : done)
+    if (!status) status = int(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  const size_t chunks = (bytes + io::Staging::kChunk - 1) / io::Staging::kChunk;
+  // DMA chunk c into buffer c % nb; the host drains chunk c - (nb - 1) meanwhile
+  for (size_t c = 0; !status && c < chunks + nb - 1; ++c) {
+    if (c < chunks) {
+      const size_t off = c * io::Staging::kChunk, len = std::min<size_t>(io::Staging::kChunk, bytes - off);
+      if ((status = int(cudaMemcpyAsync(st.buf[c % nb], in + off, len, cudaMemcpyDeviceToHost, s)))) break;
+      if ((status = int(cudaEventRecord(done[c % nb], s)))) break;
+    }
+    if (c + 1 >= size_t(nb)) {
+      const size_t d = c + 1 - nb;
+      if (d < chunks) {
+        if ((status = int(cudaEventSynchronize(done[d % nb])))) break;
+        const size_t off = d * io::Staging::kChunk, len = std::min<size_t>(io::Staging::kChunk, bytes - off);
+        memcpy_parallel(out + off, st.buf[d % nb], int64_t(len));
+      }
+    }
+  }
+  for (auto& e : done)
+    if (e) cudaEventDestroy(e);
+  return status;
+}
+
 // The host entry points run on a per-(thread, device) pair of non-blocking
 // streams created once: creating and destroying a stream per call cost more
 // than a small call's copies and kernel.  The guard only drains the stream.
@@ -792,16 +883,16 @@ static int host_gradient_common(int kind, const double* a, const double* b, int6
   int32_t* derr = reinterpret_cast<int32_t*>(dout + out_elems);
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
   if (kind == 0) {
-    DIVUQ_CUDA(cudaMemcpyAsync(din, a, size_t(n) * 8, cudaMemcpyHostToDevice, sg.s));
-    DIVUQ_CUDA(cudaMemcpyAsync(din + n, b, size_t(n) * 8, cudaMemcpyHostToDevice, sg.s));
+    DIVUQ_CUDA(h2d(din, a, size_t(n) * 8, sg.s));
+    DIVUQ_CUDA(h2d(din + n, b, size_t(n) * 8, sg.s));
     if (int r = divuq_velocity_magnitude_f64(din, din + n, n, dout, derr, sg.s)) return r;
   } else {
-    DIVUQ_CUDA(cudaMemcpyAsync(din, a, size_t(in_elems) * 8, cudaMemcpyHostToDevice, sg.s));
+    DIVUQ_CUDA(h2d(din, a, size_t(in_elems) * 8, sg.s));
     const int r = kind == 1 ? divuq_gradient2d_f64(din, nx, ny, dx, dy, dout, derr, sg.s)
                             : divuq_gradient_ensemble2d_f64(din, M, nx, ny, dx, dy, dout, derr, sg.s);
     if (r) return r;
   }
-  DIVUQ_CUDA(cudaMemcpyAsync(out, dout, size_t(out_elems) * 8, cudaMemcpyDeviceToHost, sg.s));
+  DIVUQ_CUDA(d2h(out, dout, size_t(out_elems) * 8, sg.s));
   int status = 0;
   DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
   return status;
@@ -1273,11 +1364,11 @@ int divuq_host_propagate2d_f64(const double* mu_u, const double* mu_v, const dou
   double* outs[4] = {base + 4 * n, base + 5 * n, base + 6 * n, base + 7 * n};
   int32_t* derr = reinterpret_cast<int32_t*>(base + 8 * n);
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
-  DIVUQ_CUDA(cudaMemcpyAsync(dmu, mu_u, b, cudaMemcpyHostToDevice, sg.s));
-  DIVUQ_CUDA(cudaMemcpyAsync(dmv, mu_v, b, cudaMemcpyHostToDevice, sg.s));
+  DIVUQ_CUDA(h2d(dmu, mu_u, b, sg.s));
+  DIVUQ_CUDA(h2d(dmv, mu_v, b, sg.s));
   if (has_sigma) {
-    DIVUQ_CUDA(cudaMemcpyAsync(dsu, s_u, b, cudaMemcpyHostToDevice, sg.s));
-    DIVUQ_CUDA(cudaMemcpyAsync(dsv, s_v, b, cudaMemcpyHostToDevice, sg.s));
+    DIVUQ_CUDA(h2d(dsu, s_u, b, sg.s));
+    DIVUQ_CUDA(h2d(dsv, s_v, b, sg.s));
   }
   double* host_out[4] = {out_mu, out_sigma, out_p_src, out_p_snk};
   int r = propagate2d<double>(dmu, dmv, has_sigma ? dsu : nullptr, has_sigma ? dsv : nullptr, nx, ny,
@@ -1286,7 +1377,7 @@ int divuq_host_propagate2d_f64(const double* mu_u, const double* mu_v, const dou
                               sg.s);
   if (r) return r;
   for (int q = 0; q < 4; ++q)
-    if (host_out[q]) DIVUQ_CUDA(cudaMemcpyAsync(host_out[q], outs[q], b, cudaMemcpyDeviceToHost, sg.s));
+    if (host_out[q]) DIVUQ_CUDA(d2h(host_out[q], outs[q], b, sg.s));
   int status = 0;
   DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
   return status;
@@ -1305,13 +1396,13 @@ int divuq_host_tail_probs_f64(const double* mu, const double* sigma, int64_t n, 
   double* base = d.as<double>();
   int32_t* derr = reinterpret_cast<int32_t*>(base + 4 * n);
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
-  DIVUQ_CUDA(cudaMemcpyAsync(base, mu, b, cudaMemcpyHostToDevice, sg.s));
-  DIVUQ_CUDA(cudaMemcpyAsync(base + n, sigma, b, cudaMemcpyHostToDevice, sg.s));
+  DIVUQ_CUDA(h2d(base, mu, b, sg.s));
+  DIVUQ_CUDA(h2d(base + n, sigma, b, sg.s));
   if (int r = tail_probs<double>(base, base + n, n, theta, out_below ? base + 2 * n : nullptr,
                                  out_above ? base + 3 * n : nullptr, derr, sg.s))
     return r;
-  if (out_below) DIVUQ_CUDA(cudaMemcpyAsync(out_below, base + 2 * n, b, cudaMemcpyDeviceToHost, sg.s));
-  if (out_above) DIVUQ_CUDA(cudaMemcpyAsync(out_above, base + 3 * n, b, cudaMemcpyDeviceToHost, sg.s));
+  if (out_below) DIVUQ_CUDA(d2h(out_below, base + 2 * n, b, sg.s));
+  if (out_above) DIVUQ_CUDA(d2h(out_above, base + 3 * n, b, sg.s));
   int status = 0;
   DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
   return status;
@@ -1332,10 +1423,10 @@ int divuq_host_lcp2d_f64(const double* mu, const double* sigma, int64_t nx, int6
   double* dout = dsg + n;
   int32_t* derr = reinterpret_cast<int32_t*>(dout + nc);
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
-  DIVUQ_CUDA(cudaMemcpyAsync(dmu, mu, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, sg.s));
-  DIVUQ_CUDA(cudaMemcpyAsync(dsg, sigma, size_t(n) * sizeof(double), cudaMemcpyHostToDevice, sg.s));
+  DIVUQ_CUDA(h2d(dmu, mu, size_t(n) * sizeof(double), sg.s));
+  DIVUQ_CUDA(h2d(dsg, sigma, size_t(n) * sizeof(double), sg.s));
   if (int r = divuq_lcp2d_f64(dmu, dsg, nx, ny, isovalue, dout, derr, sg.s)) return r;
-  DIVUQ_CUDA(cudaMemcpyAsync(out, dout, size_t(nc) * sizeof(double), cudaMemcpyDeviceToHost, sg.s));
+  DIVUQ_CUDA(d2h(out, dout, size_t(nc) * sizeof(double), sg.s));
   int status = 0;
   DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
   return status;
@@ -1355,10 +1446,10 @@ int divuq_host_cell_crossing_f64(const double* mu4, const double* sigma4, int64_
   double* dout = dsg + 4 * n_cells;
   int32_t* derr = reinterpret_cast<int32_t*>(dout + n_cells);
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
-  DIVUQ_CUDA(cudaMemcpyAsync(dmu, mu4, size_t(4 * n_cells) * sizeof(double), cudaMemcpyHostToDevice, sg.s));
-  DIVUQ_CUDA(cudaMemcpyAsync(dsg, sigma4, size_t(4 * n_cells) * sizeof(double), cudaMemcpyHostToDevice, sg.s));
+  DIVUQ_CUDA(h2d(dmu, mu4, size_t(4 * n_cells) * sizeof(double), sg.s));
+  DIVUQ_CUDA(h2d(dsg, sigma4, size_t(4 * n_cells) * sizeof(double), sg.s));
   if (int r = divuq_cell_crossing_f64(dmu, dsg, n_cells, isovalue, dout, derr, sg.s)) return r;
-  DIVUQ_CUDA(cudaMemcpyAsync(out, dout, size_t(n_cells) * sizeof(double), cudaMemcpyDeviceToHost, sg.s));
+  DIVUQ_CUDA(d2h(out, dout, size_t(n_cells) * sizeof(double), sg.s));
   int status = 0;
   DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
   return status;
@@ -1379,10 +1470,10 @@ int divuq_host_fit_gaussian_f64(const double* members, int64_t M, int64_t C, int
   double* dsg = dmu + C * N;
   int32_t* derr = reinterpret_cast<int32_t*>(dsg + C * N);
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
-  DIVUQ_CUDA(cudaMemcpyAsync(dm, members, in_b, cudaMemcpyHostToDevice, sg.s));
+  DIVUQ_CUDA(h2d(dm, members, in_b, sg.s));
   if (int r = fit_gaussian<double>(dm, M, C, N, dmu, dsg, derr, sg.s)) return r;
-  DIVUQ_CUDA(cudaMemcpyAsync(out_mu, dmu, out_b, cudaMemcpyDeviceToHost, sg.s));
-  DIVUQ_CUDA(cudaMemcpyAsync(out_sigma, dsg, out_b, cudaMemcpyDeviceToHost, sg.s));
+  DIVUQ_CUDA(d2h(out_mu, dmu, out_b, sg.s));
+  DIVUQ_CUDA(d2h(out_sigma, dsg, out_b, sg.s));
   int status = 0;
   DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
   return status;
@@ -1410,7 +1501,7 @@ int divuq_host_ensemble_divergence2d_f32(const float* members, int64_t M, int64_
   float* mom_sg = o + 6 * n;      // (2, n)
   int32_t* derr = reinterpret_cast<int32_t*>(o + 8 * n);
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
-  DIVUQ_CUDA(cudaMemcpyAsync(dm, members, in_b, cudaMemcpyHostToDevice, sg.s));
+  DIVUQ_CUDA(h2d(dm, members, in_b, sg.s));
   float* host_out[4] = {out_mu, out_sigma, out_p_src, out_p_snk};
   int r = divuq_ensemble_divergence2d_f32(dm, M, nx, ny, dx, dy, t, out_mu ? outs[0] : nullptr,
                                           out_sigma ? outs[1] : nullptr, out_p_src ? outs[2] : nullptr,
@@ -1418,10 +1509,10 @@ int divuq_host_ensemble_divergence2d_f32(const float* members, int64_t M, int64_
                                           out_mom_mu ? mom_sg : nullptr, derr, sg.s);
   if (r) return r;
   for (int q = 0; q < 4; ++q)
-    if (host_out[q]) DIVUQ_CUDA(cudaMemcpyAsync(host_out[q], outs[q], b, cudaMemcpyDeviceToHost, sg.s));
+    if (host_out[q]) DIVUQ_CUDA(d2h(host_out[q], outs[q], b, sg.s));
   if (out_mom_mu) {
-    DIVUQ_CUDA(cudaMemcpyAsync(out_mom_mu, mom_mu, 2 * b, cudaMemcpyDeviceToHost, sg.s));
-    DIVUQ_CUDA(cudaMemcpyAsync(out_mom_sigma, mom_sg, 2 * b, cudaMemcpyDeviceToHost, sg.s));
+    DIVUQ_CUDA(d2h(out_mom_mu, mom_mu, 2 * b, sg.s));
+    DIVUQ_CUDA(d2h(out_mom_sigma, mom_sg, 2 * b, sg.s));
   }
   int status = 0;
   DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
@@ -1449,15 +1540,15 @@ int divuq_host_mc_divergence2d_f64(const double* mu_u, const double* mu_v, const
   int32_t* derr = reinterpret_cast<int32_t*>(base + 6 * n);
   void* dscr = reinterpret_cast<char*>(base + 6 * n) + 256;
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
-  DIVUQ_CUDA(cudaMemcpyAsync(dmu, mu_u, b, cudaMemcpyHostToDevice, sg.s));
-  DIVUQ_CUDA(cudaMemcpyAsync(dmv, mu_v, b, cudaMemcpyHostToDevice, sg.s));
-  DIVUQ_CUDA(cudaMemcpyAsync(dsu, s_u, b, cudaMemcpyHostToDevice, sg.s));
-  DIVUQ_CUDA(cudaMemcpyAsync(dsv, s_v, b, cudaMemcpyHostToDevice, sg.s));
+  DIVUQ_CUDA(h2d(dmu, mu_u, b, sg.s));
+  DIVUQ_CUDA(h2d(dmv, mu_v, b, sg.s));
+  DIVUQ_CUDA(h2d(dsu, s_u, b, sg.s));
+  DIVUQ_CUDA(h2d(dsv, s_v, b, sg.s));
   int r = divuq_mc_divergence2d_f64(dmu, dmv, dsu, dsv, nx, ny, dx, dy, n_samples, seed, 0, ny, dmean,
                                     dstd, dscr, derr, sg.s);
   if (r) return r;
-  DIVUQ_CUDA(cudaMemcpyAsync(out_mean, dmean, b, cudaMemcpyDeviceToHost, sg.s));
-  DIVUQ_CUDA(cudaMemcpyAsync(out_std, dstd, b, cudaMemcpyDeviceToHost, sg.s));
+  DIVUQ_CUDA(d2h(out_mean, dmean, b, sg.s));
+  DIVUQ_CUDA(d2h(out_std, dstd, b, sg.s));
   int status = 0;
   DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
   return status;
@@ -1485,12 +1576,12 @@ int divuq_host_mc_divergence2d_ref_f64(const double* mu_u, const double* mu_v, c
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
   const double* src[4] = {mu_u, mu_v, s_u, s_v};
   for (int q = 0; q < 4; ++q)
-    DIVUQ_CUDA(cudaMemcpyAsync(base + q * n, src[q], b, cudaMemcpyHostToDevice, sg.s));
+    DIVUQ_CUDA(h2d(base + q * n, src[q], b, sg.s));
   int r = divuq_mc_divergence2d_ref_f64(base, base + n, base + 2 * n, base + 3 * n, nx, ny, dx, dy,
                                         n_samples, seed, 0, ny, base + 4 * n, base + 5 * n, derr, sg.s);
   if (r) return r;
-  DIVUQ_CUDA(cudaMemcpyAsync(out_mean, base + 4 * n, b, cudaMemcpyDeviceToHost, sg.s));
-  DIVUQ_CUDA(cudaMemcpyAsync(out_std, base + 5 * n, b, cudaMemcpyDeviceToHost, sg.s));
+  DIVUQ_CUDA(d2h(out_mean, base + 4 * n, b, sg.s));
+  DIVUQ_CUDA(d2h(out_std, base + 5 * n, b, sg.s));
   int status = 0;
   DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
   return status;
@@ -1521,9 +1612,9 @@ int divuq_host_mc_histogram1d_f64(const double* neighbors, double dx, double dy,
   if (int r = divuq_sample_divergence1d_f64(neighbors, dx, dy, n_samples, seed, vals, sg.s)) return r;
   if (int r = divuq_minmax_f64(vals, n_samples, mm, scratch, sg.s)) return r;
   double lohi[2];
-  DIVUQ_CUDA(cudaMemcpyAsync(lohi, mm, sizeof(lohi), cudaMemcpyDeviceToHost, sg.s));
+  DIVUQ_CUDA(d2h(lohi, mm, sizeof(lohi), sg.s));
   DIVUQ_CUDA(cudaStreamSynchronize(sg.s));
-  if (out_values) DIVUQ_CUDA(cudaMemcpyAsync(out_values, vals, vb, cudaMemcpyDeviceToHost, sg.s));
+  if (out_values) DIVUQ_CUDA(d2h(out_values, vals, vb, sg.s));
   if (lohi[0] == lohi[1]) {   // all draws identical: one-bin degenerate histogram (mc.py:135-137)
     out_edges[0] = lohi[0] - 0.5;
     out_edges[1] = lohi[1] + 0.5;
