@@ -242,6 +242,23 @@ int divuq_host_propagate3d_f32(const float* mu_u, const float* mu_v, const float
                                float* out_mu, float* out_sigma,
                                float* out_p_src, float* out_p_snk,
                                int64_t chunk_planes, int device);
+/* 3D fused ensemble (config 4) from host buffers, for one rank's z-slab:
+ * members (M, 3, nx*ny*nz_local) covering global planes [z0, z0+nz_local) of
+ * nz_global; ghost_lo_w / ghost_hi_w point at the w component of global plane
+ * z0-1 / z0+nz_local for member 0 (member m at + m*ghost_member_stride
+ * floats), required when that plane exists.  Three-stream z-chunk pipeline;
+ * each member byte crosses PCIe once.  Host form of K3 3D: fit_gaussian
+ * (gaussian.py:35-45) then the z-extended stencil (stencils.py:46-51, no
+ * reference 3D code) and the tail probabilities, per slab. */
+int divuq_host_ensemble_divergence3d_f32(const float* members, int64_t n_members,
+                                         int64_t nx, int64_t ny, int64_t nz_local,
+                                         int64_t z0, int64_t nz_global,
+                                         const float* ghost_lo_w, const float* ghost_hi_w,
+                                         int64_t ghost_member_stride,
+                                         double dx, double dy, double dz, double t,
+                                         float* out_mu, float* out_sigma,
+                                         float* out_p_src, float* out_p_snk,
+                                         int64_t chunk_planes, int device);
 int divuq_host_tail_probs_f64(const double* mu, const double* sigma, int64_t n, double theta,
                               double* out_below, double* out_above, int device);
 int divuq_host_lcp2d_f64(const double* mu, const double* sigma, int64_t nx, int64_t ny,

@@ -26,6 +26,7 @@ from .api import (
     Propagation,
     divergence_deterministic,
     ensemble_divergence,
+    ensemble_divergence3d,
     error_metrics,
     fit_gaussian,
     mc_divergence,
@@ -64,7 +65,7 @@ __all__ = [
     "BenchReport", "bench", "parallel_map", "Ensemble2", "EnsembleDivergence", "GaussianScalarField", "GaussianScalarField3",
     "GaussianVectorField", "GaussianVectorField3", "LcpField", "McConfig", "McDivergenceEstimate", "McHistogram",
     "ParallelConfig", "Propagation", "ScalarField2", "UniformGrid2", "UniformGrid3",
-    "VectorField2", "cell_crossing_probability", "divergence_deterministic", "ensemble_divergence", "error_metrics",
+    "VectorField2", "cell_crossing_probability", "divergence_deterministic", "ensemble_divergence", "ensemble_divergence3d", "error_metrics",
     "fit_gaussian", "gradient", "gradient_ensemble", "lcp", "mc_divergence", "mc_histogram_1d",
     "sample_divergence_1d",
     "velocity_magnitude", "propagate_divergence", "propagate_with_probabilities",

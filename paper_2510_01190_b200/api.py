@@ -29,6 +29,7 @@ from .types import (
     McHistogram,
     ParallelConfig,
     ScalarField2,
+    UniformGrid3,
     VectorField2,
 )
 
@@ -290,6 +291,50 @@ def ensemble_divergence(ensemble: Ensemble2, t: float = 0.0) -> EnsembleDivergen
     model = GaussianVectorField(g, mom_mu[0], mom_mu[1], mom_sg[0], mom_sg[1])
     return EnsembleDivergence(model, GaussianScalarField(g, o[0], o[1]), o[2].astype(np.float64),
                               o[3].astype(np.float64))
+
+
+def _wplanes(a, m, plane):
+    """(M, plane) fp32 w-component planes -> (array, member stride in floats);
+    a row-strided view (e.g. members[:, 2, k*plane:(k+1)*plane]) is passed
+    without a copy."""
+    a = np.asarray(a)
+    if a.shape != (m, plane):
+        raise ValueError(f"ghost planes must have shape ({m}, {plane})")
+    if a.dtype != np.float32 or a.strides[1] != 4 or a.strides[0] % 4:
+        a = np.ascontiguousarray(a, dtype=np.float32)
+    return a, a.strides[0] // 4
+
+
+def ensemble_divergence3d(members, grid: UniformGrid3, t: float = 0.0, *, z0: int = 0,
+                          nz_global: int | None = None, ghost_lo=None, ghost_hi=None,
+                          chunk_planes: int = 0) -> Propagation:
+    """Fused fp32 3D ensemble pipeline (BASELINE config 4) from host buffers.
+
+    members: (M, 3, nx*ny*nz) with grid the slab's grid (nz planes), covering
+    global planes [z0, z0+nz) of nz_global (default: the slab is the whole
+    volume).  ghost_lo / ghost_hi: (M, nx*ny) w-component member planes at
+    global z0-1 / z0+nz, required when those planes exist.  The member data
+    crosses PCIe once in a 3-stream z-chunk pipeline."""
+    g = grid
+    plane = g.nx * g.ny
+    mem = np.asarray(members)
+    if mem.ndim != 3 or mem.shape[1:] != (3, g.n_vertices):
+        raise ValueError(f"members must have shape (M, 3, {g.n_vertices})")
+    mem = np.ascontiguousarray(mem, dtype=np.float32)
+    m = mem.shape[0]
+    nzg = g.nz if nz_global is None else int(nz_global)
+    lo, lo_s = _wplanes(ghost_lo, m, plane) if ghost_lo is not None else (None, plane)
+    hi, hi_s = _wplanes(ghost_hi, m, plane) if ghost_hi is not None else (None, plane)
+    if lo is not None and hi is not None and lo_s != hi_s:
+        lo = np.ascontiguousarray(lo)
+        hi = np.ascontiguousarray(hi)
+        lo_s = hi_s = plane
+    stride = lo_s if lo is not None else hi_s
+    o = [np.empty(g.n_vertices, dtype=np.float32) for _ in range(4)]
+    _check(lib.divuq_host_ensemble_divergence3d_f32(
+        _p(mem), m, g.nx, g.ny, g.nz, int(z0), nzg, _p(lo), _p(hi), stride, float(g.dx),
+        float(g.dy), float(g.dz), float(t), *(_p(a) for a in o), int(chunk_planes), _DEVICE))
+    return Propagation(GaussianScalarField3(g, o[0], o[1]), o[2], o[3])
 
 
 def velocity_magnitude(member: VectorField2) -> ScalarField2:

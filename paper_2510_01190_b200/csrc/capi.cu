@@ -851,10 +851,10 @@ int d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
 // streams created once: creating and destroying a stream per call cost more
 // than a small call's copies and kernel.  The guard only drains the stream.
 cudaError_t cached_stream(int slot, cudaStream_t* out) {
-  thread_local cudaStream_t streams[64][2] = {};
+  thread_local cudaStream_t streams[64][3] = {};
   int dev = 0;
   if (cudaError_t e = cudaGetDevice(&dev)) return e;
-  if (dev >= 64 || slot < 0 || slot > 1) return cudaStreamCreateWithFlags(out, cudaStreamNonBlocking);
+  if (dev >= 64 || slot < 0 || slot > 2) return cudaStreamCreateWithFlags(out, cudaStreamNonBlocking);
   if (!streams[dev][slot])
     if (cudaError_t e = cudaStreamCreateWithFlags(&streams[dev][slot], cudaStreamNonBlocking)) return e;
   *out = streams[dev][slot];
@@ -1747,6 +1747,142 @@ int divuq_host_propagate3d_f32(const float* mu_u, const float* mu_v, const float
   DIVUQ_CUDA(cudaStreamSynchronize(sg[1].s));
   int status = 0;
   DIVUQ_CUDA(check_err_word(derr, sg[0].s, &status));
+  return status;
+}
+
+// 3D fused ensemble from host buffers: the end-to-end form of config 4 (one
+// rank's z-slab).  members: (M, 3, nx*ny*nz_local) host fp32; the slab covers
+// global planes [z0, z0 + nz_local) of nz_global.  ghost_lo_w / ghost_hi_w:
+// the w component of global planes z0-1 / z0+nz_local for member 0, member m
+// at + m * ghost_member_stride floats (required when that neighbour exists).
+// z-chunk pipeline over three cached streams -- copy-in, compute, copy-out --
+// and four buffer sets.  A chunk's reduced w halos are fitted from the
+// NEIGHBOUR chunks' edge planes already resident in HBM, so every member byte
+// crosses PCIe exactly once; the compute stream only waits for the upload of
+// chunk c+1 (its hi ghost), and the fourth set keeps the copy engine busy
+// meanwhile.
+int divuq_host_ensemble_divergence3d_f32(const float* members, int64_t M, int64_t nx, int64_t ny,
+                                         int64_t nz_local, int64_t z0, int64_t nz_global,
+                                         const float* ghost_lo_w, const float* ghost_hi_w,
+                                         int64_t ghost_member_stride, double dx, double dy,
+                                         double dz, double t, float* out_mu, float* out_sigma,
+                                         float* out_p_src, float* out_p_snk, int64_t chunk_planes,
+                                         int device) {
+  if (int r = grid_ok(nx, ny, dx, dy)) return r;
+  if (nz_global < 2 || !(dz > 0.0)) return DIVUQ_EGRID;
+  if (!members || nz_local < 1 || z0 < 0 || z0 + nz_local > nz_global) return DIVUQ_EINVAL;
+  if (M < 2) return DIVUQ_EMEMBERS;
+  const int64_t plane = nx * ny;
+  const bool has_lo = z0 > 0, has_hi = z0 + nz_local < nz_global;
+  if ((has_lo && !ghost_lo_w) || (has_hi && !ghost_hi_w)) return DIVUQ_EINVAL;
+  if ((has_lo || has_hi) && ghost_member_stride < plane) return DIVUQ_EINVAL;
+  DIVUQ_CUDA(cudaSetDevice(device));
+  const size_t plane_b = size_t(plane) * sizeof(float);
+  constexpr int kSets = 4;
+  constexpr int64_t kChunkTarget = int64_t(1) << 30;   // member bytes per chunk
+  int64_t cz = chunk_planes > 0 ? chunk_planes
+                                : std::max<int64_t>(1, kChunkTarget / int64_t(3 * M * plane_b));
+  cz = std::min(cz, nz_local);
+  const int64_t nch = (nz_local + cz - 1) / cz;
+  float* host_out[4] = {out_mu, out_sigma, out_p_src, out_p_snk};
+  // set: members (M, 3, cz planes) | halo mu_lo s_lo mu_hi s_hi | 4 outputs (cz planes)
+  const int64_t set_elems = 3 * M * cz * plane + 4 * plane + 4 * cz * plane;
+  const int64_t ghost_elems = (has_lo || has_hi) ? 2 * M * plane : 0;
+  const int nsets = int(std::min<int64_t>(kSets, nch));
+  StreamGuard cin, cmp, cout;
+  DIVUQ_CUDA(cached_stream(0, &cin.s));
+  DIVUQ_CUDA(cached_stream(1, &cmp.s));
+  DIVUQ_CUDA(cached_stream(2, &cout.s));
+  DevBuf d;
+  DIVUQ_CUDA(d.alloc(size_t(nsets * set_elems + ghost_elems) * sizeof(float) + 256, cin.s));
+  float* ghost = d.as<float>() + nsets * set_elems;
+  int32_t* derr = reinterpret_cast<int32_t*>(ghost + ghost_elems);
+  DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), cin.s));
+  struct Events {
+    cudaEvent_t up[kSets] = {}, comp[kSets] = {}, out[kSets] = {};
+    ~Events() {
+      for (int i = 0; i < kSets; ++i)
+        for (cudaEvent_t e : {up[i], comp[i], out[i]})
+          if (e) cudaEventDestroy(e);
+    }
+  } ev;
+  for (int i = 0; i < kSets; ++i) {
+    DIVUQ_CUDA(cudaEventCreateWithFlags(&ev.up[i], cudaEventDisableTiming));
+    DIVUQ_CUDA(cudaEventCreateWithFlags(&ev.comp[i], cudaEventDisableTiming));
+    DIVUQ_CUDA(cudaEventCreateWithFlags(&ev.out[i], cudaEventDisableTiming));
+  }
+  for (int side = 0; side < 2; ++side) {   // slab ghosts: the w member planes only
+    const float* g = side ? ghost_hi_w : ghost_lo_w;
+    if (!(side ? has_hi : has_lo)) continue;
+    for (int64_t m = 0; m < M; ++m)
+      DIVUQ_CUDA(cudaMemcpyAsync(ghost + (side * M + m) * plane, g + m * ghost_member_stride, plane_b,
+                                 cudaMemcpyHostToDevice, cin.s));
+  }
+  auto zc = [&](int64_t c) { return c * cz; };
+  auto nzl = [&](int64_t c) { return std::min(cz, nz_local - c * cz); };
+  auto set = [&](int64_t c) { return d.as<float>() + (c % kSets) * set_elems; };
+  auto upload = [&](int64_t c) -> int {
+    if (c >= kSets) DIVUQ_CUDA(cudaStreamWaitEvent(cin.s, ev.comp[(c - 3) % kSets], 0));
+    const size_t row_b = size_t(nzl(c)) * plane_b;
+    for (int64_t r = 0; r < 3 * M; ++r)   // rows (member, component)
+      DIVUQ_CUDA(cudaMemcpyAsync(set(c) + r * nzl(c) * plane, members + (r * nz_local + zc(c)) * plane,
+                                 row_b, cudaMemcpyHostToDevice, cin.s));
+    DIVUQ_CUDA(cudaEventRecord(ev.up[c % kSets], cin.s));
+    return 0;
+  };
+  auto compute = [&](int64_t c) -> int {
+    DIVUQ_CUDA(cudaStreamWaitEvent(cmp.s, ev.up[(c + 1 < nch ? c + 1 : c) % kSets], 0));
+    if (c >= kSets) DIVUQ_CUDA(cudaStreamWaitEvent(cmp.s, ev.out[c % kSets], 0));
+    float* s = set(c);
+    float* halo = s + 3 * M * cz * plane;
+    const float* lo = nullptr; int64_t lo_stride = plane;
+    const float* hi = nullptr; int64_t hi_stride = plane;
+    if (c > 0) {   // last plane of chunk c-1, component w
+      lo = set(c - 1) + (2 * nzl(c - 1) + nzl(c - 1) - 1) * plane;
+      lo_stride = 3 * nzl(c - 1) * plane;
+    } else if (has_lo) {
+      lo = ghost;
+    }
+    if (c + 1 < nch) {   // first plane of chunk c+1, component w
+      hi = set(c + 1) + 2 * nzl(c + 1) * plane;
+      hi_stride = 3 * nzl(c + 1) * plane;
+    } else if (has_hi) {
+      hi = ghost + M * plane;
+    }
+    if (lo)
+      if (int r = fit_gaussian<float>(lo, M, 1, plane, halo, halo + plane, derr, cmp.s, lo_stride)) return r;
+    if (hi)
+      if (int r = fit_gaussian<float>(hi, M, 1, plane, halo + 2 * plane, halo + 3 * plane, derr, cmp.s,
+                                      hi_stride))
+        return r;
+    float* outs = halo + 4 * plane;
+    float* o[4];
+    for (int q = 0; q < 4; ++q) o[q] = host_out[q] ? outs + q * cz * plane : nullptr;
+    if (int r = divuq_ensemble_divergence3d_f32(
+            s, M, lo ? halo : nullptr, lo ? halo + plane : nullptr, hi ? halo + 2 * plane : nullptr,
+            hi ? halo + 3 * plane : nullptr, nx, ny, nzl(c), z0 + zc(c), nz_global, 0, nzl(c), dx, dy, dz,
+            t, o[0], o[1], o[2], o[3], nullptr, nullptr, derr, cmp.s))
+      return r;
+    DIVUQ_CUDA(cudaEventRecord(ev.comp[c % kSets], cmp.s));
+    DIVUQ_CUDA(cudaStreamWaitEvent(cout.s, ev.comp[c % kSets], 0));
+    for (int q = 0; q < 4; ++q)
+      if (host_out[q])
+        DIVUQ_CUDA(cudaMemcpyAsync(host_out[q] + zc(c) * plane, o[q], size_t(nzl(c)) * plane_b,
+                                   cudaMemcpyDeviceToHost, cout.s));
+    DIVUQ_CUDA(cudaEventRecord(ev.out[c % kSets], cout.s));
+    return 0;
+  };
+  if (int r = upload(0)) return r;
+  for (int64_t c = 1; c < nch; ++c) {
+    if (int r = upload(c)) return r;
+    if (int r = compute(c - 1)) return r;
+  }
+  if (int r = compute(nch - 1)) return r;
+  DIVUQ_CUDA(cudaStreamSynchronize(cin.s));
+  DIVUQ_CUDA(cudaStreamSynchronize(cmp.s));
+  DIVUQ_CUDA(cudaStreamSynchronize(cout.s));
+  int status = 0;
+  DIVUQ_CUDA(check_err_word(derr, cmp.s, &status));
   return status;
 }
 

@@ -371,6 +371,43 @@ def test_ensemble_divergence3d_and_slabs(dev, m, rng):
                 assert np.array_equal(host(o[k]), host(full[k])[z0 * plane:z1 * plane]), (parts, r, k)
 
 
+@pytest.mark.parametrize("chunk", [0, 1, 3, 5])
+def test_host_ensemble_divergence3d_pipeline(dev, chunk, rng):
+    """Host-buffer 3D ensemble entry (3-stream z-chunk pipeline, halos fitted
+    from the neighbour chunks in HBM) == the device fused kernel, bitwise, for
+    any chunking and for slabs fed host ghost planes (strided views)."""
+    import paper_2510_01190_b200 as d
+
+    nx, ny, nz, m = 48, 10, 13, 6
+    plane = nx * ny
+    n = plane * nz
+    mem = (rng.normal(0, 1, (1, 3, n)) + rng.normal(0, 0.3, (m, 3, n))).astype(np.float32)
+    full = dev.ensemble_divergence3d(cu(mem), nx, ny, nz, 1.0, 0.5, 2.0, 0.1)
+    g = d.UniformGrid3(nx, ny, nz, 1.0, 0.5, 2.0)
+    r = d.ensemble_divergence3d(mem, g, 0.1, chunk_planes=chunk)
+    got = {"mu": r.field.mu, "sigma": r.field.sigma, "p_src": r.p_src, "p_snk": r.p_snk}
+    for k in ("mu", "sigma", "p_src", "p_snk"):
+        assert np.array_equal(got[k], host(full[k])), (chunk, k)
+    mu_r, sg_r = ref2d.fit_moments(mem)
+    dmu, dsg = ref3d.propagate3d(*mu_r, *sg_r, nx, ny, nz, 1.0, 0.5, 2.0)
+    assert normwise(got["mu"], dmu) <= 1e-5 and normwise(got["sigma"], dsg) <= 1e-5
+    # z-slabs with host ghost planes, ghosts passed as strided views of mem
+    bounds = [0, 4, 9, nz]
+    for z0, z1 in zip(bounds[:-1], bounds[1:]):
+        sl = np.ascontiguousarray(mem[:, :, z0 * plane:z1 * plane])
+        lo = mem[:, 2, (z0 - 1) * plane:z0 * plane] if z0 else None
+        hi = mem[:, 2, z1 * plane:(z1 + 1) * plane] if z1 < nz else None
+        gs = d.UniformGrid3(nx, ny, z1 - z0, 1.0, 0.5, 2.0)
+        rs = d.ensemble_divergence3d(sl, gs, 0.1, z0=z0, nz_global=nz, ghost_lo=lo, ghost_hi=hi,
+                                     chunk_planes=chunk)
+        for k, a in (("mu", rs.field.mu), ("sigma", rs.field.sigma), ("p_src", rs.p_src),
+                     ("p_snk", rs.p_snk)):
+            assert np.array_equal(a, host(full[k])[z0 * plane:z1 * plane]), (chunk, z0, k)
+    with pytest.raises(ValueError):   # interior slab without its ghost planes
+        d.ensemble_divergence3d(mem[:, :, plane:3 * plane], d.UniformGrid3(nx, ny, 2, 1.0, 0.5, 2.0),
+                                z0=1, nz_global=nz)
+
+
 # --------------------------------------------------------------------------
 # Monte Carlo (K4)
 # --------------------------------------------------------------------------
