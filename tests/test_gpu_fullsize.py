@@ -128,6 +128,78 @@ def test_config4_full_width_slab_vs_oracle(dev):
     assert np.all(np.abs(o["p_snk"].cpu().numpy() - pk) <= 1e-5 * pk + 1e-6)
 
 
+def _config4_oracle_block(z0, z1, nx=1024, ny=1024, nz=1024, t=0.1):
+    """Oracle outputs of global planes [z0, z1) of config 4 (from a member block
+    one plane wider on each side, clipped at the global faces)."""
+    from paper_2510_01190_b200 import configs
+
+    plane = nx * ny
+    g0, g1 = max(0, z0 - 1), min(nz, z1 + 1)
+    host = configs.config4_slab(g0, g1 - g0, nx, ny, nz).cpu().numpy().astype(np.float64)
+    mu_r, sg_r = ref2d.fit_moments(host)
+    a, b = (z0 - g0) * plane, (z1 - g0) * plane
+    fields = [mu_r[c, a:b] for c in range(3)] + [sg_r[c, a:b] for c in range(3)]
+    lo = (mu_r[2, a - plane:a], sg_r[2, a - plane:a]) if z0 > 0 else None
+    hi = (mu_r[2, b:b + plane], sg_r[2, b:b + plane]) if z1 < nz else None
+    mu, sg = ref3d.propagate3d_slab(fields, lo, hi, nx, ny, z0, nz, 1.0, 1.0, 1.0)
+    return mu, sg, ref2d.source_probability(mu, sg, t), ref2d.sink_probability(mu, sg, t)
+
+
+def test_config4_full_volume_decompositions(dev):
+    """Config 4 at its full 1024^3 x M=16 size (206 GB of members, generated
+    slab by slab), run as the 2-, 4- and 8-rank z-slab decompositions one
+    rank after another on this GPU (same per-rank calls as bench.py: reduced
+    w-moment halos from the neighbour's edge plane).  Per-plane bit-pattern
+    checksums of all four maps must agree across the decompositions, and the
+    8-rank outputs at every shard boundary +-2 planes and at both global faces
+    (full x/y extent: faces and corners) must match the oracle."""
+    from paper_2510_01190_b200 import configs
+
+    nx = ny = nz = 1024
+    plane = nx * ny
+    keys = ("mu", "sigma", "p_src", "p_snk")
+    sums, kept = {}, {}
+    for parts in (8, 4, 2):
+        per = nz // parts
+        sums[parts] = torch.empty((4, nz), dtype=torch.int64)
+        for r in range(parts):
+            z0 = r * per
+            mem = configs.config4_slab(z0, per, nx, ny, nz)
+            lo = hi = None
+            if z0 > 0:
+                lo = dev.w_moments_plane(configs.config4_slab(z0 - 1, 1, nx, ny, nz), nx, ny, 1, 0)
+            if z0 + per < nz:
+                hi = dev.w_moments_plane(configs.config4_slab(z0 + per, 1, nx, ny, nz), nx, ny, 1, 0)
+            o = dev.ensemble_divergence3d(mem, nx, ny, per, 1.0, 1.0, 1.0, 0.1, z0=z0, nz_global=nz,
+                                          halo_lo=lo, halo_hi=hi)
+            del mem
+            for q, k in enumerate(keys):
+                bits = o[k].view(torch.int32).view(per, plane).to(torch.int64)
+                sums[parts][q, z0:z0 + per] = bits.sum(dim=1).cpu()
+            if parts == 8:
+                for za, zb in ((z0, z0 + 2), (z0 + per - 2, z0 + per)):
+                    kept[(za, zb)] = {k: o[k][(za - z0) * plane:(zb - z0) * plane].cpu().numpy()
+                                      for k in keys}
+            del o
+            torch.cuda.empty_cache()
+    assert torch.equal(sums[8], sums[4]) and torch.equal(sums[8], sums[2])
+    # oracle at every 8-rank shard boundary +-2 planes and at both global faces
+    blocks = []
+    for (za, zb), got in sorted(kept.items()):   # merge the two sides of each boundary
+        if blocks and blocks[-1][1] == za:
+            pa, _, pg = blocks.pop()
+            got = {k: np.concatenate([pg[k], got[k]]) for k in keys}
+            za = pa
+        blocks.append((za, zb, got))
+    assert len(blocks) == 9
+    for za, zb, got in blocks:
+        mu, sg, ps, pk = _config4_oracle_block(za, zb)
+        assert np.abs(got["mu"] - mu).max() <= 1e-5 * np.abs(mu).max(), (za, zb)
+        assert np.abs(got["sigma"] - sg).max() <= 1e-5 * np.abs(sg).max(), (za, zb)
+        assert np.all(np.abs(got["p_src"] - ps) <= 1e-5 * ps + 1e-6), (za, zb)
+        assert np.all(np.abs(got["p_snk"] - pk) <= 1e-5 * pk + 1e-6), (za, zb)
+
+
 def test_config2_mc_full_size_statistics(dev):
     from paper_2510_01190_b200 import configs
 
