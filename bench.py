@@ -2,7 +2,7 @@
 """Benchmark of the divergence-uncertainty hot path on B200 (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config {0..4}] [--impl {ours,reference}]
-    python bench.py --workload {lcp,gradient,ingest}     # SURVEY 8f rows, 1 GPU
+    python bench.py --workload {lcp,gradient,fit,ingest,redsea}   # SURVEY 8f rows, 1 GPU
 
 Default workload = BASELINE.json config 3 (the metric's "1/2/4/8 B200" config):
 3D analytic divergence mean + sigma + P(div>0) + P(div<0) on a 512^3 fp32
@@ -265,6 +265,54 @@ def run_next(args):
         cpu_thunk = (lambda: ref2d.gradient_ensemble(sub, 1024, 256, 1.0, 1.0), 4 * 256 * 1024, 1)
         cpu_sample = "numpy restatement (hypot + reference stencil), 4 members x 1024x256, 1 thread"
         dtype = "f64"
+    elif wl == "redsea":   # K6: the Red Sea pipeline fused (gradient prologue -> K3)
+        nx = ny = 1024
+        m = 20
+        mem = configs.config1_members(nx, ny, m, 101)
+        outs = {k: torch.empty(nx * ny, dtype=torch.float32, device="cuda") for k in dev.ALL_OUTPUTS}
+        units = nx * ny
+        bpu = 2 * m * 4 + 4 * 4   # M members x (u, v) fp32 in, four fp32 maps out
+        unit = "grid points/s"
+        metric = ("grid points/sec, velocity-magnitude-gradient ensemble -> divergence mean+var+"
+                  "P(div>0)+P(div<0) (gaussian.py:48-66 + 35-45, divergence.py, lcp.py:48-68), fp32")
+        workload = ("redsea: fused |v| -> gradient -> moments -> divergence -> tails on the config-1 "
+                    "velocity ensemble (M=20, 1024^2), fp32, one kernel")
+
+        def step():
+            dev.gradient_ensemble_divergence2d(mem, nx, ny, 1.0, 1.0, 0.0, out=outs, check=False)
+
+        # the same chain unfused (gradient ensemble written + re-read), for the record
+        grad = torch.empty_like(mem)
+
+        def composed():
+            dev.gradient_ensemble2d(mem, nx, ny, 1.0, 1.0, out=grad, check=False)
+            dev.ensemble_divergence2d(grad, nx, ny, 1.0, 1.0, 0.0, out=outs, check=False)
+
+        hin = mem.cpu().pin_memory()
+        hout = [torch.empty(units, dtype=torch.float32).pin_memory() for _ in range(4)]
+
+        def e2e_call():
+            st = lib.divuq_host_gradient_ensemble_divergence2d_f32(
+                hin.data_ptr(), m, nx, ny, 1.0, 1.0, 0.0, *(t.data_ptr() for t in hout), None, None, 0)
+            assert st == 0, st
+
+        h2d, d2h = m * 2 * 4 * units, 16 * units
+        import numpy as np
+
+        sub = hin.numpy()[:, :, : 1024 * 64].astype(np.float64)
+        from oracle import ref2d
+
+        def cpu_work():
+            g = ref2d.gradient_ensemble(sub, 1024, 64, 1.0, 1.0)
+            mu_f, sg_f = ref2d.fit_moments(g)
+            mu_d, sg_d = ref2d.propagate2d(mu_f[0], mu_f[1], sg_f[0], sg_f[1], 1024, 64, 1.0, 1.0)
+            ref2d.source_probability(mu_d, sg_d, 0.0)
+            ref2d.sink_probability(mu_d, sg_d, 0.0)
+
+        cpu_thunk = (cpu_work, 1024 * 64, 1)
+        cpu_sample = ("numpy restatement of gradient_ensemble -> fit_gaussian -> propagate -> both "
+                      "tails on a 1024x64 strip (all 20 members), fp64, 1 thread")
+        dtype = "f32"
     elif wl == "fit":   # K1: the drop-in fit_gaussian (gaussian.py:35-45), fp64 bitwise
         nx = ny = 1024
         m = 20
@@ -381,6 +429,16 @@ def run_next(args):
                     "frac": achieved / peak, "traffic": committed_traffic(wl),
                     "bytes_per_unit": bpu, "units_per_launch": units, "avg_launch_ms": ms,
                     "peak_source": peak_src}
+        if wl == "redsea":   # the unfused chain on the same input, same protocol
+            comp_ms = []
+            for _ in range(args.steps):
+                flush()
+                a = ev()
+                composed()
+                b = ev()
+                comp_ms.append((a, b))
+            torch.cuda.synchronize()
+            roofline["unfused_chain_ms"] = sum(a.elapsed_time(b) for a, b in comp_ms) / len(comp_ms)
         e2e_call()
         reps = 3
         t0 = time.perf_counter()
@@ -428,7 +486,8 @@ def main():
     ap.add_argument("--exchange", default="p2p", choices=("p2p", "nccl"),
                     help="z-slab halo exchange for configs 3/4 at N>1: peer memory read in "
                          "place by the kernels (p2p) or NCCL send/recv overlapped with the interior")
-    ap.add_argument("--workload", default=None, choices=("lcp", "gradient", "ingest", "fit"),
+    ap.add_argument("--workload", default=None,
+                    choices=("lcp", "gradient", "ingest", "fit", "redsea"),
                     help="a SURVEY 8f row instead of a BASELINE config (1 GPU, ours only)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

@@ -183,6 +183,20 @@ int divuq_ensemble_divergence3d_f32(const float* members, int64_t n_members,
                                     float* out_mom_mu, float* out_mom_sigma,
                                     int32_t* err_word, void* stream);
 
+/* ---- K6: fused Red Sea pipeline -----------------------------------------
+ * velocity_magnitude -> gradient_ensemble (gaussian.py:48-66) -> fit_gaussian
+ * (gaussian.py:35-45) -> propagate_divergence (divergence.py:48-70) -> tails
+ * (lcp.py:48-68) in one pass over (M, 2, nx*ny) fp32 velocity members.
+ * Equal bit for bit to divuq_gradient_ensemble2d_f32 followed by
+ * divuq_ensemble_divergence2d_f32.  out_mom_* (optional, (2, N)) receive the
+ * moments of the gradient ensemble. */
+int divuq_gradient_ensemble_divergence2d_f32(const float* members, int64_t n_members,
+                                             int64_t nx, int64_t ny, double dx, double dy,
+                                             double t, float* out_mu, float* out_sigma,
+                                             float* out_p_src, float* out_p_snk,
+                                             float* out_mom_mu, float* out_mom_sigma,
+                                             int32_t* err_word, void* stream);
+
 /* ---- K4: Monte Carlo estimator ------------------------------------------
  * Replaces mc_divergence (mc.py:94-117) with a Philox4x32-10 + Box-Muller
  * stream (contract: oracle/philox.py).  Inputs: the full grid model (fp64).
@@ -259,6 +273,12 @@ int divuq_host_ensemble_divergence3d_f32(const float* members, int64_t n_members
                                          float* out_mu, float* out_sigma,
                                          float* out_p_src, float* out_p_snk,
                                          int64_t chunk_planes, int device);
+int divuq_host_gradient_ensemble_divergence2d_f32(const float* members, int64_t n_members,
+                                                  int64_t nx, int64_t ny, double dx, double dy,
+                                                  double t, float* out_mu, float* out_sigma,
+                                                  float* out_p_src, float* out_p_snk,
+                                                  float* out_mom_mu, float* out_mom_sigma,
+                                                  int device);
 int divuq_host_tail_probs_f64(const double* mu, const double* sigma, int64_t n, double theta,
                               double* out_below, double* out_above, int device);
 int divuq_host_lcp2d_f64(const double* mu, const double* sigma, int64_t nx, int64_t ny,

@@ -21,6 +21,7 @@ from .api import (
     cell_crossing_probability,
     gradient,
     gradient_ensemble,
+    gradient_ensemble_divergence,
     lcp,
     velocity_magnitude,
     Propagation,
@@ -62,13 +63,15 @@ from .types import (
 __version__ = "0.1.0"
 
 __all__ = [
-    "BenchReport", "bench", "parallel_map", "Ensemble2", "EnsembleDivergence", "GaussianScalarField", "GaussianScalarField3",
-    "GaussianVectorField", "GaussianVectorField3", "LcpField", "McConfig", "McDivergenceEstimate", "McHistogram",
+    "BenchReport", "bench", "parallel_map", "Ensemble2", "EnsembleDivergence",
+    "GaussianScalarField", "GaussianScalarField3", "GaussianVectorField",
+    "GaussianVectorField3", "LcpField", "McConfig", "McDivergenceEstimate", "McHistogram",
     "ParallelConfig", "Propagation", "ScalarField2", "UniformGrid2", "UniformGrid3",
-    "VectorField2", "cell_crossing_probability", "divergence_deterministic", "ensemble_divergence", "ensemble_divergence3d", "error_metrics",
-    "fit_gaussian", "gradient", "gradient_ensemble", "lcp", "mc_divergence", "mc_histogram_1d",
-    "sample_divergence_1d",
-    "velocity_magnitude", "propagate_divergence", "propagate_with_probabilities",
-    "propagate_with_probabilities3d", "set_device", "sink_probability", "source_probability",
-    "stencil_distribution", "tail_probs", "vertex_index",
+    "VectorField2", "cell_crossing_probability", "divergence_deterministic",
+    "ensemble_divergence", "ensemble_divergence3d", "gradient_ensemble_divergence",
+    "error_metrics", "fit_gaussian", "gradient", "gradient_ensemble", "lcp", "mc_divergence",
+    "mc_histogram_1d", "sample_divergence_1d", "velocity_magnitude", "propagate_divergence",
+    "propagate_with_probabilities", "propagate_with_probabilities3d", "set_device",
+    "sink_probability", "source_probability", "stencil_distribution", "tail_probs",
+    "vertex_index",
 ]

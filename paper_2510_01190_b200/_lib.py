@@ -76,6 +76,10 @@ SIGNATURES = {
         _int, [_p] * 6 + [_i64] * 3 + [_f64] * 4 + [_p] * 4 + [_i64, _int]),
     "divuq_host_ensemble_divergence3d_f32": (
         _int, [_p] + [_i64] * 6 + [_p, _p, _i64] + [_f64] * 4 + [_p] * 4 + [_i64, _int]),
+    "divuq_gradient_ensemble_divergence2d_f32": (
+        _int, [_p, _i64, _i64, _i64, _f64, _f64, _f64] + [_p] * 6 + [_p, _p]),
+    "divuq_host_gradient_ensemble_divergence2d_f32": (
+        _int, [_p, _i64, _i64, _i64, _f64, _f64, _f64] + [_p] * 6 + [_int]),
     "divuq_host_fit_gaussian_f64": (_int, [_p, _i64, _i64, _i64, _p, _p, _int]),
     "divuq_host_ensemble_divergence2d_f32": (
         _int, [_p, _i64, _i64, _i64, _f64, _f64, _f64] + [_p] * 6 + [_int]),

@@ -337,6 +337,25 @@ def ensemble_divergence3d(members, grid: UniformGrid3, t: float = 0.0, *, z0: in
     return Propagation(GaussianScalarField3(g, o[0], o[1]), o[2], o[3])
 
 
+def gradient_ensemble_divergence(ensemble: Ensemble2, t: float = 0.0) -> EnsembleDivergence:
+    """The Red Sea pipeline in one fp32 pass: gradient_ensemble (velocity
+    magnitude gradient per member) -> fit_gaussian -> propagate_divergence ->
+    tail maps.  ``model`` of the result is the gradient ensemble's Gaussian fit."""
+    g = ensemble.grid
+    stacked = np.ascontiguousarray(ensemble.stacked(), dtype=np.float32)
+    m = stacked.shape[0]
+    n = g.n_vertices
+    o = [np.empty(n, dtype=np.float32) for _ in range(4)]
+    mom_mu = np.empty((2, n), dtype=np.float32)
+    mom_sg = np.empty((2, n), dtype=np.float32)
+    _check(lib.divuq_host_gradient_ensemble_divergence2d_f32(
+        _p(stacked), m, g.nx, g.ny, float(g.dx), float(g.dy), float(t), *(_p(a) for a in o),
+        _p(mom_mu), _p(mom_sg), _DEVICE))
+    model = GaussianVectorField(g, mom_mu[0], mom_mu[1], mom_sg[0], mom_sg[1])
+    return EnsembleDivergence(model, GaussianScalarField(g, o[0], o[1]), o[2].astype(np.float64),
+                              o[3].astype(np.float64))
+
+
 def velocity_magnitude(member: VectorField2) -> ScalarField2:
     """hypot(u, v) per vertex (gaussian.py:48-50)."""
     g = member.grid

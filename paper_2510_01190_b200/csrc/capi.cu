@@ -16,6 +16,7 @@
 #include "k3row.cuh"
 #include "divuq1.cuh"
 #include "gradient.cuh"
+#include "gradfused.cuh"
 #include "lcp.cuh"
 #include "mc.cuh"
 #include "stencil.cuh"
@@ -1177,6 +1178,41 @@ int divuq_ensemble_divergence2d_f32(const float* members, int64_t M, int64_t nx,
   return dispatch_vec<float, false, kEnsemble>(p, true, static_cast<cudaStream_t>(stream));
 }
 
+int divuq_gradient_ensemble_divergence2d_f32(const float* members, int64_t M, int64_t nx,
+                                             int64_t ny, double dx, double dy, double t,
+                                             float* out_mu, float* out_sigma, float* out_p_src,
+                                             float* out_p_snk, float* out_mom_mu,
+                                             float* out_mom_sigma, int32_t* err, void* stream) {
+  if (int r = grid_ok(nx, ny, dx, dy)) return r;
+  if (!members) return DIVUQ_EINVAL;
+  if (M < 2) return DIVUQ_EMEMBERS;
+  if ((out_mom_mu == nullptr) != (out_mom_sigma == nullptr)) return DIVUQ_EINVAL;
+  const int64_t tx = (nx + kGfTX - 1) / kGfTX, ty = (ny + kGfTY - 1) / kGfTY;
+  if (tx > INT32_MAX || ty > 65535) return DIVUQ_EGRID;
+  GfParams p{};
+  p.members = members; p.M = M; p.nx = nx; p.ny = ny;
+  p.cx_in = float(1.0 / (2.0 * dx)); p.cx_bd = float(1.0 / dx);   // stencils.py:48-50
+  p.cy_in = float(1.0 / (2.0 * dy)); p.cy_bd = float(1.0 / dy);
+  p.theta = float(t);
+  p.out_mu = out_mu; p.out_sigma = out_sigma; p.out_psrc = out_p_src; p.out_psnk = out_p_snk;
+  p.out_mom_mu = out_mom_mu; p.out_mom_sigma = out_mom_sigma;
+  p.err = err;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const dim3 grid{unsigned(tx), unsigned(ty)}, block{kGfBX, kGfBY};
+  CUtensorMap map{};
+  const bool tma = !env_int("DIVUQ_NO_TMA", 0) && nx % 4 == 0 && aligned(members, 16) &&
+                   nx < (int64_t(1) << 31) && ny < (int64_t(1) << 31) && 2 * M < (int64_t(1) << 31) &&
+                   make_map3d<float>(&map, members, nx, ny, 2 * M, kGfRW, kGfRH, 256);
+  if (tma) {
+    DIVUQ_CUDA(cudaFuncSetAttribute(gradfused_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(kGfSmemTma)));
+    gradfused_kernel<true><<<grid, block, kGfSmemTma, s>>>(map, p);
+  } else {
+    gradfused_kernel<false><<<grid, block, kGfSmemLdg, s>>>(map, p);
+  }
+  return int(cudaGetLastError());
+}
+
 int divuq_ensemble_divergence3d_f32(const float* members, int64_t M, const float* hl_mu,
                                     const float* hl_s, const float* hh_mu, const float* hh_s,
                                     int64_t nx, int64_t ny, int64_t nzl, int64_t z0, int64_t nzg,
@@ -1564,6 +1600,47 @@ int divuq_host_ensemble_divergence2d_f32(const float* members, int64_t M, int64_
                                           out_sigma ? outs[1] : nullptr, out_p_src ? outs[2] : nullptr,
                                           out_p_snk ? outs[3] : nullptr, out_mom_mu ? mom_mu : nullptr,
                                           out_mom_mu ? mom_sg : nullptr, derr, sg.s);
+  if (r) return r;
+  for (int q = 0; q < 4; ++q)
+    if (host_out[q]) DIVUQ_CUDA(d2h(host_out[q], outs[q], b, sg.s));
+  if (out_mom_mu) {
+    DIVUQ_CUDA(d2h(out_mom_mu, mom_mu, 2 * b, sg.s));
+    DIVUQ_CUDA(d2h(out_mom_sigma, mom_sg, 2 * b, sg.s));
+  }
+  int status = 0;
+  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  return status;
+}
+
+int divuq_host_gradient_ensemble_divergence2d_f32(const float* members, int64_t M, int64_t nx,
+                                                  int64_t ny, double dx, double dy, double t,
+                                                  float* out_mu, float* out_sigma, float* out_p_src,
+                                                  float* out_p_snk, float* out_mom_mu,
+                                                  float* out_mom_sigma, int device) {
+  if (int r = grid_ok(nx, ny, dx, dy)) return r;
+  if (!members) return DIVUQ_EINVAL;
+  if (M < 2) return DIVUQ_EMEMBERS;
+  if ((out_mom_mu == nullptr) != (out_mom_sigma == nullptr)) return DIVUQ_EINVAL;
+  DIVUQ_CUDA(cudaSetDevice(device));
+  StreamGuard sg;
+  DIVUQ_CUDA(cached_stream(0, &sg.s));
+  const int64_t n = nx * ny;
+  const size_t in_b = size_t(M * 2 * n) * sizeof(float), b = size_t(n) * sizeof(float);
+  DevBuf d;
+  DIVUQ_CUDA(d.alloc(in_b + 8 * b + 256, sg.s));
+  float* dm = d.as<float>();
+  float* o = dm + M * 2 * n;
+  float* outs[4] = {o, o + n, o + 2 * n, o + 3 * n};
+  float* mom_mu = o + 4 * n;
+  float* mom_sg = o + 6 * n;
+  int32_t* derr = reinterpret_cast<int32_t*>(o + 8 * n);
+  DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
+  DIVUQ_CUDA(h2d(dm, members, in_b, sg.s));
+  float* host_out[4] = {out_mu, out_sigma, out_p_src, out_p_snk};
+  int r = divuq_gradient_ensemble_divergence2d_f32(
+      dm, M, nx, ny, dx, dy, t, out_mu ? outs[0] : nullptr, out_sigma ? outs[1] : nullptr,
+      out_p_src ? outs[2] : nullptr, out_p_snk ? outs[3] : nullptr, out_mom_mu ? mom_mu : nullptr,
+      out_mom_mu ? mom_sg : nullptr, derr, sg.s);
   if (r) return r;
   for (int q = 0; q < 4; ++q)
     if (host_out[q]) DIVUQ_CUDA(d2h(host_out[q], outs[q], b, sg.s));

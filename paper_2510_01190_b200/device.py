@@ -215,6 +215,29 @@ def ensemble_divergence2d(members, nx, ny, dx=1.0, dy=1.0, t=0.0, *, moments=Fal
     return o
 
 
+def gradient_ensemble_divergence2d(members, nx, ny, dx=1.0, dy=1.0, t=0.0, *, moments=False,
+                                   outputs=ALL_OUTPUTS, out=None, check=True):
+    """K6 fused Red Sea pipeline: (M, 2, nx*ny) fp32 velocity members ->
+    |v| -> gradient -> moments -> divergence -> tails in one pass (moments:
+    the gradient ensemble's (2, N) mu / sigma)."""
+    _req(members, "members", torch.float32)
+    m = members.shape[0]
+    if members.shape[1:] != (2, nx * ny):
+        raise ValueError("members must have shape (M, 2, nx*ny)")
+    n = nx * ny
+    o = _outs(members, n, outputs, out)
+    if moments:
+        o.setdefault("mom_mu", torch.empty((2, n), dtype=members.dtype, device=members.device))
+        o.setdefault("mom_sigma", torch.empty((2, n), dtype=members.dtype, device=members.device))
+    err = _ErrWord(members.device, check)
+    _check(lib.divuq_gradient_ensemble_divergence2d_f32(
+        _ptr(members), m, nx, ny, float(dx), float(dy), float(t), _ptr(o.get("mu")),
+        _ptr(o.get("sigma")), _ptr(o.get("p_src")), _ptr(o.get("p_snk")), _ptr(o.get("mom_mu")),
+        _ptr(o.get("mom_sigma")), err.ptr, _stream()))
+    err.raise_if_set()
+    return o
+
+
 def ensemble_divergence3d(members, nx, ny, nz_local, dx=1.0, dy=1.0, dz=1.0, t=0.0, *, z0=0,
                           nz_global=None, halo_lo=None, halo_hi=None, k_range=None,
                           moments=False, outputs=ALL_OUTPUTS, out=None, check=True):
@@ -317,7 +340,8 @@ def mc_divergence2d(mu_u, mu_v, s_u, s_v, nx, ny, dx, dy, n_samples, seed, *, ro
 
 __all__ = [
     "ALL_OUTPUTS", "propagate2d", "propagate3d", "tail_probs", "lcp2d", "fit_moments",
-    "ensemble_divergence2d", "ensemble_divergence3d", "w_moments_plane", "w_moments_plane_ptr",
+    "ensemble_divergence2d", "ensemble_divergence3d", "gradient_ensemble_divergence2d",
+    "w_moments_plane", "w_moments_plane_ptr",
     "mc_divergence2d",
 ]
 _ = _lib  # re-export guard

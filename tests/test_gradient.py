@@ -121,3 +121,69 @@ def test_gradient_ensemble_tiles_vs_oracle(d, shape):
                                        dx, dy).cpu().numpy()
     want32 = ref2d.gradient_ensemble(mem.astype(np.float32), nx, ny, dx, dy)
     assert np.abs(got32 - want32).max() <= 1e-5 * np.abs(want32).max()
+
+
+@pytest.mark.parametrize("shape", [(2, 2, 1.0, 1.0), (3, 70, 0.5, 0.25), (65, 17, 1.0, 2.0),
+                                   (130, 41, 0.01, 0.07), (64, 16, 1.0, 1.0), (200, 33, 0.3, 0.3)])
+@pytest.mark.parametrize("m,t", [(2, 0.0), (5, 0.3), (20, 0.0)])
+def test_fused_gradient_ensemble_divergence(d, shape, m, t):
+    """K6 (velocity magnitude -> gradient -> moments -> divergence -> tails,
+    one pass) == gradient_ensemble2d_f32 then ensemble_divergence2d_f32, bit
+    for bit, at every tile offset; and within the fp32 bar of the fp64 oracle
+    composition of the reference's functions."""
+    import torch
+
+    from oracle import ref2d
+    from paper_2510_01190_b200 import device
+
+    nx, ny, dx, dy = shape
+    rng = np.random.default_rng(nx * 7 + ny * 3 + m)
+    base = rng.normal(size=(1, 2, nx * ny))
+    mem = (base + 0.2 * rng.normal(size=(m, 2, nx * ny))).astype(np.float32)
+    gm = torch.from_numpy(mem).cuda()
+    fused = device.gradient_ensemble_divergence2d(gm, nx, ny, dx, dy, t, moments=True)
+    grad = device.gradient_ensemble2d(gm, nx, ny, dx, dy)
+    comp = device.ensemble_divergence2d(grad, nx, ny, dx, dy, t, moments=True)
+    for k in ("mu", "sigma", "p_src", "p_snk", "mom_mu", "mom_sigma"):
+        assert torch.equal(fused[k], comp[k]), k
+    g64 = ref2d.gradient_ensemble(mem.astype(np.float64), nx, ny, dx, dy)
+    mu_r, sg_r = ref2d.fit_moments(g64)
+    dmu, dsg = ref2d.propagate2d(mu_r[0], mu_r[1], sg_r[0], sg_r[1], nx, ny, dx, dy)
+    got_mu = fused["mu"].cpu().numpy()
+    got_sg = fused["sigma"].cpu().numpy()
+    assert np.abs(got_mu - dmu).max() <= 1e-5 * np.abs(dmu).max()
+    assert np.abs(got_sg - dsg).max() <= 1e-5 * np.abs(dsg).max()
+    ps_own = ref2d.source_probability(got_mu.astype(np.float64), got_sg.astype(np.float64), t)
+    p = fused["p_src"].cpu().numpy()
+    assert np.all(np.abs(p - ps_own) <= 1e-5 * ps_own + 1e-6)
+
+
+def test_fused_gradient_ensemble_divergence_host_api_and_errors(d):
+    import torch
+
+    from paper_2510_01190_b200 import device
+
+    g = d.UniformGrid2(96, 40, 0.5, 0.25)
+    x, y = _xy(g)
+    rng = np.random.default_rng(5)
+    members = []
+    for k in range(6):   # vortex ensemble with jittered centres (the Red Sea use case)
+        cx, cy = 24 + rng.normal(0, 0.5), 5 + rng.normal(0, 0.3)
+        r2 = (x - cx) ** 2 + (y - cy) ** 2
+        members.append(d.VectorField2(g, -(y - cy) * np.exp(-r2 / 20), (x - cx) * np.exp(-r2 / 20)))
+    ens = d.Ensemble2(g, members)
+    res = d.gradient_ensemble_divergence(ens, 0.0)
+    gm = torch.from_numpy(np.ascontiguousarray(ens.stacked(), dtype=np.float32)).cuda()
+    o = device.gradient_ensemble_divergence2d(gm, g.nx, g.ny, g.dx, g.dy, 0.0, moments=True)
+    assert np.array_equal(res.field.mu, o["mu"].cpu().numpy())
+    assert np.array_equal(res.field.sigma, o["sigma"].cpu().numpy())
+    assert np.array_equal(res.model.mu_u, o["mom_mu"][0].cpu().numpy())
+    # the magnitude-gradient field diverges at the vortex core
+    centre = int(np.argmin((x - 24) ** 2 + (y - 5) ** 2))
+    assert res.field.mu[centre] > 0 and res.p_src[centre] > 0.5
+    bad = gm.clone()
+    bad[1, 0, 7] = float("nan")
+    with pytest.raises(ValueError, match="non-finite"):
+        device.gradient_ensemble_divergence2d(bad, g.nx, g.ny, g.dx, g.dy)
+    with pytest.raises(ValueError):
+        device.gradient_ensemble_divergence2d(gm[:1].contiguous(), g.nx, g.ny, g.dx, g.dy)
