@@ -31,11 +31,13 @@
 #include "gradient.cuh"
 #include "tma.cuh"
 
+#include <type_traits>
+
 #ifndef DIVUQ_GF_MINB
-#define DIVUQ_GF_MINB 3   // TMA variant (the register-staged one runs 2 CTAs / SM)
+#define DIVUQ_GF_MINB 4   // TMA variant (the register-staged one runs 2 CTAs / SM)
 #endif
 #ifndef DIVUQ_GF_STAGES
-#define DIVUQ_GF_STAGES 4
+#define DIVUQ_GF_STAGES 3   // 4 CTAs x 3 stages: 12 members in flight per SM
 #endif
 
 namespace divuq {
@@ -152,10 +154,22 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
     }
   }
 
+  // shared-window addresses of the differenced magnitudes in mag buffer 0;
+  // buffer 1 is an immediate offset (the member loop is unrolled by two)
+  uint32_t a_hi[kGfSlots], a_lo[kGfSlots];
+#pragma unroll
+  for (int s = 0; s < kGfSlots; ++s) {
+    a_hi[s] = smem_u32(mag + g_hi[s]);
+    a_lo[s] = smem_u32(mag + g_lo[s]);
+  }
   ShiftedMoments<1> acc[kGfSlots];
-  int errbits = 0;
-  for (int m = 0; m < M; ++m) {
-    float* mg = mag + (m & 1) * kGfR;
+  // non-finite input: u or v inf/NaN makes r = u^2 + v^2 inf/NaN and r*0 NaN
+  // (so does |u| or |v| > ~1.8e19, whose magnitude would overflow anyway)
+  float bad = 0.0f;
+  auto member = [&](int m, auto bufc, auto firstc) {
+    constexpr int BUF = decltype(bufc)::value;
+    constexpr bool FIRST = decltype(firstc)::value;
+    float* mg = mag + BUF * kGfR;
     if constexpr (TMA) {
       const int st = m % kGfS;
       mbar_wait(&full[st], uint32_t(m / kGfS) & 1u);
@@ -164,10 +178,11 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
 #pragma unroll
       for (int k = 0; k < kGfNL; ++k) {
         const int q = tid + k * kGfThreads;
-        if (q < kGfR) {
+        if (k < kGfNL - 1 || q < kGfR) {
           const float u = su[q], v = sv[q];
-          errbits |= check_value(u) | check_value(v);
-          mg[q] = hypot_(u, v);
+          const float r = fmaf(u, u, v * v);
+          bad = fmaf(r, 0.0f, bad);
+          mg[q] = sqrt_of_sq(r);
         }
       }
       __syncthreads();   // stage st consumed by every thread: refill it
@@ -181,8 +196,12 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
     } else {
 #pragma unroll
       for (int k = 0; k < kGfNL; ++k) {
-        errbits |= check_value(a[k]) | check_value(b[k]);
-        if (tid + k * kGfThreads < kGfR) mg[tid + k * kGfThreads] = hypot_(a[k], b[k]);
+        const int q = tid + k * kGfThreads;
+        if (k < kGfNL - 1 || q < kGfR) {
+          const float r = fmaf(a[k], a[k], b[k] * b[k]);
+          bad = fmaf(r, 0.0f, bad);
+          mg[q] = sqrt_of_sq(r);
+        }
       }
       if (m + 1 < M) {   // next member's loads in flight across the barrier and the math
         const float* src = p.members + int64_t(m + 1) * 2 * N;
@@ -196,11 +215,24 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
     }
 #pragma unroll
     for (int s = 0; s < kGfSlots; ++s) {
-      // stencils.py:87-96: f[hi]*c - f[lo]*c, each product rounded
-      const float g = __fsub_rn(__fmul_rn(mg[g_hi[s]], g_c[s]), __fmul_rn(mg[g_lo[s]], g_c[s]));
-      acc[s].add(m, &g);
+      float hi, lo;
+      asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(hi) : "r"(a_hi[s]), "n"(BUF * kGfR * 4));
+      asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(lo) : "r"(a_lo[s]), "n"(BUF * kGfR * 4));
+      const float g = grad_diff(hi, lo, g_c[s]);   // stencils.py:87-96
+      acc[s].add(FIRST ? 0 : 1, &g);   // member 0 sets the shift
     }
+  };
+  using B0 = std::integral_constant<int, 0>;
+  using B1 = std::integral_constant<int, 1>;
+  using NotFirst = std::false_type;
+  member(0, B0{}, std::true_type{});
+  int m = 1;
+  for (; m + 1 < M; m += 2) {
+    member(m, B1{}, NotFirst{});
+    member(m + 1, B0{}, NotFirst{});
   }
+  if (m < M) member(m, B1{}, NotFirst{});
+  const int errbits = bad == bad ? 0 : kErrNonFinite;
   if constexpr (TMA) __syncthreads();   // the moments alias the stages
   float g_mu[kGfSlots], g_sg[kGfSlots];
 #pragma unroll

@@ -20,9 +20,21 @@ template <> __device__ __forceinline__ double hypot_(double a, double b) { retur
 // of hypotf's ~25 with its scaling branches; |err| ~2 ulp.  No overflow guard:
 // |a|, |b| must stay below ~1.8e19 (velocities).  r < FLT_MIN (|v| < 1.1e-19)
 // evaluates to <= 1.1e-19 instead of sqrt(r).
-template <> __device__ __forceinline__ float hypot_(float a, float b) {
-  const float r = fmaf(a, a, b * b);
+__device__ __forceinline__ float sqrt_of_sq(float r) {   // r = a^2 + b^2 >= 0
   return r * rsqrt_approx(fmaxf(r, 1.17549435e-38f));
+}
+template <> __device__ __forceinline__ float hypot_(float a, float b) {
+  return sqrt_of_sq(fmaf(a, a, b * b));
+}
+
+// one gradient component, stencils.py:87-96.  fp64: f[hi]*c - f[lo]*c with
+// each product rounded (the reference's order, bitwise).  fp32 (1e-5 bar):
+// c*(f[hi] - f[lo]), one rounding fewer and one instruction fewer.
+__device__ __forceinline__ double grad_diff(double hi, double lo, double c) {
+  return __dsub_rn(__dmul_rn(hi, c), __dmul_rn(lo, c));
+}
+__device__ __forceinline__ float grad_diff(float hi, float lo, float c) {
+  return __fmul_rn(c, __fsub_rn(hi, lo));
 }
 
 template <typename T>
@@ -58,7 +70,6 @@ __global__ void __launch_bounds__(kGrBX * kGrBY, 3)
 gradient2d_kernel(const T* __restrict__ in, int64_t members, int64_t in_mstride, int64_t nx,
                   int64_t ny, T cx_in, T cx_bd, T cy_in, T cy_bd, T* __restrict__ out,
                   int64_t out_mstride, int* err) {
-  using A = Arith<T>;
   __shared__ T f[kGrTY + 2][kGrTX + 2];
   T* const fl = &f[0][0];
   const int64_t n = nx * ny;
@@ -118,9 +129,8 @@ gradient2d_kernel(const T* __restrict__ in, int64_t members, int64_t in_mstride,
 #pragma unroll
     for (int e = 0; e < kGrPY * kGrPX; ++e) {
       if (o_off[e] < 0) continue;
-      // stencils.py:87-96: f[hi]*c - f[lo]*c per axis, each product rounded
-      dst[o_off[e]] = A::sub(A::mul(fl[o_xh[e]], o_cx[e]), A::mul(fl[o_xl[e]], o_cx[e]));
-      dst[n + o_off[e]] = A::sub(A::mul(fl[o_yh[e]], o_cy[e]), A::mul(fl[o_yl[e]], o_cy[e]));
+      dst[o_off[e]] = grad_diff(fl[o_xh[e]], fl[o_xl[e]], o_cx[e]);
+      dst[n + o_off[e]] = grad_diff(fl[o_yh[e]], fl[o_yl[e]], o_cy[e]);
     }
     __syncthreads();
   }
