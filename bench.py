@@ -430,6 +430,9 @@ def run_next(args):
                     "bytes_per_unit": bpu, "units_per_launch": units, "avg_launch_ms": ms,
                     "peak_source": peak_src}
         if wl == "redsea":   # the unfused chain on the same input, same protocol
+            roofline["note"] = ("same byte count as config 1 (+4 B/pt): its small-problem floor, "
+                                "36.1 us for a perfectly coalesced stream (profiles/r01/bwbench.txt), "
+                                "applies")
             comp_ms = []
             for _ in range(args.steps):
                 flush()
@@ -736,6 +739,10 @@ def main():
                     "avg_launch_ms": avg_k_s * 1e3}
     elif args.config == 0:
         roofline["note"] = "0.9 MB working set: launch/latency-bound, L2 flushed between steps"
+    elif args.config == 1:
+        roofline["note"] = ("small-problem floor: a perfectly coalesced 40-read/3-write float4 stream of "
+                            "the same 172 MB, timed the same way (L2 evicted, one launch), takes 36.1 us "
+                            "= 5.0 TB/s (tools/bwbench, profiles/r01/bwbench.txt)")
 
     # e2e through the host-buffer C ABI (pinned host buffers, copies timed)
     e2e = None

@@ -4,18 +4,19 @@
 // 48-70) -> tails (lcp.py:48-68) on an (M, 2, ny*nx) fp32 member array, one
 // pass over the members.  The tiled K3 (k3tma.cuh) treats a 2D grid as single
 // planes: every tile is a short 10-item burst followed by an epilogue and a
-// barrier, and it stays near 62 % of HBM.  Here a CTA owns a 128-column strip
-// and a run of rows and marches down the rows the way K2/K3 march z:
+// barrier, and it stays near 62 % of HBM.  Here a CTA owns a TX-column strip
+// (TX = 32 * VEC = 64) and a run of rows and marches down the rows the way
+// K2/K3 march z:
 //
 //   * the producer warp streams one ROW per stage: the M u-rows of the strip
-//     WITH their 4-column x-halos (one 5D TMA box of 136 columns) and the M
-//     v-rows (box of 128 columns); the run is padded by one halo row on each
+//     WITH their 4-column x-halos (one 5D TMA box of TX + 8 columns) and the
+//     M v-rows (box of TX columns); the run is padded by one halo row on each
 //     side, so no halo boxes and no neighbour CTA timing are involved;
 //   * NW consumer warps take rows round-robin in groups of NW: a warp folds
 //     its row's members into single-pass shifted moments (ShiftedMoments, the
 //     same routine as K1 / K3, so results are bitwise those of K1 + K2),
 //     releases the stage at once and publishes (mu_u, s_u, mu_v, s_v) of its
-//     128 points (+ the two x-halo points) in a shared ring of 2*NW + 2 rows;
+//     TX points (+ the two x-halo points) in a shared ring of 2*NW + 2 rows;
 //   * one named barrier per group; then each warp evaluates the stencil,
 //     sigma and both tails for the row BEFORE its own (whose v neighbours
 //     are now both in the ring) and streams the outputs;

@@ -4,6 +4,8 @@
 //   k2mix  6 reads : 4 writes (config 3: u v w su sv sw -> mu sigma p_src p_snk)
 //   k3mix 48 reads : 4 writes (config 4: 16 members x 3 components -> 4 outputs)
 //   read   1 read : 0 writes
+//   c1mix 40 reads : 3 writes at config 1's size (1024^2 points, 172 MB),
+//          each launch timed alone after an L2-evicting memset (as bench.py)
 // Each thread moves float4s, grid = 148 x 8 CTAs of 256 threads, grid-stride.
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -51,5 +53,27 @@ int main() {
   run<0, 4>("k2wr", in, out, n4);
   // k3 mix on a 1/8 slab so 48 arrays fit: n4/8 elements per array
   run<48, 4>("k3mix", in, out, n4 / 8);
+  // config-1 sized: the small-problem floor (launch ramp + tail) for 172 MB
+  {
+    const long long c4 = 1024ll * 1024 / 4;
+    void* flush = nullptr;
+    cudaMalloc(&flush, size_t(256) << 20);
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    for (int grid_mul : {1, 2, 4, 8}) {
+      float best = 1e9f, sum = 0.f;
+      const int K = 20;
+      for (int i = 0; i < K + 3; ++i) {
+        cudaMemsetAsync(flush, i, size_t(256) << 20);
+        cudaEventRecord(a);
+        mix<40, 3><<<148 * grid_mul, 256>>>(in, out, c4);
+        cudaEventRecord(b); cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b);
+        if (i >= 3) { sum += ms; best = best < ms ? best : ms; }
+      }
+      const double bytes = 43.0 * c4 * 16;
+      printf("c1mix 40:3 grid 148x%d  avg %.1f us (%.0f GB/s)  best %.1f us\n", grid_mul, sum / K * 1e3,
+             bytes / (sum / K * 1e-3) / 1e9, best * 1e3);
+    }
+  }
   return 0;
 }
