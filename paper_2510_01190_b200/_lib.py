@@ -12,7 +12,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdivuq_b200.so")
+# DIVUQ_LIB_PATH: load an experimental build instead (tools/ sweeps only)
+LIB_PATH = os.environ.get("DIVUQ_LIB_PATH") or os.path.join(_HERE, "libdivuq_b200.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

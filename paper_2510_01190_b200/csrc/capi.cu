@@ -1126,11 +1126,17 @@ int try_k3_rowmarch(const StencilParams<float>& sp, cudaStream_t s, bool* used) 
   p.stage_stride = (p.v_off + v_bytes + 127) / 128 * 128;
   p.stage_bytes = u_bytes + v_bytes;
   const size_t ring = (sizeof(RmRing) + 1023) / 1024 * 1024;
-  const size_t budget = 227 * 1024 - ring - 2 * C::SMAX * sizeof(uint64_t) - 1024;
-  p.S = int(std::min<size_t>(C::SMAX, budget / p.stage_stride));
-  // every consumer warp of a group waits on its own stage: S >= NW, or two
-  // rows one phase apart would share a stage (parity aliasing)
-  if (p.S < C::NW) return DIVUQ_OK;
+  // CTAs per SM: DIVUQ_RM_MINB (2) when its share of shared memory holds
+  // S >= NW stages, else 1.  Every consumer warp of a group waits on its own
+  // stage: S >= NW, or two rows one phase apart would share a stage (parity
+  // aliasing).
+  int64_t cps = std::max<int64_t>(1, std::min<int64_t>(4, env_int("DIVUQ_RM_CPS", DIVUQ_RM_MINB)));
+  for (;; --cps) {
+    const size_t budget = 227 * 1024 / size_t(cps) - ring - 2 * C::SMAX * sizeof(uint64_t) - 1024;
+    p.S = int(std::min<size_t>(C::SMAX, budget / p.stage_stride));
+    if (p.S >= C::NW) break;
+    if (cps == 1) return DIVUQ_OK;
+  }
   RmMaps tm;
   std::memset(&tm, 0, sizeof(tm));
   if (!make_map5d_members(&tm.u, sp.members, sp.nx, sp.ny, 1, 2, M, C::TXP, 1, int(M), 256) ||
@@ -1139,7 +1145,7 @@ int try_k3_rowmarch(const StencilParams<float>& sp, cudaStream_t s, bool* used) 
   p.nx = int(sp.nx); p.ny = int(sp.ny); p.M = int(M);
   p.strips = int((sp.nx + C::TX - 1) / C::TX);
   const int64_t sms = sm_count();
-  const int64_t segs_wanted = std::max<int64_t>(1, sms / p.strips);
+  const int64_t segs_wanted = std::max<int64_t>(1, cps * sms / p.strips);
   p.seg_rows = int(std::max<int64_t>(C::NW, (sp.ny + segs_wanted - 1) / segs_wanted));
   const int64_t segs = (sp.ny + p.seg_rows - 1) / p.seg_rows;
   p.cx_in = sp.cx_in; p.cx_bd = sp.cx_bd; p.cy_in = sp.cy_in; p.cy_bd = sp.cy_bd; p.theta = sp.theta;

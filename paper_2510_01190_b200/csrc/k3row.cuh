@@ -29,8 +29,14 @@
 
 namespace divuq {
 
+// 2 CTAs x 8 consumer warps per SM: 37.6 us at config 1 vs 42.4 for 1 x 10
+// (tools/sweep_c1.py over tools/variants builds; the small-problem floor of a
+// perfect stream of the same bytes is 36.1 us, profiles/r01/bwbench.txt)
 #ifndef DIVUQ_RM_NW
-#define DIVUQ_RM_NW 10
+#define DIVUQ_RM_NW 8
+#endif
+#ifndef DIVUQ_RM_MINB
+#define DIVUQ_RM_MINB 2
 #endif
 #ifndef DIVUQ_RM_VEC
 #define DIVUQ_RM_VEC 2
@@ -64,7 +70,7 @@ struct RmRing {
   float h[RmCfg::R][4];
 };
 
-__global__ void __launch_bounds__(RmCfg::THREADS, 1)
+__global__ void __launch_bounds__(RmCfg::THREADS, DIVUQ_RM_MINB)
 k3_rowmarch_kernel(const __grid_constant__ RmMaps tm, const RmParams p) {
   using C = RmCfg;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
