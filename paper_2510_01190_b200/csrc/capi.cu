@@ -629,6 +629,74 @@ __global__ void __launch_bounds__(256) fit_smem_kernel(const double* __restrict_
   flush_error(err, errbits);
 }
 
+// fp64 K1, bulk-staged: a CTA streams tiles of 256 points; for each tile one
+// warp issues M 1D bulk copies (one 2 KB member row each) into a stage of
+// S per CTA, completion on one mbarrier, so a whole tile's members are in
+// flight at once (the register-loaded fit_smem_kernel keeps 8 loads per
+// thread in flight and was latency-bound: ncu long-scoreboard 7.9 per
+// issue).  Both passes then read the stage: thread j owns point j, sums in
+// member order (bitwise numpy, gaussian.py:41-44) and writes mu / sigma.
+constexpr int kFbTile = 256;
+__global__ void __launch_bounds__(kFbTile, 2) fit_bulk_kernel(const double* __restrict__ members, int M,
+                                                              int64_t C, int64_t N, int64_t mstride,
+                                                              int S, double* __restrict__ out_mu,
+                                                              double* __restrict__ out_sigma, int* err) {
+  using A = Arith<double>;
+  extern __shared__ __align__(128) unsigned char fb_smem[];
+  const size_t stage_bytes = size_t(M) * kFbTile * sizeof(double);
+  uint64_t* full = reinterpret_cast<uint64_t*>(fb_smem + size_t(S) * stage_bytes);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t tpc = (N + kFbTile - 1) / kFbTile, ntiles = C * tpc;
+  auto issue = [&](int64_t t, int s) {   // warp 0
+    const int64_t c = t / tpc, n0 = (t - c * tpc) * kFbTile;
+    const uint32_t bytes = uint32_t(min(int64_t(kFbTile), N - n0) * sizeof(double));
+    double* dst = reinterpret_cast<double*>(fb_smem + size_t(s) * stage_bytes);
+    if (lane == 0) mbar_expect_tx(&full[s], uint32_t(M) * bytes);
+    __syncwarp();
+    for (int m = lane; m < M; m += 32)
+      bulk_load(dst + m * kFbTile, members + m * mstride + c * N + n0, bytes, &full[s]);
+  };
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == 0)
+    for (int s = 0; s < S; ++s)
+      if (blockIdx.x + int64_t(s) * gridDim.x < ntiles) issue(blockIdx.x + int64_t(s) * gridDim.x, s);
+  int errbits = 0;
+  for (int64_t k = 0;; ++k) {
+    const int64_t t = blockIdx.x + k * gridDim.x;
+    if (t >= ntiles) break;
+    const int s = int(k % S);
+    mbar_wait(&full[s], uint32_t(k / S) & 1u);
+    const double* x = reinterpret_cast<const double*>(fb_smem + size_t(s) * stage_bytes);
+    const int64_t c = t / tpc, n0 = (t - c * tpc) * kFbTile;
+    if (n0 + tid < N) {
+      double sum = x[tid];
+      errbits |= check_value(sum);
+      for (int m = 1; m < M; ++m) {   // pass 1: member order
+        const double v = x[m * kFbTile + tid];
+        errbits |= check_value(v);
+        sum = A::add(sum, v);
+      }
+      const double mu = A::div(sum, double(M));
+      double d = A::sub(x[tid], mu);
+      double q = A::mul(d, d);
+      for (int m = 1; m < M; ++m) {   // pass 2 from the stage
+        d = A::sub(x[m * kFbTile + tid], mu);
+        q = A::add(q, A::mul(d, d));
+      }
+      __stcs(out_mu + c * N + n0 + tid, mu);
+      __stcs(out_sigma + c * N + n0 + tid, A::sqrt_(A::div(q, double(M - 1))));
+    }
+    __syncthreads();   // stage s consumed: refill it
+    const int64_t tn = t + int64_t(S) * gridDim.x;
+    if (warp == 0 && tn < ntiles) issue(tn, s);
+  }
+  flush_error(err, errbits);
+}
+
 template <typename T, int VEC, int U, int MINB, bool REREAD = true>
 int launch_fit_stream(const T* m, int64_t M, int64_t C, int64_t N, int64_t ms, T* mu, T* sg,
                       int32_t* err, cudaStream_t s) {
@@ -655,6 +723,20 @@ int fit_stream(const T* m, int64_t M, int64_t C, int64_t N, int64_t ms, T* mu, T
     // holding all M doubles for both passes spills at these register caps;
     // parking them in shared memory keeps HBM at one read (measured faster
     // than the L2 re-read below, which remains for very large M)
+    const size_t stage = size_t(M) * kFbTile * sizeof(double);
+    if (!env_int("DIVUQ_FIT_NOBULK", 0) && N % 2 == 0 && ms % 2 == 0 && aligned(m, 16) &&
+        2 * stage <= 200 * 1024) {
+      // 2 CTAs / SM x S stages (S = 4 for M <= 12 .. 1 for M <= 50), <= ~200 KB per SM
+      const int S = int(std::max<size_t>(1, std::min<size_t>(4, (100 * 1024) / stage)));
+      const size_t smem = size_t(S) * stage + size_t(S) * sizeof(uint64_t);
+      DIVUQ_CUDA(cudaFuncSetAttribute(fit_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      int per_sm = 0;
+      DIVUQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fit_bulk_kernel, kFbTile, smem));
+      const int64_t tiles = C * ((N + kFbTile - 1) / kFbTile);
+      const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(std::max(1, per_sm)) * sm_count()));
+      fit_bulk_kernel<<<unsigned(grid), kFbTile, smem, s>>>(m, int(M), C, N, ms, S, mu, sg, err);
+      return int(cudaGetLastError());
+    }
     const size_t park = size_t(M) * 256 * sizeof(double);
     if (M <= 64 && !env_int("DIVUQ_FIT_REREAD", 0)) {
       auto kern = fit_smem_kernel<8>;
