@@ -7,7 +7,7 @@ for c in 3 4 1 0 2; do
   extra=""; [ $c = 4 ] && extra="--steps 20"; [ $c = 2 ] && extra="--steps 5"
   timeout 600 python bench.py --config $c $extra > gpurun_out/bench_c$c.json 2> gpurun_out/bench_c$c.err || tail -5 gpurun_out/bench_c$c.err
 done
-for w in lcp gradient fit ingest; do
+for w in lcp gradient fit ingest redsea; do
   timeout 600 python bench.py --workload $w --steps 20 > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err || tail -5 gpurun_out/bench_$w.err
 done
 timeout 600 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2>&1
