@@ -963,6 +963,20 @@ int launch_gradient(const T* in, int64_t members, int64_t in_mstride, int64_t nx
   if ((nx + kGrTX - 1) / kGrTX > INT32_MAX || (ny + kGrTY - 1) / kGrTY > 65535) return DIVUQ_EGRID;
   const T cxi = T(1.0 / (2.0 * dx)), cxb = T(1.0 / dx), cyi = T(1.0 / (2.0 * dy)), cyb = T(1.0 / dy);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CUtensorMap map{};
+  if (mag && in_mstride == 2 * nx * ny && out_mstride == 2 * nx * ny && !env_int("DIVUQ_NO_TMA", 0) &&
+      (nx * int64_t(sizeof(T))) % 16 == 0 && aligned(in, 16) && nx < (int64_t(1) << 31) &&
+      ny < (int64_t(1) << 31) && 2 * members < (int64_t(1) << 31) &&
+      make_map3d<T>(&map, in, nx, ny, 2 * members, GrTma<T>::RW, GrTma<T>::RH, 256)) {
+    // one CTA per tile walks all members (DIVUQ_GR_MPC splits them)
+    const int64_t mpc = std::max<int64_t>(1, env_int("DIVUQ_GR_MPC", members));
+    const dim3 g3{grid.x, grid.y, unsigned(std::min<int64_t>((members + mpc - 1) / mpc, 65535))};
+    DIVUQ_CUDA(cudaFuncSetAttribute(gradient_tma_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    int(GrTma<T>::SMEM)));
+    gradient_tma_kernel<T><<<g3, dim3(kGrBX, kGrBY), GrTma<T>::SMEM, s>>>(map, members, nx, ny, cxi, cxb,
+                                                                          cyi, cyb, out, out_mstride, err);
+    return int(cudaGetLastError());
+  }
   if (mag)
     gradient2d_kernel<T, true><<<grid, dim3(kGrBX, kGrBY), 0, s>>>(in, members, in_mstride, nx, ny, cxi, cxb,
                                                               cyi, cyb, out, out_mstride, err);

@@ -11,6 +11,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace divuq {
 
@@ -133,6 +134,102 @@ gradient2d_kernel(const T* __restrict__ in, int64_t members, int64_t in_mstride,
       dst[n + o_off[e]] = grad_diff(fl[o_yh[e]], fl[o_yl[e]], o_cy[e]);
     }
     __syncthreads();
+  }
+  flush_error(err, errbits);
+}
+
+// gradient_ensemble, TMA-staged (nx * sizeof(T) % 16 == 0): a CTA owns a
+// 64 x 16 tile and walks its members; each member's (u, v) region (x-halo of
+// 16 bytes -- a TMA box must start on a 16-byte boundary -- and a 1-row
+// y-halo) arrives by cp.async.bulk.tensor into one of S stages, so S members
+// are in flight while the CTA differentiates the current one (the
+// register-loaded kernel above only has a member's loads in flight during
+// its load phase: 70 % of HBM).  Magnitudes go to a double-buffered tile,
+// one barrier per member; same arithmetic as gradient2d_kernel.
+template <typename T>
+struct GrTma {
+  static constexpr int HX = 16 / int(sizeof(T)), HY = 1;
+  static constexpr int RW = kGrTX + 2 * HX, RH = kGrTY + 2 * HY, R = RW * RH;
+  static constexpr int NL = (R + kGrBX * kGrBY - 1) / (kGrBX * kGrBY);
+  static constexpr int S = 4;
+  static constexpr uint32_t COMP = ((R * sizeof(T) + 127) / 128) * 128;
+  static constexpr uint32_t STAGE = 2 * COMP;
+  static constexpr uint32_t MAG = S * STAGE;
+  static constexpr uint32_t BAR = MAG + 2 * R * sizeof(T);
+  static constexpr uint32_t SMEM = BAR + S * 8;
+  static constexpr int MINB = sizeof(T) == 8 ? 2 : 4;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kGrBX * kGrBY, GrTma<T>::MINB)
+gradient_tma_kernel(const __grid_constant__ CUtensorMap map, int64_t members, int64_t nx, int64_t ny,
+                    T cx_in, T cx_bd, T cy_in, T cy_bd, T* __restrict__ out, int64_t out_mstride,
+                    int* err) {
+  using G = GrTma<T>;
+  extern __shared__ __align__(128) unsigned char gr_smem[];
+  T* const mag = reinterpret_cast<T*>(gr_smem + G::MAG);
+  uint64_t* const full = reinterpret_cast<uint64_t*>(gr_smem + G::BAR);
+  const int tid = threadIdx.y * kGrBX + threadIdx.x;
+  const int64_t n = nx * ny;
+  const int64_t i0 = int64_t(blockIdx.x) * kGrTX, j0 = int64_t(blockIdx.y) * kGrTY;
+  // this CTA's members: blockIdx.z, blockIdx.z + gridDim.z, ...
+  const int64_t cnt = blockIdx.z < members ? (members - blockIdx.z + gridDim.z - 1) / gridDim.z : 0;
+  auto issue = [&](int64_t k, int st) {
+    const int64_t m = blockIdx.z + k * gridDim.z;
+    unsigned char* dst = gr_smem + st * G::STAGE;
+    mbar_expect_tx(&full[st], 2 * G::R * sizeof(T));
+    tma_load_3d(dst, &map, &full[st], int(i0) - G::HX, int(j0) - G::HY, int(2 * m));
+    tma_load_3d(dst + G::COMP, &map, &full[st], int(i0) - G::HX, int(j0) - G::HY, int(2 * m + 1));
+  };
+  if (tid == 0) {
+    for (int st = 0; st < G::S; ++st) mbar_init(&full[st], 1);
+    mbar_fence_init();
+    for (int st = 0; st < G::S && st < cnt; ++st) issue(st, st);
+  }
+  // this thread's points: output offset (-1: outside), coefficients, slots
+  int64_t o_off[kGrPY * kGrPX];
+  T o_cx[kGrPY * kGrPX], o_cy[kGrPY * kGrPX];
+  int o_xh[kGrPY * kGrPX], o_xl[kGrPY * kGrPX], o_yh[kGrPY * kGrPX], o_yl[kGrPY * kGrPX];
+#pragma unroll
+  for (int e = 0; e < kGrPY * kGrPX; ++e) {
+    const int py = e / kGrPX, px = e % kGrPX;
+    const int64_t i = i0 + threadIdx.x + px * kGrBX, j = j0 + threadIdx.y + py * kGrBY;
+    const int64_t gi = min(i, nx - 1), gj = min(j, ny - 1);
+    const int x = int(gi - i0) + G::HX, y = int(gj - j0) + G::HY;
+    o_off[e] = (i < nx && j < ny) ? j * nx + i : -1;
+    o_cx[e] = (gi == 0 || gi == nx - 1) ? cx_bd : cx_in;
+    o_cy[e] = (gj == 0 || gj == ny - 1) ? cy_bd : cy_in;
+    o_xh[e] = y * G::RW + (gi < nx - 1 ? x + 1 : x);
+    o_xl[e] = y * G::RW + (gi > 0 ? x - 1 : x);
+    o_yh[e] = (gj < ny - 1 ? y + 1 : y) * G::RW + x;
+    o_yl[e] = (gj > 0 ? y - 1 : y) * G::RW + x;
+  }
+  __syncthreads();
+  int errbits = 0;
+  for (int64_t k = 0; k < cnt; ++k) {
+    const int st = int(k % G::S);
+    mbar_wait(&full[st], uint32_t(k / G::S) & 1u);
+    const T* su = reinterpret_cast<const T*>(gr_smem + st * G::STAGE);
+    const T* sv = reinterpret_cast<const T*>(gr_smem + st * G::STAGE + G::COMP);
+    T* const fl = mag + (k & 1) * G::R;
+#pragma unroll
+    for (int q0 = 0; q0 < G::NL; ++q0) {
+      const int q = tid + q0 * kGrBX * kGrBY;
+      if (q0 < G::NL - 1 || q < G::R) {
+        const T u = su[q], v = sv[q];
+        errbits |= check_value(u) | check_value(v);
+        fl[q] = hypot_(u, v);
+      }
+    }
+    __syncthreads();   // stage st consumed by every thread: refill it
+    if (tid == 0 && k + G::S < cnt) issue(k + G::S, st);
+    T* dst = out + (blockIdx.z + k * gridDim.z) * out_mstride;
+#pragma unroll
+    for (int e = 0; e < kGrPY * kGrPX; ++e) {
+      if (o_off[e] < 0) continue;
+      dst[o_off[e]] = grad_diff(fl[o_xh[e]], fl[o_xl[e]], o_cx[e]);
+      dst[n + o_off[e]] = grad_diff(fl[o_yh[e]], fl[o_yl[e]], o_cy[e]);
+    }
   }
   flush_error(err, errbits);
 }

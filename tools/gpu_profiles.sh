@@ -17,7 +17,7 @@ prof k3 k3_tma --config 4 --steps 3 --warmup 3 --no-e2e --no-cpu
 prof c1 k3_rowmarch --config 1 --steps 5 --warmup 3 --no-e2e --no-cpu
 prof mc mc_chunk --config 2 --steps 3 --warmup 3 --no-e2e --no-cpu
 prof lcp lcp2d --workload lcp --steps 3 --no-cpu --no-e2e
-prof gradient gradient2d --workload gradient --steps 3 --no-cpu --no-e2e
+prof gradient gradient_tma --workload gradient --steps 3 --no-cpu --no-e2e
 prof fit fit_bulk --workload fit --steps 3 --no-cpu --no-e2e
 prof redsea gradfused --workload redsea --steps 3 --no-cpu --no-e2e
 rm -f gpurun_out/prof_c1.ncu-rep gpurun_out/prof_mc.ncu-rep gpurun_out/prof_lcp.ncu-rep \
