@@ -543,6 +543,7 @@ def main():
         e.record(stream)
         return e
 
+    exchange_used = args.exchange
     if args.config == 3:
         nx, ny, nz = cfg.nx, cfg.ny, cfg.nz
         step = SlabStep(nx, ny, nz, rank, world, device="cuda", exchange=args.exchange)
@@ -551,6 +552,8 @@ def main():
         out = {k: torch.empty(n_local, dtype=torch.float32, device="cuda") for k in dev.ALL_OUTPUTS}
         plane = nx * ny
         mu_w, s_w = fields[2], fields[5]
+        shard.ensure_p2p(step, {"mu_w": mu_w, "s_w": s_w})   # falls back to NCCL on every rank
+        exchange_used = step.exchange
         total_pts = nx * ny * nz
         scaling = "strong"
 
@@ -584,6 +587,8 @@ def main():
         nz = args.planes_per_gpu * world
         step = SlabStep(nx, ny, nz, rank, world, device="cuda", exchange=args.exchange)
         members = configs.config4_slab(step.z0, step.nzl, nx, ny, nz, cfg.members, cfg.seed)
+        shard.ensure_p2p(step, {"members": members})
+        exchange_used = step.exchange
         n_local = nx * ny * step.nzl
         out = {k: torch.empty(n_local, dtype=torch.float32, device="cuda") for k in dev.ALL_OUTPUTS}
         total_pts = nx * ny * nz
@@ -908,7 +913,9 @@ def main():
         "config": {"workload": workload, "grid_points": total_pts, "t": cfg.t,
                    "parallelism": f"z-slab x{world}" if args.config in (3, 4) else f"replicas x{world}",
                    "exchange": (("peer memory (CUDA IPC over NVLink), read in place by the kernels"
-                                 if args.exchange == "p2p" else "NCCL send/recv overlapped with the interior")
+                                 if exchange_used == "p2p" else "NCCL send/recv overlapped with the interior")
+                                + ("" if exchange_used == args.exchange else
+                                   " (fallback: peer mapping failed on some rank)")
                                 if args.config in (3, 4) and world > 1 else None),
                    **({"dry_run": "DIVUQ_BENCH_ONE_DEVICE=1: every rank on cuda:0 over gloo "
                                   "(orchestration check, not a multi-GPU number)"}

@@ -62,8 +62,14 @@ def exchange_handles(arrays: dict[str, torch.Tensor], rank: int, world: int, gro
                      want=None) -> dict[int, dict[str, PeerArray]]:
     """Export ``arrays``, all-gather every rank's handles, map the ranks in
     ``want`` (default: the z-neighbours rank-1 and rank+1).  Collective."""
-    mine = {k: export_tensor(v) for k, v in arrays.items()}
+    try:
+        mine = {k: export_tensor(v) for k, v in arrays.items()}
+    except Exception as exc:   # still join the collective, so no rank blocks in it
+        mine = {"__error__": repr(exc)}
     allh = [None] * world
     dist.all_gather_object(allh, mine, group=group)
+    bad = [r for r in range(world) if "__error__" in allh[r]]
+    if bad:
+        raise RuntimeError(f"peer export failed on rank(s) {bad}: {allh[bad[0]]['__error__']}")
     want = [r for r in (rank - 1, rank + 1) if 0 <= r < world] if want is None else want
     return {r: {k: PeerArray(*allh[r][k]) for k in allh[r]} for r in want}

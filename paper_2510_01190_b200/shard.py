@@ -149,6 +149,29 @@ def _sync_inputs(step: SlabStep):
     dist.barrier(group=step.group)
 
 
+def ensure_p2p(step: SlabStep, arrays: dict) -> bool:
+    """Collective: map the neighbours' ``arrays`` for the p2p exchange; if any
+    rank cannot (no peer access, IPC refused), every rank switches this step
+    to the NCCL schedule instead.  Returns whether p2p is in use."""
+    if step.exchange != "p2p" or step.world == 1:
+        return step.exchange == "p2p"
+    ok = 1
+    try:
+        step.attach(arrays)
+    except Exception:   # export failures are raised on every rank alike
+        ok = 0
+    flag = torch.tensor([ok], dtype=torch.int32, device=step.device if dist.get_backend(step.group) == "nccl"
+                        else "cpu")
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=step.group)
+    if int(flag.item()) == 1:
+        return True
+    for arrs in (step.peers or {}).values():
+        for a in arrs.values():
+            a.close()
+    step.peers, step._attached, step.exchange = {}, None, "nccl"
+    return False
+
+
 def propagate3d_step(step: SlabStep, fields, out, dx, dy, dz, t, check=False, sync_inputs=False):
     """K2 sharded step on this rank's slab tensors (fields = 6 slab tensors)."""
     from . import device as dev

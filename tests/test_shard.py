@@ -155,3 +155,35 @@ def test_exchange_modes_and_neighbour_extents():
     # the first plane of rank+1 (byte offsets into their slabs)
     plane, es = 16, 4
     assert (s.neighbour_nzl(0) - 1) * plane * es == 192
+
+
+def _fallback_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2510_01190_b200 import shard
+
+        step = shard.SlabStep(NX, NY, NZ, rank, world, dtype=torch.float64, device="cpu", exchange="p2p")
+        plane = NX * NY
+        w = torch.zeros(step.nzl * plane, dtype=torch.float64)
+        used = shard.ensure_p2p(step, {"mu_w": w, "s_w": w.clone()})   # host memory: no IPC handle
+        q.put((rank, used, step.exchange, step.peers))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_p2p_mapping_failure_falls_back_to_nccl_on_every_rank():
+    """bench.py calls shard.ensure_p2p before timing: if any rank cannot map
+    its neighbours' buffers, all ranks agree (one all-reduce) and run the NCCL
+    schedule instead -- nobody is left blocked in the handle all-gather."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fallback_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=120) for _ in range(2)])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [(r[1], r[2], r[3]) for r in res] == [(False, "nccl", {})] * 2
