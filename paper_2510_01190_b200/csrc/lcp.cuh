@@ -21,30 +21,30 @@ namespace divuq {
 // libdevice's erfc takes different code paths by range, so a warp whose
 // vertices straddle the ranges runs several of them (ncu: the LCP kernel was
 // issue-bound at ~330 instructions per cell).  Here: erfc(a) =
-// exp(-a^2) * h(q) / (a + K), q = (a - K) / (a + K), K = 3.75, h a degree-20
-// polynomial fitted offline against scipy's erfcx (tools/fit_erfc.py: fit64;
-// max relative error 3.8e-15 on [0, 26.5]), one reciprocal, one branch-free
-// exp, and the a*a rounding corrected by one FMA.  The LCP bar is absolute (1e-12) on
-// products of tail probabilities, far above this.  Past a = 26.6 erfc is
-// below the smallest normal double: 0 (also for a = inf, sigma -> 0+).
-__constant__ double kErfcLcp[21] = {
-    0x1.17884282534a6p+0, -0x1.eae02d0a14575p-1, 0x1.78fecb4e81911p-1, -0x1.f63dd81197172p-2,
-    0x1.1dc27118a572ap-2, -0x1.0e3ea22487d15p-3, 0x1.92618b748e0dbp-5, -0x1.9ac695838042dp-7,
-    0x1.02900c1cc2f87p-10, 0x1.a0b7617bbe006p-11, -0x1.6d95991270bd9p-12, 0x1.63741a4632739p-17,
-    0x1.3a61910987620p-15, -0x1.2ab497b501b66p-17, -0x1.bb2922abacccep-19, 0x1.bb2c732d1672ap-20,
-    0x1.3f8939719327ap-22, -0x1.1066ac54efe96p-22, -0x1.6288b0af8129ap-25, 0x1.f6c45f0bc1fb5p-26,
-    0x1.1081b6baf64d4p-27};
+// exp(-a^2) * h(q) / (a + K), q = (a - K) / (a + K), K = 3, h a degree-16
+// polynomial fitted offline against scipy's erfcx on [0, 6.2]
+// (tools/fit_erfc.py: fit64(3.0, 16, amax=6.2); max error 1.3e-15 absolute,
+// 2.9e-15 relative), one reciprocal (one Newton step), one branch-free exp,
+// and the a*a rounding corrected by one FMA.  The LCP bar is ABSOLUTE
+// (1e-12 on products of tail probabilities): past a = 6.2 erfc(a) < 1.9e-18,
+// returned as 0 (also for a = inf, sigma -> 0+).  (The first version fitted
+// degree 20 on [0, 26.5] to 3.8e-15 relative: 4 more FMAs per vertex.)
+__constant__ double kErfcLcp[17] = {
+    0x1.12f21ddd9f5e1p+0, -0x1.c44c471baa268p-1, 0x1.2e326945de38ap-1, -0x1.3deb21416ca90p-2,
+    0x1.e995f11b16886p-4, -0x1.b78993b5e4be8p-6, -0x1.3dd3e5fc26ebfp-10, 0x1.8dae28f56a401p-9,
+    -0x1.1f7943276e395p-11, -0x1.2234c8a90349bp-12, 0x1.c350cc2d97cf3p-14, 0x1.fd736047b47bdp-16,
+    -0x1.28c763237c059p-16, -0x1.4c4280ee09a7ap-18, 0x1.9657f8bc02840p-19, 0x1.d4b67a91621acp-20,
+    0x1.2479dd117d25fp-22};
 
-// exp(t) for t in [-708, 0] (the caller discards t < -707): k = rint(t/ln2),
-// r = t - k ln2 (fdlibm's hi/lo split), e^r by its Taylor series to r^12
-// (|r| <= 0.347: truncation < 2e-16), times 2^k built in the exponent bits.
+// exp(t) for t in [-39, 0] (a <= 6.2): k = rint(t/ln2), r = t - k ln2
+// (fdlibm's hi/lo split), e^r by its Taylor series to r^11 (|r| <= 0.347:
+// truncation < 7e-15 relative), times 2^k built in the exponent bits.
 // Coefficients come from constant memory (no UMOV-materialised literals), no
 // range branches.
-__constant__ double kExpTaylor[13] = {
+__constant__ double kExpTaylor[12] = {
     0x1.0000000000000p+0, 0x1.0000000000000p+0, 0x1.0000000000000p-1, 0x1.5555555555555p-3,
     0x1.5555555555555p-5, 0x1.1111111111111p-7, 0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-13,
-    0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19, 0x1.27e4fb7789f5cp-22, 0x1.ae64567f544e4p-26,
-    0x1.1eed8eff8d898p-29};
+    0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19, 0x1.27e4fb7789f5cp-22, 0x1.ae64567f544e4p-26};
 
 __device__ __forceinline__ double exp_neg_lcp(double t) {
   const double y = fma(t, 0x1.71547652b82fep+0, 0x1.8p52);   // 1.5*2^52 + rint(t*log2(e))
@@ -52,45 +52,43 @@ __device__ __forceinline__ double exp_neg_lcp(double t) {
   const int ki = __double2loint(y);
   double r = fma(kd, -6.93147180369123816490e-01, t);
   r = fma(kd, -1.90821492927058770002e-10, r);
-  double p = kExpTaylor[12];
+  double p = kExpTaylor[11];
 #pragma unroll
-  for (int k = 11; k >= 0; --k) p = fma(p, r, kExpTaylor[k]);
+  for (int k = 10; k >= 0; --k) p = fma(p, r, kExpTaylor[k]);
   return p * __hiloint2double((ki + 1023) << 20, 0);
 }
 
-__device__ __forceinline__ double erfc_abs_lcp(double x) {
-  constexpr double K = 3.75;
-  const double a = fabs(x);
-  const double d = a + K;
+// 1/d: rcp.approx (~2^-23) and one Newton step (~2^-46 relative) -- ample for
+// the absolute 1e-12 LCP bar; lcp_div below adds a residual correction
+__device__ __forceinline__ double rcp_lcp(double d) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-  double e = fma(-d, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-d, r, 1.0);
-  r = fma(r, e, r);
+  return fma(r, fma(-d, r, 1.0), r);
+}
+
+__device__ __forceinline__ double erfc_abs_lcp(double x) {
+  constexpr double K = 3.0;
+  const double a = fabs(x);
+  const double r = rcp_lcp(a + K);
   const double q = (a - K) * r;
-  double p = kErfcLcp[20];
+  double p = kErfcLcp[16];
 #pragma unroll
-  for (int k = 19; k >= 0; --k) p = fma(p, q, kErfcLcp[k]);
+  for (int k = 15; k >= 0; --k) p = fma(p, q, kErfcLcp[k]);
   const double s = a * a;
   const double lo = fma(a, a, -s);   // a*a - s exactly
-  double y = p * r * exp_neg_lcp(fmax(-s, -707.0));
+  double y = p * r * exp_neg_lcp(fmax(-s, -39.0));
   y = fma(y, -lo, y);                // * exp(-lo) ~ (1 - lo)
-  return a > 26.6 ? 0.0 : y;
+  return a > 6.2 ? 0.0 : y;
 }
 __device__ __forceinline__ float erfc_abs_lcp(float x) { return erfc_abs(x); }
 
-// (theta - mu) / sigma: fp64 by reciprocal + two Newton steps (<= 1 ulp; no
+// (theta - mu) / sigma: fp64 by reciprocal + one Newton step + one residual
+// correction (~1 ulp; no
 // IEEE-division slow path: sigma > 0 and finite here); fp32 IEEE as before
 __device__ __forceinline__ double lcp_div(double n, double d) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-  double e = fma(-d, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-d, r, 1.0);
-  r = fma(r, e, r);
+  const double r = rcp_lcp(d);
   const double q = n * r;
-  return fma(fma(-d, q, n), r, q);   // one residual correction
+  return fma(fma(-d, q, n), r, q);   // one residual correction: ~1 ulp
 }
 __device__ __forceinline__ float lcp_div(float n, float d) { return __fdiv_rn(n, d); }
 
