@@ -1361,6 +1361,15 @@ int divuq_lcp2d_f64(const double* mu, const double* sigma, int64_t nx, int64_t n
   if (nx < 2 || ny < 2) return DIVUQ_EGRID;
   if (!mu || !sigma || !out) return DIVUQ_EINVAL;
   dim3 grid(unsigned((nx - 1 + kLcpTX - 1) / kLcpTX), unsigned((ny - 1 + kLcpTY - 1) / kLcpTY));
+  CUtensorMap mm{}, ms{};
+  if (!env_int("DIVUQ_NO_TMA", 0) && nx % 2 == 0 && aligned(mu, 16) && aligned(sigma, 16) &&
+      nx < (int64_t(1) << 31) && ny < (int64_t(1) << 31) &&
+      make_map3d<double>(&mm, mu, nx, ny, 1, LcpTma<double>::W, LcpTma<double>::H, 0) &&
+      make_map3d<double>(&ms, sigma, nx, ny, 1, LcpTma<double>::W, LcpTma<double>::H, 0)) {
+    lcp2d_tma_kernel<double><<<grid, dim3(kLcpBX, kLcpBY), 0, static_cast<cudaStream_t>(stream)>>>(
+        mm, ms, nx, ny, isovalue, out, err);
+    return int(cudaGetLastError());
+  }
   lcp2d_kernel<double><<<grid, dim3(kLcpBX, kLcpBY), 0, static_cast<cudaStream_t>(stream)>>>(
       mu, sigma, nx, ny, isovalue, out, err);
   return int(cudaGetLastError());

@@ -14,6 +14,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace divuq {
 
@@ -148,6 +149,70 @@ lcp2d_kernel(const T* __restrict__ mu, const T* __restrict__ sigma, int64_t nx, 
   }
 #pragma unroll 1
   for (int v = tid; v < kLcpV; v += kLcpBX * kLcpBY) {   // own slots only: no barrier needed
+    const T m = bl[v], sg = ab[v];
+    errbits |= check_value(m) | check_sigma(sg);
+    T b, a;
+    tail_pair_lcp(m, sg, theta, b, a);
+    bl[v] = b;
+    ab[v] = a;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int ry = 0; ry < kLcpTY; ry += kLcpBY) {
+#pragma unroll
+    for (int rx = 0; rx < kLcpTX; rx += kLcpBX) {
+      const int x = threadIdx.x + rx, y = threadIdx.y + ry;
+      const int64_t ci = ci0 + x, cj = cj0 + y;
+      if (ci < nx - 1 && cj < ny - 1) {
+        // corners in lcp.py order: v00, v00+1, v00+nx, v00+nx+1
+        const T pb = A::mul(A::mul(A::mul(below[y][x], below[y][x + 1]), below[y + 1][x]), below[y + 1][x + 1]);
+        const T pa = A::mul(A::mul(A::mul(above[y][x], above[y][x + 1]), above[y + 1][x]), above[y + 1][x + 1]);
+        const T r = A::sub(T(1), A::add(pb, pa));
+        out[cj * (nx - 1) + ci] = r < T(0) ? T(0) : (r > T(1) ? T(1) : r);
+      }
+    }
+  }
+  flush_error(err, errbits);
+}
+
+// TMA variant (nx * sizeof(T) % 16 == 0): one thread stages the tile's
+// (mu, sigma) boxes of 17 x (64 + 16 B) vertices straight into the two tables
+// with cp.async.bulk.tensor (out-of-grid vertices arrive as 0, 0: a finite
+// step-function tail pair in cells that are never written), so the per-vertex
+// index arithmetic, bounds checks and parking of the register-loaded kernel
+// disappear (~40 of its ~200 instructions per vertex); the tail-pair loop runs
+// over every table slot without coordinates.  Same arithmetic as above.
+template <typename T>
+struct LcpTma {
+  static constexpr int W = kLcpTX + 16 / int(sizeof(T));   // box width: 16-byte multiple
+  static constexpr int H = kLcpTY + 1;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kLcpBX * kLcpBY)
+lcp2d_tma_kernel(const __grid_constant__ CUtensorMap map_mu, const __grid_constant__ CUtensorMap map_sg,
+                 int64_t nx, int64_t ny, T theta, T* __restrict__ out, int* err) {
+  using A = Arith<T>;
+  using L = LcpTma<T>;
+  __shared__ __align__(128) T below[L::H][L::W];
+  __shared__ __align__(128) T above[L::H][L::W];
+  __shared__ uint64_t bar;
+  const int tid = threadIdx.y * kLcpBX + threadIdx.x;
+  const int64_t ci0 = int64_t(blockIdx.x) * kLcpTX, cj0 = int64_t(blockIdx.y) * kLcpTY;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+    mbar_expect_tx(&bar, 2 * L::H * L::W * sizeof(T));
+    tma_load_3d(&below[0][0], &map_mu, &bar, int(ci0), int(cj0), 0);
+    tma_load_3d(&above[0][0], &map_sg, &bar, int(ci0), int(cj0), 0);
+  }
+  __syncthreads();
+  mbar_wait(&bar, 0);
+  int errbits = 0;
+  T* const bl = &below[0][0];
+  T* const ab = &above[0][0];
+#pragma unroll 1
+  for (int v = tid; v < L::H * L::W; v += kLcpBX * kLcpBY) {   // own slots only: no barrier needed
     const T m = bl[v], sg = ab[v];
     errbits |= check_value(m) | check_sigma(sg);
     T b, a;

@@ -16,7 +16,7 @@ prof k2 k2_tma --config 3 --steps 5 --warmup 3 --no-e2e --no-cpu
 prof k3 k3_tma --config 4 --steps 3 --warmup 3 --no-e2e --no-cpu
 prof c1 k3_rowmarch --config 1 --steps 5 --warmup 3 --no-e2e --no-cpu
 prof mc mc_chunk --config 2 --steps 3 --warmup 3 --no-e2e --no-cpu
-prof lcp lcp2d --workload lcp --steps 3 --no-cpu --no-e2e
+prof lcp lcp2d_tma --workload lcp --steps 3 --no-cpu --no-e2e
 prof gradient gradient_tma --workload gradient --steps 3 --no-cpu --no-e2e
 prof fit fit_bulk --workload fit --steps 3 --no-cpu --no-e2e
 prof redsea gradfused --workload redsea --steps 3 --no-cpu --no-e2e
