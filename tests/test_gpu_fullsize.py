@@ -240,3 +240,29 @@ def test_config1_full_size_vs_oracle(dev):
     assert np.all(np.abs(p - ps_own) <= 1e-5 * ps_own + 1e-6)
     ps = ref2d.source_probability(dmu, dsg, 0.0)
     assert np.abs(p - ps).max() <= 1e-3
+
+
+def test_redsea_chain_full_size(dev):
+    """K6 at the redsea bench size (config-1 velocity ensemble, M=20, 1024^2):
+    bitwise equal to gradient_ensemble2d_f32 + ensemble_divergence2d_f32 on
+    the whole grid, and within the fp32 bar of the fp64 oracle chain on a
+    full-width strip that includes the y = 0 face."""
+    from paper_2510_01190_b200 import configs
+
+    nx = ny = 1024
+    mem = configs.config1_members(nx, ny, 20)
+    fused = dev.gradient_ensemble_divergence2d(mem, nx, ny, 1.0, 1.0, 0.0, moments=True)
+    grad = dev.gradient_ensemble2d(mem, nx, ny, 1.0, 1.0)
+    comp = dev.ensemble_divergence2d(grad, nx, ny, 1.0, 1.0, 0.0, moments=True)
+    for k in ("mu", "sigma", "p_src", "p_snk", "mom_mu", "mom_sigma"):
+        assert torch.equal(fused[k], comp[k]), k
+    rows = 40   # the strip's last 2 rows only serve as neighbours
+    host = mem[:, :, : rows * nx].cpu().numpy().astype(np.float64)
+    g = ref2d.gradient_ensemble(host, nx, rows, 1.0, 1.0)
+    mu_r, sg_r = ref2d.fit_moments(g)
+    dmu, dsg = ref2d.propagate2d(mu_r[0], mu_r[1], sg_r[0], sg_r[1], nx, rows, 1.0, 1.0)
+    keep = slice(0, (rows - 2) * nx)   # rows whose stencil does not see the strip's cut
+    got_mu = fused["mu"][: rows * nx].cpu().numpy()[keep]
+    got_sg = fused["sigma"][: rows * nx].cpu().numpy()[keep]
+    assert np.abs(got_mu - dmu[keep]).max() <= 1e-5 * np.abs(dmu[keep]).max()
+    assert np.abs(got_sg - dsg[keep]).max() <= 1e-5 * np.abs(dsg[keep]).max()
