@@ -755,7 +755,7 @@ def main():
         host_in = [f.cpu().pin_memory() for f in fields]
         host_out = [torch.empty(n_local, dtype=torch.float32).pin_memory() for _ in range(4)]
         g_nz = step.nzl  # each rank pushes its own slab through the host entry point
-        chunk = 32
+        chunk = 16       # tools/e2e_chunk_probe.py: 8/16/32/64/128 -> 67.8/67.3/68.9/72.5/80.7 ms
 
         def e2e_call():
             st = lib.divuq_host_propagate3d_f32(
@@ -776,12 +776,10 @@ def main():
             t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
-        nchunks = -(-g_nz // chunk)
-        w_planes = sum(min(g_nz, (c + 1) * chunk + 1) - max(0, c * chunk - 1) for c in range(nchunks))
-        h2d = 4 * (4 * n_local + 2 * w_planes * nx * ny)
+        h2d = 4 * 6 * n_local   # every field byte crosses PCIe once (halos read from HBM)
         e2e = {"value": total_pts / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
                "d2h_bytes_per_step": 16 * n_local * world, "ms_per_step": e2e_s * 1e3,
-               "path": "divuq_host_propagate3d_f32 (pinned host buffers, 2-stream z-chunk pipeline)"}
+               "path": "divuq_host_propagate3d_f32 (pinned host buffers, 3-stream z-chunk pipeline)"}
     elif not args.no_e2e and args.config == 4:
         # each rank pushes its slab from pinned host memory through the host
         # entry; bounded so all ranks' pinned copies fit in 40% of host RAM

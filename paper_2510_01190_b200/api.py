@@ -103,7 +103,7 @@ def propagate_with_probabilities(model: GaussianVectorField, t: float = 0.0, *,
 
 
 def propagate_with_probabilities3d(model: GaussianVectorField3, t: float = 0.0, *,
-                                   probabilities: bool = True, chunk_planes: int = 32) -> Propagation:
+                                   probabilities: bool = True, chunk_planes: int = 16) -> Propagation:
     """3D twin (fp32 models use the pipelined host entry point; fp64 models
     are staged through torch and run the fp64 kernel)."""
     g = model.grid

@@ -1879,6 +1879,12 @@ int divuq_host_mc_histogram1d_f64(const double* neighbors, double dx, double dy,
   return DIVUQ_OK;
 }
 
+// 3D analytic propagation from host buffers (the e2e leg of config 3): a
+// z-chunk pipeline over three cached streams -- copy-in, compute, copy-out --
+// and four buffer sets.  Chunk c's w halo planes are read in place from the
+// neighbour chunks' sets already in HBM (no ghost-plane re-upload), so the
+// copy-in stream only waits for a set to be released (compute of chunk c-3)
+// and never for a device-to-host copy: both PCIe directions stay busy.
 int divuq_host_propagate3d_f32(const float* mu_u, const float* mu_v, const float* mu_w,
                                const float* s_u, const float* s_v, const float* s_w, int64_t nx,
                                int64_t ny, int64_t nz, double dx, double dy, double dz, double t,
@@ -1892,49 +1898,76 @@ int divuq_host_propagate3d_f32(const float* mu_u, const float* mu_v, const float
   float* host_out[4] = {out_mu, out_sigma, out_p_src, out_p_snk};
   DIVUQ_CUDA(cudaSetDevice(device));
   const int64_t plane = nx * ny;
+  const size_t plane_b = size_t(plane) * sizeof(float);
   const int64_t cz = std::max<int64_t>(1, std::min<int64_t>(chunk_planes > 0 ? chunk_planes : 32, nz));
-  const int64_t nchunks = (nz + cz - 1) / cz;
-  StreamGuard sg[2];
-  for (int q = 0; q < 2; ++q) DIVUQ_CUDA(cached_stream(q, &sg[q].s));
-  // per buffer set: u, v, su, sv: cz planes; w, sw: cz + 2 planes; 4 outputs: cz planes
-  const int64_t set_elems = 4 * cz * plane + 2 * (cz + 2) * plane + 4 * cz * plane;
+  const int64_t nch = (nz + cz - 1) / cz;
+  constexpr int kSets = 4;
+  const int nsets = int(std::min<int64_t>(kSets, nch));
+  const int64_t set_elems = 10 * cz * plane;   // 6 fields + 4 outputs, cz planes each
+  StreamGuard cin, cmp, cout;
+  DIVUQ_CUDA(cached_stream(0, &cin.s));
+  DIVUQ_CUDA(cached_stream(1, &cmp.s));
+  DIVUQ_CUDA(cached_stream(2, &cout.s));
   DevBuf d;
-  DIVUQ_CUDA(d.alloc(size_t(2 * set_elems) * sizeof(float) + 256, sg[0].s));
-  DIVUQ_CUDA(cudaStreamSynchronize(sg[0].s));
-  int32_t* derr = reinterpret_cast<int32_t*>(d.as<float>() + 2 * set_elems);
-  DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg[0].s));
-  DIVUQ_CUDA(cudaStreamSynchronize(sg[0].s));
-  for (int64_t c = 0; c < nchunks; ++c) {
-    cudaStream_t s = sg[c % 2].s;
-    float* set = d.as<float>() + (c % 2) * set_elems;
-    float* uv[4] = {set, set + cz * plane, set + 2 * cz * plane, set + 3 * cz * plane};  // u v su sv
-    float* wbuf = set + 4 * cz * plane;                 // (cz+2) planes
-    float* swbuf = wbuf + (cz + 2) * plane;
-    float* outs = swbuf + (cz + 2) * plane;
-    const int64_t z0 = c * cz, nzl = std::min(cz, nz - z0);
-    const size_t nb = size_t(nzl * plane) * sizeof(float);
-    const int src_idx[4] = {0, 1, 3, 4};
-    for (int q = 0; q < 4; ++q)
-      DIVUQ_CUDA(cudaMemcpyAsync(uv[q], in[src_idx[q]] + z0 * plane, nb, cudaMemcpyHostToDevice, s));
-    // w with one ghost plane each side (slot 0 = z0-1, slot 1.. = z0..)
-    const int64_t wlo = std::max<int64_t>(0, z0 - 1), whi = std::min<int64_t>(nz, z0 + nzl + 1);
-    const int64_t slot0 = 1 - (z0 - wlo);
-    const size_t wb = size_t((whi - wlo) * plane) * sizeof(float);
-    DIVUQ_CUDA(cudaMemcpyAsync(wbuf + slot0 * plane, mu_w + wlo * plane, wb, cudaMemcpyHostToDevice, s));
-    DIVUQ_CUDA(cudaMemcpyAsync(swbuf + slot0 * plane, s_w + wlo * plane, wb, cudaMemcpyHostToDevice, s));
+  DIVUQ_CUDA(d.alloc(size_t(nsets * set_elems) * sizeof(float) + 256, cin.s));
+  int32_t* derr = reinterpret_cast<int32_t*>(d.as<float>() + nsets * set_elems);
+  DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), cin.s));
+  struct Events {
+    cudaEvent_t up[kSets] = {}, comp[kSets] = {}, out[kSets] = {};
+    ~Events() {
+      for (int i = 0; i < kSets; ++i)
+        for (cudaEvent_t e : {up[i], comp[i], out[i]})
+          if (e) cudaEventDestroy(e);
+    }
+  } ev;
+  for (int i = 0; i < kSets; ++i) {
+    DIVUQ_CUDA(cudaEventCreateWithFlags(&ev.up[i], cudaEventDisableTiming));
+    DIVUQ_CUDA(cudaEventCreateWithFlags(&ev.comp[i], cudaEventDisableTiming));
+    DIVUQ_CUDA(cudaEventCreateWithFlags(&ev.out[i], cudaEventDisableTiming));
+  }
+  auto nzl = [&](int64_t c) { return std::min(cz, nz - c * cz); };
+  auto field = [&](int64_t c, int a) { return d.as<float>() + (c % kSets) * set_elems + a * cz * plane; };
+  auto upload = [&](int64_t c) -> int {
+    if (c >= kSets) DIVUQ_CUDA(cudaStreamWaitEvent(cin.s, ev.comp[(c - 3) % kSets], 0));
+    for (int a = 0; a < 6; ++a)
+      DIVUQ_CUDA(cudaMemcpyAsync(field(c, a), in[a] + c * cz * plane, size_t(nzl(c)) * plane_b,
+                                 cudaMemcpyHostToDevice, cin.s));
+    DIVUQ_CUDA(cudaEventRecord(ev.up[c % kSets], cin.s));
+    return 0;
+  };
+  auto compute = [&](int64_t c) -> int {
+    DIVUQ_CUDA(cudaStreamWaitEvent(cmp.s, ev.up[(c + 1 < nch ? c + 1 : c) % kSets], 0));
+    if (c >= kSets) DIVUQ_CUDA(cudaStreamWaitEvent(cmp.s, ev.out[c % kSets], 0));
+    const float* hl_mu = c > 0 ? field(c - 1, 2) + (nzl(c - 1) - 1) * plane : nullptr;
+    const float* hl_s = c > 0 ? field(c - 1, 5) + (nzl(c - 1) - 1) * plane : nullptr;
+    const float* hh_mu = c + 1 < nch ? field(c + 1, 2) : nullptr;
+    const float* hh_s = c + 1 < nch ? field(c + 1, 5) : nullptr;
     float* o[4];
-    for (int q = 0; q < 4; ++q) o[q] = host_out[q] ? outs + q * cz * plane : nullptr;
-    int r = propagate3d<float>(uv[0], uv[1], wbuf + plane, uv[2], uv[3], swbuf + plane, wbuf, swbuf,
-                               wbuf + (nzl + 1) * plane, swbuf + (nzl + 1) * plane, nx, ny, nzl, z0, nz,
-                               0, nzl, dx, dy, dz, t, o[0], o[1], o[2], o[3], derr, s);
-    if (r) return r;
+    for (int q = 0; q < 4; ++q) o[q] = host_out[q] ? field(c, 6 + q) : nullptr;
+    if (int r = propagate3d<float>(field(c, 0), field(c, 1), field(c, 2), field(c, 3), field(c, 4),
+                                   field(c, 5), hl_mu, hl_s, hh_mu, hh_s, nx, ny, nzl(c), c * cz, nz, 0,
+                                   nzl(c), dx, dy, dz, t, o[0], o[1], o[2], o[3], derr, cmp.s))
+      return r;
+    DIVUQ_CUDA(cudaEventRecord(ev.comp[c % kSets], cmp.s));
+    DIVUQ_CUDA(cudaStreamWaitEvent(cout.s, ev.comp[c % kSets], 0));
     for (int q = 0; q < 4; ++q)
       if (host_out[q])
-        DIVUQ_CUDA(cudaMemcpyAsync(host_out[q] + z0 * plane, o[q], nb, cudaMemcpyDeviceToHost, s));
+        DIVUQ_CUDA(cudaMemcpyAsync(host_out[q] + c * cz * plane, o[q], size_t(nzl(c)) * plane_b,
+                                   cudaMemcpyDeviceToHost, cout.s));
+    DIVUQ_CUDA(cudaEventRecord(ev.out[c % kSets], cout.s));
+    return 0;
+  };
+  if (int r = upload(0)) return r;
+  for (int64_t c = 1; c < nch; ++c) {
+    if (int r = upload(c)) return r;
+    if (int r = compute(c - 1)) return r;
   }
-  DIVUQ_CUDA(cudaStreamSynchronize(sg[1].s));
+  if (int r = compute(nch - 1)) return r;
+  DIVUQ_CUDA(cudaStreamSynchronize(cin.s));
+  DIVUQ_CUDA(cudaStreamSynchronize(cmp.s));
+  DIVUQ_CUDA(cudaStreamSynchronize(cout.s));
   int status = 0;
-  DIVUQ_CUDA(check_err_word(derr, sg[0].s, &status));
+  DIVUQ_CUDA(check_err_word(derr, cmp.s, &status));
   return status;
 }
 

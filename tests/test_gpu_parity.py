@@ -371,6 +371,25 @@ def test_ensemble_divergence3d_and_slabs(dev, m, rng):
                 assert np.array_equal(host(o[k]), host(full[k])[z0 * plane:z1 * plane]), (parts, r, k)
 
 
+@pytest.mark.parametrize("chunk", [1, 3, 5, 32])
+def test_host_propagate3d_pipeline(dev, chunk, rng):
+    """Host-buffer 3D propagation (3-stream z-chunk pipeline; halo planes read
+    from the neighbour chunks in HBM) == the device K2 call, bitwise, for any
+    chunking; the reference-facing wrapper returns the same maps."""
+    import paper_2510_01190_b200 as d
+
+    nx, ny, nz = 64, 9, 13
+    n = nx * ny * nz
+    f = [rng.normal(size=n).astype(np.float32) for _ in range(3)] + \
+        [rng.uniform(0.05, 0.4, n).astype(np.float32) for _ in range(3)]
+    whole = dev.propagate3d(*(cu(x) for x in f), nx, ny, nz, 1.0, 0.5, 2.0, 0.1)
+    g = d.UniformGrid3(nx, ny, nz, 1.0, 0.5, 2.0)
+    model = d.GaussianVectorField3(g, *f)
+    r = d.propagate_with_probabilities3d(model, 0.1, chunk_planes=chunk)
+    for k, a in (("mu", r.field.mu), ("sigma", r.field.sigma), ("p_src", r.p_src), ("p_snk", r.p_snk)):
+        assert np.array_equal(a, host(whole[k])), (chunk, k)
+
+
 @pytest.mark.parametrize("chunk", [0, 1, 3, 5])
 def test_host_ensemble_divergence3d_pipeline(dev, chunk, rng):
     """Host-buffer 3D ensemble entry (3-stream z-chunk pipeline, halos fitted
