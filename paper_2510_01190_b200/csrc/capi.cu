@@ -855,12 +855,10 @@ static void memcpy_parallel(char* dst, const char* src, int64_t len) {
   const int nt = int(std::min<int64_t>(std::min<int64_t>(kMaxThreads, hw), (len + kSlice - 1) / kSlice));
   if (nt <= 1) { std::memcpy(dst, src, size_t(len)); return; }
   const int64_t per = (len + nt - 1) / nt;
-  std::thread th[kMaxThreads];
-  for (int t = 0; t < nt; ++t) {
+  io::HostPool::get().run(nt, [&](int t) {
     const int64_t a = t * per, n = std::min(per, len - a);
-    th[t] = std::thread([=] { if (n > 0) std::memcpy(dst + a, src + a, size_t(n)); });
-  }
-  for (int t = 0; t < nt; ++t) th[t].join();
+    if (n > 0) std::memcpy(dst + a, src + a, size_t(n));
+  });
 }
 
 static bool pageable(const void* p) {

@@ -24,6 +24,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <condition_variable>
+#include <functional>
 #include <thread>
 #include <vector>
 
@@ -181,6 +183,74 @@ inline Staging& staging() {
   return *s;
 }
 
+// Persistent host workers for the parallel page-cache reads and staging
+// copies: spawning 16 std::threads per 32 MB chunk cost ~0.3 ms per chunk.
+// run(n, fn) executes fn(0..n-1) spread over the caller and the workers and
+// returns when all are done; calls are serialised.  Workers are never joined (detached at
+// process exit with the pool, which is never destroyed).
+class HostPool {
+ public:
+  static constexpr int kMax = 16;
+  static HostPool& get() {
+    static HostPool* p = new HostPool();
+    return *p;
+  }
+  int size() const { return n_; }
+  template <typename F>
+  void run(int n, F&& fn) {
+    if (n <= 1 || n_ == 1) {
+      for (int t = 0; t < n; ++t) fn(t);
+      return;
+    }
+    std::lock_guard<std::mutex> serial(call_mu_);
+    const int workers = std::min(n, n_);
+    // worker w runs tasks w, w + workers, ... so any n is covered
+    std::function<void(int)> task = [&, workers](int w) {
+      for (int t = w; t < n; t += workers) fn(t);
+    };
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      task_ = &task;
+      ntask_ = workers;
+      pending_ = workers - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    task(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [&] { return pending_ == 0; });
+    task_ = nullptr;
+  }
+
+ private:
+  HostPool() {
+    n_ = int(std::min<unsigned>(kMax, std::max(1u, std::thread::hardware_concurrency())));
+    for (int id = 1; id < n_; ++id) std::thread([this, id] { loop(id); }).detach();
+  }
+  void loop(int id) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* task;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (id >= ntask_) continue;
+        task = task_;
+      }
+      (*task)(id);
+      std::lock_guard<std::mutex> lk(mu_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  int n_ = 1;
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_, done_;
+  uint64_t gen_ = 0;
+  int ntask_ = 0, pending_ = 0;
+  const std::function<void(int)>* task_ = nullptr;
+};
+
 // read len bytes at file offset off into dst with up to 16 concurrent
 // pread()s, one per host core (page-cache copies are per-thread memcpy-bound)
 inline bool pread_span(int fd, char* dst, int64_t len, int64_t off) {
@@ -202,14 +272,13 @@ inline bool pread_parallel(int fd, char* dst, int64_t len, int64_t off) {
   const int nt = int(std::min<int64_t>(std::min<int64_t>(kMaxThreads, hw), (len + kSlice - 1) / kSlice));
   if (nt <= 1) return pread_span(fd, dst, len, off);
   const int64_t per = (len + nt - 1) / nt;
-  bool ok[kMaxThreads];
-  std::thread th[kMaxThreads];
-  for (int t = 0; t < nt; ++t) {
+  bool ok[kMaxThreads] = {};
+  HostPool::get().run(nt, [&](int t) {
     const int64_t a = t * per, n = std::min(per, len - a);
-    th[t] = std::thread([=, &ok] { ok[t] = n <= 0 || pread_span(fd, dst + a, n, off + a); });
-  }
+    ok[t] = n <= 0 || pread_span(fd, dst + a, n, off + a);
+  });
   bool all = true;
-  for (int t = 0; t < nt; ++t) { th[t].join(); all = all && ok[t]; }
+  for (int t = 0; t < nt; ++t) all = all && ok[t];
   return all;
 }
 
