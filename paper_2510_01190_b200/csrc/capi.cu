@@ -2125,11 +2125,11 @@ int divuq_divuq1_read_f32(const char* path, float* out, int64_t count, int check
   io::Header h;
   if (int r = io::read_header(path, &h)) return r;
   if (count != h.members * 2 * h.nx * h.ny) return DIVUQ_EINVAL;
-  FILE* f = std::fopen(path, "rb");
-  if (!f) return io::kOsError;
-  const bool ok = std::fseek(f, long(h.offset), SEEK_SET) == 0 &&
-                  std::fread(out, sizeof(float), size_t(count), f) == size_t(count);
-  std::fclose(f);
+  const int fd = ::open(path, O_RDONLY);
+  if (fd < 0) return io::kOsError;
+  const bool ok = io::pread_parallel(fd, reinterpret_cast<char*>(out), count * int64_t(sizeof(float)),
+                                     h.offset);
+  ::close(fd);
   if (!ok) return io::kOsError;
   if (check_finite)
     for (int64_t i = 0; i < count; ++i)

@@ -192,7 +192,16 @@ class HostPool {
  public:
   static constexpr int kMax = 16;
   static HostPool& get() {
-    static HostPool* p = new HostPool();
+    // a fork()ed child has none of the parent's workers: it builds its own
+    // pool (the parent's copy is leaked), so run() never waits on ghosts
+    static std::mutex mu;
+    static HostPool* p = nullptr;
+    static pid_t owner = 0;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!p || owner != ::getpid()) {
+      p = new HostPool();
+      owner = ::getpid();
+    }
     return *p;
   }
   int size() const { return n_; }

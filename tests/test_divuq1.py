@@ -317,3 +317,30 @@ def test_ingest_non_finite_rejected_by_consumer(d, io, torch_cuda, tmp_path):
         device.ensemble_divergence2d(x, 3, 3)
     with pytest.raises(io.DataError):
         io.read_ensemble(p)
+
+
+def _read_in_child(path, q):
+    from paper_2510_01190_b200 import io as dio
+
+    ens = dio.read_ensemble(path)
+    q.put(float(sum(float(m.u.sum()) + float(m.v.sum()) for m in ens.members)))
+
+
+def test_parallel_reader_survives_fork(d, io, tmp_path, rng):
+    """The native reader splits large payloads over a persistent host worker
+    pool; a fork()ed child (multiprocessing's default on Linux) has none of
+    the parent's workers and must build its own instead of waiting forever."""
+    import multiprocessing as mp
+
+    ens = _ens(d, rng, nx=512, ny=512, members=2)    # 4 MB payload: 4 workers
+    p = tmp_path / "big.duq"
+    io.write_ensemble(ens, p)
+    back = io.read_ensemble(p)                        # the parent's pool exists now
+    want = float(sum(float(m.u.sum()) + float(m.v.sum()) for m in back.members))
+    ctx = mp.get_context("fork")
+    q = ctx.Queue()
+    proc = ctx.Process(target=_read_in_child, args=(str(p), q))
+    proc.start()
+    got = q.get(timeout=60)
+    proc.join(timeout=30)
+    assert proc.exitcode == 0 and got == want
