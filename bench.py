@@ -585,7 +585,7 @@ def main():
     elif args.config == 4:
         nx, ny = cfg.nx, cfg.ny
         nz = args.planes_per_gpu * world
-        step = SlabStep(nx, ny, nz, rank, world, device="cuda", exchange=args.exchange)
+        step = SlabStep(nx, ny, nz, rank, world, n_arrays=3, device="cuda", exchange=args.exchange)
         members = configs.config4_slab(step.z0, step.nzl, nx, ny, nz, cfg.members, cfg.seed)
         shard.ensure_p2p(step, {"members": members})
         exchange_used = step.exchange

@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define DIVUQ_ABI_VERSION 1
+#define DIVUQ_ABI_VERSION 2
 
 #define DIVUQ_OK 0
 #define DIVUQ_EINVAL (-1)          /* null pointer / bad size */
@@ -163,9 +163,11 @@ int divuq_fit_gaussian_f32(const float* members, int64_t n_members, int64_t n_co
  * fit_gaussian followed by propagate_divergence and _tail_probs in one pass
  * over the members.  members: (M, 2, nx*ny) [2D] or (M, 3, nx*ny*nz_local)
  * [3D slab].  out_mom_mu/out_mom_sigma (optional, (C, N)) receive the
- * fitted moments.  3D halos are REDUCED w moments (mu_w, s_w) of the
- * neighbouring planes (compute them with divuq_fit_gaussian_f32 on the
- * owner's edge plane). */
+ * fitted moments.  3D halos are REDUCED w moments (mu_w, s_w, r_w) of the
+ * neighbouring planes (compute them with divuq_fit_gaussian_strided_f32 on
+ * the owner's edge plane; r_w -- the means' rounding residuals, see
+ * ShiftedMoments in csrc/common.cuh -- may be NULL and then reads as 0, at
+ * the cost of bitwise agreement with the unsharded run). */
 int divuq_ensemble_divergence2d_f32(const float* members, int64_t n_members,
                                     int64_t nx, int64_t ny, double dx, double dy, double t,
                                     float* out_mu, float* out_sigma,
@@ -174,7 +176,9 @@ int divuq_ensemble_divergence2d_f32(const float* members, int64_t n_members,
                                     int32_t* err_word, void* stream);
 int divuq_ensemble_divergence3d_f32(const float* members, int64_t n_members,
                                     const float* halo_lo_mu_w, const float* halo_lo_s_w,
+                                    const float* halo_lo_r_w,
                                     const float* halo_hi_mu_w, const float* halo_hi_s_w,
+                                    const float* halo_hi_r_w,
                                     int64_t nx, int64_t ny, int64_t nz_local,
                                     int64_t z0, int64_t nz_global, int64_t k_begin, int64_t k_end,
                                     double dx, double dy, double dz, double t,
@@ -334,10 +338,11 @@ int divuq_host_mc_divergence2d_f64(const double* mu_u, const double* mu_v,
 
 /* K1 on a member-strided view: member m's N values start at members + m*member_stride
  * (e.g. the w plane of a z-slab: stride 3*n_local) -- the reduced halo a slab
- * neighbour needs, read in place (also through peer memory). */
+ * neighbour needs, read in place (also through peer memory).  out_r
+ * (optional): the means' rounding residuals the fused kernels difference. */
 int divuq_fit_gaussian_strided_f32(const float* members, int64_t n_members, int64_t member_stride,
                                    int64_t n_points, float* out_mu, float* out_sigma,
-                                   int32_t* err_word, void* stream);
+                                   float* out_r, int32_t* err_word, void* stream);
 
 /* Peer memory (CUDA IPC) for the z-slab exchange over NVLink: export the
  * allocation holding `ptr` (handle: divuq_ipc_handle_bytes() bytes, plus the

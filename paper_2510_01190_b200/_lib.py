@@ -44,7 +44,7 @@ SIGNATURES = {
     "divuq_ensemble_divergence2d_f32": (
         _int, [_p, _i64, _i64, _i64, _f64, _f64, _f64] + [_p] * 6 + [_p, _p]),
     "divuq_ensemble_divergence3d_f32": (
-        _int, [_p, _i64] + [_p] * 4 + [_i64] * 7 + [_f64] * 4 + [_p] * 6 + [_p, _p]),
+        _int, [_p, _i64] + [_p] * 6 + [_i64] * 7 + [_f64] * 4 + [_p] * 6 + [_p, _p]),
     "divuq_tail_probs_f64": (_int, [_p, _p, _i64, _f64, _p, _p, _p, _p]),
     "divuq_tail_probs_f32": (_int, [_p, _p, _i64, _f64, _p, _p, _p, _p]),
     "divuq_host_tail_probs_f64": (_int, [_p, _p, _i64, _f64, _p, _p, _int]),
@@ -93,7 +93,7 @@ SIGNATURES = {
     "divuq_histogram_uniform_f64": (_int, [_p, _i64, _f64, _f64, _i64, _p, _p, _p]),
     "divuq_host_mc_divergence2d_ref_f64": (
         _int, [_p] * 4 + [_i64, _i64, _f64, _f64, _i64, _u64, _p, _p, _int]),
-    "divuq_fit_gaussian_strided_f32": (_int, [_p, _i64, _i64, _i64, _p, _p, _p, _p]),
+    "divuq_fit_gaussian_strided_f32": (_int, [_p, _i64, _i64, _i64, _p, _p, _p, _p, _p]),
     "divuq_ipc_handle_bytes": (_i64, []),
     "divuq_ipc_export": (_int, [_p, _p, _p]),
     "divuq_ipc_import": (_int, [_p, _i64, _p, _p]),
@@ -108,8 +108,8 @@ for _name, (_res, _args) in SIGNATURES.items():
     _fn.argtypes = _args
 
 ABI_VERSION = lib.divuq_abi_version()
-if ABI_VERSION != 1:
-    raise ImportError(f"libdivuq_b200 ABI {ABI_VERSION} != 1")
+if ABI_VERSION != 2:
+    raise ImportError(f"libdivuq_b200 ABI {ABI_VERSION} != 2 (rebuild: __graft_entry__.build())")
 
 # status codes (include/divuq_b200.h)
 OK, EINVAL, EGRID, EMEMBERS, ESAMPLES, ENONFINITE, ENEGSIGMA = 0, -1, -2, -3, -4, -10, -11

@@ -79,10 +79,10 @@ void set_coeffs(StencilParams<T>& p, double dx, double dy, double dz) {
   p.cz_in = T(1.0 / (2.0 * dz)); p.cz_bd = T(1.0 / dz);
 }
 
-template <typename T, int VEC, bool HAS_W, bool HAS_SIGMA, int SRC, int MR>
+template <typename T, int VEC, bool HAS_W, bool HAS_SIGMA, int SRC>
 int launch_stencil_impl(StencilParams<T> p, cudaStream_t s) {
-  using K = StencilKernel<T, VEC, HAS_W, HAS_SIGMA, SRC, MR>;
-  auto kern = stencil_kernel<T, VEC, HAS_W, HAS_SIGMA, SRC, MR>;
+  using K = StencilKernel<T, VEC, HAS_W, HAS_SIGMA, SRC>;
+  auto kern = stencil_kernel<T, VEC, HAS_W, HAS_SIGMA, SRC>;
   const int threads = 32 * kStencilTY;
   const int64_t nk = p.kend - p.kbeg;
   if (nk <= 0) return DIVUQ_OK;
@@ -106,15 +106,11 @@ int launch_stencil_impl(StencilParams<T> p, cudaStream_t s) {
 
 template <typename T, int VEC, bool HAS_W, int SRC>
 int dispatch_sigma(const StencilParams<T>& p, bool has_sigma, cudaStream_t s) {
-  if constexpr (SRC == kEnsemble) {
-    const int64_t m = p.n_members;
-    if (m <= 8) return launch_stencil_impl<T, VEC, HAS_W, true, SRC, 8>(p, s);
-    if (m <= 16) return launch_stencil_impl<T, VEC, HAS_W, true, SRC, 16>(p, s);
-    if (m <= 24) return launch_stencil_impl<T, VEC, HAS_W, true, SRC, 24>(p, s);
-    return launch_stencil_impl<T, VEC, HAS_W, true, SRC, 32>(p, s);
+  if constexpr (SRC == kResidual) {
+    return launch_stencil_impl<T, VEC, HAS_W, true, SRC>(p, s);
   } else {
-    if (has_sigma) return launch_stencil_impl<T, VEC, HAS_W, true, SRC, 1>(p, s);
-    return launch_stencil_impl<T, VEC, HAS_W, false, SRC, 1>(p, s);
+    if (has_sigma) return launch_stencil_impl<T, VEC, HAS_W, true, SRC>(p, s);
+    return launch_stencil_impl<T, VEC, HAS_W, false, SRC>(p, s);
   }
 }
 
@@ -122,14 +118,14 @@ template <typename T, bool HAS_W, int SRC>
 int dispatch_vec(const StencilParams<T>& p, bool has_sigma, cudaStream_t s) {
   constexpr int VW = (sizeof(T) == 4) ? 4 : 2;
   bool vec = (p.nx % VW) == 0;
-  const void* ptrs[] = {p.mu_u, p.mu_v, p.mu_w, p.s_u, p.s_v, p.s_w, p.members,
+  const void* ptrs[] = {p.mu_u, p.mu_v, p.mu_w, p.s_u, p.s_v, p.s_w, p.r_u, p.r_v, p.r_w,
                         p.halo_lo_mu_w, p.halo_lo_s_w, p.halo_hi_mu_w, p.halo_hi_s_w,
-                        p.out_mu, p.out_sigma, p.out_psrc, p.out_psnk, p.out_mom_mu, p.out_mom_sigma};
+                        p.halo_lo_r_w, p.halo_hi_r_w,
+                        p.out_mu, p.out_sigma, p.out_psrc, p.out_psnk};
   for (const void* q : ptrs) vec = vec && aligned(q, 16);
-  if (SRC == kEnsemble) vec = vec && ((p.comp_stride % VW) == 0);
   // latency-bound small grids (config 0: 128^2 fp64): one point per lane
   // doubles the CTAs and halves each lane's dependent erfc chain
-  if (vec && SRC != kEnsemble) {
+  if (vec) {
     const int64_t tiles_vec = ((p.nx + 32 * VW - 1) / (32 * VW)) * ((p.ny + kStencilTY - 1) / kStencilTY);
     if (tiles_vec * (p.kend - p.kbeg) < sm_count()) vec = false;
   }
@@ -289,11 +285,8 @@ int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
   if (n_work <= 0) { *used = true; return DIVUQ_OK; }
   auto kern = k2_tma_kernel<T, HAS_SIGMA>;
   const size_t smem = sizeof(TmaStage<T>) * C::S + 2 * C::S * sizeof(uint64_t);
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    DIVUQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr_set = true;
-  }
+  // function attributes are per device context: set on every launch (cheap)
+  DIVUQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const int64_t grid = std::min<int64_t>(p.n_tiles, sms);
   kern<<<unsigned(grid), C::THREADS, smem, s>>>(tm, p);
   *used = true;
@@ -326,7 +319,7 @@ int try_k3_tma(const StencilParams<float>& sp, int comps, cudaStream_t s, bool* 
   if (env_int("DIVUQ_NO_TMA", 0)) return DIVUQ_OK;
   if (sp.nx % 4 || sp.n_members < 2) return DIVUQ_OK;
   const void* ptrs[] = {sp.members, sp.halo_lo_mu_w, sp.halo_lo_s_w, sp.halo_hi_mu_w, sp.halo_hi_s_w,
-                        sp.out_mu, sp.out_sigma, sp.out_psrc, sp.out_psnk, sp.out_mom_mu, sp.out_mom_sigma};
+                        sp.halo_lo_r_w, sp.halo_hi_r_w, sp.out_mu, sp.out_sigma, sp.out_psrc, sp.out_psnk, sp.out_mom_mu, sp.out_mom_sigma};
   for (const void* q : ptrs)
     if (!aligned(q, 16)) return DIVUQ_OK;
   if (sp.nx > (int64_t(1) << 30) || sp.ny > (int64_t(1) << 30) || sp.nzl > (int64_t(1) << 30)) return DIVUQ_OK;
@@ -352,17 +345,13 @@ int try_k3_tma(const StencilParams<float>& sp, int comps, cudaStream_t s, bool* 
   std::memset(&p, 0, sizeof(p));
   p.halo_lo_mu_w = sp.halo_lo_mu_w; p.halo_lo_s_w = sp.halo_lo_s_w;
   p.halo_hi_mu_w = sp.halo_hi_mu_w; p.halo_hi_s_w = sp.halo_hi_s_w;
+  p.halo_lo_r_w = sp.halo_lo_r_w; p.halo_hi_r_w = sp.halo_hi_r_w;
   p.nzl = sp.nzl; p.z0 = sp.z0; p.nzg = sp.nzg; p.kbeg = sp.kbeg; p.kend = sp.kend;
   p.comp_stride = sp.comp_stride;
   p.nx = int(sp.nx); p.ny = int(sp.ny); p.ty = ty; p.tiles_x = int(tiles_x);
   p.n_tiles = int(tiles_x * ((sp.ny + ty - 1) / ty));
   p.M = int(sp.n_members);
   p.has_w = comps == 3;
-  // halo boxes go out with their main box (hdelay 0): a trailing halo delays
-  // the stage it completes, and the 5-stage ring's depth is worth more than
-  // the neighbour's L2 lines (measured: config-4 slab 5.11 ms at hdelay 3,
-  // 4.26 ms at 0 -- DRAM reads stay within 1 % of algorithmic either way)
-  p.hdelay = int(std::max<int64_t>(0, std::min<int64_t>(C::D, env_int("DIVUQ_K3_HDELAY", 0))));
   p.sync_w = int(env_int("DIVUQ_K3_SYNC_W", 0));   // lockstep off: no gain measured for K3
   p.sync_spin = int(env_int("DIVUQ_K3_SYNC_SPIN", 256));
   p.sync_sleep = int(env_int("DIVUQ_K3_SYNC_SLEEP", 500));
@@ -380,11 +369,8 @@ int try_k3_tma(const StencilParams<float>& sp, int comps, cudaStream_t s, bool* 
   *used = true;
   if (sp.kend <= sp.kbeg) return DIVUQ_OK;
   const size_t smem = sizeof(K3Stage) * C::S + sizeof(K3Xchg) + 2 * C::S * sizeof(uint64_t);
-  static bool attr_set = false;
-  if (!attr_set) {
-    DIVUQ_CUDA(cudaFuncSetAttribute(k3_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    attr_set = true;
-  }
+  // function attributes are per device context: set on every launch (cheap)
+  DIVUQ_CUDA(cudaFuncSetAttribute(k3_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   const int64_t grid = std::min<int64_t>(p.n_tiles, sms);
   k3_tma_kernel<<<unsigned(grid), C::THREADS, smem, s>>>(tm, p);
   return int(cudaGetLastError());
@@ -433,44 +419,6 @@ int propagate3d(const T* mu_u, const T* mu_v, const T* mu_w, const T* s_u, const
 }
 
 // ---- K1: per-point moments over members, all components ----------------
-template <typename T, int VEC, int MR>
-__global__ void __launch_bounds__(256) fit_kernel(const T* __restrict__ members, int64_t M, int64_t C,
-                                                  int64_t N, int64_t mstride, T* __restrict__ out_mu,
-                                                  T* __restrict__ out_sigma, int* err) {
-  const int64_t groups = N / VEC;
-  int errbits = 0;
-  for (int64_t g = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; g < groups;
-       g += int64_t(gridDim.x) * blockDim.x) {
-    for (int64_t c = 0; c < C; ++c) {
-      Vec<T, VEC> mu, sg;
-      member_moments<T, VEC, MR>(members + c * N + g * VEC, mstride, int(M), mu, sg, errbits);
-      st_stream<T, VEC>(out_mu + c * N + g * VEC, mu);
-      st_stream<T, VEC>(out_sigma + c * N + g * VEC, sg);
-    }
-  }
-  flush_error(err, errbits);
-}
-
-template <typename T, int VEC, int MR>
-int launch_fit(const T* m, int64_t M, int64_t C, int64_t N, int64_t ms, T* mu, T* sg, int32_t* err,
-               cudaStream_t s) {
-  auto kern = fit_kernel<T, VEC, MR>;
-  const int64_t groups = N / VEC;
-  const int64_t cap = int64_t(blocks_per_sm(kern, 256, 0)) * sm_count();
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((groups + 255) / 256, cap));
-  kern<<<unsigned(grid), 256, 0, s>>>(m, M, C, N, ms, mu, sg, err);
-  return int(cudaGetLastError());
-}
-
-template <typename T, int VEC>
-int fit_mr(const T* m, int64_t M, int64_t C, int64_t N, int64_t ms, T* mu, T* sg, int32_t* err,
-           cudaStream_t s) {
-  if (M <= 8) return launch_fit<T, VEC, 8>(m, M, C, N, ms, mu, sg, err, s);
-  if (M <= 16) return launch_fit<T, VEC, 16>(m, M, C, N, ms, mu, sg, err, s);
-  if (M <= 24) return launch_fit<T, VEC, 24>(m, M, C, N, ms, mu, sg, err, s);
-  return launch_fit<T, VEC, 32>(m, M, C, N, ms, mu, sg, err, s);
-}
-
 // K1 streaming form: one thread per (component, VEC points), a handful of
 // registers, U member loads (16 B each) in flight per thread and every SM full
 // of threads.  fp64 keeps numpy's two-pass algorithm bit for bit (sequential
@@ -482,7 +430,8 @@ template <typename T, int VEC, int U, int MINB, bool REREAD>
 __global__ void __launch_bounds__(256, MINB) fit_stream_kernel(const T* __restrict__ members, int64_t M,
                                                             int64_t C, int64_t N, int64_t mstride,
                                                             T* __restrict__ out_mu,
-                                                            T* __restrict__ out_sigma, int* err) {
+                                                            T* __restrict__ out_sigma,
+                                                            T* __restrict__ out_r, int* err) {
   using A = Arith<T>;
   using V = Vec<T, VEC>;
   int errbits = 0;
@@ -576,7 +525,9 @@ __global__ void __launch_bounds__(256, MINB) fit_stream_kernel(const T* __restri
             acc.add(int(k0 + j), x[j].v);
           }
       }
-      acc.finish(int(M), mu.v, sg.v);
+      V rr;
+      acc.finish(int(M), mu.v, rr.v, sg.v);
+      if (out_r != nullptr) st_stream<T, VEC>(out_r + off, rr);
     }
     st_stream<T, VEC>(out_mu + off, mu);
     st_stream<T, VEC>(out_sigma + off, sg);
@@ -699,11 +650,11 @@ __global__ void __launch_bounds__(kFbTile, 2) fit_bulk_kernel(const double* __re
 
 template <typename T, int VEC, int U, int MINB, bool REREAD = true>
 int launch_fit_stream(const T* m, int64_t M, int64_t C, int64_t N, int64_t ms, T* mu, T* sg,
-                      int32_t* err, cudaStream_t s) {
+                      T* r, int32_t* err, cudaStream_t s) {
   auto kern = fit_stream_kernel<T, VEC, U, MINB, REREAD>;
   const int64_t cap = int64_t(blocks_per_sm(kern, 256, 0)) * sm_count();
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((C * (N / VEC) + 255) / 256, cap));
-  kern<<<unsigned(grid), 256, 0, s>>>(m, M, C, N, ms, mu, sg, err);
+  kern<<<unsigned(grid), 256, 0, s>>>(m, M, C, N, ms, mu, sg, r, err);
   return int(cudaGetLastError());
 }
 
@@ -712,13 +663,13 @@ int launch_fit_stream(const T* m, int64_t M, int64_t C, int64_t N, int64_t ms, T
 // point per lane, 8 loads in flight, second pass re-read from L2: 113 us
 // (50 %, was 194 us) -- the two passes serialise per thread
 template <typename T>
-int fit_stream(const T* m, int64_t M, int64_t C, int64_t N, int64_t ms, T* mu, T* sg, int32_t* err,
-               cudaStream_t s) {
+int fit_stream(const T* m, int64_t M, int64_t C, int64_t N, int64_t ms, T* mu, T* sg, T* r,
+               int32_t* err, cudaStream_t s) {
   const bool v16 = (N % (16 / int(sizeof(T)))) == 0 && (ms % (16 / int(sizeof(T)))) == 0 &&
-                   aligned(m, 16) && aligned(mu, 16) && aligned(sg, 16);
+                   aligned(m, 16) && aligned(mu, 16) && aligned(sg, 16) && aligned(r, 16);
   if constexpr (sizeof(T) == 4) {
-    if (v16) return launch_fit_stream<T, 4, 4, 4>(m, M, C, N, ms, mu, sg, err, s);
-    return launch_fit_stream<T, 1, 8, 4>(m, M, C, N, ms, mu, sg, err, s);
+    if (v16) return launch_fit_stream<T, 4, 4, 4>(m, M, C, N, ms, mu, sg, r, err, s);
+    return launch_fit_stream<T, 1, 8, 4>(m, M, C, N, ms, mu, sg, r, err, s);
   } else {
     // holding all M doubles for both passes spills at these register caps;
     // parking them in shared memory keeps HBM at one read (measured faster
@@ -748,26 +699,21 @@ int fit_stream(const T* m, int64_t M, int64_t C, int64_t N, int64_t ms, T* mu, T
       kern<<<unsigned(grid), 256, park, s>>>(m, M, C, N, ms, mu, sg, err);
       return int(cudaGetLastError());
     }
-    return launch_fit_stream<T, 1, 8, 4, true>(m, M, C, N, ms, mu, sg, err, s);
+    return launch_fit_stream<T, 1, 8, 4, true>(m, M, C, N, ms, mu, sg, nullptr, err, s);
   }
 }
 
+// out_r (fp32 only, optional): the means' rounding residuals (ShiftedMoments)
 template <typename T>
 int fit_gaussian(const T* members, int64_t M, int64_t C, int64_t N, T* out_mu, T* out_sigma,
-                 int32_t* err, void* stream, int64_t mstride = -1) {
+                 int32_t* err, void* stream, int64_t mstride = -1, T* out_r = nullptr) {
   if (!members || !out_mu || !out_sigma || C < 1 || N < 1) return DIVUQ_EINVAL;
   if (M < 2) return DIVUQ_EMEMBERS;
   if (mstride < 0) mstride = C * N;
   if (mstride < C * N) return DIVUQ_EINVAL;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (env_int("DIVUQ_FIT_LEGACY", 0)) {   // the register-array K1 (kept for comparison)
-    constexpr int VW = (sizeof(T) == 4) ? 4 : 2;
-    const bool vec = M <= 16 && (N % VW) == 0 && (mstride % VW) == 0 && aligned(members, 16) &&
-                     aligned(out_mu, 16) && aligned(out_sigma, 16);
-    if (vec) return fit_mr<T, VW>(members, M, C, N, mstride, out_mu, out_sigma, err, s);
-    return fit_mr<T, 1>(members, M, C, N, mstride, out_mu, out_sigma, err, s);
-  }
-  return fit_stream<T>(members, M, C, N, mstride, out_mu, out_sigma, err, s);
+  if (sizeof(T) == 8 && out_r) return DIVUQ_EINVAL;
+  return fit_stream<T>(members, M, C, N, mstride, out_mu, out_sigma, out_r, err,
+                       static_cast<cudaStream_t>(stream));
 }
 
 // ---- probability map on an existing Gaussian scalar field (lcp.py:48-68)
@@ -1151,9 +1097,9 @@ int divuq_fit_gaussian_f32(const float* members, int64_t M, int64_t C, int64_t N
 }
 
 int divuq_fit_gaussian_strided_f32(const float* members, int64_t M, int64_t member_stride,
-                                   int64_t N, float* out_mu, float* out_sigma, int32_t* err,
-                                   void* stream) {
-  return fit_gaussian<float>(members, M, 1, N, out_mu, out_sigma, err, stream, member_stride);
+                                   int64_t N, float* out_mu, float* out_sigma, float* out_r,
+                                   int32_t* err, void* stream) {
+  return fit_gaussian<float>(members, M, 1, N, out_mu, out_sigma, err, stream, member_stride, out_r);
 }
 
 // ---- peer memory (CUDA IPC) for the z-slab exchange over NVLink ----------
@@ -1254,6 +1200,29 @@ int try_k3_rowmarch(const StencilParams<float>& sp, cudaStream_t s, bool* used) 
   return int(cudaGetLastError());
 }
 
+// Fused-ensemble fallback for the shapes the TMA kernels do not take
+// (nx % 4 != 0, unaligned pointers): K1 writes the ShiftedMoments triples
+// (mu, r, sigma), the kResidual stencil differences the (mu, r) pairs exactly
+// as the fused kernels do, so every path agrees bit for bit.  Scratch comes
+// from the stream-ordered pool (the moments go straight to out_mom_* when the
+// caller asked for them).
+static int ensemble_fallback(StencilParams<float> p, int comps, cudaStream_t s) {
+  const int64_t nl = p.comp_stride;
+  const bool own = p.out_mom_mu != nullptr;
+  DevBuf scratch;
+  DIVUQ_CUDA(scratch.alloc(size_t(comps) * nl * (own ? 1 : 3) * sizeof(float), s));
+  float* r = scratch.as<float>();
+  float* mu = own ? p.out_mom_mu : r + comps * nl;
+  float* sg = own ? p.out_mom_sigma : r + 2 * comps * nl;
+  if (int e = fit_gaussian<float>(p.members, p.n_members, comps, nl, mu, sg, p.err, s, p.member_stride, r))
+    return e;
+  p.mu_u = mu; p.mu_v = mu + nl; p.mu_w = comps == 3 ? mu + 2 * nl : nullptr;
+  p.s_u = sg; p.s_v = sg + nl; p.s_w = comps == 3 ? sg + 2 * nl : nullptr;
+  p.r_u = r; p.r_v = r + nl; p.r_w = comps == 3 ? r + 2 * nl : nullptr;
+  if (comps == 3) return dispatch_vec<float, true, kResidual>(p, true, s);
+  return dispatch_vec<float, false, kResidual>(p, true, s);
+}
+
 int divuq_ensemble_divergence2d_f32(const float* members, int64_t M, int64_t nx, int64_t ny, double dx,
                                     double dy, double t, float* out_mu, float* out_sigma,
                                     float* out_p_src, float* out_p_snk, float* out_mom_mu,
@@ -1275,7 +1244,7 @@ int divuq_ensemble_divergence2d_f32(const float* members, int64_t M, int64_t nx,
   if (used) return DIVUQ_OK;
   if (int r = try_k3_tma(p, 2, static_cast<cudaStream_t>(stream), &used)) return r;
   if (used) return DIVUQ_OK;
-  return dispatch_vec<float, false, kEnsemble>(p, true, static_cast<cudaStream_t>(stream));
+  return ensemble_fallback(p, 2, static_cast<cudaStream_t>(stream));
 }
 
 int divuq_gradient_ensemble_divergence2d_f32(const float* members, int64_t M, int64_t nx,
@@ -1314,7 +1283,8 @@ int divuq_gradient_ensemble_divergence2d_f32(const float* members, int64_t M, in
 }
 
 int divuq_ensemble_divergence3d_f32(const float* members, int64_t M, const float* hl_mu,
-                                    const float* hl_s, const float* hh_mu, const float* hh_s,
+                                    const float* hl_s, const float* hl_r, const float* hh_mu,
+                                    const float* hh_s, const float* hh_r,
                                     int64_t nx, int64_t ny, int64_t nzl, int64_t z0, int64_t nzg,
                                     int64_t kb, int64_t ke, double dx, double dy, double dz, double t,
                                     float* out_mu, float* out_sigma, float* out_p_src,
@@ -1332,6 +1302,7 @@ int divuq_ensemble_divergence3d_f32(const float* members, int64_t M, const float
   const int64_t nl = nx * ny * nzl;
   p.members = members; p.n_members = M; p.comp_stride = nl; p.member_stride = 3 * nl;
   p.halo_lo_mu_w = hl_mu; p.halo_lo_s_w = hl_s; p.halo_hi_mu_w = hh_mu; p.halo_hi_s_w = hh_s;
+  p.halo_lo_r_w = hl_r; p.halo_hi_r_w = hh_r;
   p.nx = nx; p.ny = ny; p.nzl = nzl; p.z0 = z0; p.nzg = nzg; p.kbeg = kb; p.kend = ke;
   set_coeffs(p, dx, dy, dz);
   p.theta = float(t);
@@ -1341,7 +1312,7 @@ int divuq_ensemble_divergence3d_f32(const float* members, int64_t M, const float
   bool used = false;
   if (int r = try_k3_tma(p, 3, static_cast<cudaStream_t>(stream), &used)) return r;
   if (used) return DIVUQ_OK;
-  return dispatch_vec<float, true, kEnsemble>(p, true, static_cast<cudaStream_t>(stream));
+  return ensemble_fallback(p, 3, static_cast<cudaStream_t>(stream));
 }
 
 int divuq_tail_probs_f64(const double* mu, const double* sigma, int64_t n, double theta,
@@ -2004,8 +1975,8 @@ int divuq_host_ensemble_divergence3d_f32(const float* members, int64_t M, int64_
   cz = std::min(cz, nz_local);
   const int64_t nch = (nz_local + cz - 1) / cz;
   float* host_out[4] = {out_mu, out_sigma, out_p_src, out_p_snk};
-  // set: members (M, 3, cz planes) | halo mu_lo s_lo mu_hi s_hi | 4 outputs (cz planes)
-  const int64_t set_elems = 3 * M * cz * plane + 4 * plane + 4 * cz * plane;
+  // set: members (M, 3, cz planes) | halo mu_lo s_lo r_lo mu_hi s_hi r_hi | 4 outputs (cz planes)
+  const int64_t set_elems = 3 * M * cz * plane + 6 * plane + 4 * cz * plane;
   const int64_t ghost_elems = (has_lo || has_hi) ? 2 * M * plane : 0;
   const int nsets = int(std::min<int64_t>(kSets, nch));
   StreamGuard cin, cmp, cout;
@@ -2068,18 +2039,20 @@ int divuq_host_ensemble_divergence3d_f32(const float* members, int64_t M, int64_
     } else if (has_hi) {
       hi = ghost + M * plane;
     }
+    float* hlo = halo;              // mu, s, r of the plane below the chunk
+    float* hhi = halo + 3 * plane;  // ... and above
     if (lo)
-      if (int r = fit_gaussian<float>(lo, M, 1, plane, halo, halo + plane, derr, cmp.s, lo_stride)) return r;
-    if (hi)
-      if (int r = fit_gaussian<float>(hi, M, 1, plane, halo + 2 * plane, halo + 3 * plane, derr, cmp.s,
-                                      hi_stride))
+      if (int r = fit_gaussian<float>(lo, M, 1, plane, hlo, hlo + plane, derr, cmp.s, lo_stride, hlo + 2 * plane))
         return r;
-    float* outs = halo + 4 * plane;
+    if (hi)
+      if (int r = fit_gaussian<float>(hi, M, 1, plane, hhi, hhi + plane, derr, cmp.s, hi_stride, hhi + 2 * plane))
+        return r;
+    float* outs = halo + 6 * plane;
     float* o[4];
     for (int q = 0; q < 4; ++q) o[q] = host_out[q] ? outs + q * cz * plane : nullptr;
     if (int r = divuq_ensemble_divergence3d_f32(
-            s, M, lo ? halo : nullptr, lo ? halo + plane : nullptr, hi ? halo + 2 * plane : nullptr,
-            hi ? halo + 3 * plane : nullptr, nx, ny, nzl(c), z0 + zc(c), nz_global, 0, nzl(c), dx, dy, dz,
+            s, M, lo ? hlo : nullptr, lo ? hlo + plane : nullptr, lo ? hlo + 2 * plane : nullptr,
+            hi ? hhi : nullptr, hi ? hhi + plane : nullptr, hi ? hhi + 2 * plane : nullptr, nx, ny, nzl(c), z0 + zc(c), nz_global, 0, nzl(c), dx, dy, dz,
             t, o[0], o[1], o[2], o[3], nullptr, nullptr, derr, cmp.s))
       return r;
     DIVUQ_CUDA(cudaEventRecord(ev.comp[c % kSets], cmp.s));

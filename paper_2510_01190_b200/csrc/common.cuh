@@ -9,6 +9,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 namespace divuq {
@@ -98,12 +99,32 @@ __device__ __forceinline__ float ndtr_(float a) {
 }
 
 // ---- fp32 ensemble moments: one pass, shifted by the first member ----------
-// d_m = x_m - x_0; s = sum d, q = sum d^2 (FMA);  mu = x_0 + s/M;
-// var = (q - s*s/M) / (M-1) clamped at 0 (ddof = 1, gaussian.py:41-44).
+// d_m = x_m - x_0; s = sum d, q = sum d^2 (FMA);  lo = s/M;  mu = x_0 + lo;
+// var = (q - s*lo) / (M-1) clamped at 0 (ddof = 1, gaussian.py:41-44).
 // Shifting by a member keeps the cancellation benign (|mu - x_0| ~ sigma), and
 // a single pass lets the streaming kernels consume each member once without
 // holding M values per point.  Every fp32 moment in the library goes through
 // this one routine, so the fused, unfused and sharded paths agree bitwise.
+//
+// The fused kernels also keep the mean's rounding residual r = (x_0 - mu) +
+// lo (|r| <= ulp(mu)/2, rounded to bf16 so it packs into 16 bits where shared
+// memory is tight) and difference (mu, r) PAIRS in the stencil: rounding mu
+// to fp32 before differencing loses ~ulp(mu) per neighbour, which at
+// |mu| / sigma ~ 5e3 (config 1: |u| ~ 110, sigma down to 0.02) moves the
+// tail argument by ~3e-4 and P(div > 0) by ~1e-4; with the pair the fp32
+// fused maps meet |dP| <= 1e-5 P + 1e-6 against the fp64 oracle
+// (tests/test_gpu_fullsize.py).
+__device__ __forceinline__ float bf16_round(float x) {
+  return __bfloat162float(__float2bfloat16_rn(x));
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo_half, float hi_half) {
+  // both already bf16-exact: the conversion is exact
+  const __nv_bfloat162 h = __floats2bfloat162_rn(lo_half, hi_half);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ float unpack_bf16_lo(uint32_t w) { return __uint_as_float(w << 16); }
+__device__ __forceinline__ float unpack_bf16_hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+
 template <int VEC>
 struct ShiftedMoments {
   float x0[VEC], s[VEC], q[VEC];
@@ -120,15 +141,34 @@ struct ShiftedMoments {
       }
     }
   }
-  __device__ __forceinline__ void finish(int M, float* mu, float* sg) const {
+  // branch-free forms for callers that peel member 0
+  __device__ __forceinline__ void first(const float* x) {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) { x0[e] = x[e]; s[e] = 0.0f; q[e] = 0.0f; }
+  }
+  __device__ __forceinline__ void next(const float* x) {
+#pragma unroll
+    for (int e = 0; e < VEC; ++e) {
+      const float d = x[e] - x0[e];
+      s[e] += d;
+      q[e] = fmaf(d, d, q[e]);
+    }
+  }
+  // mu (rounded), its residual r (bf16-exact) and sigma
+  __device__ __forceinline__ void finish(int M, float* mu, float* r, float* sg) const {
     const float inv_m = __fdiv_rn(1.0f, float(M));
     const float inv_m1 = __fdiv_rn(1.0f, float(M - 1));
 #pragma unroll
     for (int e = 0; e < VEC; ++e) {
-      mu[e] = fmaf(s[e], inv_m, x0[e]);
-      const float var = fmaxf(0.0f, fmaf(-s[e], s[e] * inv_m, q[e])) * inv_m1;
+      const float lo = __fmul_rn(s[e], inv_m);
+      mu[e] = __fadd_rn(x0[e], lo);
+      if (r != nullptr) r[e] = bf16_round(__fadd_rn(__fsub_rn(x0[e], mu[e]), lo));
+      const float var = __fmul_rn(fmaxf(0.0f, fmaf(-s[e], lo, q[e])), inv_m1);
       sg[e] = __fsqrt_rn(var);
     }
+  }
+  __device__ __forceinline__ void finish(int M, float* mu, float* sg) const {
+    finish(M, mu, nullptr, sg);
   }
 };
 
@@ -168,6 +208,16 @@ template <bool HAS_W> struct StencilMath<float, HAS_W> {
                                                float wl, float cx, float cy, float cz) {
     const float z = HAS_W ? cz * (wh - wl) : 0.0f;
     return fmaf(cx, uh - ul, fmaf(cy, vh - vl, z));
+  }
+  // (mu, r) pairs (ShiftedMoments): each difference is (hi_h - hi_l) + (r_h - r_l)
+  static __device__ __forceinline__ float dpair(float h, float l, float rh, float rl) {
+    return __fadd_rn(__fsub_rn(h, l), __fsub_rn(rh, rl));
+  }
+  static __device__ __forceinline__ float mean_r(float uh, float ul, float ruh, float rul, float vh,
+                                                 float vl, float rvh, float rvl, float wh, float wl,
+                                                 float rwh, float rwl, float cx, float cy, float cz) {
+    const float z = HAS_W ? __fmul_rn(cz, dpair(wh, wl, rwh, rwl)) : 0.0f;
+    return fmaf(cx, dpair(uh, ul, ruh, rul), fmaf(cy, dpair(vh, vl, rvh, rvl), z));
   }
   static __device__ __forceinline__ float var(float sh, float sl, float svh, float svl, float swh,
                                               float swl, float cx, float cy, float cz) {

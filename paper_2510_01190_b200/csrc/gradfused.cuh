@@ -58,7 +58,7 @@ constexpr uint32_t kGfStageBytes = 2 * kGfCompBytes;
 constexpr uint32_t kGfMagOff = kGfS * kGfStageBytes;
 constexpr uint32_t kGfBarOff = kGfMagOff + 2 * kGfR * 4;
 constexpr uint32_t kGfSmemTma = kGfBarOff + kGfS * 8;
-constexpr uint32_t kGfMomBytes = 2 * (kGfTY * (kGfTX + 2) + (kGfTY + 2) * kGfTX) * 4;
+constexpr uint32_t kGfMomBytes = 3 * (kGfTY * (kGfTX + 2) + (kGfTY + 2) * kGfTX) * 4;   // mu, sigma, r
 static_assert(kGfMomBytes <= kGfS * kGfStageBytes || kGfS == 0, "moments alias the stages");
 constexpr uint32_t kGfSmemLdg = 2 * kGfR * 4 + kGfMomBytes;
 
@@ -102,6 +102,8 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
   float* const mx_sg = mx_mu + kGfTY * (kGfTX + 2);
   float* const my_mu = mx_sg + kGfTY * (kGfTX + 2);          // [kGfTY + 2][kGfTX]
   float* const my_sg = my_mu + (kGfTY + 2) * kGfTX;
+  float* const mx_r = my_sg + (kGfTY + 2) * kGfTX;            // the means' residuals
+  float* const my_r = mx_r + kGfTY * (kGfTX + 2);
   uint64_t* full = reinterpret_cast<uint64_t*>(gf_smem + kGfBarOff);
 
   // the two differenced region slots and the coefficient of each gradient slot
@@ -237,7 +239,8 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
   float g_mu[kGfSlots], g_sg[kGfSlots];
 #pragma unroll
   for (int s = 0; s < kGfSlots; ++s) {
-    acc[s].finish(M, &g_mu[s], &g_sg[s]);
+    float g_r;
+    acc[s].finish(M, &g_mu[s], &g_r, &g_sg[s]);
     bool isx;
     int r, c;
     gf_slot(s, tid, isx, r, c);
@@ -245,6 +248,7 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
       const int d = isx ? r * (kGfTX + 2) + c + 1 : (r + 1) * kGfTX + c;
       (isx ? mx_mu : my_mu)[d] = g_mu[s];
       (isx ? mx_sg : my_sg)[d] = g_sg[s];
+      (isx ? mx_r : my_r)[d] = g_r;
     }
   }
   __syncthreads();
@@ -261,7 +265,8 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
     const int yl = ((j > 0 ? r - 1 : r) + 1) * kGfTX + c;
     const float cxe = (i == 0 || i == nx - 1) ? p.cx_bd : p.cx_in;
     const float cye = (j == 0 || j == ny - 1) ? p.cy_bd : p.cy_in;
-    const float mean = SM::mean(mx_mu[xh], mx_mu[xl], my_mu[yh], my_mu[yl], 0.0f, 0.0f, cxe, cye, 0.0f);
+    const float mean = SM::mean_r(mx_mu[xh], mx_mu[xl], mx_r[xh], mx_r[xl], my_mu[yh], my_mu[yl],
+                                  my_r[yh], my_r[yl], 0.0f, 0.0f, 0.0f, 0.0f, cxe, cye, 0.0f);
     const float var = SM::var(mx_sg[xh], mx_sg[xl], my_sg[yh], my_sg[yl], 0.0f, 0.0f, cxe, cye, 0.0f);
     float sg, ps, pk;
     Tails<float>::eval(mean, var, p.theta, t_zero, sg, ps, pk);

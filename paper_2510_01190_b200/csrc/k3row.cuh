@@ -15,8 +15,9 @@
 //   * NW consumer warps take rows round-robin in groups of NW: a warp folds
 //     its row's members into single-pass shifted moments (ShiftedMoments, the
 //     same routine as K1 / K3, so results are bitwise those of K1 + K2),
-//     releases the stage at once and publishes (mu_u, s_u, mu_v, s_v) of its
-//     TX points (+ the two x-halo points) in a shared ring of 2*NW + 2 rows;
+//     releases the stage at once and publishes (mu_u, r_u, s_u, mu_v, r_v,
+//     s_v) of its TX points (+ the two x-halo points) in a shared ring of
+//     2*NW + 2 rows (r = the mean's rounding residual, see ShiftedMoments);
 //   * one named barrier per group; then each warp evaluates the stencil,
 //     sigma and both tails for the row BEFORE its own (whose v neighbours
 //     are now both in the ring) and streams the outputs;
@@ -63,11 +64,14 @@ struct RmParams {
   int* err;
 };
 
-// per ring row: mu_u, s_u, mu_v, s_v of the 128 points, then the x-halo
-// points' (mu_u, s_u) left and right
+// per ring row: mu_u, s_u, mu_v, s_v of the TX points, their residuals
+// (r_u, r_v) packed as bf16x2 (keeps 2 CTAs x 8 stages per SM), then the
+// x-halo points' (mu_u, s_u) left, right and their r_u
+enum { kRmU = 0, kRmSU = 1, kRmV = 2, kRmSV = 3 };
 struct RmRing {
   float m[RmCfg::R][4][RmCfg::TX];
-  float h[RmCfg::R][4];
+  uint32_t r[RmCfg::R][RmCfg::TX];
+  float h[RmCfg::R][6];
 };
 
 __global__ void __launch_bounds__(RmCfg::THREADS, DIVUQ_RM_MINB)
@@ -137,32 +141,51 @@ k3_rowmarch_kernel(const __grid_constant__ RmMaps tm, const RmParams p) {
       ShiftedMoments<1> ah;
       const int row = y0 - 1 + i;
       const bool owned = i >= 1 && i <= nrows - 2;
-      for (int m = 0; m < M; ++m) {
-        const Vec<float, C::VEC> xu = *reinterpret_cast<const Vec<float, C::VEC>*>(su + m * C::TXP + C::PAD + cx0);
-        const Vec<float, C::VEC> xv = *reinterpret_cast<const Vec<float, C::VEC>*>(sv + m * C::TX + cx0);
-        const float xh = su[m * C::TXP + hcol];
+      auto load = [&](int m, Vec<float, C::VEC>& xu, Vec<float, C::VEC>& xv, float& xh) {
+        xu = *reinterpret_cast<const Vec<float, C::VEC>*>(su + m * C::TXP + C::PAD + cx0);
+        xv = *reinterpret_cast<const Vec<float, C::VEC>*>(sv + m * C::TX + cx0);
+        xh = su[m * C::TXP + hcol];
         if (validate && owned && act_x) {
 #pragma unroll
           for (int e = 0; e < C::VEC; ++e) errbits |= check_value(xu.v[e]) | check_value(xv.v[e]);
         }
-        au.add(m, xu.v);
-        av.add(m, xv.v);
-        ah.add(m, &xh);
+      };
+      {  // member 0 sets the shift (peeled: no per-member branch)
+        Vec<float, C::VEC> xu, xv;
+        float xh;
+        load(0, xu, xv, xh);
+        au.first(xu.v);
+        av.first(xv.v);
+        ah.first(&xh);
+      }
+      for (int m = 1; m < M; ++m) {
+        Vec<float, C::VEC> xu, xv;
+        float xh;
+        load(m, xu, xv, xh);
+        au.next(xu.v);
+        av.next(xv.v);
+        ah.next(&xh);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);   // the stage can be refilled now
-      Vec<float, C::VEC> mu_u, s_u, mu_v, s_v;
-      au.finish(M, mu_u.v, s_u.v);
-      av.finish(M, mu_v.v, s_v.v);
-      float hmu, hsg;
-      ah.finish(M, &hmu, &hsg);
+      Vec<float, C::VEC> mu_u, s_u, mu_v, s_v, r_u, r_v;
+      au.finish(M, mu_u.v, r_u.v, s_u.v);
+      av.finish(M, mu_v.v, r_v.v, s_v.v);
+      float hmu, hsg, hr;
+      ah.finish(M, &hmu, &hr, &hsg);
       const int q = i % C::R;
-      *reinterpret_cast<Vec<float, C::VEC>*>(&ring.m[q][0][cx0]) = mu_u;
-      *reinterpret_cast<Vec<float, C::VEC>*>(&ring.m[q][1][cx0]) = s_u;
-      *reinterpret_cast<Vec<float, C::VEC>*>(&ring.m[q][2][cx0]) = mu_v;
-      *reinterpret_cast<Vec<float, C::VEC>*>(&ring.m[q][3][cx0]) = s_v;
-      if (lane == 0) { ring.h[q][0] = hmu; ring.h[q][1] = hsg; }
-      if (lane == 31) { ring.h[q][2] = hmu; ring.h[q][3] = hsg; }
+      *reinterpret_cast<Vec<float, C::VEC>*>(&ring.m[q][kRmU][cx0]) = mu_u;
+      *reinterpret_cast<Vec<float, C::VEC>*>(&ring.m[q][kRmSU][cx0]) = s_u;
+      *reinterpret_cast<Vec<float, C::VEC>*>(&ring.m[q][kRmV][cx0]) = mu_v;
+      *reinterpret_cast<Vec<float, C::VEC>*>(&ring.m[q][kRmSV][cx0]) = s_v;
+      {
+        Vec<uint32_t, C::VEC> pr;
+#pragma unroll
+        for (int e = 0; e < C::VEC; ++e) pr.v[e] = pack_bf16x2(r_u.v[e], r_v.v[e]);
+        *reinterpret_cast<Vec<uint32_t, C::VEC>*>(&ring.r[q][cx0]) = pr;
+      }
+      if (lane == 0) { ring.h[q][0] = hmu; ring.h[q][1] = hsg; ring.h[q][4] = hr; }
+      if (lane == 31) { ring.h[q][2] = hmu; ring.h[q][3] = hsg; ring.h[q][5] = hr; }
       (void)row;
     }
     named_sync(1, 32 * C::NW);   // the group's rows are in the ring
@@ -173,23 +196,32 @@ k3_rowmarch_kernel(const __grid_constant__ RmMaps tm, const RmParams p) {
       const int q = j % C::R, ql = (j - 1) % C::R, qh = (j + 1) % C::R;
       const bool jlo = row == 0, jhi = row == p.ny - 1;
       const float cy = (jlo || jhi) ? p.cy_bd : p.cy_in;
-      const Vec<float, C::VEC> mu_u = *reinterpret_cast<const Vec<float, C::VEC>*>(&ring.m[q][0][cx0]);
-      const Vec<float, C::VEC> s_u = *reinterpret_cast<const Vec<float, C::VEC>*>(&ring.m[q][1][cx0]);
-      const Vec<float, C::VEC> mu_v = *reinterpret_cast<const Vec<float, C::VEC>*>(&ring.m[q][2][cx0]);
-      const Vec<float, C::VEC> s_v = *reinterpret_cast<const Vec<float, C::VEC>*>(&ring.m[q][3][cx0]);
+      using V = Vec<float, C::VEC>;
+      const V mu_u = *reinterpret_cast<const V*>(&ring.m[q][kRmU][cx0]);
+      const V s_u = *reinterpret_cast<const V*>(&ring.m[q][kRmSU][cx0]);
+      using VU = Vec<uint32_t, C::VEC>;
+      const VU pr = *reinterpret_cast<const VU*>(&ring.r[q][cx0]);
       // v rows below / above (the point itself at the global y faces)
       const int qlo = jlo ? q : ql, qhi = jhi ? q : qh;
-      const Vec<float, C::VEC> vl = *reinterpret_cast<const Vec<float, C::VEC>*>(&ring.m[qlo][2][cx0]);
-      const Vec<float, C::VEC> svl = *reinterpret_cast<const Vec<float, C::VEC>*>(&ring.m[qlo][3][cx0]);
-      const Vec<float, C::VEC> vh = *reinterpret_cast<const Vec<float, C::VEC>*>(&ring.m[qhi][2][cx0]);
-      const Vec<float, C::VEC> svh = *reinterpret_cast<const Vec<float, C::VEC>*>(&ring.m[qhi][3][cx0]);
+      const V vl = *reinterpret_cast<const V*>(&ring.m[qlo][kRmV][cx0]);
+      const V svl = *reinterpret_cast<const V*>(&ring.m[qlo][kRmSV][cx0]);
+      const VU prl = *reinterpret_cast<const VU*>(&ring.r[qlo][cx0]);
+      const V vh = *reinterpret_cast<const V*>(&ring.m[qhi][kRmV][cx0]);
+      const V svh = *reinterpret_cast<const V*>(&ring.m[qhi][kRmSV][cx0]);
+      const VU prh = *reinterpret_cast<const VU*>(&ring.r[qhi][cx0]);
+      V r_u;
+#pragma unroll
+      for (int e = 0; e < C::VEC; ++e) r_u.v[e] = unpack_bf16_lo(pr.v[e]);
       // u x-neighbours of the lane's edge points: neighbour lanes or the halo points
-      float ul = lane == 0 ? ring.h[q][0] : ring.m[q][0][cx0 - 1];
-      float sl = lane == 0 ? ring.h[q][1] : ring.m[q][1][cx0 - 1];
-      float ur = lane == 31 ? ring.h[q][2] : ring.m[q][0][cx0 + C::VEC < C::TX ? cx0 + C::VEC : cx0];
-      float sr = lane == 31 ? ring.h[q][3] : ring.m[q][1][cx0 + C::VEC < C::TX ? cx0 + C::VEC : cx0];
-      if (x_lo_edge) { ul = mu_u.v[0]; sl = s_u.v[0]; }
-      if (x_hi_edge) { ur = mu_u.v[C::VEC - 1]; sr = s_u.v[C::VEC - 1]; }
+      const int cr = cx0 + C::VEC < C::TX ? cx0 + C::VEC : cx0;
+      float ul = lane == 0 ? ring.h[q][0] : ring.m[q][kRmU][cx0 - 1];
+      float sl = lane == 0 ? ring.h[q][1] : ring.m[q][kRmSU][cx0 - 1];
+      float rl = lane == 0 ? ring.h[q][4] : unpack_bf16_lo(ring.r[q][cx0 - 1]);
+      float ur = lane == 31 ? ring.h[q][2] : ring.m[q][kRmU][cr];
+      float sr = lane == 31 ? ring.h[q][3] : ring.m[q][kRmSU][cr];
+      float rr = lane == 31 ? ring.h[q][5] : unpack_bf16_lo(ring.r[q][cr]);
+      if (x_lo_edge) { ul = mu_u.v[0]; sl = s_u.v[0]; rl = r_u.v[0]; }
+      if (x_hi_edge) { ur = mu_u.v[C::VEC - 1]; sr = s_u.v[C::VEC - 1]; rr = r_u.v[C::VEC - 1]; }
       Vec<float, C::VEC> omu, osg, ops, opk;
       // with VEC = 2 and nx = 2 one lane holds both x edges: cx_first/last cover it
       using SM = StencilMath<float, true>;
@@ -201,7 +233,10 @@ k3_rowmarch_kernel(const __grid_constant__ RmMaps tm, const RmParams p) {
         const float uH = e == L ? ur : mu_u.v[e == L ? 0 : e + 1];
         const float sL = e == 0 ? sl : s_u.v[e == 0 ? 0 : e - 1];
         const float sH = e == L ? sr : s_u.v[e == L ? 0 : e + 1];
-        const float m = SM::mean(uH, uL, vh.v[e], vl.v[e], 0.0f, 0.0f, cxe, cy, 0.0f);
+        const float rL = e == 0 ? rl : r_u.v[e == 0 ? 0 : e - 1];
+        const float rH = e == L ? rr : r_u.v[e == L ? 0 : e + 1];
+        const float m = SM::mean_r(uH, uL, rH, rL, vh.v[e], vl.v[e], unpack_bf16_hi(prh.v[e]), unpack_bf16_hi(prl.v[e]), 0.0f, 0.0f,
+                                   0.0f, 0.0f, cxe, cy, 0.0f);
         omu.v[e] = m;
         Tails<float>::eval(m, SM::var(sH, sL, svh.v[e], svl.v[e], 0.0f, 0.0f, cxe, cy, 0.0f),
                            p.theta, t_zero, osg.v[e], ops.v[e], opk.v[e]);
@@ -212,6 +247,8 @@ k3_rowmarch_kernel(const __grid_constant__ RmMaps tm, const RmParams p) {
       if (p.out_psrc) st_stream<float, C::VEC>(p.out_psrc + o, ops);
       if (p.out_psnk) st_stream<float, C::VEC>(p.out_psnk + o, opk);
       if (p.out_mom_mu) {
+        const V mu_v = *reinterpret_cast<const V*>(&ring.m[q][kRmV][cx0]);
+        const V s_v = *reinterpret_cast<const V*>(&ring.m[q][kRmSV][cx0]);
         st_stream<float, C::VEC>(p.out_mom_mu + o, mu_u);
         st_stream<float, C::VEC>(p.out_mom_mu + N + o, mu_v);
         st_stream<float, C::VEC>(p.out_mom_sigma + o, s_u);

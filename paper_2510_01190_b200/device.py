@@ -243,8 +243,9 @@ def ensemble_divergence3d(members, nx, ny, nz_local, dx=1.0, dy=1.0, dz=1.0, t=0
                           moments=False, outputs=ALL_OUTPUTS, out=None, check=True):
     """K3 3D fused on a z-slab: (M, 3, nx*ny*nz_local) fp32 members.
 
-    Halos are REDUCED w moments (mu_w, s_w) of the planes just outside the
-    slab (see ``w_moments_plane``)."""
+    Halos are REDUCED w moments (mu_w, s_w, r_w) of the planes just outside
+    the slab (see ``w_moments_plane``; r_w, the means' rounding residuals,
+    may be omitted and then reads as 0)."""
     _req(members, "members", torch.float32)
     m = members.shape[0]
     n = nx * ny * nz_local
@@ -252,15 +253,19 @@ def ensemble_divergence3d(members, nx, ny, nz_local, dx=1.0, dy=1.0, dz=1.0, t=0
         raise ValueError("members must have shape (M, 3, nx*ny*nz_local)")
     nzg = nz_local if nz_global is None else nz_global
     kb, ke = (0, nz_local) if k_range is None else k_range
-    hl = halo_lo or (None, None)
-    hh = halo_hi or (None, None)
+    hl = tuple(halo_lo or ()) + (None,) * (3 - len(halo_lo or ()))
+    hh = tuple(halo_hi or ()) + (None,) * (3 - len(halo_hi or ()))
+    for h in hl + hh:
+        if h is not None:
+            _req(h, "halo", torch.float32, nx * ny)
     o = _outs(members, n, outputs, out)
     if moments:
         o.setdefault("mom_mu", torch.empty((3, n), dtype=members.dtype, device=members.device))
         o.setdefault("mom_sigma", torch.empty((3, n), dtype=members.dtype, device=members.device))
     err = _ErrWord(members.device, check)
     _check(lib.divuq_ensemble_divergence3d_f32(
-        _ptr(members), m, _ptr(hl[0]), _ptr(hl[1]), _ptr(hh[0]), _ptr(hh[1]), nx, ny, nz_local,
+        _ptr(members), m, _ptr(hl[0]), _ptr(hl[1]), _ptr(hl[2]), _ptr(hh[0]), _ptr(hh[1]),
+        _ptr(hh[2]), nx, ny, nz_local,
         z0, nzg, kb, ke, float(dx), float(dy), float(dz), float(t), _ptr(o.get("mu")),
         _ptr(o.get("sigma")), _ptr(o.get("p_src")), _ptr(o.get("p_snk")), _ptr(o.get("mom_mu")),
         _ptr(o.get("mom_sigma")), err.ptr, _stream()))
@@ -269,7 +274,7 @@ def ensemble_divergence3d(members, nx, ny, nz_local, dx=1.0, dy=1.0, dz=1.0, t=0
 
 
 def w_moments_plane(members, nx, ny, nz_local, k, *, out=None, check=True):
-    """(mu_w, s_w) of local plane k of a 3D member slab -- the reduced halo
+    """(mu_w, s_w, r_w) of local plane k of a 3D member slab -- the reduced halo
     a z-slab neighbour needs.  Same K1 arithmetic as the fused kernel, so the
     sharded result stays bit-identical to the single-GPU one.  Read in place
     (member-strided), no gather copy."""
@@ -290,14 +295,14 @@ def w_moments_plane_ptr(members_ptr: int, m, nx, ny, nz_local, k, *, device, out
     n = plane * nz_local
     if not (0 <= k < nz_local):
         raise ValueError("plane index outside the slab")
-    mu, sg = out if out is not None else (torch.empty(plane, dtype=torch.float32, device=device),
-                                          torch.empty(plane, dtype=torch.float32, device=device))
+    mu, sg, r = out if out is not None else tuple(
+        torch.empty(plane, dtype=torch.float32, device=device) for _ in range(3))
     err = _ErrWord(device, check)
     base = int(members_ptr) + (2 * n + k * plane) * 4   # component w, plane k, member 0
-    _check(lib.divuq_fit_gaussian_strided_f32(base, m, 3 * n, plane, _ptr(mu), _ptr(sg), err.ptr,
-                                              _stream()))
+    _check(lib.divuq_fit_gaussian_strided_f32(base, m, 3 * n, plane, _ptr(mu), _ptr(sg), _ptr(r),
+                                              err.ptr, _stream()))
     err.raise_if_set()
-    return mu, sg
+    return mu, sg, r
 
 
 def mc_divergence2d(mu_u, mu_v, s_u, s_v, nx, ny, dx, dy, n_samples, seed, *, rows=None,

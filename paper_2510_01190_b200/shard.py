@@ -7,8 +7,9 @@ is ONE plane per neighbour per array:
 
 * K2 (analytic, config 3): the raw (mu_w, s_w) edge planes;
 * K3 (fused ensemble, config 4): the REDUCED w moments of the edge planes
-  (2 planes instead of 2*M), computed by the owner with the same moment
-  arithmetic, so sharded results are bit-identical to the 1-GPU run.
+  (3 planes -- mu, sigma and the means' rounding residual r -- instead of
+  2*M), computed by the owner with the same moment arithmetic, so sharded
+  results are bit-identical to the 1-GPU run.
 
 Two exchange modes (``SlabStep(exchange=...)``):
 
@@ -19,8 +20,13 @@ Two exchange modes (``SlabStep(exchange=...)``):
   at the neighbours' edge planes; K3 reduces the neighbours' edge-plane w
   moments with a strided K1 reading their member planes in place (side
   stream), overlapped with the interior planes, then the two edge planes.
-  Inputs are read in place, so a producer that rewrites them must finish
-  (e.g. ``dist.barrier()``) before the step -- ``sync_inputs=True`` does it.
+  Inputs are read in place, so the p2p step is fenced on both sides by
+  default: ``sync_inputs=True`` drains every rank's producers before the
+  first peer read, and the closing fence (stream sync + barrier) keeps a
+  neighbour from rewriting or freeing its slab while this rank still reads
+  it.  Re-mapping after a buffer moved is a collective decision (every rank
+  learns whether ANY rank's buffers changed), so no rank skips the handle
+  exchange another rank enters.
 * ``"nccl"``: the classic schedule (``SlabStep.run``) --
   1. post the neighbour sends/receives (``batch_isend_irecv``; NCCL runs them
      on its own stream over NVLink),
@@ -66,7 +72,7 @@ class SlabStep:
     nz_global: int
     rank: int
     world: int
-    n_arrays: int = 2          # arrays per exchanged plane (mu_w, s_w)
+    n_arrays: int = 2          # arrays per exchanged plane: K2 (mu_w, s_w); K3 3 (mu_w, s_w, r_w)
     dtype: torch.dtype = torch.float32
     device: str | torch.device = "cuda"
     group: object = None
@@ -92,12 +98,20 @@ class SlabStep:
         return z1 - z0
 
     def attach(self, arrays: dict) -> None:
-        """p2p: export ``arrays`` and map the neighbours' (collective, once per
-        set of buffers; re-attaching the same buffers is free)."""
+        """p2p: export ``arrays`` and map the neighbours' (collective).  Every
+        rank calls it every step; the handles are re-exchanged when ANY rank's
+        buffers moved (one all-reduced flag), so all ranks agree on entering
+        the handle all-gather and nobody keeps a stale mapping."""
         from . import peer
 
         key = tuple((k, v.data_ptr()) for k, v in sorted(arrays.items()))
-        if self._attached == key:
+        if self.world > 1:
+            dev = self.device if dist.get_backend(self.group) == "nccl" else "cpu"
+            changed = torch.tensor([int(self._attached != key)], dtype=torch.int32, device=dev)
+            dist.all_reduce(changed, op=dist.ReduceOp.MAX, group=self.group)
+            if int(changed.item()) == 0:
+                return
+        elif self._attached == key:
             return
         if self.peers:
             for arrs in self.peers.values():
@@ -149,6 +163,13 @@ def _sync_inputs(step: SlabStep):
     dist.barrier(group=step.group)
 
 
+def _fence(step: SlabStep):
+    """Closing fence of a p2p step: this rank's peer reads are complete before
+    any neighbour may rewrite or free the slab they read."""
+    torch.cuda.current_stream().synchronize()
+    dist.barrier(group=step.group)
+
+
 def ensure_p2p(step: SlabStep, arrays: dict) -> bool:
     """Collective: map the neighbours' ``arrays`` for the p2p exchange; if any
     rank cannot (no peer access, IPC refused), every rank switches this step
@@ -172,7 +193,8 @@ def ensure_p2p(step: SlabStep, arrays: dict) -> bool:
     return False
 
 
-def propagate3d_step(step: SlabStep, fields, out, dx, dy, dz, t, check=False, sync_inputs=False):
+def propagate3d_step(step: SlabStep, fields, out, dx, dy, dz, t, check=False, sync_inputs=True,
+                     fence=True):
     """K2 sharded step on this rank's slab tensors (fields = 6 slab tensors)."""
     from . import device as dev
 
@@ -193,6 +215,8 @@ def propagate3d_step(step: SlabStep, fields, out, dx, dy, dz, t, check=False, sy
             hi = (nb["mu_w"].at(0), nb["s_w"].at(0))
         dev.propagate3d(*fields, step.nx, step.ny, step.nzl, dx, dy, dz, t, z0=step.z0,
                         nz_global=step.nz_global, halo_lo=lo, halo_hi=hi, out=out, check=check)
+        if fence:
+            _fence(step)
         step.launches = 1
         return 1
 
@@ -208,7 +232,8 @@ def propagate3d_step(step: SlabStep, fields, out, dx, dy, dz, t, check=False, sy
     return step.run(edges, compute)
 
 
-def ensemble3d_step(step: SlabStep, members, out, dx, dy, dz, t, check=False, sync_inputs=False):
+def ensemble3d_step(step: SlabStep, members, out, dx, dy, dz, t, check=False, sync_inputs=True,
+                    fence=True):
     """K3 sharded step.  nccl: the owner reduces its edge planes' w moments and
     the neighbours receive 2 planes each instead of 2*M raw member planes.
     p2p: each rank reduces its neighbours' edge planes itself, reading their
@@ -216,6 +241,8 @@ def ensemble3d_step(step: SlabStep, members, out, dx, dy, dz, t, check=False, sy
     interior planes."""
     from . import device as dev
 
+    if step.world > 1 and step.n_arrays != 3:
+        raise ValueError("ensemble3d_step exchanges (mu_w, s_w, r_w): build the SlabStep with n_arrays=3")
     if step.exchange == "p2p" and step.world > 1:
         step.attach({"members": members})
         if sync_inputs:
@@ -248,6 +275,8 @@ def ensemble3d_step(step: SlabStep, members, out, dx, dy, dz, t, check=False, sy
             dev.ensemble_divergence3d(members, step.nx, step.ny, step.nzl, dx, dy, dz, t,
                                       k_range=kr, **common)
         n += 2
+        if fence:
+            _fence(step)
         step.launches = n
         return n
 

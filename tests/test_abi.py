@@ -38,7 +38,7 @@ def test_library_exports_every_declared_symbol(pkg):
 
 def test_abi_version_and_status_strings(pkg):
     lib = pkg._lib.lib
-    assert lib.divuq_abi_version() == 1
+    assert lib.divuq_abi_version() == 2
     assert lib.divuq_status_string(-2).decode().startswith("grid must be")
     assert "non-finite" in lib.divuq_status_string(-10).decode()
     with pytest.raises(ValueError):

@@ -228,18 +228,15 @@ def test_config1_full_size_vs_oracle(dev):
     dmu, dsg = ref2d.propagate2d(mu_r[0], mu_r[1], sg_r[0], sg_r[1], nx, ny, 1.0, 1.0)
     assert np.abs(o["mu"].cpu().numpy() - dmu).max() <= 1e-5 * np.abs(dmu).max()
     assert np.abs(o["sigma"].cpu().numpy() - dsg).max() <= 1e-5 * np.abs(dsg).max()
-    # P is ill-conditioned in fp32 here: sigma(x) goes down to 0.02 while the
-    # fields reach ~5, so dP ~ phi(t) * dmu / sigma.  Check (a) the tail map
-    # against the oracle evaluated at the kernel's own fp32 mu / sigma (the
-    # kernel's job), and (b) the end-to-end deviation, which is fp32 mu
-    # rounding amplified by 1/sigma.
-    gmu = o["mu"].cpu().numpy().astype(np.float64)
-    gsg = o["sigma"].cpu().numpy().astype(np.float64)
-    ps_own = ref2d.source_probability(gmu, gsg, 0.0)
-    p = o["p_src"].cpu().numpy()
-    assert np.all(np.abs(p - ps_own) <= 1e-5 * ps_own + 1e-6)
+    # the fp32 bar on the probabilities (|dP| <= 1e-5 P + 1e-6) against the
+    # fp64 oracle at the full config-1 size: the vortex reaches |u| ~ 110
+    # while sigma(x) drops to 0.02, so this holds only because the fused
+    # kernel differences the (mu, r) pairs instead of fp32-rounded means
     ps = ref2d.source_probability(dmu, dsg, 0.0)
-    assert np.abs(p - ps).max() <= 1e-3
+    pk = ref2d.sink_probability(dmu, dsg, 0.0)
+    p_src, p_snk = o["p_src"].cpu().numpy(), o["p_snk"].cpu().numpy()
+    assert np.all(np.abs(p_src - ps) <= 1e-5 * ps + 1e-6), np.abs(p_src - ps).max()
+    assert np.all(np.abs(p_snk - pk) <= 1e-5 * pk + 1e-6), np.abs(p_snk - pk).max()
 
 
 def test_redsea_chain_full_size(dev):

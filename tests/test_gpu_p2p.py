@@ -63,7 +63,7 @@ def _worker(rank, world, port, outdir):
         torch.cuda.synchronize()
         res = {f"k2_{k}": v.cpu().numpy() for k, v in out.items()}
 
-        step3 = shard.SlabStep(NX, NY, NZ, rank, world, exchange="p2p", device="cuda")
+        step3 = shard.SlabStep(NX, NY, NZ, rank, world, n_arrays=3, exchange="p2p", device="cuda")
         members = torch.from_numpy(np.ascontiguousarray(mem[:, :, z0 * plane:z1 * plane])).cuda()
         out3 = {k: torch.empty(step.nzl * plane, device="cuda") for k in ("mu", "sigma", "p_src", "p_snk")}
         n3 = shard.ensemble3d_step(step3, members, out3, 1.0, 0.5, 2.0, 0.1, check=True,

@@ -316,7 +316,7 @@ def test_propagate3d_slabs_and_k_ranges_bitwise(dev, dtype, rng):
                                      # lane, 2-3 row runs, segment boundaries, many members
                                      (3, (4, 2)), (20, (68, 5)), (5, (100, 200)), (20, (132, 3)),
                                      (20, (1024, 64)), (30, (192, 130))])
-def test_ensemble_divergence2d(dev, m, shape, rng):
+def test_ensemble_divergence2d(dev, m, shape, rng, monkeypatch):
     nx, ny = shape
     n = nx * ny
     base = rng.normal(0, 1, (1, 2, n))
@@ -330,16 +330,22 @@ def test_ensemble_divergence2d(dev, m, shape, rng):
     assert normwise(host(o["sigma"]), dsg) <= 1e-5
     ps = ref2d.source_probability(dmu, dsg, 0.0)
     assert np.all(np.abs(host(o["p_src"]) - ps) <= 1e-5 * ps + 1e-6)
-    # fused == K1 + K2 composition on the device, bit for bit
+    # the fused moments are K1's, bit for bit
     mu_g, sg_g = dev.fit_moments(cu(mem))
-    o2 = dev.propagate2d(mu_g[0].contiguous(), mu_g[1].contiguous(), sg_g[0].contiguous(),
-                         sg_g[1].contiguous(), nx, ny, 0.5, 0.5, 0.0)
-    for k in ("mu", "sigma", "p_src", "p_snk"):
-        assert np.array_equal(host(o[k]), host(o2[k])), k
+    assert np.array_equal(host(o["mom_mu"]), host(mu_g))
+    assert np.array_equal(host(o["mom_sigma"]), host(sg_g))
+    # every fused path (row march, tiled K3, K1 triples + residual stencil)
+    # differences the same (mu, r) pairs: identical maps
+    for env in ("DIVUQ_NO_ROWMARCH", "DIVUQ_NO_TMA"):
+        monkeypatch.setenv(env, "1")
+        o2 = dev.ensemble_divergence2d(cu(mem), nx, ny, 0.5, 0.5, 0.0, moments=True)
+        monkeypatch.delenv(env)
+        for k in o:
+            assert np.array_equal(host(o[k]), host(o2[k])), (env, k)
 
 
 @pytest.mark.parametrize("m", [16, 5])
-def test_ensemble_divergence3d_and_slabs(dev, m, rng):
+def test_ensemble_divergence3d_and_slabs(dev, m, rng, monkeypatch):
     nx, ny, nz = 64, 12, 14
     plane = nx * ny
     n = plane * nz
@@ -351,11 +357,16 @@ def test_ensemble_divergence3d_and_slabs(dev, m, rng):
     dmu, dsg = ref3d.propagate3d(*mu_r, *sg_r, nx, ny, nz, 1.0, 1.0, 1.0)
     assert normwise(host(full["mu"]), dmu) <= 1e-5
     assert normwise(host(full["sigma"]), dsg) <= 1e-5
-    # fused == K1 + K2 on the device, bitwise
+    pk = ref2d.sink_probability(dmu, dsg, 0.1)
+    assert np.all(np.abs(host(full["p_snk"]) - pk) <= 1e-5 * pk + 1e-6)
+    # the fused moments are K1's; the fallback (K1 triples + residual stencil)
+    # gives the same maps bit for bit
     mu_g, sg_g = dev.fit_moments(gm)
-    o2 = dev.propagate3d(*(mu_g[c].contiguous() for c in range(3)), *(sg_g[c].contiguous() for c in range(3)),
-                         nx, ny, nz, 1.0, 1.0, 1.0, 0.1)
-    for k in ("mu", "sigma", "p_src", "p_snk"):
+    assert np.array_equal(host(full["mom_mu"]), host(mu_g))
+    monkeypatch.setenv("DIVUQ_NO_TMA", "1")
+    o2 = dev.ensemble_divergence3d(gm, nx, ny, nz, 1.0, 1.0, 1.0, 0.1, moments=True)
+    monkeypatch.delenv("DIVUQ_NO_TMA")
+    for k in full:
         assert np.array_equal(host(full[k]), host(o2[k])), k
     # slabs with reduced w-moment halos == whole domain, bitwise
     for parts in (2, 3):
