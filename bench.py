@@ -19,9 +19,14 @@ Prints ONE JSON line (rank 0).  Keys beyond the base contract:
   gpu_launches  our kernel launches inside the timed region
   clocks        NVML SM clock / throttle reasons sampled during the timed region
 
-``--impl reference`` times the reference's CPU algorithm (the oracle port,
-``oracle/cpu_baseline.py``; the Python reference cannot travel to this box) on
-a bounded sample of the same workload with all host threads; rank 0 only.
+``--impl reference`` times the reference's CPU implementation on this box's
+host cores, rank 0 only, on the same fixed sample as the cpu_baseline leg
+(oracle/cpu_baseline.cpu_leg): the unmodified reference package
+(baseline/_ref, its own pip install) for the 2D configs, the oracle
+restatement for the 3D configs (the reference has no 3D code).
+
+``--gpus N`` outside torchrun launches the N ranks itself (one process per
+GPU, torch.distributed.run on 127.0.0.1, NCCL_DEBUG=INFO).
 """
 
 from __future__ import annotations
@@ -36,6 +41,19 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+
+ERR = None   # the device validation word of the timed calls (int32 CUDA tensor)
+
+
+def validation_note():
+    """Read the validation word once after the timed loop; raise like the
+    reference would on bad inputs, else describe the check for the JSON line."""
+    from paper_2510_01190_b200.device import raise_for_bits
+
+    bits = int(ERR.item())
+    raise_for_bits(bits)
+    return "on: kernels validate every input (non-finite, sigma < 0) into a device word, read once after the timed loop (clean)"
+
 
 METRIC = "grid points/sec (analytic div mean+var+prob) and % HBM roofline at 1/2/4/8 B200"
 UNIT = "grid points/s"
@@ -136,6 +154,11 @@ class L2Flush:
 # ---------------------------------------------------------------------------
 
 def run_reference(args):
+    """The reference's own CPU implementation of the path on this box's host
+    cores (oracle/cpu_baseline.cpu_leg: the unmodified reference from
+    baseline/_ref for the 2D configs, the oracle restatement for the 3D ones
+    that have no reference code), the SAME fixed sample the repo arm's
+    cpu_baseline leg times, each step one call.  Rank 0 only."""
     if int(os.environ.get("RANK", "0")) != 0:
         return  # rank 0 alone runs the CPU reference
     from oracle import cpu_baseline as cb
@@ -143,41 +166,87 @@ def run_reference(args):
     cid = args.config
     threads = os.cpu_count() or 1
     steps, warm = args.steps, args.warmup
-    budget = 150.0  # seconds for warm-up + steps: the arm must end within minutes
-    if cid == 4:
-        make = lambda p: cb.ensemble3d_thunk(1024, 1024, p, 16, threads=threads)
-        sample = "fit_gaussian(M=16) + 3D propagation + P(div>0.1), P(div<-0.1) on 1024x1024x{p}"
-    elif cid == 1:
-        make = lambda p: cb.ensemble3d_thunk(1024, 64, p, 20, threads=threads)
-        sample = "fit_gaussian(M=20) + propagation + tails on 1024x64x{p}"
-    else:
-        make = lambda p: cb.propagate3d_thunk(512, 512, p, threads=threads)
-        sample = "3D propagation + P(div>0) + P(div<0) on 512x512x{p} sub-volume"
-    thunk, n, _ = make(2)
-    thunk()
-    t0 = time.perf_counter()
-    thunk()
-    per_plane = (time.perf_counter() - t0) / 2.0
-    planes = int(max(2, min(64, budget / max(1, steps + warm) / max(per_plane, 1e-6))))
-    thunk, n, _ = make(planes)
+    work, units, unit, sample, kind = cb.cpu_leg(cid, threads)
+    par = True
+    if cid in (0, 1):   # the faster of the reference's threaded and serial paths
+        t0 = time.perf_counter(); work(True); work(True); tp = time.perf_counter() - t0
+        t0 = time.perf_counter(); work(False); work(False); ts = time.perf_counter() - t0
+        par = tp <= ts
     times = []
     for it in range(warm + steps):
         t0 = time.perf_counter()
-        thunk()
+        work(par) if cid in (0, 1) else work()
         if it >= warm:
             times.append(time.perf_counter() - t0)
     mean_s = sum(times) / len(times)
-    value = n / mean_s
+    value = units / mean_s
+    cores = threads if par else 1
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": METRIC if cid != 2 else "vertex-samples/sec (Monte Carlo divergence mean+std)",
+        "value": value, "unit": unit, "n_gpus": args.gpus,
         "steps": steps, "warmup": warm, "ms_per_step": mean_s * 1e3, "higher_is_better": True,
         "scaling": "strong" if cid == 3 else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": f"config{cid} (bounded CPU sample)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample.format(p=planes) + f", {threads} threads, fp64 like the reference"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": kind,
+                         "sample": sample + ("" if par else "; serial path (faster than threaded)")},
+        "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def maybe_spawn(args) -> bool:
+    """``--gpus N`` without a torchrun environment: launch N ranks ourselves
+    (torch.distributed.run, one process per GPU, rendezvous on 127.0.0.1) and
+    exit with their status.  Under torchrun the world size must equal N."""
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is not None:
+        if int(env_world) != args.gpus:
+            raise SystemExit(f"bench.py: WORLD_SIZE={env_world} but --gpus {args.gpus}")
+        return False
+    if args.gpus <= 1:
+        return False
+    if os.environ.get("DIVUQ_BENCH_ONE_DEVICE") != "1" and not args.plumbing_check:
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible")
+    import socket
+    import subprocess
+
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    sys.exit(subprocess.call(cmd, env=env))
+
+
+def plumbing_check(args):
+    """--plumbing-check: the multi-rank launch path without GPU work (CPU
+    test): every rank joins a gloo group, the ranks all-reduce their count,
+    rank 0 prints the JSON skeleton with n_gpus = the world size."""
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.ones(1)
+    if world > 1:
+        dist.all_reduce(t)
+    print(f"rank {rank}/{world}: process group up ({'gloo' if world > 1 else 'none'})", file=sys.stderr,
+          flush=True)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "n_gpus": world, "ranks_seen": int(t.item()),
+                          "plumbing_check": True}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 # ---------------------------------------------------------------------------
@@ -195,6 +264,8 @@ def run_next(args):
     from paper_2510_01190_b200._lib import lib
 
     torch.cuda.set_device(0)
+    global ERR
+    ERR = torch.zeros(1, dtype=torch.int32, device="cuda")
     stream = torch.cuda.current_stream()
     peak, peak_src = measured_peak()
     ev_pairs = []
@@ -219,7 +290,7 @@ def run_next(args):
         workload = "lcp: per-cell P(div field crosses 0) on a 4096^2 fp64 divergence (mu, sigma) field"
 
         def step():
-            dev.lcp2d(mu, sg, nx, ny, 0.0, check=False)
+            dev.lcp2d(mu, sg, nx, ny, 0.0, check=ERR)
 
         hm, hs = mu.cpu().pin_memory(), sg.cpu().pin_memory()
         hout = torch.empty(units, dtype=torch.float64).pin_memory()
@@ -248,7 +319,7 @@ def run_next(args):
         workload = "gradient: gradient_ensemble of the config-1 ensemble (M=20, 1024^2), fp64"
 
         def step():
-            dev.gradient_ensemble2d(mem, nx, ny, 1.0, 1.0, out=out, check=False)
+            dev.gradient_ensemble2d(mem, nx, ny, 1.0, 1.0, out=out, check=ERR)
 
         hin = mem.cpu().pin_memory()
         hout = torch.empty_like(hin).pin_memory()
@@ -279,14 +350,14 @@ def run_next(args):
                     "velocity ensemble (M=20, 1024^2), fp32, one kernel")
 
         def step():
-            dev.gradient_ensemble_divergence2d(mem, nx, ny, 1.0, 1.0, 0.0, out=outs, check=False)
+            dev.gradient_ensemble_divergence2d(mem, nx, ny, 1.0, 1.0, 0.0, out=outs, check=ERR)
 
         # the same chain unfused (gradient ensemble written + re-read), for the record
         grad = torch.empty_like(mem)
 
         def composed():
-            dev.gradient_ensemble2d(mem, nx, ny, 1.0, 1.0, out=grad, check=False)
-            dev.ensemble_divergence2d(grad, nx, ny, 1.0, 1.0, 0.0, out=outs, check=False)
+            dev.gradient_ensemble2d(mem, nx, ny, 1.0, 1.0, out=grad, check=ERR)
+            dev.ensemble_divergence2d(grad, nx, ny, 1.0, 1.0, 0.0, out=outs, check=ERR)
 
         hin = mem.cpu().pin_memory()
         hout = [torch.empty(units, dtype=torch.float32).pin_memory() for _ in range(4)]
@@ -326,7 +397,7 @@ def run_next(args):
         workload = "fit: fit_gaussian of the config-1 ensemble (M=20, 1024^2) in fp64"
 
         def step():
-            dev.fit_moments(mem, out=(mu_o, sg_o), check=False)
+            dev.fit_moments(mem, out=(mu_o, sg_o), check=ERR)
 
         hin = mem.cpu().pin_memory()
         hmu = torch.empty((2, nx * ny), dtype=torch.float64).pin_memory()
@@ -366,7 +437,7 @@ def run_next(args):
         def step():
             _, x = dio.load_ensemble_device(path)
             dev.ensemble_divergence2d(x, nx, ny, 1.0, 1.0, 0.0, outputs=("mu", "sigma", "p_src"),
-                                      out=outs, check=False)
+                                      out=outs, check=ERR)
 
         e2e_call = None
         h2d, d2h = file_bytes, 0
@@ -465,7 +536,8 @@ def run_next(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": dtype, "data": "synthetic (seeded generator)",
         "config": {"workload": workload, "parallelism": "replicas x1",
-                   "l2": L2Flush.NOTE if wl != "ingest" else "n/a (host-bound)"},
+                   "l2": L2Flush.NOTE if wl != "ingest" else "n/a (host-bound)",
+                   "validation": validation_note()},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches_per_step * args.steps, "clocks": clocks.summary(),
     }
@@ -485,15 +557,23 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fp64", action="store_true", help="skip config 3's fp64 side measurement")
     ap.add_argument("--planes-per-gpu", type=int, default=128, help="config 4 slab depth")
     ap.add_argument("--exchange", default="p2p", choices=("p2p", "nccl"),
                     help="z-slab halo exchange for configs 3/4 at N>1: peer memory read in "
                          "place by the kernels (p2p) or NCCL send/recv overlapped with the interior")
+    ap.add_argument("--plumbing-check", action="store_true",
+                    help="multi-rank launch/rendezvous only (no GPU work): CPU test of --gpus N")
     ap.add_argument("--workload", default=None,
                     choices=("lcp", "gradient", "ingest", "fit", "redsea"),
                     help="a SURVEY 8f row instead of a BASELINE config (1 GPU, ours only)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.impl == "ours" and args.workload is None:
+        maybe_spawn(args)      # exits after the ranks finish when it launched them
+    if args.plumbing_check:
+        plumbing_check(args)
+        return
     if args.workload is not None:
         if args.impl == "reference" or int(os.environ.get("RANK", "0")) != 0:
             return
@@ -523,6 +603,8 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    global ERR
+    ERR = torch.zeros(1, dtype=torch.int32, device="cuda")
     import __graft_entry__
 
     if rank == 0:
@@ -565,7 +647,7 @@ def main():
             e0 = ev() if timed and dominant else None
             dev.propagate3d(*fields, nx, ny, step.nzl, 1.0, 1.0, 1.0, cfg.t, z0=step.z0,
                             nz_global=nz, halo_lo=step.halo_lo, halo_hi=step.halo_hi,
-                            k_range=k_range, out=out, check=False)
+                            k_range=k_range, out=out, check=ERR)
             if e0 is not None:
                 kernel_events.append((e0, ev(), (k_range[1] - k_range[0]) * plane))
             return 1
@@ -573,7 +655,7 @@ def main():
         def one_step(timed):
             if step.exchange == "p2p" and world > 1:   # one launch, halos read over NVLink
                 e0 = ev() if timed else None
-                n = shard.propagate3d_step(step, fields, out, 1.0, 1.0, 1.0, cfg.t)
+                n = shard.propagate3d_step(step, fields, out, 1.0, 1.0, 1.0, cfg.t, check=ERR)
                 if timed:
                     kernel_events.append((e0, ev(), step.nzl * plane))
                 return n
@@ -595,8 +677,8 @@ def main():
         scaling = "weak"
 
         def edges():
-            first = dev.w_moments_plane(members, nx, ny, step.nzl, 0, check=False)
-            last = dev.w_moments_plane(members, nx, ny, step.nzl, step.nzl - 1, check=False)
+            first = dev.w_moments_plane(members, nx, ny, step.nzl, 0, check=ERR)
+            last = dev.w_moments_plane(members, nx, ny, step.nzl, step.nzl - 1, check=ERR)
             return first, last
 
         def compute(k_range, lo, hi, timed):
@@ -604,7 +686,7 @@ def main():
             e0 = ev() if timed and dominant else None
             dev.ensemble_divergence3d(members, nx, ny, step.nzl, 1.0, 1.0, 1.0, cfg.t, z0=step.z0,
                                       nz_global=nz, halo_lo=step.halo_lo, halo_hi=step.halo_hi,
-                                      k_range=k_range, out=out, check=False)
+                                      k_range=k_range, out=out, check=ERR)
             if e0 is not None:
                 kernel_events.append((e0, ev(), (k_range[1] - k_range[0]) * nx * ny))
             return 1
@@ -612,7 +694,7 @@ def main():
         def one_step(timed):
             if step.exchange == "p2p" and world > 1:   # neighbours' edge moments read over NVLink
                 e0 = ev() if timed else None           # (whole step timed: conservative roofline)
-                n = shard.ensemble3d_step(step, members, out, 1.0, 1.0, 1.0, cfg.t)
+                n = shard.ensemble3d_step(step, members, out, 1.0, 1.0, 1.0, cfg.t, check=ERR)
                 if timed:
                     kernel_events.append((e0, ev(), step.nzl * nx * ny))
                 return n
@@ -637,7 +719,7 @@ def main():
             if timed:
                 flush()  # L2 flush between steps; outside the kernel events
             e0 = ev() if timed else None
-            dev.propagate2d(*model, nx, ny, 1.0, 1.0, cfg.t, out=out, check=False)
+            dev.propagate2d(*model, nx, ny, 1.0, 1.0, cfg.t, out=out, check=ERR)
             if timed:
                 kernel_events.append((e0, ev(), nx * ny))
             return 1
@@ -657,7 +739,7 @@ def main():
         def one_step(timed):
             e0 = ev() if timed else None
             dev.mc_divergence2d(*model, nx, ny, 1.0, 1.0, cfg.n_samples, 2024, out=(mean, std),
-                                check=False)
+                                check=ERR)
             if timed:
                 kernel_events.append((e0, ev(), nx * ny))
             return 2
@@ -679,7 +761,7 @@ def main():
                 flush()  # L2 flush (inputs 168 MB are ~L2-sized); outside the kernel events
             e0 = ev() if timed else None
             dev.ensemble_divergence2d(members, nx, ny, 1.0, 1.0, cfg.t, outputs=("mu", "sigma", "p_src"),
-                                      out=out, check=False)
+                                      out=out, check=ERR)
             if timed:
                 kernel_events.append((e0, ev(), nx * ny))
             return 1
@@ -748,6 +830,32 @@ def main():
         roofline["note"] = ("small-problem floor: a perfectly coalesced 40-read/3-write float4 stream of "
                             "the same 172 MB, timed the same way (L2 evicted, one launch), takes 36.1 us "
                             "= 5.0 TB/s (tools/bwbench, profiles/r01/bwbench.txt)")
+
+    # the same config-3 workload in fp64 (the reference's precision), next to
+    # the fp32 headline: single-GPU launches of the fp64 K2, same protocol
+    fp64_variant = None
+    if args.config == 3 and world == 1 and not args.no_fp64:
+        f64 = [f.double() for f in fields]
+        o64 = {k: torch.empty(n_local, dtype=torch.float64, device="cuda") for k in dev.ALL_OUTPUTS}
+        for _ in range(3):
+            dev.propagate3d(*f64, nx, ny, nz, 1.0, 1.0, 1.0, cfg.t, out=o64, check=ERR)
+        pairs = []
+        for _ in range(10):
+            a = ev()
+            dev.propagate3d(*f64, nx, ny, nz, 1.0, 1.0, 1.0, cfg.t, out=o64, check=ERR)
+            pairs.append((a, ev()))
+        torch.cuda.synchronize()
+        ms64 = sum(a.elapsed_time(b) for a, b in pairs) / len(pairs)
+        bpp64 = 6 * 8 + 4 * 8
+        ach64 = bpp64 * n_local / (ms64 * 1e-3) / 1e9
+        fp64_variant = {"dtype": "f64", "ms_per_step": ms64, "value": total_pts / (ms64 * 1e-3),
+                        "unit": UNIT, "roofline": {"bound": "hbm", "achieved": ach64, "peak": peak,
+                                                   "unit": "GB/s", "frac": ach64 / peak,
+                                                   "bytes_per_point": bpp64},
+                        "note": "k2_tma_kernel<double>: the reference's fp64 arithmetic, bitwise to the "
+                                "reference order; 10 launches, inputs 6.4 GB (> L2)"}
+        del f64, o64
+        torch.cuda.empty_cache()
 
     # e2e through the host-buffer C ABI (pinned host buffers, copies timed)
     e2e = None
@@ -882,26 +990,9 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         from oracle import cpu_baseline as cb
 
-        if args.config == 4:
-            v, thr, runs = cb.rate(cb.ensemble3d_thunk(1024, 1024, 2, 16), seconds=10.0)
-            sample = f"fit_gaussian(M=16)+3D propagation+tails on 1024x1024x2 sub-volume, {runs} runs"
-        elif args.config == 1:
-            v, thr, runs = cb.rate(cb.ensemble3d_thunk(1024, 64, 2, 20), seconds=5.0)
-            sample = f"fit_gaussian(M=20)+propagation+tails on 1024x64x2, {runs} runs"
-        elif args.config == 0:
-            v, thr, runs = cb.rate(cb.propagate2d_thunk(host_model, nx, ny, cfg.t), seconds=5.0)
-            sample = f"reference-order 2D propagation + both tails, 128^2 fp64, serial, {runs} runs"
-        elif args.config == 2:
-            v, thr, runs = cb.rate(cb.mc_thunk(host_model, nx, ny, 8), seconds=10.0)
-            sample = f"Philox MC estimator restated in numpy, 256^2 x 8 samples, {runs} runs"
-        else:
-            v, thr, runs = cb.rate(cb.propagate3d_thunk(512, 512, 16), seconds=10.0)
-            sample = f"3D propagation + P(div>0) + P(div<0) on 512x512x16 sub-volume, {runs} runs"
-        cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": "port", "sample": sample}
+        cpu = cb.time_leg(args.config, seconds=10.0)   # the reference arm's exact sample
 
     unit = "vertex-samples/s" if args.config == 2 else UNIT
-    if cpu is not None:
-        cpu["unit"] = unit
     line = {
         "metric": METRIC if args.config != 2 else "vertex-samples/sec (Monte Carlo divergence mean+std)",
         "value": value, "unit": unit, "n_gpus": world, "steps": args.steps,
@@ -918,12 +1009,15 @@ def main():
                    **({"dry_run": "DIVUQ_BENCH_ONE_DEVICE=1: every rank on cuda:0 over gloo "
                                   "(orchestration check, not a multi-GPU number)"}
                       if one_device and world > 1 else {}),
+                   "validation": validation_note(),
                    "l2": (L2Flush.NOTE if args.config in (0, 1) else
                           "inputs larger than L2 (126 MB); no flush" if args.config in (3, 4) else
                           "compute-bound; 2 MB model stays in L2")},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": clocks.summary(),
     }
+    if fp64_variant is not None:
+        line["fp64_variant"] = fp64_variant
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -1,17 +1,23 @@
-"""Threaded CPU baseline of the hot path -- TEST INFRASTRUCTURE ONLY.
+"""CPU baselines of the hot path -- TEST INFRASTRUCTURE ONLY.
 
 Only ``bench.py``'s ``cpu_baseline`` leg and ``--impl reference`` arm call
-this.  It times the oracle restatement of the reference's algorithm (the
-reference itself is pure Python and cannot travel to the GPU box, and there is
-no 3D reference -- SURVEY F2), parallelised the way the reference parallelises:
-static contiguous chunks of the index space on a ThreadPoolExecutor
-(parallel.py:65-116), numpy releasing the GIL inside each chunk.  Arithmetic
-is fp64 like the reference (grid.py:23), on the same fp32-exact inputs.
+this, and both call the SAME ``cpu_leg`` (same sample, same threads):
+
+* 2D configs 0-2: the UNMODIFIED reference itself -- its own pip install in
+  ``baseline/_ref`` (made by ``__graft_entry__.build()``, shipped to the GPU
+  box) -- through its public API, with ``ParallelConfig(threads=
+  os.cpu_count())`` where the reference takes one (propagate_divergence,
+  divergence.py:48-70; parallel.py:65-116), ``kind: "reference"``;
+* 3D configs 3-4 (no reference code): the oracle restatement,
+  parallelised the way the reference parallelises (static contiguous chunks
+  of the index space on a thread pool, numpy releasing the GIL), fp64 like
+  the reference (grid.py:23), ``kind: "port"``.
 """
 
 from __future__ import annotations
 
 import os
+import sys
 import time
 from concurrent.futures import ThreadPoolExecutor
 
@@ -107,3 +113,124 @@ def mc_thunk(model, nx, ny, n_samples):
     mu_u, mu_v, s_u, s_v = model
     return (lambda: philox.mc_divergence(mu_u, mu_v, s_u, s_v, nx, ny, 1.0, 1.0, n_samples, 7),
             nx * ny * n_samples, 1)
+
+
+# ---------------------------------------------------------------------------
+# the unified CPU leg (both bench arms)
+# ---------------------------------------------------------------------------
+
+REF_ROOT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+
+
+def reference_package():
+    """The unmodified reference ``divuq`` (baseline/_ref), or None if absent."""
+    if not os.path.isdir(os.path.join(REF_ROOT, "divuq")):
+        return None
+    if REF_ROOT not in sys.path:
+        sys.path.insert(0, REF_ROOT)
+    import divuq
+
+    return divuq
+
+
+def _config1_members_host(nx, ny, m, seed):
+    """Config-1 recipe on the host (24 sources/sinks + vortex, smooth sigma in
+    [0.02, 0.5], iid normal perturbations): same shapes and value ranges as the
+    device generator, for CPU timing only."""
+    from paper_2510_01190_b200 import configs
+
+    u, v, _, _ = configs.host_model2d(nx, ny, 24, seed)
+    j, i = np.divmod(np.arange(nx * ny), nx)
+    sig = 0.02 + 0.48 * (0.5 + 0.5 * np.sin(i / 37.0) * np.cos(j / 53.0))
+    rng = np.random.default_rng(seed + 7)
+    return [(u + sig * rng.standard_normal(nx * ny), v + sig * rng.standard_normal(nx * ny))
+            for _ in range(m)]
+
+
+def cpu_leg(cid, threads=None):
+    """(thunk, units per call, unit, sample text, kind, extra) for config cid.
+
+    The sample is fixed per config (not budget-derived), so the two bench
+    arms time exactly the same work."""
+    threads = threads or os.cpu_count() or 1
+    ref = reference_package() if cid in (0, 1, 2) else None
+    if cid in (0, 1, 2) and ref is None:
+        raise RuntimeError("baseline/_ref (the reference install) is missing: run "
+                           "__graft_entry__.build() where /root/reference exists")
+    from paper_2510_01190_b200 import configs
+
+    if cid == 0:
+        mu_u, mu_v, s_u, s_v = configs.config0_model()
+        g = ref.UniformGrid2(128, 128)
+        model = ref.GaussianVectorField(g, mu_u, mu_v, s_u, s_v)
+        pc = ref.ParallelConfig(threads=threads)
+        from divuq.lcp import _tail_probs
+
+        def work(par=True):
+            f = ref.propagate_divergence(model, pc if par else None)
+            _tail_probs(f.mu, f.sigma, 0.0)        # P(div <= 0), P(div > 0)
+            _tail_probs(f.mu, f.sigma, -0.0)       # the sink map at -t
+
+        return (work, g.n_vertices, "grid points/s",
+                f"reference propagate_divergence(ParallelConfig(threads={threads})) + _tail_probs "
+                "for P(div>0), P(div<0) on the full config-0 128^2 model", "reference")
+    if cid == 1:
+        nx, ny, m = 1024, 256, 20
+        g = ref.UniformGrid2(nx, ny)
+        ens = ref.Ensemble2(g, tuple(ref.VectorField2(g, a, b)
+                                     for a, b in _config1_members_host(nx, ny, m, 101)))
+        pc = ref.ParallelConfig(threads=threads)
+        from divuq.lcp import _tail_probs
+
+        def work(par=True):
+            model = ref.fit_gaussian(ens)
+            f = ref.propagate_divergence(model, pc if par else None)
+            _tail_probs(f.mu, f.sigma, 0.0)
+
+        return (work, g.n_vertices, "grid points/s",
+                f"reference fit_gaussian (M=20) + propagate_divergence(ParallelConfig(threads="
+                f"{threads})) + _tail_probs P(div>0), config-1 recipe on 1024x256 (a quarter of "
+                "the 1024^2 grid)", "reference")
+    if cid == 2:
+        mu_u, mu_v, s_u, s_v = configs.config2_model()
+        g = ref.UniformGrid2(256, 256)
+        model = ref.GaussianVectorField(g, mu_u, mu_v, s_u, s_v)
+        n = 100
+        cfgm = ref.McConfig(n, seed=2024)
+
+        def work(par=True):
+            ref.mc_divergence(model, cfgm)
+
+        return (work, g.n_vertices * n, "vertex-samples/s",
+                "reference mc_divergence (numba RNG, numpy stencil, Welford) on the config-2 256^2 "
+                f"model with N={n} samples (of 2000)", "reference")
+    if cid == 3:
+        work, n, _ = propagate3d_thunk(512, 512, 32, threads=threads)
+        return (work, n, "grid points/s",
+                f"oracle 3D propagation + P(div>0) + P(div<0), fp64, on a 512x512x32 sub-volume of "
+                f"config 3, {threads} threads (no 3D reference code exists)", "port")
+    work, n, _ = ensemble3d_thunk(1024, 1024, 2, 16, threads=threads)
+    return (work, n, "grid points/s",
+            f"oracle fit_gaussian (M=16) + 3D propagation + P(div>+-0.1), fp64, on 1024x1024x2 of "
+            f"config 4, {threads} threads (no 3D reference code exists)", "port")
+
+
+def time_leg(cid, seconds=10.0, threads=None):
+    """The cpu_baseline dict of bench.py: one warm-up, then repeated calls for
+    ~seconds (the reference's bench() protocol, parallel.py:119-129).  For the
+    2D configs with a ParallelConfig seam (0, 1) both the threaded and the
+    serial reference path are timed and the FASTER one is the baseline (at
+    128^2 the reference's thread pool costs more than the work)."""
+    threads = threads or os.cpu_count() or 1
+    work, units, unit, sample, kind = cpu_leg(cid, threads)
+    v, _, runs = rate((work, units, threads), seconds=seconds)
+    out = {"value": v, "unit": unit, "cores": threads, "kind": kind,
+           "sample": sample + f", {runs} timed runs after 1 warm-up"}
+    if cid in (0, 1):   # the serial path too (ParallelConfig omitted)
+        sv, _, sruns = rate((lambda: work(False), units, 1), seconds=min(seconds, 5.0))
+        out["threaded_value"], out["serial_value"] = v, sv
+        if sv > v:
+            out.update(value=sv, cores=1,
+                       sample=out["sample"] + f"; the serial path (config=None, {sruns} runs) is "
+                              "faster and is the baseline value")
+    return out

@@ -83,7 +83,9 @@ __device__ __forceinline__ float erfc_abs(float x) {
   const float lo = fmaf(a, a, -s);  // a*a - s exactly
   float y = __fmul_rn(__fmul_rn(p, r), expf(-s));
   y = fmaf(y, -lo, y);              // * exp(-lo) ~ (1 - lo)
-  return a > 10.0546875f ? 0.0f : y;  // fp32 erfc underflows past here (and a = inf)
+  // fp32 erfc underflows past 10.05 (and a = inf); erfc(0) = 1 exactly (both
+  // tails 1/2 at a zero argument, as ndtr(0))
+  return a > 10.0546875f ? 0.0f : (a == 0.0f ? 1.0f : y);
 }
 
 __device__ __forceinline__ double ndtr_(double a) {

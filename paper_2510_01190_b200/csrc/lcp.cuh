@@ -79,17 +79,27 @@ __device__ __forceinline__ double erfc_abs_lcp(double x) {
   const double lo = fma(a, a, -s);   // a*a - s exactly
   double y = p * r * exp_neg_lcp(fmax(-s, -39.0));
   y = fma(y, -lo, y);                // * exp(-lo) ~ (1 - lo)
-  return a > 6.2 ? 0.0 : y;
+  // erfc(0) = 1 exactly, so a tail argument of exactly 0 gives 1/2 on both
+  // sides like ndtr(0) -- the reference's exact negation symmetry of the
+  // LCP (test_lcp.py:53-62) needs it (the fit is ~1e-15 off at 0)
+  return a > 6.2 ? 0.0 : (a == 0.0 ? 1.0 : y);
 }
 __device__ __forceinline__ float erfc_abs_lcp(float x) { return erfc_abs(x); }
 
 // (theta - mu) / sigma: fp64 by reciprocal + one Newton step + one residual
-// correction (~1 ulp; no
-// IEEE-division slow path: sigma > 0 and finite here); fp32 IEEE as before
+// correction (~1 ulp; no IEEE-division slow path: sigma > 0 and finite
+// here).  Two edges follow the reference's "overflow allowed" division
+// (lcp.py:62-65) exactly: a tiny sigma (rcp.approx.ftz flushes subnormals and
+// 1/sigma overflows below 2^-1022) takes the IEEE division, and a quotient
+// that overflows stays +-inf (the residual step would turn inf into NaN).
+// Both found by the reference's own test_lcp.py run through the drop-in hook
+// (tests/test_reference_boundary.py).
 __device__ __forceinline__ double lcp_div(double n, double d) {
+  if (d < 0x1p-1000) return __ddiv_rn(n, d);
   const double r = rcp_lcp(d);
   const double q = n * r;
-  return fma(fma(-d, q, n), r, q);   // one residual correction: ~1 ulp
+  const double c = fma(fma(-d, q, n), r, q);   // one residual correction: ~1 ulp
+  return isinf(q) ? q : c;
 }
 __device__ __forceinline__ float lcp_div(float n, float d) { return __fdiv_rn(n, d); }
 

@@ -43,24 +43,39 @@ def _req(t, name, dtype=None, numel=None):
     return t
 
 
-class _ErrWord:
-    """Device int32 validation word; raises after the call when asked."""
+def raise_for_bits(bits: int) -> None:
+    """The reference's exceptions for the kernels' validation bits
+    (grid.py:26-27 non-finite; divergence.py:34-35 / gaussian.py:28-29 sigma < 0)."""
+    if bits & 1:
+        raise ValueError("non-finite values are not allowed")
+    if bits & 2:
+        raise ValueError("sigma must be non-negative")
 
-    def __init__(self, device, enabled: bool):
-        self.t = torch.zeros(1, dtype=torch.int32, device=device) if enabled else None
+
+class _ErrWord:
+    """Device int32 validation word.  ``check=True``: a fresh word, read (one
+    sync) and raised after the call; ``check=<int32 CUDA tensor>``: the
+    kernels OR their bits into the caller's word and nothing is read back --
+    the caller checks once after many calls (``raise_for_bits``);
+    ``check=False``: no validation."""
+
+    def __init__(self, device, enabled):
+        if isinstance(enabled, torch.Tensor):
+            if enabled.dtype != torch.int32 or not enabled.is_cuda or enabled.numel() < 1:
+                raise TypeError("check: an int32 CUDA tensor (the validation word)")
+            self.t, self.deferred = enabled, True
+        else:
+            self.t = torch.zeros(1, dtype=torch.int32, device=device) if enabled else None
+            self.deferred = False
 
     @property
     def ptr(self):
         return _ptr(self.t)
 
     def raise_if_set(self):
-        if self.t is None:
+        if self.t is None or self.deferred:
             return
-        bits = int(self.t.item())
-        if bits & 1:
-            raise ValueError("non-finite values are not allowed")
-        if bits & 2:
-            raise ValueError("sigma must be non-negative")
+        raise_for_bits(int(self.t.item()))
 
 
 def _outs(like, n, names, out):

@@ -80,6 +80,20 @@ def test_lcp_reference_suite_properties(gpu, rng):
     assert np.array_equal(d.cell_crossing_probability(mus, np.zeros_like(mus), theta), crossing.astype(float))
     shrunk = d.cell_crossing_probability(mus, np.full_like(mus, 1e-300), theta)
     assert np.abs(shrunk - crossing).max() <= 1e-12
+    # subnormal / tiny sigma and quotients that overflow: the reference's
+    # "overflow allowed" division (lcp.py:62-65) -> the 0/1 limits, never NaN
+    # (regression: the reciprocal-based quotient returned NaN; found by the
+    # reference's own test_lcp.py through the drop-in hook)
+    cases = [([0.0] * 4, [0.0, 0.0, 0.0, 5e-324], 0.0),
+             ([0.0, 1.0, -1.0, 2.0], [5e-324, 1e-310, 2.2e-308, 1e-300], 0.5),
+             ([1e300, -1e300, 1e300, -1e300], [1e-10, 1e-10, 1e-300, 1e-300], 0.0),
+             ([3.0, 3.0, 3.0, 3.0], [1e-320, 1e-320, 1e-320, 1e-320], 3.0)]
+    for mu4, s4, th in cases:
+        got = d.cell_crossing_probability(np.array([mu4]), np.array([s4]), th)
+        with np.errstate(over="ignore", divide="ignore", invalid="ignore"):
+            want = ref2d.cell_crossing_probability(np.array([mu4]), np.array([s4]), th)
+        assert np.all(np.isfinite(got)) and 0.0 <= got[0] <= 1.0, (mu4, s4, th, got)
+        assert np.abs(got - want).max() <= 1e-12, (mu4, s4, th, got, want)
 
 
 @pytest.mark.gpu

