@@ -11,8 +11,9 @@ Stream contract (mirrored by csrc/mc.cu):
     key     = (seed & 0xffffffff, seed >> 32)
     counter = (vertex & 0xffffffff, vertex >> 32, sample & 0xffffffff, sample >> 32)
     r0..r3  = Philox4x32-10(counter, key)           # Salmon et al., SC'11
-    u1      = (((r1 << 32 | r0) >> 11) + 0.5) * 2^-53  # in (0, 1), like rng.py:31-34
-    u2      = (((r3 << 32 | r2) >> 11) + 0.5) * 2^-53
+    U1      = (r1 << 32 | r0) >> 12                  # top 52 bits
+    u1      = 2 - (1 + U1 * 2^-52)                    # in (0, 1]   (exact)
+    u2      = (1 + ((r3 << 32 | r2) >> 12) * 2^-52) - 1   # in [0, 1)   (exact)
     rad     = sqrt(-2 ln u1)
     z_u     = rad * cos(2 pi u2);  z_v = rad * sin(2 pi u2)
 
@@ -21,7 +22,8 @@ mc.py:106-117, but over fixed chunks of CHUNK samples so the GPU can spread the
 sample axis over thread blocks):
     chunk r = samples [r*CHUNK, min(n, (r+1)*CHUNK)), Welford in sample order
     with mean += delta * (1/count);
-    lane l (0..31) left-folds chunks l, l+32, ... with Chan's merge, then a
+    slot l (0..min(chunks, 32)-1) left-folds chunks l, l+32, ... with Chan's
+    merge (with fewer than 32 chunks every slot holds one chunk), then a
     fixed shuffle tree (offsets 16, 8, 4, 2, 1) merges the 32 lanes;
     std = sqrt(M2 / (n - 1)).
 The chunking depends on n only, so results are invariant to launch shape and
@@ -64,9 +66,11 @@ def philox4x32_10(c0, c1, c2, c3, k0, k1):
     return c0, c1, c2, c3
 
 
-def _u53(lo, hi):
+def _one_plus_u52(lo, hi):
+    """1 + (top 52 bits of hi:lo) * 2^-52 in [1, 2): the GPU builds this double
+    from the bits directly (csrc/mc.cuh one_plus_u52)."""
     x = (hi.astype(np.uint64) << np.uint64(32)) | lo.astype(np.uint64)
-    return ((x >> np.uint64(11)).astype(np.float64) + 0.5) * (2.0**-53)
+    return 1.0 + (x >> np.uint64(12)).astype(np.float64) * (2.0**-52)
 
 
 def uniforms(seed: int, vertex, sample):
@@ -82,7 +86,7 @@ def uniforms(seed: int, vertex, sample):
         np.uint32(seed & 0xFFFFFFFF),
         np.uint32((seed >> 32) & 0xFFFFFFFF),
     )
-    return _u53(r0, r1), _u53(r2, r3)
+    return 2.0 - _one_plus_u52(r0, r1), _one_plus_u52(r2, r3) - 1.0
 
 
 def normals(seed: int, vertex, sample):

@@ -1364,10 +1364,13 @@ int divuq_cell_crossing_f64(const double* mu4, const double* sigma4, int64_t n_c
   return int(cudaGetLastError());
 }
 
+int64_t mc_slots(int64_t n_samples) {   // a function of n_samples only (launch-invariant)
+  return std::min<int64_t>(32, (n_samples + kMcChunk - 1) / kMcChunk);
+}
+
 int64_t divuq_mc_scratch_bytes(int64_t nx, int64_t row_begin, int64_t row_end, int64_t n_samples) {
   if (nx < 1 || row_end <= row_begin || n_samples < 1) return 0;
-  const int64_t chunks = (n_samples + kMcChunk - 1) / kMcChunk;
-  return 2 * chunks * (row_end - row_begin) * nx * int64_t(sizeof(double));
+  return 2 * mc_slots(n_samples) * (row_end - row_begin) * nx * int64_t(sizeof(double));
 }
 
 int divuq_mc_divergence2d_f64(const double* mu_u, const double* mu_v, const double* s_u,
@@ -1384,6 +1387,7 @@ int divuq_mc_divergence2d_f64(const double* mu_u, const double* mu_v, const doub
   p.mu_u = mu_u; p.mu_v = mu_v; p.s_u = s_u; p.s_v = s_v;
   p.nx = nx; p.ny = ny; p.row_begin = row_begin; p.row_end = row_end;
   p.n_samples = n_samples; p.n_chunks = (n_samples + kMcChunk - 1) / kMcChunk;
+  p.n_slots = mc_slots(n_samples);
   p.seed = seed;
   for (int r = 0; r < 10; ++r) {  // Philox round keys: key + r * (W0, W1) mod 2^32
     p.k0[r] = uint32_t(seed) + uint32_t(r) * 0x9E3779B9u;
@@ -1392,11 +1396,12 @@ int divuq_mc_divergence2d_f64(const double* mu_u, const double* mu_v, const doub
   p.cx_in = 1.0 / (2.0 * dx); p.cx_bd = 1.0 / dx; p.cy_in = 1.0 / (2.0 * dy); p.cy_bd = 1.0 / dy;
   const int64_t nv = (row_end - row_begin) * nx;
   p.part_mean = static_cast<double*>(scratch);
-  p.part_m2 = p.part_mean + p.n_chunks * nv;
+  p.part_m2 = p.part_mean + p.n_slots * nv;
   p.out_mean = out_mean; p.out_std = out_std; p.err = err;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  dim3 grid(unsigned((nx + kMcTX - 1) / kMcTX), unsigned((row_end - row_begin + kMcTY - 1) / kMcTY),
-            unsigned(p.n_chunks));
+  const int64_t gx = (nx + kMcTX - 1) / kMcTX, gy = (row_end - row_begin + kMcTY - 1) / kMcTY;
+  if (gx > INT32_MAX || gy > 65535) return DIVUQ_EGRID;   // grid.z = slots <= 32
+  dim3 grid(unsigned(gx), unsigned(gy), unsigned(p.n_slots));
   DIVUQ_CUDA(cudaFuncSetAttribute(mc_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(sizeof(McSmem))));
   mc_chunk_kernel<<<grid, dim3(kMcTX, kMcTY), sizeof(McSmem), s>>>(p);
