@@ -31,6 +31,29 @@ def demangle(names):
     return res.stdout.splitlines()
 
 
+def ptxas_table():
+    path = os.path.join(ROOT, "paper_2510_01190_b200", "csrc", "ptxas.log")
+    if not os.path.exists(path):
+        return ["(ptxas.log absent: build with __graft_entry__.build(force=True))"]
+    out, name = [], None
+    mangled, stats = [], {}
+    for ln in open(path):
+        m = re.search(r"Compiling entry function '([^']+)'", ln)
+        if m:
+            name = m.group(1)
+            mangled.append(name)
+            stats[name] = ["", ""]
+            continue
+        if name and "spill stores" in ln:
+            stats[name][0] = ln.strip()
+        if name and "Used" in ln and "registers" in ln:
+            stats[name][1] = re.sub(r"^ptxas info\s*:\s*", "", ln.strip())
+    for m, pretty in zip(mangled, demangle(mangled)):
+        short = re.sub(r"^void |\(anonymous namespace\)::|divuq::", "", pretty).split("(")[0]
+        out.append(f"{short:60s} {stats[m][1]}; {stats[m][0]}")
+    return sorted(out)
+
+
 def main():
     sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True, check=True).stdout
     blocks = re.split(r"\n\s*Function : ", sass)[1:]
@@ -60,6 +83,9 @@ def main():
         fh.write("UTMALDG = cp.async.bulk.tensor (TMA) loads; SYNCS = mbarrier ops; "
                  "HMMA/UTC = tensor-core ops (none by design: no contraction).\n\n")
         fh.write("\n".join(sorted(lines)) + "\n")
+        fh.write("\nptxas -v (registers, spills) per function, from the same build "
+                 "(paper_2510_01190_b200/csrc/ptxas.log):\n")
+        fh.write("\n".join(ptxas_table()) + "\n")
     for family, items in fam.items():
         # keep the file small: at most 4 instantiations per family
         with open(os.path.join(OUT, f"{family}.sass"), "w") as fh:
