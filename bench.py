@@ -307,6 +307,47 @@ def run_next(args):
         cpu_thunk = (lambda: ref2d.lcp(mu_h, sg_h, 1024, 1024, 0.0), 1023 * 1023, 1)
         cpu_sample = "numpy restatement of lcp() on a 1024x1024 corner of the field, 1 thread"
         dtype = "f64"
+    elif wl == "lcpfused":   # propagate -> lcp in one pass (fused)
+        nx = ny = 4096
+        model = configs.host_model2d(nx, ny, 24, 105)
+        dm = [torch.from_numpy(a).cuda() for a in model]
+        outs = {"lcp": torch.empty((nx - 1) * (ny - 1), dtype=torch.float64, device="cuda")}
+        units = (nx - 1) * (ny - 1)
+        bpu = 8 * 4 * nx * ny / units + 8  # (mu_u, mu_v, s_u, s_v) read once per vertex + one fp64 out per cell
+        unit = "cells/s"
+        metric = ("level-crossing probability cells/sec of the divergence field, fused "
+                  "propagate_divergence -> lcp (divergence.py:48-70 + lcp.py:80-100), fp64")
+        workload = ("lcpfused: P(div crosses 0) per cell straight from the 4096^2 fp64 Gaussian (u, v) "
+                    "model, one kernel (moments not written)")
+
+        def step():
+            dev.propagate_lcp2d(*dm, nx, ny, 1.0, 1.0, 0.0, moments=False, out=outs, check=ERR)
+
+        k2o = {k: torch.empty(nx * ny, dtype=torch.float64, device="cuda") for k in ("mu", "sigma")}
+
+        def composed():
+            dev.propagate2d(*dm, nx, ny, 1.0, 1.0, 0.0, outputs=("mu", "sigma"), out=k2o, check=ERR)
+            dev.lcp2d(k2o["mu"], k2o["sigma"], nx, ny, 0.0, check=ERR)
+
+        hin = [torch.from_numpy(a).pin_memory() for a in model]
+        hout = torch.empty(units, dtype=torch.float64).pin_memory()
+
+        def e2e_call():
+            st = lib.divuq_host_propagate_lcp2d_f64(*(t.data_ptr() for t in hin), nx, ny, 1.0, 1.0, 0.0,
+                                                    None, None, hout.data_ptr(), 0)
+            assert st == 0, st
+
+        h2d, d2h = 32 * nx * ny, 8 * units
+        sub = [a[: 1024 * 1024] for a in model]
+        from oracle import ref2d
+
+        def cpu_work():
+            mu_d, sg_d = ref2d.propagate2d(*sub, 1024, 1024, 1.0, 1.0)
+            ref2d.lcp(mu_d, sg_d, 1024, 1024, 0.0)
+
+        cpu_thunk = (cpu_work, 1023 * 1023, 1)
+        cpu_sample = "numpy restatement of propagate_divergence + lcp() on a 1024x1024 corner, 1 thread"
+        dtype = "f64"
     elif wl == "gradient":
         nx = ny = 1024
         m = 20
@@ -500,10 +541,11 @@ def run_next(args):
                     "frac": achieved / peak, "traffic": committed_traffic(wl),
                     "bytes_per_unit": bpu, "units_per_launch": units, "avg_launch_ms": ms,
                     "peak_source": peak_src}
-        if wl == "redsea":   # the unfused chain on the same input, same protocol
-            roofline["note"] = ("same byte count as config 1 (+4 B/pt): its small-problem floor, "
-                                "36.1 us for a perfectly coalesced stream (profiles/r01/bwbench.txt), "
-                                "applies")
+        if wl in ("redsea", "lcpfused"):   # the unfused chain on the same input, same protocol
+            if wl == "redsea":
+                roofline["note"] = ("same byte count as config 1 (+4 B/pt): its small-problem floor, "
+                                    "36.1 us for a perfectly coalesced stream (profiles/r01/bwbench.txt), "
+                                    "applies")
             comp_ms = []
             for _ in range(args.steps):
                 flush()
@@ -565,7 +607,7 @@ def main():
     ap.add_argument("--plumbing-check", action="store_true",
                     help="multi-rank launch/rendezvous only (no GPU work): CPU test of --gpus N")
     ap.add_argument("--workload", default=None,
-                    choices=("lcp", "gradient", "ingest", "fit", "redsea"),
+                    choices=("lcp", "lcpfused", "gradient", "ingest", "fit", "redsea"),
                     help="a SURVEY 8f row instead of a BASELINE config (1 GPU, ours only)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

@@ -128,6 +128,16 @@ int divuq_lcp2d_f32(const float* mu, const float* sigma, int64_t nx, int64_t ny,
                     float* out_cells, int32_t* err_word, void* stream);
 int divuq_cell_crossing_f64(const double* mu4, const double* sigma4, int64_t n_cells,
                             double isovalue, double* out, int32_t* err_word, void* stream);
+/* propagate_divergence (divergence.py:48-70) followed by lcp (lcp.py:80-100)
+ * in ONE pass: the crossing probability of `isovalue` per cell of the
+ * divergence field of the Gaussian (u, v) model, without the (mu, sigma)
+ * round trip through HBM.  out_mu / out_sigma (optional) receive the
+ * divergence moments.  Bitwise equal to divuq_propagate2d_f64 followed by
+ * divuq_lcp2d_f64 (same arithmetic, same corner order). */
+int divuq_propagate_lcp2d_f64(const double* mu_u, const double* mu_v, const double* s_u,
+                              const double* s_v, int64_t nx, int64_t ny, double dx, double dy,
+                              double isovalue, double* out_mu, double* out_sigma, double* out_lcp,
+                              int32_t* err_word, void* stream);
 
 /* ---- velocity-magnitude-gradient prologue ---------------
  * velocity_magnitude (gaussian.py:48-50) = hypot(u, v); gradient
@@ -285,6 +295,10 @@ int divuq_host_gradient_ensemble_divergence2d_f32(const float* members, int64_t 
                                                   int device);
 int divuq_host_tail_probs_f64(const double* mu, const double* sigma, int64_t n, double theta,
                               double* out_below, double* out_above, int device);
+int divuq_host_propagate_lcp2d_f64(const double* mu_u, const double* mu_v, const double* s_u,
+                                   const double* s_v, int64_t nx, int64_t ny, double dx, double dy,
+                                   double isovalue, double* out_mu, double* out_sigma,
+                                   double* out_lcp, int device);
 int divuq_host_lcp2d_f64(const double* mu, const double* sigma, int64_t nx, int64_t ny,
                          double isovalue, double* out_cells, int device);
 int divuq_host_cell_crossing_f64(const double* mu4, const double* sigma4, int64_t n_cells,
@@ -362,6 +376,17 @@ int divuq_host_mc_divergence2d_ref_f64(const double* mu_u, const double* mu_v,
 /* mc_histogram_1d (mc.py:120-139): out_edges n_bins+1, out_counts n_bins,
  * *out_nbins = bins used (1 for the all-identical degenerate case),
  * out_values (nullable) = the raw samples. */
+/* error_metrics (mc.py:159-175): (e_m, e_sigma, sse) = (mean|est.mean - mu|,
+ * mean|est.std - sigma|, sum (est.mean - mu)^2 + sum (est.std - sigma)^2)
+ * in one launch (grid-stride partials, the last block folds them in block
+ * order: deterministic).  Device: out3 is 3 device doubles; scratch is
+ * divuq_error_metrics_scratch_bytes() bytes, zeroed once before first use. */
+int divuq_error_metrics_f64(const double* est_mean, const double* est_std, const double* mu,
+                            const double* sigma, int64_t n, double* out3, void* scratch,
+                            void* stream);
+int64_t divuq_error_metrics_scratch_bytes(void);
+int divuq_host_error_metrics_f64(const double* est_mean, const double* est_std, const double* mu,
+                                 const double* sigma, int64_t n, double* out3, int device);
 int divuq_host_mc_histogram1d_f64(const double* neighbors, double dx, double dy,
                                   int64_t n_samples, uint64_t seed, int64_t n_bins,
                                   double* out_edges, int64_t* out_counts, int64_t* out_nbins,

@@ -33,6 +33,7 @@ from .api import (
     mc_divergence,
     mc_histogram_1d,
     propagate_divergence,
+    propagate_lcp,
     propagate_with_probabilities,
     propagate_with_probabilities3d,
     set_device,
@@ -69,7 +70,8 @@ __all__ = [
     "ParallelConfig", "Propagation", "ScalarField2", "UniformGrid2", "UniformGrid3",
     "VectorField2", "cell_crossing_probability", "divergence_deterministic",
     "ensemble_divergence", "ensemble_divergence3d", "gradient_ensemble_divergence",
-    "error_metrics", "fit_gaussian", "gradient", "gradient_ensemble", "lcp", "mc_divergence",
+    "error_metrics", "fit_gaussian", "gradient", "gradient_ensemble", "lcp", "propagate_lcp",
+    "mc_divergence",
     "mc_histogram_1d", "sample_divergence_1d", "velocity_magnitude", "propagate_divergence",
     "propagate_with_probabilities", "propagate_with_probabilities3d", "set_device",
     "sink_probability", "source_probability", "stencil_distribution", "tail_probs",

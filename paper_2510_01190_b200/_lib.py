@@ -52,6 +52,11 @@ SIGNATURES = {
     "divuq_lcp2d_f32": (_int, [_p, _p, _i64, _i64, _f64, _p, _p, _p]),
     "divuq_cell_crossing_f64": (_int, [_p, _p, _i64, _f64, _p, _p, _p]),
     "divuq_host_lcp2d_f64": (_int, [_p, _p, _i64, _i64, _f64, _p, _int]),
+    "divuq_error_metrics_f64": (_int, [_p] * 4 + [_i64, _p, _p, _p]),
+    "divuq_error_metrics_scratch_bytes": (_i64, []),
+    "divuq_host_error_metrics_f64": (_int, [_p] * 4 + [_i64, _p, _int]),
+    "divuq_propagate_lcp2d_f64": (_int, [_p] * 4 + [_i64, _i64, _f64, _f64, _f64] + [_p] * 4 + [_p]),
+    "divuq_host_propagate_lcp2d_f64": (_int, [_p] * 4 + [_i64, _i64, _f64, _f64, _f64] + [_p] * 3 + [_int]),
     "divuq_host_cell_crossing_f64": (_int, [_p, _p, _i64, _f64, _p, _int]),
     "divuq_velocity_magnitude_f64": (_int, [_p, _p, _i64, _p, _p, _p]),
     "divuq_gradient2d_f64": (_int, [_p, _i64, _i64, _f64, _f64, _p, _p, _p]),

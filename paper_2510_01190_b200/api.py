@@ -256,16 +256,16 @@ def mc_histogram_1d(neighbors, spacing: tuple[float, float], config: McConfig,
 
 
 def error_metrics(estimate: McDivergenceEstimate, analytic: GaussianScalarField):
-    """(e_m, e_sigma, sse) between estimate and model (mc.py:159-175)."""
+    """(e_m, e_sigma, sse) between estimate and model (mc.py:159-175), one
+    device reduction (divuq_host_error_metrics_f64); within ~1e-15 relative of
+    numpy's pairwise sums."""
     if estimate.grid != analytic.grid:
         raise ValueError("estimate and analytic fields are on different grids")
-    dm = estimate.mean - analytic.mu
-    ds = estimate.std - analytic.sigma
-    return (
-        float(np.abs(dm).mean()),
-        float(np.abs(ds).mean()),
-        float(np.sum(dm**2) + np.sum(ds**2)),
-    )
+    out = np.empty(3)
+    _check(lib.divuq_host_error_metrics_f64(_p(estimate.mean), _p(estimate.std), _p(analytic.mu),
+                                            _p(analytic.sigma), estimate.grid.n_vertices, _p(out),
+                                            _DEVICE))
+    return float(out[0]), float(out[1]), float(out[2])
 
 
 class EnsembleDivergence(NamedTuple):
@@ -395,6 +395,20 @@ def cell_crossing_probability(mu, sigma, isovalue: float) -> np.ndarray:
     _check(lib.divuq_host_cell_crossing_f64(_p(mu), _p(sigma), out.size, float(isovalue), _p(out),
                                             _DEVICE))
     return out
+
+
+def propagate_lcp(model, isovalue: float) -> tuple[GaussianScalarField, LcpField]:
+    """propagate_divergence(model) then lcp(field, isovalue) in one fused pass
+    (divergence.py:48-70 + lcp.py:80-100): both results bitwise equal to the
+    two-call chain (and so to the reference's), without staging the
+    divergence field through host memory in between."""
+    g = model.grid
+    n = g.n_vertices
+    mu, sg, out = np.empty(n), np.empty(n), np.empty(g.n_cells)
+    _check(lib.divuq_host_propagate_lcp2d_f64(
+        _p(model.mu_u), _p(model.mu_v), _p(model.sigma_u), _p(model.sigma_v), g.nx, g.ny,
+        float(g.dx), float(g.dy), float(isovalue), _p(mu), _p(sg), _p(out), _DEVICE))
+    return GaussianScalarField(g, mu, sg), LcpField(g, isovalue, out)
 
 
 def lcp(fld: GaussianScalarField, isovalue: float, config: ParallelConfig | None = None) -> LcpField:

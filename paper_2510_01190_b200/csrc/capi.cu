@@ -1344,6 +1344,52 @@ int divuq_lcp2d_f64(const double* mu, const double* sigma, int64_t nx, int64_t n
   return int(cudaGetLastError());
 }
 
+// propagate_divergence -> lcp in one pass (lcp2d_fused_kernel); shapes the
+// TMA boxes cannot take run K2 then the LCP kernel: the same bits either way
+int divuq_propagate_lcp2d_f64(const double* mu_u, const double* mu_v, const double* s_u,
+                              const double* s_v, int64_t nx, int64_t ny, double dx, double dy,
+                              double isovalue, double* out_mu, double* out_sigma, double* out_lcp,
+                              int32_t* err, void* stream) {
+  if (int r = grid_ok(nx, ny, dx, dy)) return r;
+  if (!mu_u || !mu_v || !s_u || !s_v || !out_lcp) return DIVUQ_EINVAL;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CUtensorMap m[4];
+  const double* in[4] = {mu_u, s_u, mu_v, s_v};
+  bool tma = !env_int("DIVUQ_NO_TMA", 0) && nx % 2 == 0 && nx < (int64_t(1) << 31) &&
+             ny < (int64_t(1) << 31);
+  for (int k = 0; k < 4 && tma; ++k)
+    tma = aligned(in[k], 16) &&
+          make_map3d<double>(&m[k], in[k], nx, ny, 1, k < 2 ? LcpFused::UW : LcpFused::VW,
+                             k < 2 ? LcpFused::UH : LcpFused::VH, 0);
+  if (!tma) {
+    const int64_t n = nx * ny;
+    DevBuf scratch;
+    double* mu = out_mu;
+    double* sg = out_sigma;
+    if (!mu || !sg) {
+      DIVUQ_CUDA(scratch.alloc(size_t(2 * n) * sizeof(double), s));
+      if (!mu) mu = scratch.as<double>();
+      if (!sg) sg = scratch.as<double>() + n;
+    }
+    if (int r = propagate2d<double>(mu_u, mu_v, s_u, s_v, nx, ny, dx, dy, 0.0, mu, sg, nullptr, nullptr,
+                                    err, stream))
+      return r;
+    return divuq_lcp2d_f64(mu, sg, nx, ny, isovalue, out_lcp, err, stream);
+  }
+  LcpFusedParams p{};
+  p.nx = nx; p.ny = ny;
+  p.cx_in = 1.0 / (2.0 * dx); p.cx_bd = 1.0 / dx;   // stencils.py:48-50, fp64 on the host
+  p.cy_in = 1.0 / (2.0 * dy); p.cy_bd = 1.0 / dy;
+  p.theta = isovalue;
+  p.out_mu = out_mu; p.out_sigma = out_sigma; p.out_lcp = out_lcp; p.err = err;
+  const dim3 grid(unsigned((nx - 1 + kLcpTX - 1) / kLcpTX), unsigned((ny - 1 + kLcpTY - 1) / kLcpTY));
+  if (grid.y > 65535) return DIVUQ_EGRID;
+  DIVUQ_CUDA(cudaFuncSetAttribute(lcp2d_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(sizeof(LcpFusedSmem))));
+  lcp2d_fused_kernel<<<grid, dim3(kLcpBX, kLcpBY), sizeof(LcpFusedSmem), s>>>(m[0], m[1], m[2], m[3], p);
+  return int(cudaGetLastError());
+}
+
 int divuq_lcp2d_f32(const float* mu, const float* sigma, int64_t nx, int64_t ny, double isovalue,
                     float* out, int32_t* err, void* stream) {
   if (nx < 2 || ny < 2) return DIVUQ_EGRID;
@@ -1586,6 +1632,38 @@ int divuq_host_tail_probs_f64(const double* mu, const double* sigma, int64_t n, 
   return status;
 }
 
+int divuq_host_propagate_lcp2d_f64(const double* mu_u, const double* mu_v, const double* s_u,
+                                   const double* s_v, int64_t nx, int64_t ny, double dx, double dy,
+                                   double isovalue, double* out_mu, double* out_sigma,
+                                   double* out_lcp, int device) {
+  if (int r = grid_ok(nx, ny, dx, dy)) return r;
+  if (!mu_u || !mu_v || !s_u || !s_v || !out_lcp) return DIVUQ_EINVAL;
+  DIVUQ_CUDA(cudaSetDevice(device));
+  StreamGuard sg;
+  DIVUQ_CUDA(cached_stream(0, &sg.s));
+  const int64_t n = nx * ny, nc = (nx - 1) * (ny - 1);
+  DevBuf d;
+  DIVUQ_CUDA(d.alloc(size_t(6 * n + nc) * sizeof(double) + 256, sg.s));
+  double* din = d.as<double>();
+  double* dmu = din + 4 * n;
+  double* dsg = dmu + n;
+  double* dout = dsg + n;
+  int32_t* derr = reinterpret_cast<int32_t*>(dout + nc);
+  DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
+  const double* ins[4] = {mu_u, mu_v, s_u, s_v};
+  for (int k = 0; k < 4; ++k) DIVUQ_CUDA(h2d(din + k * n, ins[k], size_t(n) * sizeof(double), sg.s));
+  if (int r = divuq_propagate_lcp2d_f64(din, din + n, din + 2 * n, din + 3 * n, nx, ny, dx, dy, isovalue,
+                                        out_mu ? dmu : nullptr, out_sigma ? dsg : nullptr, dout, derr,
+                                        sg.s))
+    return r;
+  if (out_mu) DIVUQ_CUDA(d2h(out_mu, dmu, size_t(n) * sizeof(double), sg.s));
+  if (out_sigma) DIVUQ_CUDA(d2h(out_sigma, dsg, size_t(n) * sizeof(double), sg.s));
+  DIVUQ_CUDA(d2h(out_lcp, dout, size_t(nc) * sizeof(double), sg.s));
+  int status = 0;
+  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  return status;
+}
+
 int divuq_host_lcp2d_f64(const double* mu, const double* sigma, int64_t nx, int64_t ny,
                          double isovalue, double* out, int device) {
   if (nx < 2 || ny < 2) return DIVUQ_EGRID;
@@ -1811,6 +1889,46 @@ int divuq_host_mc_divergence2d_ref_f64(const double* mu_u, const double* mu_v, c
 // [lo - 0.5, hi + 0.5].  out_edges: n_bins + 1 doubles, out_counts: n_bins
 // int64; *out_nbins receives the bin count actually used (1 when degenerate).
 // out_values (nullable) receives the raw samples (sample_divergence_1d).
+// error_metrics (mc.py:159-175), one launch; out3 = (e_m, e_sigma, sse) on the device
+int divuq_error_metrics_f64(const double* est_mean, const double* est_std, const double* mu,
+                            const double* sigma, int64_t n, double* out3, void* scratch,
+                            void* stream) {
+  if (!est_mean || !est_std || !mu || !sigma || !out3 || !scratch || n < 1) return DIVUQ_EINVAL;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(kEmMaxBlocks, (n + 4 * kEmThreads - 1) /
+                                                                             (4 * kEmThreads)));
+  double* partials = static_cast<double*>(scratch);
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(partials + 4 * kEmMaxBlocks);
+  error_metrics_kernel<<<unsigned(blocks), kEmThreads, 0, static_cast<cudaStream_t>(stream)>>>(
+      est_mean, est_std, mu, sigma, n, partials, ticket, out3);
+  return int(cudaGetLastError());
+}
+
+int64_t divuq_error_metrics_scratch_bytes(void) {
+  return int64_t(4 * kEmMaxBlocks * sizeof(double) + 256);   // partials + ticket (zeroed once)
+}
+
+int divuq_host_error_metrics_f64(const double* est_mean, const double* est_std, const double* mu,
+                                 const double* sigma, int64_t n, double* out3, int device) {
+  if (!est_mean || !est_std || !mu || !sigma || !out3 || n < 1) return DIVUQ_EINVAL;
+  DIVUQ_CUDA(cudaSetDevice(device));
+  StreamGuard sg;
+  DIVUQ_CUDA(cached_stream(0, &sg.s));
+  const size_t sb = size_t(divuq_error_metrics_scratch_bytes());
+  DevBuf d;
+  DIVUQ_CUDA(d.alloc(size_t(4 * n + 3) * sizeof(double) + sb, sg.s));
+  double* din = d.as<double>();
+  double* dout = din + 4 * n;
+  void* scratch = dout + 3;
+  DIVUQ_CUDA(cudaMemsetAsync(scratch, 0, sb, sg.s));
+  const double* ins[4] = {est_mean, est_std, mu, sigma};
+  for (int k = 0; k < 4; ++k) DIVUQ_CUDA(h2d(din + k * n, ins[k], size_t(n) * sizeof(double), sg.s));
+  if (int r = divuq_error_metrics_f64(din, din + n, din + 2 * n, din + 3 * n, n, dout, scratch, sg.s))
+    return r;
+  DIVUQ_CUDA(cudaMemcpyAsync(out3, dout, 3 * sizeof(double), cudaMemcpyDeviceToHost, sg.s));
+  DIVUQ_CUDA(cudaStreamSynchronize(sg.s));
+  return DIVUQ_OK;
+}
+
 int divuq_host_mc_histogram1d_f64(const double* neighbors, double dx, double dy,
                                   int64_t n_samples, uint64_t seed, int64_t n_bins,
                                   double* out_edges, int64_t* out_counts, int64_t* out_nbins,

@@ -274,3 +274,123 @@ __global__ void cell_crossing_kernel(const T* __restrict__ mu4, const T* __restr
 }
 
 }  // namespace divuq
+
+namespace divuq {
+
+// ---------------------------------------------------------------------------
+// propagate_divergence -> lcp fused ("fused into the K2
+// epilogue"): the (u, v) moments of a tile's 65 x 17 vertices plus their
+// stencil halo are TMA-staged, every vertex's divergence (mu, sigma) is
+// evaluated with K2's arithmetic (StencilMath<double>: the reference order,
+// stencils.py:64-84, IEEE sqrt -- bitwise equal to propagate_divergence),
+// its tail pair with the LCP kernels' tail_pair_lcp, and the cells' crossing
+// probability with lcp.py:71-100's corner order -- so the result is bitwise
+// K2 followed by lcp2d_tma_kernel, without writing (mu, sigma) to HBM and
+// reading them back unless the caller asks for them.
+// Boxes (fp64, 16-byte aligned starts): u moments rows j0..j0+16, columns
+// i0-2..i0+65 (68 wide); v moments rows j0-1..j0+17, columns i0..i0+65
+// (66 wide).  Out-of-grid slots arrive as 0 and feed only vertices that are
+// never written and cells that are never written.
+// ---------------------------------------------------------------------------
+struct LcpFused {
+  static constexpr int UW = kLcpTX + 4, UH = kLcpTY + 1;   // u box: x from i0 - 2
+  static constexpr int VW = kLcpTX + 2, VH = kLcpTY + 3;   // v box: y from j0 - 1
+  static constexpr int W = kLcpTX + 2, H = kLcpTY + 1;     // vertex / tail tables
+  static constexpr uint32_t kBytes = uint32_t(2 * UW * UH + 2 * VW * VH) * 8u;
+};
+
+struct LcpFusedSmem {
+  alignas(128) double mu_u[LcpFused::UH][LcpFused::UW];
+  alignas(128) double s_u[LcpFused::UH][LcpFused::UW];
+  alignas(128) double mu_v[LcpFused::VH][LcpFused::VW];
+  alignas(128) double s_v[LcpFused::VH][LcpFused::VW];
+  alignas(16) double below[LcpFused::H][LcpFused::W];
+  alignas(16) double above[LcpFused::H][LcpFused::W];
+  uint64_t bar;
+};
+
+struct LcpFusedParams {
+  int64_t nx, ny;
+  double cx_in, cx_bd, cy_in, cy_bd, theta;
+  double *out_mu, *out_sigma, *out_lcp;
+  int* err;
+};
+
+__global__ void __launch_bounds__(kLcpBX * kLcpBY)
+lcp2d_fused_kernel(const __grid_constant__ CUtensorMap m_mu_u, const __grid_constant__ CUtensorMap m_s_u,
+                   const __grid_constant__ CUtensorMap m_mu_v, const __grid_constant__ CUtensorMap m_s_v,
+                   const LcpFusedParams p) {
+  using A = Arith<double>;
+  using F = LcpFused;
+  using SM = StencilMath<double, false>;
+  extern __shared__ __align__(128) unsigned char lf_smem[];
+  LcpFusedSmem& s = *reinterpret_cast<LcpFusedSmem*>(lf_smem);
+  const int tid = threadIdx.y * kLcpBX + threadIdx.x;
+  const int64_t i0 = int64_t(blockIdx.x) * kLcpTX, j0 = int64_t(blockIdx.y) * kLcpTY;
+  if (tid == 0) {
+    mbar_init(&s.bar, 1);
+    mbar_fence_init();
+    mbar_expect_tx(&s.bar, F::kBytes);
+    tma_load_3d(&s.mu_u[0][0], &m_mu_u, &s.bar, int(i0) - 2, int(j0), 0);
+    tma_load_3d(&s.s_u[0][0], &m_s_u, &s.bar, int(i0) - 2, int(j0), 0);
+    tma_load_3d(&s.mu_v[0][0], &m_mu_v, &s.bar, int(i0), int(j0) - 1, 0);
+    tma_load_3d(&s.s_v[0][0], &m_s_v, &s.bar, int(i0), int(j0) - 1, 0);
+  }
+  __syncthreads();
+  mbar_wait(&s.bar, 0);
+  const int64_t nx = p.nx, ny = p.ny;
+  int errbits = 0;
+  // vertices (x, y) of the tile, x in [0, 65), y in [0, 17): global (i0 + x, j0 + y)
+#pragma unroll 1
+  for (int v = tid; v < F::H * (kLcpTX + 1); v += kLcpBX * kLcpBY) {
+    const int y = v / (kLcpTX + 1), x = v - y * (kLcpTX + 1);
+    const int64_t i = i0 + x, j = j0 + y;
+    if (i >= nx || j >= ny) continue;
+    // stencils.py:46-51: the point itself at the global faces, c = 1/h there
+    const bool ilo = i == 0, ihi = i == nx - 1, jlo = j == 0, jhi = j == ny - 1;
+    const int ux = x + 2, vy = y + 1;            // this vertex in the u / v boxes
+    const double cx = (ilo || ihi) ? p.cx_bd : p.cx_in;
+    const double cy = (jlo || jhi) ? p.cy_bd : p.cy_in;
+    const int xl = ilo ? ux : ux - 1, xh = ihi ? ux : ux + 1;
+    const int yl = jlo ? vy : vy - 1, yh = jhi ? vy : vy + 1;
+    const double m = SM::mean(s.mu_u[y][xh], s.mu_u[y][xl], s.mu_v[yh][x], s.mu_v[yl][x], 0.0, 0.0,
+                              cx, cy, 0.0);
+    const double var = SM::var(s.s_u[y][xh], s.s_u[y][xl], s.s_v[yh][x], s.s_v[yl][x], 0.0, 0.0,
+                               cx, cy, 0.0);
+    const double sg = A::sqrt_(var);
+    // validation: every in-grid input point is some tile's vertex exactly once
+    const bool owned = (x < kLcpTX || i == nx - 1) && (y < kLcpTY || j == ny - 1);
+    if (owned) {
+      errbits |= check_value(s.mu_u[y][ux]) | check_value(s.mu_v[vy][x]) |
+                 check_sigma(s.s_u[y][ux]) | check_sigma(s.s_v[vy][x]);
+      const int64_t o = j * nx + i;
+      if (p.out_mu) p.out_mu[o] = m;
+      if (p.out_sigma) p.out_sigma[o] = sg;
+    }
+    double b, a;
+    tail_pair_lcp(m, sg, p.theta, b, a);
+    s.below[y][x] = b;
+    s.above[y][x] = a;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int ry = 0; ry < kLcpTY; ry += kLcpBY) {
+#pragma unroll
+    for (int rx = 0; rx < kLcpTX; rx += kLcpBX) {
+      const int x = threadIdx.x + rx, y = threadIdx.y + ry;
+      const int64_t ci = i0 + x, cj = j0 + y;
+      if (ci < nx - 1 && cj < ny - 1) {
+        // corners in lcp.py order: v00, v00+1, v00+nx, v00+nx+1
+        const double pb = A::mul(A::mul(A::mul(s.below[y][x], s.below[y][x + 1]), s.below[y + 1][x]),
+                                 s.below[y + 1][x + 1]);
+        const double pa = A::mul(A::mul(A::mul(s.above[y][x], s.above[y][x + 1]), s.above[y + 1][x]),
+                                 s.above[y + 1][x + 1]);
+        const double r = A::sub(1.0, A::add(pb, pa));
+        p.out_lcp[cj * (nx - 1) + ci] = r < 0.0 ? 0.0 : (r > 1.0 ? 1.0 : r);
+      }
+    }
+  }
+  flush_error(p.err, errbits);
+}
+
+}  // namespace divuq

@@ -179,6 +179,27 @@ def lcp2d(mu, sigma, nx, ny, isovalue, *, check=True):
     return out
 
 
+def propagate_lcp2d(mu_u, mu_v, s_u, s_v, nx, ny, dx=1.0, dy=1.0, isovalue=0.0, *,
+                    moments=True, out=None, check=True):
+    """propagate_divergence -> lcp fused (one pass, fp64): dict with "lcp"
+    ((ny-1)*(nx-1),) and, if ``moments``, the divergence "mu", "sigma" (N,).
+    Bitwise equal to propagate2d followed by lcp2d."""
+    n = nx * ny
+    for name, x in (("mu_u", mu_u), ("mu_v", mu_v), ("s_u", s_u), ("s_v", s_v)):
+        _req(x, name, torch.float64, n)
+    o = dict(out or {})
+    o.setdefault("lcp", torch.empty((nx - 1) * (ny - 1), dtype=torch.float64, device=mu_u.device))
+    if moments:
+        o.setdefault("mu", torch.empty(n, dtype=torch.float64, device=mu_u.device))
+        o.setdefault("sigma", torch.empty(n, dtype=torch.float64, device=mu_u.device))
+    err = _ErrWord(mu_u.device, check)
+    _check(lib.divuq_propagate_lcp2d_f64(
+        _ptr(mu_u), _ptr(mu_v), _ptr(s_u), _ptr(s_v), nx, ny, float(dx), float(dy), float(isovalue),
+        _ptr(o.get("mu")), _ptr(o.get("sigma")), _ptr(o["lcp"]), err.ptr, _stream()))
+    err.raise_if_set()
+    return o
+
+
 def gradient_ensemble2d(members, nx, ny, dx=1.0, dy=1.0, *, out=None, check=True):
     """(M, 2, nx*ny) members -> (M, 2, nx*ny) gradients of |(u, v)| (gaussian.py:61-66)."""
     _req(members, "members")
@@ -320,6 +341,26 @@ def w_moments_plane_ptr(members_ptr: int, m, nx, ny, nz_local, k, *, device, out
     return mu, sg, r
 
 
+_EM_SCRATCH = {}
+
+
+def error_metrics(est_mean, est_std, mu, sigma):
+    """error_metrics (mc.py:159-175) on the device, one launch: a (3,) fp64
+    CUDA tensor (e_m, e_sigma, sse); nothing is read back."""
+    n = est_mean.numel()
+    for name, x in (("est_mean", est_mean), ("est_std", est_std), ("mu", mu), ("sigma", sigma)):
+        _req(x, name, torch.float64, n)
+    dev = est_mean.device
+    key = (dev.index, torch.cuda.current_stream(dev).cuda_stream)
+    if key not in _EM_SCRATCH:   # zeroed once; the kernel leaves its ticket at 0
+        _EM_SCRATCH[key] = torch.zeros(lib.divuq_error_metrics_scratch_bytes(), dtype=torch.uint8,
+                                       device=dev)
+    out = torch.empty(3, dtype=torch.float64, device=dev)
+    _check(lib.divuq_error_metrics_f64(_ptr(est_mean), _ptr(est_std), _ptr(mu), _ptr(sigma), n,
+                                       _ptr(out), _ptr(_EM_SCRATCH[key]), _stream()))
+    return out
+
+
 def mc_divergence2d(mu_u, mu_v, s_u, s_v, nx, ny, dx, dy, n_samples, seed, *, rows=None,
                     out=None, check=True, stream="philox"):
     """K4: Monte Carlo estimate for rows [r0, r1) (default all).
@@ -359,9 +400,10 @@ def mc_divergence2d(mu_u, mu_v, s_u, s_v, nx, ny, dx, dy, n_samples, seed, *, ro
 
 
 __all__ = [
-    "ALL_OUTPUTS", "propagate2d", "propagate3d", "tail_probs", "lcp2d", "fit_moments",
+    "ALL_OUTPUTS", "propagate2d", "propagate3d", "tail_probs", "lcp2d", "propagate_lcp2d",
+    "fit_moments",
     "ensemble_divergence2d", "ensemble_divergence3d", "gradient_ensemble_divergence2d",
     "w_moments_plane", "w_moments_plane_ptr",
-    "mc_divergence2d",
+    "mc_divergence2d", "error_metrics",
 ]
 _ = _lib  # re-export guard

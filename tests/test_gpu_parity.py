@@ -516,6 +516,30 @@ def test_mc_dropin_fig1_error_scale(dev):
         d.mc_divergence(model, d.McConfig(1))
 
 
+@pytest.mark.parametrize("n", [1, 7, 1000, 65536, 3_000_001])
+def test_error_metrics_on_device(dev, rng, n):
+    """error_metrics (mc.py:159-175) as one device reduction: within 1e-13
+    relative of the reference's numpy formula, deterministic run to run,
+    and the drop-in keeps the reference's grid-mismatch ValueError."""
+    import paper_2510_01190_b200 as d
+
+    em, es, mu, sg = rng.normal(size=n), rng.uniform(0.5, 1.5, n), rng.normal(size=n), rng.uniform(0.5, 1.5, n)
+    t = [cu(x) for x in (em, es, mu, sg)]
+    got = dev.error_metrics(*t)
+    again = dev.error_metrics(*t)
+    assert torch.equal(got, again)
+    dm, ds = em - mu, es - sg
+    want = np.array([np.abs(dm).mean(), np.abs(ds).mean(), np.sum(dm**2) + np.sum(ds**2)])
+    assert np.allclose(host(got), want, rtol=1e-13, atol=0)
+    if n == 1000:
+        g = d.UniformGrid2(40, 25)
+        est = d.McDivergenceEstimate(g, em, es, 10)
+        an = d.GaussianScalarField(g, mu, sg)
+        assert np.allclose(d.error_metrics(est, an), want, rtol=1e-13, atol=0)
+        with pytest.raises(ValueError):
+            d.error_metrics(est, d.GaussianScalarField(d.UniformGrid2(25, 40), mu, sg))
+
+
 # --------------------------------------------------------------------------
 # validation word -> reference exceptions
 # --------------------------------------------------------------------------

@@ -113,3 +113,42 @@ def test_lcp_field_matches_cell_formula_and_device_api(gpu, rng):
                         torch.from_numpy(sg.astype(np.float32)).cuda(), nx, ny, -0.1).cpu().numpy()
         ref32 = ref2d.lcp(mu.astype(np.float32), sg.astype(np.float32), nx, ny, -0.1)
         assert np.abs(o32 - ref32).max() <= 2e-5
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(4096, 64), (130, 67), (65, 33), (2, 2), (3, 5), (64, 16), (66, 18)])
+def test_propagate_lcp_fused(gpu, rng, shape):
+    """propagate -> lcp fused (8f next #1): bitwise equal to K2 then the LCP
+    kernel, the divergence moments bitwise equal to the reference order, the
+    LCP within 1e-12 of the oracle chain (pinned bitwise to the reference's
+    lcp()); odd nx takes the two-kernel path with the same bits."""
+    import torch
+
+    from paper_2510_01190_b200 import device as dev
+
+    d = gpu
+    nx, ny = shape
+    n = nx * ny
+    a = [rng.normal(0, 2, n), rng.normal(0, 2, n), rng.uniform(0.05, 0.6, n), rng.uniform(0.05, 0.6, n)]
+    t = [torch.from_numpy(x).cuda() for x in a]
+    for iso in (0.0, -0.3):
+        f = dev.propagate_lcp2d(*t, nx, ny, 0.7, 1.3, iso)
+        k2 = dev.propagate2d(*t, nx, ny, 0.7, 1.3, 0.0, outputs=("mu", "sigma"))
+        l2 = dev.lcp2d(k2["mu"], k2["sigma"], nx, ny, iso)
+        assert torch.equal(f["mu"], k2["mu"]) and torch.equal(f["sigma"], k2["sigma"])
+        assert torch.equal(f["lcp"], l2)
+        mu, sg = ref2d.propagate2d(*a, nx, ny, 0.7, 1.3)
+        assert np.array_equal(f["mu"].cpu().numpy(), mu)
+        assert np.abs(f["lcp"].cpu().numpy() - ref2d.lcp(mu, sg, nx, ny, iso)).max() <= 1e-12
+    # moments not requested: same LCP; reference-facing entry point
+    g = dev.propagate_lcp2d(*t, nx, ny, 0.7, 1.3, 0.0, moments=False)
+    assert torch.equal(g["lcp"], dev.propagate_lcp2d(*t, nx, ny, 0.7, 1.3, 0.0)["lcp"])
+    grid = d.UniformGrid2(nx, ny, 0.7, 1.3)
+    fld, lf = d.propagate_lcp(d.GaussianVectorField(grid, *a), 0.0)
+    assert np.array_equal(fld.mu, mu) and np.array_equal(fld.sigma, sg)
+    assert np.array_equal(lf.probabilities, g["lcp"].cpu().numpy())
+    # validation: a negative sigma raises the reference's ValueError
+    bad = [x.clone() for x in t]
+    bad[2][n // 2] = -1.0
+    with pytest.raises(ValueError):
+        dev.propagate_lcp2d(*bad, nx, ny, 0.7, 1.3, 0.0)
