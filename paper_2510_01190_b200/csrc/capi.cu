@@ -753,33 +753,44 @@ int check_err_word(const int32_t* d_err, cudaStream_t s, int* status) {
   return 0;
 }
 
-// The host entry points stage through the device's default stream-ordered
-// pool.  With the pool's default release threshold (0) every call handed its
-// scratch back to the driver and the next call re-mapped it: ~40 ms per
-// 180 MB call on B200, more than the copies themselves.  Keep the pool's
-// memory cached across calls (DIVUQ_POOL_KEEP=0 restores the driver default).
-cudaError_t keep_pool_cached() {
-  static bool done[64] = {};
+// The host entry points stage through a stream-ordered pool.  With a release
+// threshold of 0 every call handed its scratch back to the driver and the
+// next call re-mapped it: ~40 ms per 180 MB call on B200, more than the
+// copies themselves.  The library keeps its OWN pool per device (the
+// process-wide default pool -- and so any other user of it -- is left
+// alone), and caps what that pool keeps cached between calls at
+// DIVUQ_POOL_KEEP_MB (default 4096 MB): larger peaks (the 3D pipelines,
+// MC scratch) go back to the driver at the next synchronisation.
+cudaError_t library_pool(cudaMemPool_t* out) {
+  static cudaMemPool_t pools[64] = {};
   static std::mutex mu;
   std::lock_guard<std::mutex> lock(mu);
   int dev = 0;
   if (cudaError_t e = cudaGetDevice(&dev)) return e;
-  if (dev >= 64 || done[dev]) return cudaSuccess;
-  done[dev] = true;
-  if (!env_int("DIVUQ_POOL_KEEP", 1)) return cudaSuccess;
-  cudaMemPool_t pool;
-  if (cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, dev)) return e;
-  uint64_t keep = ~uint64_t(0);
-  return cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  if (dev >= 64) return cudaErrorInvalidDevice;
+  if (!pools[dev]) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if (cudaError_t e = cudaMemPoolCreate(&pools[dev], &props)) return e;
+    uint64_t keep = uint64_t(std::max<int64_t>(0, env_int("DIVUQ_POOL_KEEP_MB", 4096))) << 20;
+    if (cudaError_t e = cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &keep))
+      return e;
+  }
+  *out = pools[dev];
+  return cudaSuccess;
 }
 
-// RAII device scratch from the stream-ordered pool; released with a
-// synchronising cudaFree so no stream of the call can still be using it
+// RAII device scratch from the library pool; released with a synchronising
+// cudaFree so no stream of the call can still be using it
 struct DevBuf {
   void* p = nullptr;
   cudaError_t alloc(size_t bytes, cudaStream_t st) {
-    if (cudaError_t e = keep_pool_cached()) return e;
-    return cudaMallocAsync(&p, bytes ? bytes : 1, st);
+    cudaMemPool_t pool;
+    if (cudaError_t e = library_pool(&pool)) return e;
+    return cudaMallocFromPoolAsync(&p, bytes ? bytes : 1, pool, st);
   }
   ~DevBuf() { if (p) cudaFree(p); }
   template <typename T> T* as() const { return static_cast<T*>(p); }

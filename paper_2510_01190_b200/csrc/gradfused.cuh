@@ -37,7 +37,7 @@
 #define DIVUQ_GF_MINB 4   // TMA variant (the register-staged one runs 2 CTAs / SM)
 #endif
 #ifndef DIVUQ_GF_STAGES
-#define DIVUQ_GF_STAGES 3   // 4 CTAs x 3 stages: 12 members in flight per SM
+#define DIVUQ_GF_STAGES 2   // 4 CTAs x 2 TMA stages: 8 members (92 KB) in flight per SM
 #endif
 
 namespace divuq {
@@ -55,12 +55,15 @@ constexpr int kGfSlots = 9;                                  // 4 gx + 4 gy + 1 
 constexpr int kGfS = DIVUQ_GF_STAGES;
 constexpr uint32_t kGfCompBytes = ((kGfR * 4 + 127) / 128) * 128;   // one component, aligned
 constexpr uint32_t kGfStageBytes = 2 * kGfCompBytes;
+// the magnitude tile holds (hi, lo) pairs (mag_pair, gradient.cuh): one
+// 8-byte load per differenced neighbour, double-buffered by member parity
 constexpr uint32_t kGfMagOff = kGfS * kGfStageBytes;
-constexpr uint32_t kGfBarOff = kGfMagOff + 2 * kGfR * 4;
+constexpr uint32_t kGfMagBytes = 2 * kGfR * 8;
+constexpr uint32_t kGfBarOff = kGfMagOff + kGfMagBytes;
 constexpr uint32_t kGfSmemTma = kGfBarOff + kGfS * 8;
 constexpr uint32_t kGfMomBytes = 3 * (kGfTY * (kGfTX + 2) + (kGfTY + 2) * kGfTX) * 4;   // mu, sigma, r
-static_assert(kGfMomBytes <= kGfS * kGfStageBytes || kGfS == 0, "moments alias the stages");
-constexpr uint32_t kGfSmemLdg = 2 * kGfR * 4 + kGfMomBytes;
+static_assert(kGfMomBytes <= kGfS * kGfStageBytes + kGfMagBytes, "moments alias the stages + tile");
+constexpr uint32_t kGfSmemLdg = kGfMagBytes > kGfMomBytes ? kGfMagBytes : kGfMomBytes;   // aliased
 
 struct GfParams {
   const float* members;
@@ -96,8 +99,8 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
   const int64_t nx = p.nx, ny = p.ny, N = nx * ny;
   const int tid = threadIdx.y * kGfBX + threadIdx.x;
   const int64_t i0 = int64_t(blockIdx.x) * kGfTX, j0 = int64_t(blockIdx.y) * kGfTY;
-  float* mag = reinterpret_cast<float*>(gf_smem + (TMA ? kGfMagOff : 0));
-  float* mom = reinterpret_cast<float*>(gf_smem + (TMA ? 0 : 2 * kGfR * 4));
+  float2* mag = reinterpret_cast<float2*>(gf_smem + (TMA ? kGfMagOff : 0));
+  float* mom = reinterpret_cast<float*>(gf_smem);   // after the last member: aliases stages / tile
   float* const mx_mu = mom;                                  // [kGfTY][kGfTX + 2]
   float* const mx_sg = mx_mu + kGfTY * (kGfTX + 2);
   float* const my_mu = mx_sg + kGfTY * (kGfTX + 2);          // [kGfTY + 2][kGfTX]
@@ -165,13 +168,14 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
     a_lo[s] = smem_u32(mag + g_lo[s]);
   }
   ShiftedMoments<1> acc[kGfSlots];
-  // non-finite input: u or v inf/NaN makes r = u^2 + v^2 inf/NaN and r*0 NaN
-  // (so does |u| or |v| > ~1.8e19, whose magnitude would overflow anyway)
+  // non-finite input: u or v inf/NaN makes the pair's lo NaN (fma(u, u, -u*u)
+  // is NaN for u = inf; fmax/fmin would drop a NaN, the error terms do not),
+  // and lo*0 NaN (so does |u| or |v| > ~1.8e19, whose square overflows)
   float bad = 0.0f;
   auto member = [&](int m, auto bufc, auto firstc) {
     constexpr int BUF = decltype(bufc)::value;
     constexpr bool FIRST = decltype(firstc)::value;
-    float* mg = mag + BUF * kGfR;
+    float2* mg = mag + BUF * kGfR;
     if constexpr (TMA) {
       const int st = m % kGfS;
       mbar_wait(&full[st], uint32_t(m / kGfS) & 1u);
@@ -181,10 +185,10 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
       for (int k = 0; k < kGfNL; ++k) {
         const int q = tid + k * kGfThreads;
         if (k < kGfNL - 1 || q < kGfR) {
-          const float u = su[q], v = sv[q];
-          const float r = fmaf(u, u, v * v);
-          bad = fmaf(r, 0.0f, bad);
-          mg[q] = sqrt_of_sq(r);
+          float h, l;
+          mag_pair(su[q], sv[q], h, l);
+          bad = fmaf(l, 0.0f, bad);   // lo is NaN iff u or v is not finite (its e1/e2 terms)
+          mg[q] = make_float2(h, l);
         }
       }
       __syncthreads();   // stage st consumed by every thread: refill it
@@ -200,9 +204,10 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
       for (int k = 0; k < kGfNL; ++k) {
         const int q = tid + k * kGfThreads;
         if (k < kGfNL - 1 || q < kGfR) {
-          const float r = fmaf(a[k], a[k], b[k] * b[k]);
-          bad = fmaf(r, 0.0f, bad);
-          mg[q] = sqrt_of_sq(r);
+          float h, l;
+          mag_pair(a[k], b[k], h, l);
+          bad = fmaf(l, 0.0f, bad);   // lo is NaN iff u or v is not finite (its e1/e2 terms)
+          mg[q] = make_float2(h, l);
         }
       }
       if (m + 1 < M) {   // next member's loads in flight across the barrier and the math
@@ -217,10 +222,10 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
     }
 #pragma unroll
     for (int s = 0; s < kGfSlots; ++s) {
-      float hi, lo;
-      asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(hi) : "r"(a_hi[s]), "n"(BUF * kGfR * 4));
-      asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(lo) : "r"(a_lo[s]), "n"(BUF * kGfR * 4));
-      const float g = grad_diff(hi, lo, g_c[s]);   // stencils.py:87-96
+      float hh, hl, lh, ll;   // (hi, lo) of the high and the low neighbour
+      asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+%3];" : "=f"(hh), "=f"(hl) : "r"(a_hi[s]), "n"(BUF * kGfR * 8));
+      asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+%3];" : "=f"(lh), "=f"(ll) : "r"(a_lo[s]), "n"(BUF * kGfR * 8));
+      const float g = grad_diff_pair(hh, lh, hl, ll, g_c[s]);   // stencils.py:87-96
       acc[s].add(FIRST ? 0 : 1, &g);   // member 0 sets the shift
     }
   };
@@ -235,7 +240,7 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
   }
   if (m < M) member(m, B1{}, NotFirst{});
   const int errbits = bad == bad ? 0 : kErrNonFinite;
-  if constexpr (TMA) __syncthreads();   // the moments alias the stages
+  __syncthreads();   // the moments alias the stages and the magnitude tile
   float g_mu[kGfSlots], g_sg[kGfSlots];
 #pragma unroll
   for (int s = 0; s < kGfSlots; ++s) {

@@ -28,6 +28,29 @@ template <> __device__ __forceinline__ float hypot_(float a, float b) {
   return sqrt_of_sq(fmaf(a, a, b * b));
 }
 
+// fp32 magnitude as a (hi, lo) pair.  Differencing fp32-rounded magnitudes
+// loses ~ulp(|v|) per member (|v| ~ 110 at the config-1 vortex against
+// gradient noise ~0.01), which moved the Red Sea chain's P maps by ~1e-4;
+// with the pair the gradient is c * ((H.hi - L.hi) + (H.lo - L.lo)) and the
+// chain meets the fp32 probability bar against the fp64 oracle.
+//   s = u^2 + v^2 with its exact rounding errors (two FMA products, Fast2Sum),
+//   hi = s * rsqrt(s), lo = (s + err - hi^2) / (2 hi)  (bf16-exact: the
+//   fused kernel keeps it in 16 bits; every fp32 path rounds it the same).
+__device__ __forceinline__ void mag_pair(float u, float v, float& hi, float& lo) {
+  const float p1 = __fmul_rn(u, u), p2 = __fmul_rn(v, v);
+  const float e1 = fmaf(u, u, -p1), e2 = fmaf(v, v, -p2);
+  const float a = fmaxf(p1, p2), b = fminf(p1, p2);
+  const float s = __fadd_rn(a, b);
+  const float es = __fsub_rn(b, __fsub_rn(s, a));   // Fast2Sum (a >= b >= 0): exact
+  const float rs = rsqrt_approx(fmaxf(s, 1.17549435e-38f));
+  hi = __fmul_rn(s, rs);
+  const float E = __fadd_rn(fmaf(-hi, hi, s), __fadd_rn(es, __fadd_rn(e1, e2)));
+  lo = bf16_round(__fmul_rn(E, __fmul_rn(0.5f, rs)));
+}
+__device__ __forceinline__ float grad_diff_pair(float h_hi, float l_hi, float h_lo, float l_lo, float c) {
+  return __fmul_rn(c, __fadd_rn(__fsub_rn(h_hi, l_hi), __fsub_rn(h_lo, l_lo)));
+}
+
 // one gradient component, stencils.py:87-96.  fp64: f[hi]*c - f[lo]*c with
 // each product rounded (the reference's order, bitwise).  fp32 (1e-5 bar):
 // c*(f[hi] - f[lo]), one rounding fewer and one instruction fewer.
@@ -71,8 +94,11 @@ __global__ void __launch_bounds__(kGrBX * kGrBY, 3)
 gradient2d_kernel(const T* __restrict__ in, int64_t members, int64_t in_mstride, int64_t nx,
                   int64_t ny, T cx_in, T cx_bd, T cy_in, T cy_bd, T* __restrict__ out,
                   int64_t out_mstride, int* err) {
+  constexpr bool PAIR = MAG && sizeof(T) == 4;   // fp32 magnitudes as (hi, lo) pairs
   __shared__ T f[kGrTY + 2][kGrTX + 2];
+  __shared__ T flo_[PAIR ? kGrTY + 2 : 1][PAIR ? kGrTX + 2 : 1];
   T* const fl = &f[0][0];
+  T* const flo = &flo_[0][0];
   const int64_t n = nx * ny;
   const int tid = threadIdx.y * kGrBX + threadIdx.x;
   const int64_t i0 = int64_t(blockIdx.x) * kGrTX, j0 = int64_t(blockIdx.y) * kGrTY;
@@ -121,7 +147,16 @@ gradient2d_kernel(const T* __restrict__ in, int64_t members, int64_t in_mstride,
     }
 #pragma unroll
     for (int k = 0; k < kGrNQ; ++k) {
-      if (ld_st[k]) fl[tid + k * kGrBX * kGrBY] = MAG ? hypot_(a[k], b[k]) : a[k];
+      if (ld_st[k]) {
+        if constexpr (PAIR) {
+          float h, l;
+          mag_pair(a[k], b[k], h, l);
+          fl[tid + k * kGrBX * kGrBY] = h;
+          flo[tid + k * kGrBX * kGrBY] = l;
+        } else {
+          fl[tid + k * kGrBX * kGrBY] = MAG ? hypot_(a[k], b[k]) : a[k];
+        }
+      }
       errbits |= check_value(a[k]);
       if constexpr (MAG) errbits |= check_value(b[k]);
     }
@@ -130,8 +165,13 @@ gradient2d_kernel(const T* __restrict__ in, int64_t members, int64_t in_mstride,
 #pragma unroll
     for (int e = 0; e < kGrPY * kGrPX; ++e) {
       if (o_off[e] < 0) continue;
-      dst[o_off[e]] = grad_diff(fl[o_xh[e]], fl[o_xl[e]], o_cx[e]);
-      dst[n + o_off[e]] = grad_diff(fl[o_yh[e]], fl[o_yl[e]], o_cy[e]);
+      if constexpr (PAIR) {
+        dst[o_off[e]] = grad_diff_pair(fl[o_xh[e]], fl[o_xl[e]], flo[o_xh[e]], flo[o_xl[e]], o_cx[e]);
+        dst[n + o_off[e]] = grad_diff_pair(fl[o_yh[e]], fl[o_yl[e]], flo[o_yh[e]], flo[o_yl[e]], o_cy[e]);
+      } else {
+        dst[o_off[e]] = grad_diff(fl[o_xh[e]], fl[o_xl[e]], o_cx[e]);
+        dst[n + o_off[e]] = grad_diff(fl[o_yh[e]], fl[o_yl[e]], o_cy[e]);
+      }
     }
     __syncthreads();
   }
@@ -155,7 +195,8 @@ struct GrTma {
   static constexpr uint32_t COMP = ((R * sizeof(T) + 127) / 128) * 128;
   static constexpr uint32_t STAGE = 2 * COMP;
   static constexpr uint32_t MAG = S * STAGE;
-  static constexpr uint32_t BAR = MAG + 2 * R * sizeof(T);
+  static constexpr uint32_t LO = MAG + 2 * R * sizeof(T);      // fp32: the pairs' lo parts
+  static constexpr uint32_t BAR = LO + (sizeof(T) == 4 ? 2 * R * sizeof(T) : 0);
   static constexpr uint32_t SMEM = BAR + S * 8;
   static constexpr int MINB = sizeof(T) == 8 ? 2 : 4;
 };
@@ -167,7 +208,9 @@ gradient_tma_kernel(const __grid_constant__ CUtensorMap map, int64_t members, in
                     int* err) {
   using G = GrTma<T>;
   extern __shared__ __align__(128) unsigned char gr_smem[];
+  constexpr bool PAIR = sizeof(T) == 4;
   T* const mag = reinterpret_cast<T*>(gr_smem + G::MAG);
+  T* const mlo = reinterpret_cast<T*>(gr_smem + G::LO);
   uint64_t* const full = reinterpret_cast<uint64_t*>(gr_smem + G::BAR);
   const int tid = threadIdx.y * kGrBX + threadIdx.x;
   const int64_t n = nx * ny;
@@ -212,13 +255,21 @@ gradient_tma_kernel(const __grid_constant__ CUtensorMap map, int64_t members, in
     const T* su = reinterpret_cast<const T*>(gr_smem + st * G::STAGE);
     const T* sv = reinterpret_cast<const T*>(gr_smem + st * G::STAGE + G::COMP);
     T* const fl = mag + (k & 1) * G::R;
+    T* const flo = mlo + (k & 1) * G::R;
 #pragma unroll
     for (int q0 = 0; q0 < G::NL; ++q0) {
       const int q = tid + q0 * kGrBX * kGrBY;
       if (q0 < G::NL - 1 || q < G::R) {
         const T u = su[q], v = sv[q];
         errbits |= check_value(u) | check_value(v);
-        fl[q] = hypot_(u, v);
+        if constexpr (PAIR) {
+          float h, l;
+          mag_pair(u, v, h, l);
+          fl[q] = h;
+          flo[q] = l;
+        } else {
+          fl[q] = hypot_(u, v);
+        }
       }
     }
     __syncthreads();   // stage st consumed by every thread: refill it
@@ -227,8 +278,13 @@ gradient_tma_kernel(const __grid_constant__ CUtensorMap map, int64_t members, in
 #pragma unroll
     for (int e = 0; e < kGrPY * kGrPX; ++e) {
       if (o_off[e] < 0) continue;
-      dst[o_off[e]] = grad_diff(fl[o_xh[e]], fl[o_xl[e]], o_cx[e]);
-      dst[n + o_off[e]] = grad_diff(fl[o_yh[e]], fl[o_yl[e]], o_cy[e]);
+      if constexpr (PAIR) {
+        dst[o_off[e]] = grad_diff_pair(fl[o_xh[e]], fl[o_xl[e]], flo[o_xh[e]], flo[o_xl[e]], o_cx[e]);
+        dst[n + o_off[e]] = grad_diff_pair(fl[o_yh[e]], fl[o_yl[e]], flo[o_yh[e]], flo[o_yl[e]], o_cy[e]);
+      } else {
+        dst[o_off[e]] = grad_diff(fl[o_xh[e]], fl[o_xl[e]], o_cx[e]);
+        dst[n + o_off[e]] = grad_diff(fl[o_yh[e]], fl[o_yl[e]], o_cy[e]);
+      }
     }
   }
   flush_error(err, errbits);

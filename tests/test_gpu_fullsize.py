@@ -263,3 +263,9 @@ def test_redsea_chain_full_size(dev):
     got_sg = fused["sigma"][: rows * nx].cpu().numpy()[keep]
     assert np.abs(got_mu - dmu[keep]).max() <= 1e-5 * np.abs(dmu[keep]).max()
     assert np.abs(got_sg - dsg[keep]).max() <= 1e-5 * np.abs(dsg[keep]).max()
+    # the fp32 probability bar vs the fp64 oracle chain: holds because the
+    # magnitudes are (hi, lo) pairs (mag_pair) -- fp32-rounded |v| ~ 110 moved
+    # P by ~2e-4 here
+    ps = ref2d.source_probability(dmu[keep], dsg[keep], 0.0)
+    got_p = fused["p_src"][: rows * nx].cpu().numpy()[keep]
+    assert np.all(np.abs(got_p - ps) <= 1e-5 * ps + 1e-6), np.abs(got_p - ps).max()
