@@ -57,8 +57,11 @@ constexpr uint32_t kGfCompBytes = ((kGfR * 4 + 127) / 128) * 128;   // one compo
 constexpr uint32_t kGfStageBytes = 2 * kGfCompBytes;
 // the magnitude tile holds (hi, lo) pairs (mag_pair, gradient.cuh): one
 // 8-byte load per differenced neighbour, double-buffered by member parity
+// (a magnitude slot per thread and pass, kGfRP = kGfNL * threads >= kGfR: the
+// region pass has no tail branch; the extra slots are never differenced)
+constexpr int kGfRP = kGfNL * kGfThreads;
 constexpr uint32_t kGfMagOff = kGfS * kGfStageBytes;
-constexpr uint32_t kGfMagBytes = 2 * kGfR * 8;
+constexpr uint32_t kGfMagBytes = 2 * kGfRP * 8;
 constexpr uint32_t kGfBarOff = kGfMagOff + kGfMagBytes;
 constexpr uint32_t kGfSmemTma = kGfBarOff + kGfS * 8;
 constexpr uint32_t kGfMomBytes = 3 * (kGfTY * (kGfTX + 2) + (kGfTY + 2) * kGfTX) * 4;   // mu, sigma, r
@@ -168,28 +171,26 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
     a_lo[s] = smem_u32(mag + g_lo[s]);
   }
   ShiftedMoments<1> acc[kGfSlots];
-  // non-finite input: u or v inf/NaN makes the pair's lo NaN (fma(u, u, -u*u)
-  // is NaN for u = inf; fmax/fmin would drop a NaN, the error terms do not),
-  // and lo*0 NaN (so does |u| or |v| > ~1.8e19, whose square overflows)
-  float bad = 0.0f;
+  // non-finite input: u or v inf/NaN makes its magnitude pair NaN (mag_pair),
+  // every gradient differencing it NaN, and so the divergence mean of some
+  // in-grid output point (every grid point is a stencil neighbour of one) --
+  // validated once per output instead of once per member and region point
+  int errbits = 0;
   auto member = [&](int m, auto bufc, auto firstc) {
     constexpr int BUF = decltype(bufc)::value;
     constexpr bool FIRST = decltype(firstc)::value;
-    float2* mg = mag + BUF * kGfR;
+    float2* mg = mag + BUF * kGfRP;
     if constexpr (TMA) {
       const int st = m % kGfS;
       mbar_wait(&full[st], uint32_t(m / kGfS) & 1u);
       const float* su = reinterpret_cast<const float*>(gf_smem + st * kGfStageBytes);
       const float* sv = reinterpret_cast<const float*>(gf_smem + st * kGfStageBytes + kGfCompBytes);
 #pragma unroll
-      for (int k = 0; k < kGfNL; ++k) {
+      for (int k = 0; k < kGfNL; ++k) {   // slots past kGfR read in-bounds garbage, never used
         const int q = tid + k * kGfThreads;
-        if (k < kGfNL - 1 || q < kGfR) {
-          float h, l;
-          mag_pair(su[q], sv[q], h, l);
-          bad = fmaf(l, 0.0f, bad);   // lo is NaN iff u or v is not finite (its e1/e2 terms)
-          mg[q] = make_float2(h, l);
-        }
+        float h, l;
+        mag_pair(su[q], sv[q], h, l);
+        mg[q] = make_float2(h, l);
       }
       __syncthreads();   // stage st consumed by every thread: refill it
       if (tid == 0 && m + kGfS < M) {
@@ -203,12 +204,9 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
 #pragma unroll
       for (int k = 0; k < kGfNL; ++k) {
         const int q = tid + k * kGfThreads;
-        if (k < kGfNL - 1 || q < kGfR) {
-          float h, l;
-          mag_pair(a[k], b[k], h, l);
-          bad = fmaf(l, 0.0f, bad);   // lo is NaN iff u or v is not finite (its e1/e2 terms)
-          mg[q] = make_float2(h, l);
-        }
+        float h, l;
+        mag_pair(a[k], b[k], h, l);
+        mg[q] = make_float2(h, l);
       }
       if (m + 1 < M) {   // next member's loads in flight across the barrier and the math
         const float* src = p.members + int64_t(m + 1) * 2 * N;
@@ -223,8 +221,8 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
 #pragma unroll
     for (int s = 0; s < kGfSlots; ++s) {
       float hh, hl, lh, ll;   // (hi, lo) of the high and the low neighbour
-      asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+%3];" : "=f"(hh), "=f"(hl) : "r"(a_hi[s]), "n"(BUF * kGfR * 8));
-      asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+%3];" : "=f"(lh), "=f"(ll) : "r"(a_lo[s]), "n"(BUF * kGfR * 8));
+      asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+%3];" : "=f"(hh), "=f"(hl) : "r"(a_hi[s]), "n"(BUF * kGfRP * 8));
+      asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+%3];" : "=f"(lh), "=f"(ll) : "r"(a_lo[s]), "n"(BUF * kGfRP * 8));
       const float g = grad_diff_pair(hh, lh, hl, ll, g_c[s]);   // stencils.py:87-96
       acc[s].add(FIRST ? 0 : 1, &g);   // member 0 sets the shift
     }
@@ -239,7 +237,6 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
     member(m + 1, B0{}, NotFirst{});
   }
   if (m < M) member(m, B1{}, NotFirst{});
-  const int errbits = bad == bad ? 0 : kErrNonFinite;
   __syncthreads();   // the moments alias the stages and the magnitude tile
   float g_mu[kGfSlots], g_sg[kGfSlots];
 #pragma unroll
@@ -273,6 +270,7 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
     const float mean = SM::mean_r(mx_mu[xh], mx_mu[xl], mx_r[xh], mx_r[xl], my_mu[yh], my_mu[yl],
                                   my_r[yh], my_r[yl], 0.0f, 0.0f, 0.0f, 0.0f, cxe, cye, 0.0f);
     const float var = SM::var(mx_sg[xh], mx_sg[xl], my_sg[yh], my_sg[yl], 0.0f, 0.0f, cxe, cye, 0.0f);
+    errbits |= check_value(mean);
     float sg, ps, pk;
     Tails<float>::eval(mean, var, p.theta, t_zero, sg, ps, pk);
     const int64_t o = j * nx + i;

@@ -34,9 +34,11 @@ template <> __device__ __forceinline__ float hypot_(float a, float b) {
 // with the pair the gradient is c * ((H.hi - L.hi) + (H.lo - L.lo)) and the
 // chain meets the fp32 probability bar against the fp64 oracle.
 //   s = u^2 + v^2 with its exact rounding errors (two FMA products, Fast2Sum),
-//   hi = s * rsqrt(s), lo = (s + err - hi^2) / (2 hi)  (bf16-exact: the
-//   fused kernel keeps it in 16 bits; every fp32 path rounds it the same).
-__device__ __forceinline__ void mag_pair(float u, float v, float& hi, float& lo) {
+//   hi = s * rsqrt(s), lo2 = 2 * lo = (s + err - hi^2) / hi  (kept doubled:
+//   one multiply fewer; grad_diff_pair halves the difference exactly).
+// A non-finite u or v makes lo2 NaN (fma(u, u, -u*u) is NaN for u = inf, and
+// the error terms keep a NaN that fmax / fmin would drop).
+__device__ __forceinline__ void mag_pair(float u, float v, float& hi, float& lo2) {
   const float p1 = __fmul_rn(u, u), p2 = __fmul_rn(v, v);
   const float e1 = fmaf(u, u, -p1), e2 = fmaf(v, v, -p2);
   const float a = fmaxf(p1, p2), b = fminf(p1, p2);
@@ -45,10 +47,11 @@ __device__ __forceinline__ void mag_pair(float u, float v, float& hi, float& lo)
   const float rs = rsqrt_approx(fmaxf(s, 1.17549435e-38f));
   hi = __fmul_rn(s, rs);
   const float E = __fadd_rn(fmaf(-hi, hi, s), __fadd_rn(es, __fadd_rn(e1, e2)));
-  lo = bf16_round(__fmul_rn(E, __fmul_rn(0.5f, rs)));
+  lo2 = __fmul_rn(E, rs);
 }
-__device__ __forceinline__ float grad_diff_pair(float h_hi, float l_hi, float h_lo, float l_lo, float c) {
-  return __fmul_rn(c, __fadd_rn(__fsub_rn(h_hi, l_hi), __fsub_rn(h_lo, l_lo)));
+// c * ((h_hi - l_hi) + (h_lo2 - l_lo2) / 2): the half is exact, one rounding
+__device__ __forceinline__ float grad_diff_pair(float h_hi, float l_hi, float h_lo2, float l_lo2, float c) {
+  return __fmul_rn(c, fmaf(0.5f, __fsub_rn(h_lo2, l_lo2), __fsub_rn(h_hi, l_hi)));
 }
 
 // one gradient component, stencils.py:87-96.  fp64: f[hi]*c - f[lo]*c with
