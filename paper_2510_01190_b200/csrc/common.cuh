@@ -44,14 +44,69 @@ template <> struct Arith<float> {
 // (ndtr switches to 0.5 + 0.5*erf(x) for |x| < sqrt(1/2), where both tails are
 // ~1/2 and the two forms agree to an ulp; dropping that branch keeps warps
 // convergent.)  Within ~1e-13 relative of scipy even at x ~ -37.
-// erfc(|x|).  fp64: libdevice erfc (~5 ulp), needed for the 1e-12 parity bar.
-// fp32: erfc(a) = exp(-a^2) * h(q) / (a + 2) with q = (a - 2)/(a + 2) and h a
+// erfc(|x|).  fp32: erfc(a) = exp(-a^2) * h(q) / (a + 2) with q = (a - 2)/(a + 2) and h a
 // degree-9 polynomial fitted offline against scipy's erfcx
 // (tools/fit_erfc.py; max relative error 3.1e-7 ~ 5 ulp in fp32 evaluation,
 // the same class as libdevice erfcf at about half the instructions: one
 // reciprocal, one exp, 9 FMA).  exp(-a^2) is corrected for the rounding of
 // a*a with one FMA so the deep tail keeps its relative accuracy.
-__device__ __forceinline__ double erfc_abs(double x) { return erfc(fabs(x)); }
+//
+// fp64 (round 2): libdevice erfc branches by range (a warp straddling the
+// ranges runs several paths) and materialises its rational coefficients with
+// UMOV pairs: the fp64 K2 was issue-bound at ~450 instructions per point
+// (ncu: 15 % UMOV, 12 % of stalls on branches).  Now branch-free like the LCP
+// kernels, but to RELATIVE accuracy over the whole normal range:
+// erfc(a) = exp(-a^2) * h(q) / (a + K), q = (a - K) / (a + K), K = 3.75, h a
+// degree-18 polynomial fitted against erfcx on [0, 26.6]
+// (tools/fit_erfc.py: fit64(3.75, 18, amax=26.6); 5.7e-15 max relative with
+// the a*a rounding corrected and exp accurate, checked against mpmath), the
+// reciprocal refined twice (2^-92), exp(-a^2) by exp_neg_rel.  erfc(a) for
+// a > 26.6 underflows below 2^-1022 (P < 1e-300: returned as 0); erfc(0) = 1.
+__constant__ double kErfcRel[19] = {
+    0x1.17884282534aap+0, -0x1.eae02d0a14626p-1, 0x1.78fecb4e7fc5cp-1, -0x1.f63dd8118e691p-2,
+    0x1.1dc271193b4a5p-2, -0x1.0e3ea225f266ep-3, 0x1.92618b2aa95e2p-5, -0x1.9ac694d9730adp-7,
+    0x1.0290567e9387bp-10, 0x1.a0b74c910b513p-11, -0x1.6d9aecf8f4edbp-12, 0x1.63539a4679492p-17,
+    0x1.3ad4a1b185870p-15, -0x1.29def7758bfbcp-17, -0x1.c6492fe76ae91p-19, 0x1.ab2c7340f5fc5p-20,
+    0x1.8466796e3554ap-22, -0x1.9136493b7ad22p-23, -0x1.cabef9fb414ddp-25};
+// e^r Taylor coefficients 1/k!, k = 0..13 (|r| <= ln2/2: truncation < 2e-16)
+__constant__ double kExpRel[14] = {
+    0x1.0000000000000p+0, 0x1.0000000000000p+0, 0x1.0000000000000p-1, 0x1.5555555555555p-3,
+    0x1.5555555555555p-5, 0x1.1111111111111p-7, 0x1.6c16c16c16c17p-10, 0x1.a01a01a01a01ap-13,
+    0x1.a01a01a01a01ap-16, 0x1.71de3a556c734p-19, 0x1.27e4fb7789f5cp-22, 0x1.ae64567f544e4p-26,
+    0x1.1eed8eff8d898p-29, 0x1.6124613a86d09p-33};
+
+// exp(t) for t in [-708, 0]: k = rint(t log2 e), r = t - k ln2 (fdlibm's hi/lo
+// split), e^r by Taylor to r^13, times 2^k built in the exponent bits (k >= -1022)
+__device__ __forceinline__ double exp_neg_rel(double t) {
+  const double y = fma(t, 0x1.71547652b82fep+0, 0x1.8p52);   // 1.5*2^52 + rint(t*log2(e))
+  const double kd = y - 0x1.8p52;
+  const int ki = __double2loint(y);
+  double r = fma(kd, -6.93147180369123816490e-01, t);
+  r = fma(kd, -1.90821492927058770002e-10, r);
+  double p = kExpRel[13];
+#pragma unroll
+  for (int k = 12; k >= 0; --k) p = fma(p, r, kExpRel[k]);
+  return p * __hiloint2double((ki + 1023) << 20, 0);
+}
+
+__device__ __forceinline__ double erfc_abs(double x) {
+  constexpr double K = 3.75;
+  const double a = fabs(x);
+  const double d = a + K;
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  r = fma(r, fma(-d, r, 1.0), r);
+  r = fma(r, fma(-d, r, 1.0), r);
+  const double q = (a - K) * r;
+  double p = kErfcRel[18];
+#pragma unroll
+  for (int k = 17; k >= 0; --k) p = fma(p, q, kErfcRel[k]);
+  const double s = a * a;
+  const double lo = fma(a, a, -s);   // a*a - s exactly
+  double y = p * r * exp_neg_rel(fmax(-s, -708.0));
+  y = fma(y, -lo, y);                // * exp(-lo) ~ (1 - lo)
+  return a > 26.6 ? 0.0 : (a == 0.0 ? 1.0 : y);
+}
 
 __device__ __forceinline__ float rcp_approx(float x) {
   float r;

@@ -1,1 +1,5 @@
-for lib in "" tools/variants/mc_u2m1.so tools/variants/mc_u4m1.so tools/variants/mc_u2m2.so; do DIVUQ_LIB_PATH=$lib timeout 300 python bench.py --config 2 --no-cpu --no-e2e --steps 20 > gpurun_out/mc.json 2>gpurun_out/mc.err || tail -3 gpurun_out/mc.err; python -c "import json;d=json.load(open('gpurun_out/mc.json'));print('$lib',d['ms_per_step'],d['roofline']['frac'])"; done
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider -x > gpurun_out/alltest.txt 2>&1
+timeout 300 python bench.py --config 3 --steps 20 --no-cpu --no-e2e > gpurun_out/c3.json 2>gpurun_out/c3.err || tail -3 gpurun_out/c3.err
+timeout 300 python bench.py --config 0 --steps 50 --no-cpu --no-e2e > gpurun_out/c0.json 2>gpurun_out/c0.err || tail -3 gpurun_out/c0.err
+python -c "import json;d=json.load(open('gpurun_out/c3.json'));print('c3',d['ms_per_step'],d['roofline']['frac'],d['fp64_variant']['ms_per_step'],d['fp64_variant']['roofline']['frac']); d=json.load(open('gpurun_out/c0.json')); print('c0', d['ms_per_step'])"
+tail -3 gpurun_out/alltest.txt
