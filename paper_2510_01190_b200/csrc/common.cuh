@@ -344,25 +344,45 @@ __device__ __forceinline__ void tail_pair(T mu, T sigma, T theta, T& below, T& a
   ndtr_pair(Arith<T>::div(Arith<T>::sub(theta, mu), sigma), below, above);
 }
 
+// n / d for d > 0 finite, branch-free: reciprocal (rcp.approx, two Newton
+// steps) and one residual correction (<= 1 ulp).  The reference divides with
+// overflow allowed (lcp.py:62-65): a tiny d (rcp.approx.ftz flushes
+// subnormals; 1/d overflows below 2^-1022) is scaled by 2^128 together with n
+// (exact), and a quotient that overflows stays +-inf (the residual step would
+// turn it into NaN).
+// (NEWTON = 1: ~2^-46 before the correction -- enough for the LCP's
+// absolute bar; the relative fp64 maps use 2)
+template <int NEWTON = 2>
+__device__ __forceinline__ double div_pos(double n, double d) {
+  const bool tiny = d < 0x1p-896;
+  const double sc = tiny ? 0x1p128 : 1.0;
+  const double dd = d * sc, nn = n * sc;
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(dd));
+#pragma unroll
+  for (int k = 0; k < NEWTON; ++k) r = fma(r, fma(-dd, r, 1.0), r);
+  const double q = nn * r;
+  const double c = fma(fma(-dd, q, nn), r, q);
+  return isinf(q) ? q : c;
+}
+
+// fp64 tails, branch-free: sigma = 0 (the step function) is selected after
+// the erfc instead of branched around (0/0 and x/0 quotients are discarded)
 __device__ __forceinline__ void Tails<double>::eval(double m, double var, double t, bool t_zero,
                                                     double& sg, double& ps, double& pk) {
   using A = Arith<double>;
-  sg = A::sqrt_(var);
-  if (sg == 0.0) {
-    ps = m <= t ? 0.0 : 1.0;
-    pk = m <= -t ? 1.0 : 0.0;
-    return;
-  }
+  sg = A::sqrt_(var);                        // IEEE: sigma bitwise equal to the reference
+  const bool z = sg == 0.0;
+  const double d = z ? 1.0 : sg;
   double b1, a1, b2, a2;
-  ndtr_pair(A::div(A::sub(t, m), sg), b1, a1);
+  ndtr_pair(div_pos(A::sub(t, m), d), b1, a1);
   if (t_zero) {  // theta = +0 and -0 give the same quotient: one erfc serves both
-    ps = a1;
-    pk = b1;
+    b2 = b1;
   } else {
-    ndtr_pair(A::div(A::sub(-t, m), sg), b2, a2);
-    ps = a1;
-    pk = b2;
+    ndtr_pair(div_pos(A::sub(-t, m), d), b2, a2);
   }
+  ps = z ? (m <= t ? 0.0 : 1.0) : a1;
+  pk = z ? (m <= -t ? 1.0 : 0.0) : b2;
 }
 
 __device__ __forceinline__ void Tails<float>::eval(float m, float var, float t, bool t_zero,

@@ -94,13 +94,7 @@ __device__ __forceinline__ float erfc_abs_lcp(float x) { return erfc_abs(x); }
 // that overflows stays +-inf (the residual step would turn inf into NaN).
 // Both found by the reference's own test_lcp.py run through the drop-in hook
 // (tests/test_reference_boundary.py).
-__device__ __forceinline__ double lcp_div(double n, double d) {
-  if (d < 0x1p-1000) return __ddiv_rn(n, d);
-  const double r = rcp_lcp(d);
-  const double q = n * r;
-  const double c = fma(fma(-d, q, n), r, q);   // one residual correction: ~1 ulp
-  return isinf(q) ? q : c;
-}
+__device__ __forceinline__ double lcp_div(double n, double d) { return div_pos<1>(n, d); }
 __device__ __forceinline__ float lcp_div(float n, float d) { return __fdiv_rn(n, d); }
 
 // tail pair of one vertex for the LCP kernels: _tail_probs semantics
