@@ -855,8 +855,9 @@ def main():
                 "avg_launch_ms": avg_k_s * 1e3, "peak_source": peak_src}
     if args.config == 2:  # fp64-ALU bound: the HBM fraction is not the bound that matters
         # fp64 flops per vertex-sample of mc_chunk_kernel, counted from the ncu
-        # SASS profile (predicated-on DFMA x2 + DMUL + DADD; profiles/r01/mc_chunk_config2*)
-        flops_vs = 108.7
+        # SASS source page (predicated-on thread instructions: DFMA x2 + DMUL +
+        # DADD; round 2 after the table sin/cos: 92.3 -- round 1 counted 108.7)
+        flops_vs = 92.3
         fp64_peak = 148 * 64 * 2 * 1.965e9 / 1e12   # vector fp64 FMA pipe, TFLOP/s at max clock
         vs_launch = cfg.n_samples * nx * ny
         achieved_tf = flops_vs * vs_launch / avg_k_s / 1e12
@@ -864,7 +865,9 @@ def main():
                     "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved_tf / fp64_peak,
                     "traffic": traffic, "flops_per_vertex_sample": flops_vs,
                     "peak_source": "148 SMs x 64 fp64 FMA/clk x 2 x 1.965 GHz (nominal; ncu: fp64 pipe ~49 % busy)",
-                    "note": "Philox + Box-Muller per vertex-sample; HBM traffic is ~48 B/vertex",
+                    "note": ("Philox + Box-Muller per vertex-sample; HBM traffic is ~48 B/vertex; the "
+                             "kernel is issue-bound: 207 thread instructions per vertex-sample (ncu), "
+                             "0.73 ms at 100 % of the issue slots"),
                     "avg_launch_ms": avg_k_s * 1e3}
     elif args.config == 0:
         roofline["note"] = "0.9 MB working set: launch/latency-bound, L2 flushed between steps"

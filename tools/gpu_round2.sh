@@ -1,4 +1,4 @@
-timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -x -k "mc or MC or config2 or smoke or philox" > gpurun_out/mctest.txt 2>&1
-timeout 300 python bench.py --config 2 --no-cpu --no-e2e --steps 20 > gpurun_out/mc.json 2>gpurun_out/mc.err || tail -3 gpurun_out/mc.err
-python -c "import json;d=json.load(open('gpurun_out/mc.json'));print('mc',d['ms_per_step'],d['roofline']['frac'])"
-tail -1 gpurun_out/mctest.txt
+ncu --set full --clock-control none --import-source on -k regex:mc_chunk -s 3 -c 1 -o gpurun_out/prof_mc python bench.py --config 2 --steps 3 --warmup 3 --no-e2e --no-cpu > gpurun_out/ncu_mc.log 2>&1
+python tools/ncu_summary.py gpurun_out/prof_mc.ncu-rep > gpurun_out/sum_mc.txt
+ncu -i gpurun_out/prof_mc.ncu-rep --page source --csv --print-source sass > gpurun_out/src_mc.csv 2>/dev/null
+rm -f gpurun_out/prof_mc.ncu-rep
