@@ -17,6 +17,7 @@
 #include "divuq1.cuh"
 #include "gradient.cuh"
 #include "gradfused.cuh"
+#include "gradmarch.cuh"
 #include "lcp.cuh"
 #include "mc.cuh"
 #include "stencil.cuh"
@@ -1258,6 +1259,67 @@ int divuq_ensemble_divergence2d_f32(const float* members, int64_t M, int64_t nx,
   return ensemble_fallback(p, 2, static_cast<cudaStream_t>(stream));
 }
 
+// K6 as a strip march (gradmarch.cuh; DIVUQ_GRADMARCH=1) when TMA applies and the rings fit:
+// returns -1 when launched, 0 when not eligible, >0 on a CUDA error
+static int try_gradmarch(const GfParams& g, cudaStream_t s) {
+  // opt-in: measured 81 us against the tiled K6's 63 us at 1024^2 x 20 (18 warps
+  // per SM with two CTA barriers per two-row step: latency-bound, 47 % issue)
+  if (env_int("DIVUQ_NO_TMA", 0) || !env_int("DIVUQ_GRADMARCH", 0)) return 0;
+  const int64_t nx = g.nx, ny = g.ny, M = g.M;
+  if (nx % 4 || !aligned(g.members, 16) || 2 * M > 256 || nx >= (int64_t(1) << 31) ||
+      ny >= (int64_t(1) << 30))
+    return 0;
+  GmParams p{};
+  p.nx = int(nx); p.ny = int(ny); p.M = int(M);
+  p.stage_bytes = uint32_t(kGmW * kGmRows * 2 * M * 4);
+  p.stage_stride = (p.stage_bytes + 127) / 128 * 128;
+  const uint32_t mag_bytes = uint32_t(kGmRing * M * kGmW * 8);
+  const uint32_t mom_bytes = uint32_t(kGmRing * sizeof(GmMomRow));
+  // 2 CTAs / SM with >= 2 stages, else 1 CTA / SM, else not eligible
+  const size_t limit = 227 * 1024;
+  int cps = 2, S = 0;
+  for (; cps >= 1; --cps) {
+    const size_t budget = limit / size_t(cps) - (cps > 1 ? 1024 : 0);
+    const size_t fixed = size_t(mag_bytes) + mom_bytes + kGmMaxStages * 8 + 256;
+    if (budget <= fixed) continue;
+    S = int(std::min<size_t>(kGmMaxStages, (budget - fixed) / p.stage_stride));
+    if (S >= 2) break;
+  }
+  if (S < 2) return 0;
+  p.S = S;
+  p.mag_off = uint32_t(S) * p.stage_stride;
+  p.mom_off = (p.mag_off + mag_bytes + 127) / 128 * 128;
+  p.bar_off = (p.mom_off + mom_bytes + 15) / 16 * 16;
+  const size_t smem = p.bar_off + kGmMaxStages * 8;
+  CUtensorMap map{};
+  if (!make_map3d<float>(&map, g.members, nx, ny, 2 * M, kGmW, kGmRows, 256)) return 0;
+  // the TMA box holds all 2M planes: make_map3d's box z is 1 -- re-encode
+  {
+    EncodeTiledFn fn = encode_tiled();
+    const cuuint64_t dims[3] = {cuuint64_t(nx), cuuint64_t(ny), cuuint64_t(2 * M)};
+    const cuuint64_t strides[2] = {cuuint64_t(nx) * 4, cuuint64_t(nx * ny) * 4};
+    const cuuint32_t box[3] = {cuuint32_t(kGmW), cuuint32_t(kGmRows), cuuint32_t(2 * M)};
+    const cuuint32_t es[3] = {1, 1, 1};
+    if (fn(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(g.members), dims, strides, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return 0;
+  }
+  p.strips = int((nx + kGmTX - 1) / kGmTX);
+  const int64_t want = std::max<int64_t>(1, int64_t(cps) * sm_count() / p.strips);
+  p.seg_rows = int(std::max<int64_t>(8, (ny + want - 1) / want));
+  p.seg_rows += p.seg_rows & 1;
+  const int64_t segs = (ny + p.seg_rows - 1) / p.seg_rows;
+  p.cx_in = g.cx_in; p.cx_bd = g.cx_bd; p.cy_in = g.cy_in; p.cy_bd = g.cy_bd; p.theta = g.theta;
+  p.out_mu = g.out_mu; p.out_sigma = g.out_sigma; p.out_psrc = g.out_psrc; p.out_psnk = g.out_psnk;
+  p.out_mom_mu = g.out_mom_mu; p.out_mom_sigma = g.out_mom_sigma;
+  p.err = g.err;
+  DIVUQ_CUDA(cudaFuncSetAttribute(gradmarch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  gradmarch_kernel<<<unsigned(int64_t(p.strips) * segs), kGmThreads, smem, s>>>(map, p);
+  if (int e = int(cudaGetLastError())) return e;
+  return -1;
+}
+
 int divuq_gradient_ensemble_divergence2d_f32(const float* members, int64_t M, int64_t nx,
                                              int64_t ny, double dx, double dy, double t,
                                              float* out_mu, float* out_sigma, float* out_p_src,
@@ -1278,6 +1340,7 @@ int divuq_gradient_ensemble_divergence2d_f32(const float* members, int64_t M, in
   p.out_mom_mu = out_mom_mu; p.out_mom_sigma = out_mom_sigma;
   p.err = err;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (int r = try_gradmarch(p, s)) return r < 0 ? 0 : r;   // -1: launched
   const dim3 grid{unsigned(tx), unsigned(ty)}, block{kGfBX, kGfBY};
   CUtensorMap map{};
   const bool tma = !env_int("DIVUQ_NO_TMA", 0) && nx % 4 == 0 && aligned(members, 16) &&

@@ -124,9 +124,10 @@ def test_gradient_ensemble_tiles_vs_oracle(d, shape):
 
 
 @pytest.mark.parametrize("shape", [(2, 2, 1.0, 1.0), (3, 70, 0.5, 0.25), (65, 17, 1.0, 2.0),
-                                   (130, 41, 0.01, 0.07), (64, 16, 1.0, 1.0), (200, 33, 0.3, 0.3)])
+                                   (130, 41, 0.01, 0.07), (64, 16, 1.0, 1.0), (200, 33, 0.3, 0.3),
+                                   (4, 3, 1.0, 1.0), (128, 300, 0.5, 0.5), (68, 2, 1.0, 1.0)])
 @pytest.mark.parametrize("m,t", [(2, 0.0), (5, 0.3), (20, 0.0)])
-def test_fused_gradient_ensemble_divergence(d, shape, m, t):
+def test_fused_gradient_ensemble_divergence(d, shape, m, t, monkeypatch):
     """K6 (velocity magnitude -> gradient -> moments -> divergence -> tails,
     one pass) == gradient_ensemble2d_f32 then ensemble_divergence2d_f32, bit
     for bit, at every tile offset; and within the fp32 bar of the fp64 oracle
@@ -146,6 +147,12 @@ def test_fused_gradient_ensemble_divergence(d, shape, m, t):
     comp = device.ensemble_divergence2d(grad, nx, ny, dx, dy, t, moments=True)
     for k in ("mu", "sigma", "p_src", "p_snk", "mom_mu", "mom_sigma"):
         assert torch.equal(fused[k], comp[k]), k
+    # the opt-in strip march (nx % 4 == 0) and the tiled K6 are the same arithmetic
+    monkeypatch.setenv("DIVUQ_GRADMARCH", "1")
+    march = device.gradient_ensemble_divergence2d(gm, nx, ny, dx, dy, t, moments=True)
+    monkeypatch.delenv("DIVUQ_GRADMARCH")
+    for k in ("mu", "sigma", "p_src", "p_snk", "mom_mu", "mom_sigma"):
+        assert torch.equal(fused[k], march[k]), k
     g64 = ref2d.gradient_ensemble(mem.astype(np.float64), nx, ny, dx, dy)
     mu_r, sg_r = ref2d.fit_moments(g64)
     dmu, dsg = ref2d.propagate2d(mu_r[0], mu_r[1], sg_r[0], sg_r[1], nx, ny, dx, dy)
