@@ -466,8 +466,9 @@ def test_mc_statistics_vs_analytic_and_reference(dev):
     mean, std = dev.mc_divergence2d(*ins, nx, ny, dx, dy, n, 5)
     mean, std = host(mean), host(std)
     s = g["an_sigma"]
-    assert np.mean(np.abs(mean - g["an_mu"]) <= 4 * s / np.sqrt(n)) >= 0.99
-    assert np.mean(np.abs(std - s) <= 4 * s / np.sqrt(2 * n)) >= 0.99
+    # SURVEY 8d's MC gate: >= 99.9 % of vertices within 4 sigma / sqrt(N)
+    assert np.mean(np.abs(mean - g["an_mu"]) <= 4 * s / np.sqrt(n)) >= 0.999
+    assert np.mean(np.abs(std - s) <= 4 * s / np.sqrt(2 * n)) >= 0.999
     assert np.mean(np.abs(mean - g["mean"]) <= 4 * np.sqrt(2) * s / np.sqrt(n)) >= 0.99
     z = (mean - g["an_mu"]) / (s / np.sqrt(n))
     assert abs(z.mean()) < 0.5 and 0.5 < z.var() < 1.6

@@ -1,14 +1,25 @@
-"""Time the drop-in (numpy in / numpy out) API on the GPU box at the sizes the
-SURVEY probed the reference at (SURVEY 8a / BASELINE.md 3), host copies included."""
+"""Time the drop-in (numpy in / numpy out) API against the unmodified
+reference (baseline/_ref) on the SAME box, same inputs, at the sizes SURVEY
+8a probed (host copies included on our side; the reference serial and with
+ParallelConfig(threads=os.cpu_count()) where it takes one).
+
+    python tools/dropin_probe.py        # on the GPU box, after build()
+"""
+import os
 import sys
 import time
 
 import numpy as np
 
-sys.path.insert(0, ".")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
 import __graft_entry__  # noqa: E402
 
 __graft_entry__.build()
+import divuq as ref  # noqa: E402  (the reference's own pip install)
+from divuq.lcp import _tail_probs  # noqa: E402
+
 import paper_2510_01190_b200 as d  # noqa: E402
 
 
@@ -22,26 +33,41 @@ def best(fn, runs=5):
     return min(ts)
 
 
+threads = os.cpu_count() or 1
 rng = np.random.default_rng(1)
-g = d.UniformGrid2(1024, 1024)
-n = g.n_vertices
-model = d.GaussianVectorField(g, rng.normal(0, 2, n), rng.normal(0, 2, n),
-                              rng.uniform(0.05, 0.6, n), rng.uniform(0.05, 0.6, n))
-members = tuple(d.VectorField2(g, rng.normal(size=n), rng.normal(size=n)) for _ in range(20))
-ens = d.Ensemble2(g, members)
-fld = d.propagate_divergence(model)
-g2 = d.UniformGrid2(256, 256)
-n2 = g2.n_vertices
-model2 = d.GaussianVectorField(g2, rng.normal(0, 2, n2), rng.normal(0, 2, n2),
-                               rng.uniform(0.05, 0.6, n2), rng.uniform(0.05, 0.6, n2))
+arrs = [rng.normal(0, 2, 1024 * 1024), rng.normal(0, 2, 1024 * 1024),
+        rng.uniform(0.05, 0.6, 1024 * 1024), rng.uniform(0.05, 0.6, 1024 * 1024)]
+mem = [(rng.normal(size=1024 * 1024), rng.normal(size=1024 * 1024)) for _ in range(20)]
+a2 = [rng.normal(0, 2, 256 * 256), rng.normal(0, 2, 256 * 256),
+      rng.uniform(0.05, 0.6, 256 * 256), rng.uniform(0.05, 0.6, 256 * 256)]
+ours = {}
+theirs = {}
+for pkg, out in ((d, ours), (ref, theirs)):
+    g = pkg.UniformGrid2(1024, 1024)
+    out["model"] = pkg.GaussianVectorField(g, *arrs)
+    out["ens"] = pkg.Ensemble2(g, tuple(pkg.VectorField2(g, u, v) for u, v in mem))
+    out["fld"] = pkg.propagate_divergence(out["model"])
+    out["model2"] = pkg.GaussianVectorField(pkg.UniformGrid2(256, 256), *a2)
+pc = ref.ParallelConfig(threads=threads)
 rows = [
-    ("propagate_divergence 1024^2 fp64", lambda: d.propagate_divergence(model), 189e-3),
-    ("fit_gaussian 1024^2 x 20", lambda: d.fit_gaussian(ens), 408e-3),
-    ("source_probability (tail map) 1024^2", lambda: d.source_probability(fld, 0.0), 89e-3),
-    ("mc_divergence 256^2 N=2000 (Philox)", lambda: d.mc_divergence(model2, d.McConfig(2000, seed=5)), 8.67),
-    ("mc_divergence 256^2 N=2000 (reference stream)",
-     lambda: d.mc_divergence(model2, d.McConfig(2000, seed=5), stream="reference"), 8.67),
+    ("propagate_divergence 1024^2 fp64", lambda: d.propagate_divergence(ours["model"]),
+     lambda: ref.propagate_divergence(theirs["model"]), lambda: ref.propagate_divergence(theirs["model"], pc)),
+    ("fit_gaussian 1024^2 x 20", lambda: d.fit_gaussian(ours["ens"]), lambda: ref.fit_gaussian(theirs["ens"]),
+     None),
+    ("P(div > 0) map 1024^2", lambda: d.source_probability(ours["fld"], 0.0),
+     lambda: _tail_probs(theirs["fld"].mu, theirs["fld"].sigma, 0.0), None),
+    ("lcp 1024^2", lambda: d.lcp(ours["fld"], 0.0), lambda: ref.lcp(theirs["fld"], 0.0),
+     lambda: ref.lcp(theirs["fld"], 0.0, pc)),
+    ("mc_divergence 256^2 N=200 (reference stream)",
+     lambda: d.mc_divergence(ours["model2"], d.McConfig(200, seed=5), stream="reference"),
+     lambda: ref.mc_divergence(theirs["model2"], ref.McConfig(200, seed=5)), None),
 ]
-for name, fn, ref_s in rows:
-    t = best(fn)
-    print(f"{name:48s} {t * 1e3:9.2f} ms   reference probe {ref_s * 1e3:9.1f} ms   x{ref_s / t:8.1f}")
+print(f"host: {threads} cores; times are the best of 5 after one warm-up")
+for name, fo, fr, fp in rows:
+    t = best(fo)
+    tr = best(fr, runs=3)
+    tp = best(fp, runs=3) if fp else None
+    tb = min(tr, tp) if tp else tr
+    print(f"{name:46s} ours {t * 1e3:9.2f} ms | reference serial {tr * 1e3:9.1f} ms"
+          + (f", {threads} threads {tp * 1e3:9.1f} ms" if tp else "")
+          + f" | x{tb / t:7.1f} vs the faster")
