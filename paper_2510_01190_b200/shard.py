@@ -194,15 +194,22 @@ def ensure_p2p(step: SlabStep, arrays: dict) -> bool:
 
 
 def propagate3d_step(step: SlabStep, fields, out, dx, dy, dz, t, check=False, sync_inputs=True,
-                     fence=True):
-    """K2 sharded step on this rank's slab tensors (fields = 6 slab tensors)."""
+                     fence=True, remap=True):
+    """K2 sharded step on this rank's slab tensors (fields = 6 slab tensors).
+
+    p2p safety defaults: ``remap`` (collective re-attach check), ``sync_inputs``
+    and ``fence`` (see the module docstring).  A caller whose slabs are neither
+    moved nor rewritten between steps (bench.py's timed loop, after one
+    ``ensure_p2p`` and one barrier) may pass all three False: the step is then
+    one kernel launch with no collective."""
     from . import device as dev
 
     plane = step.nx * step.ny
     mu_w, s_w = fields[2], fields[5]
     if step.exchange == "p2p" and step.world > 1:
         # ONE launch: the halo planes are read from the neighbours' HBM in place
-        step.attach({"mu_w": mu_w, "s_w": s_w})
+        if remap:
+            step.attach({"mu_w": mu_w, "s_w": s_w})
         if sync_inputs:
             _sync_inputs(step)
         es = mu_w.element_size()
@@ -233,7 +240,7 @@ def propagate3d_step(step: SlabStep, fields, out, dx, dy, dz, t, check=False, sy
 
 
 def ensemble3d_step(step: SlabStep, members, out, dx, dy, dz, t, check=False, sync_inputs=True,
-                    fence=True):
+                    fence=True, remap=True):
     """K3 sharded step.  nccl: the owner reduces its edge planes' w moments and
     the neighbours receive 2 planes each instead of 2*M raw member planes.
     p2p: each rank reduces its neighbours' edge planes itself, reading their
@@ -244,7 +251,8 @@ def ensemble3d_step(step: SlabStep, members, out, dx, dy, dz, t, check=False, sy
     if step.world > 1 and step.n_arrays != 3:
         raise ValueError("ensemble3d_step exchanges (mu_w, s_w, r_w): build the SlabStep with n_arrays=3")
     if step.exchange == "p2p" and step.world > 1:
-        step.attach({"members": members})
+        if remap:
+            step.attach({"members": members})
         if sync_inputs:
             _sync_inputs(step)
         m = members.shape[0]
