@@ -125,17 +125,17 @@ class SlabStep:
             self._side = torch.cuda.Stream(device=self.device)
         return self._side
 
-    def _exchange_ops(self, first, last):
+    def _exchange_ops(self, first, last, halo_lo, halo_hi):
         ops = []
         lo, hi = self.rank - 1, self.rank + 1
         if self.rank > 0:
             for a in range(self.n_arrays):
                 ops.append(dist.P2POp(dist.isend, first[a], lo, self.group))
-                ops.append(dist.P2POp(dist.irecv, self.halo_lo[a], lo, self.group))
+                ops.append(dist.P2POp(dist.irecv, halo_lo[a], lo, self.group))
         if self.rank < self.world - 1:
             for a in range(self.n_arrays):
                 ops.append(dist.P2POp(dist.isend, last[a], hi, self.group))
-                ops.append(dist.P2POp(dist.irecv, self.halo_hi[a], hi, self.group))
+                ops.append(dist.P2POp(dist.irecv, halo_hi[a], hi, self.group))
         return ops
 
     def run(self, edge_planes, compute):
@@ -146,12 +146,26 @@ class SlabStep:
             self.launches = launches
             return launches
         first, last = edge_planes()
-        reqs = dist.batch_isend_irecv(self._exchange_ops(first, last))
+        # gloo cannot move CUDA tensors (the one-device dry runs of bench.py and
+        # the tests): stage the edge and halo planes through host memory there
+        staged = (dist.get_backend(self.group) == "gloo" and first is not None
+                  and len(first) and first[0].is_cuda)
+        hlo, hhi = self.halo_lo, self.halo_hi
+        if staged:
+            first = tuple(x.cpu() for x in first)
+            last = tuple(x.cpu() for x in last)
+            hlo = tuple(torch.empty_like(x, device="cpu") for x in hlo) if hlo else None
+            hhi = tuple(torch.empty_like(x, device="cpu") for x in hhi) if hhi else None
+        reqs = dist.batch_isend_irecv(self._exchange_ops(first, last, hlo, hhi))
         # interior planes need no halo: overlap them with the exchange
         if self.nzl > 2:
             launches += compute((1, self.nzl - 1), None, None)
         for r in reqs:
             r.wait()
+        if staged:
+            for dst, src in ((self.halo_lo, hlo), (self.halo_hi, hhi)):
+                for d, s_ in zip(dst or (), src or ()):
+                    d.copy_(s_)
         launches += compute((0, 1), self.halo_lo, self.halo_hi)
         launches += compute((self.nzl - 1, self.nzl), self.halo_lo, self.halo_hi)
         self.launches = launches

@@ -35,3 +35,22 @@ def test_world_size_mismatch_fails_loudly():
              {"WORLD_SIZE": "2", "RANK": "0", "LOCAL_RANK": "0"})
     assert r.returncode != 0
     assert "WORLD_SIZE=2 but --gpus 4" in r.stderr
+
+
+import pytest
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("exchange", ["p2p", "nccl"])
+def test_bench_two_ranks_one_device_dry_run(exchange):
+    """bench.py --gpus 2 end to end on one B200 (DIVUQ_BENCH_ONE_DEVICE=1:
+    both ranks on cuda:0 over gloo; p2p through CUDA IPC, the NCCL schedule
+    with host-staged planes): both ranks run the sharded config-3 step and
+    rank 0 reports n_gpus = 2 with the exchange used."""
+    r = _run(["--gpus", "2", "--config", "3", "--steps", "2", "--warmup", "3", "--no-cpu", "--no-e2e",
+              "--no-fp64", "--exchange", exchange], {"DIVUQ_BENCH_ONE_DEVICE": "1"})
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "z-slab x2"
+    assert ("peer memory" if exchange == "p2p" else "NCCL") in line["config"]["exchange"]
+    assert "clean" in line["config"]["validation"]
