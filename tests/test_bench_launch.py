@@ -11,6 +11,8 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -35,9 +37,6 @@ def test_world_size_mismatch_fails_loudly():
              {"WORLD_SIZE": "2", "RANK": "0", "LOCAL_RANK": "0"})
     assert r.returncode != 0
     assert "WORLD_SIZE=2 but --gpus 4" in r.stderr
-
-
-import pytest
 
 
 @pytest.mark.gpu
