@@ -42,7 +42,10 @@
 
 namespace divuq {
 
-constexpr int kGfTX = 64, kGfTY = 16, kGfBX = 32, kGfBY = 8, kGfThreads = kGfBX * kGfBY;
+#ifndef DIVUQ_GF_BY
+#define DIVUQ_GF_BY 8
+#endif
+constexpr int kGfTX = 64, kGfBX = 32, kGfBY = DIVUQ_GF_BY, kGfTY = 2 * kGfBY, kGfThreads = kGfBX * kGfBY;
 // staged region: 2-point halo, x extended to 4 left / 4 right so the TMA box
 // starts on a 16-byte boundary (a start at x = i0 - 2 raises an illegal
 // instruction on sm_100a: tools/gfprobe/tmabox.cu)
