@@ -86,6 +86,39 @@ __device__ __forceinline__ double erfc_abs_lcp(double x) {
 }
 __device__ __forceinline__ float erfc_abs_lcp(float x) { return erfc_abs(x); }
 
+// erfc(a) / 2 for a = |x| >= 0: erfc_abs_lcp with the 1/2 folded into the
+// coefficients (every Horner step, product and the FMA correction are the
+// halved values exactly: bitwise 0.5 * erfc_abs_lcp(a)) and without the
+// exponent clamp -- past a = 6.2 (and for a = inf) the exp's garbage is
+// discarded by the final select, never propagated.
+__constant__ double kErfcLcpHalf[17] = {
+    0x1.12f21ddd9f5e1p-1, -0x1.c44c471baa268p-2, 0x1.2e326945de38ap-2, -0x1.3deb21416ca90p-3,
+    0x1.e995f11b16886p-5, -0x1.b78993b5e4be8p-7, -0x1.3dd3e5fc26ebfp-11, 0x1.8dae28f56a401p-10,
+    -0x1.1f7943276e395p-12, -0x1.2234c8a90349bp-13, 0x1.c350cc2d97cf3p-15, 0x1.fd736047b47bdp-17,
+    -0x1.28c763237c059p-17, -0x1.4c4280ee09a7ap-19, 0x1.9657f8bc02840p-20, 0x1.d4b67a91621acp-21,
+    0x1.2479dd117d25fp-23};
+__device__ __forceinline__ double half_erfc_lcp(double a) {
+  constexpr double K = 3.0;
+  const double r = rcp_lcp(a + K);
+  const double q = (a - K) * r;
+  double p = kErfcLcpHalf[16];
+#pragma unroll
+  for (int k = 15; k >= 0; --k) p = fma(p, q, kErfcLcpHalf[k]);
+  const double s = a * a;
+  const double lo = fma(a, a, -s);
+  double y = p * r * exp_neg_lcp(-s);
+  y = fma(y, -lo, y);
+  return a > 6.2 ? 0.0 : (a == 0.0 ? 0.5 : y);
+}
+
+// the tail argument (theta - mu) / sigma * sqrt(1/2) for the LCP kernels,
+// rounded as before (lcp_div, then the multiply): the CLI's LCP CSV must stay
+// within 1e-12 relative + 1e-15 absolute of the reference's (tests/test_cli.py),
+// which a one-Newton quotient without the residual step (~2^-46) misses
+__device__ __forceinline__ double lcp_arg(double n, double sigma) {
+  return div_pos<1>(n, sigma) * 0.70710678118654752440;
+}
+
 // (theta - mu) / sigma: fp64 by reciprocal + one Newton step + one residual
 // correction (~1 ulp; no IEEE-division slow path: sigma > 0 and finite
 // here).  Two edges follow the reference's "overflow allowed" division
@@ -99,6 +132,22 @@ __device__ __forceinline__ float lcp_div(float n, float d) { return __fdiv_rn(n,
 
 // tail pair of one vertex for the LCP kernels: _tail_probs semantics
 // (lcp.py:48-68) with the branch-free erfc above (fp32: the shared fp32 erfc)
+// fp64, branch-free: sigma = 0 (the reference's step function, lcp.py:58-61:
+// below = mu <= theta) becomes x = +inf for theta - mu >= 0 and -inf below,
+// which the erfc maps to exactly (1, 0) / (0, 1)
+__device__ __forceinline__ void tail_pair_lcp(double mu, double sigma, double theta, double& below,
+                                              double& above) {
+  const double n = theta - mu;
+  const double xs = lcp_arg(n, sigma);
+  const double x = sigma == 0.0 ? (n >= 0.0 ? __longlong_as_double(0x7ff0000000000000ll)
+                                            : __longlong_as_double(0xfff0000000000000ll))
+                                : xs;
+  const double y = half_erfc_lcp(fabs(x));
+  const double c = 1.0 - y;
+  below = x > 0.0 ? c : y;
+  above = x > 0.0 ? y : c;
+}
+
 template <typename T>
 __device__ __forceinline__ void tail_pair_lcp(T mu, T sigma, T theta, T& below, T& above) {
   using A = Arith<T>;
@@ -115,6 +164,40 @@ __device__ __forceinline__ void tail_pair_lcp(T mu, T sigma, T theta, T& below, 
 }
 
 constexpr int kLcpTX = 64, kLcpTY = 16, kLcpBX = 32, kLcpBY = 8;
+
+// max(r, 0) keeping NaN: r = 1 - (pb + pa) is never -0, and the GPU's NaN
+// is positive, so the sign bit alone says r < 0 (fp32: the plain compare)
+__device__ __forceinline__ double lcp_clip0(double r) { return __double2hiint(r) < 0 ? 0.0 : r; }
+__device__ __forceinline__ float lcp_clip0(float r) { return r < 0.0f ? 0.0f : r; }
+
+// the tile's cells from its tail tables (row pitch W): lcp.py:88-100, corners
+// v00, v00+1, v00+nx, v00+nx+1, np.prod's order.  clip(r, 0, 1): r <= 1 always
+// (1 minus a sum of products of tails in [0, 1]; the erfc fit is relative, so
+// no tail is ever below 0), so only the lower clip is evaluated; NaN passes
+// through both ways like np.clip.  Bounds and addressing in 32-bit per tile.
+template <typename T, int W>
+__device__ __forceinline__ void lcp_tile_cells(const T* below, const T* above, int64_t ci0, int64_t cj0,
+                                               int64_t nx, int64_t ny, T* __restrict__ out) {
+  using A = Arith<T>;
+  const int xl = int(min(nx - 1 - ci0, int64_t(kLcpTX))), yl = int(min(ny - 1 - cj0, int64_t(kLcpTY)));
+  const int64_t ld = nx - 1;
+  T* const o = out + cj0 * ld + ci0;
+#pragma unroll
+  for (int ry = 0; ry < kLcpTY; ry += kLcpBY) {
+#pragma unroll
+    for (int rx = 0; rx < kLcpTX; rx += kLcpBX) {
+      const int x = threadIdx.x + rx, y = threadIdx.y + ry;
+      if (x < xl && y < yl) {
+        const T* b = below + y * W + x;
+        const T* a = above + y * W + x;
+        const T pb = A::mul(A::mul(A::mul(b[0], b[1]), b[W]), b[W + 1]);
+        const T pa = A::mul(A::mul(A::mul(a[0], a[1]), a[W]), a[W + 1]);
+        const T r = A::sub(T(1), A::add(pb, pa));
+        o[int64_t(y) * ld + x] = lcp_clip0(r);
+      }
+    }
+  }
+}
 constexpr int kLcpV = (kLcpTX + 1) * (kLcpTY + 1);
 constexpr int kLcpNQ = (kLcpV + kLcpBX * kLcpBY - 1) / (kLcpBX * kLcpBY);
 
@@ -127,7 +210,7 @@ lcp2d_kernel(const T* __restrict__ mu, const T* __restrict__ sigma, int64_t nx, 
   __shared__ T above[kLcpTY + 1][kLcpTX + 1];
   const int tid = threadIdx.y * kLcpBX + threadIdx.x;
   const int64_t ci0 = int64_t(blockIdx.x) * kLcpTX, cj0 = int64_t(blockIdx.y) * kLcpTY;
-  int errbits = 0;
+  bool nonfinite = false, negative = false;   // validation flags (check_value / check_sigma)
   T* const bl = &below[0][0];
   T* const ab = &above[0][0];
   T mv[kLcpNQ], sv[kLcpNQ];
@@ -154,28 +237,16 @@ lcp2d_kernel(const T* __restrict__ mu, const T* __restrict__ sigma, int64_t nx, 
 #pragma unroll 1
   for (int v = tid; v < kLcpV; v += kLcpBX * kLcpBY) {   // own slots only: no barrier needed
     const T m = bl[v], sg = ab[v];
-    errbits |= check_value(m) | check_sigma(sg);
+    nonfinite |= !isfinite(m) | !isfinite(sg);
+    negative |= sg < T(0);
     T b, a;
     tail_pair_lcp(m, sg, theta, b, a);
     bl[v] = b;
     ab[v] = a;
   }
+  const int errbits = (nonfinite ? kErrNonFinite : 0) | (negative ? kErrNegativeSigma : 0);
   __syncthreads();
-#pragma unroll
-  for (int ry = 0; ry < kLcpTY; ry += kLcpBY) {
-#pragma unroll
-    for (int rx = 0; rx < kLcpTX; rx += kLcpBX) {
-      const int x = threadIdx.x + rx, y = threadIdx.y + ry;
-      const int64_t ci = ci0 + x, cj = cj0 + y;
-      if (ci < nx - 1 && cj < ny - 1) {
-        // corners in lcp.py order: v00, v00+1, v00+nx, v00+nx+1
-        const T pb = A::mul(A::mul(A::mul(below[y][x], below[y][x + 1]), below[y + 1][x]), below[y + 1][x + 1]);
-        const T pa = A::mul(A::mul(A::mul(above[y][x], above[y][x + 1]), above[y + 1][x]), above[y + 1][x + 1]);
-        const T r = A::sub(T(1), A::add(pb, pa));
-        out[cj * (nx - 1) + ci] = r < T(0) ? T(0) : (r > T(1) ? T(1) : r);
-      }
-    }
-  }
+  lcp_tile_cells<T, kLcpTX + 1>(&below[0][0], &above[0][0], ci0, cj0, nx, ny, out);
   flush_error(err, errbits);
 }
 
@@ -212,34 +283,22 @@ lcp2d_tma_kernel(const __grid_constant__ CUtensorMap map_mu, const __grid_consta
   }
   __syncthreads();
   mbar_wait(&bar, 0);
-  int errbits = 0;
+  bool nonfinite = false, negative = false;   // validation flags (check_value / check_sigma)
   T* const bl = &below[0][0];
   T* const ab = &above[0][0];
 #pragma unroll 1
   for (int v = tid; v < L::H * L::W; v += kLcpBX * kLcpBY) {   // own slots only: no barrier needed
     const T m = bl[v], sg = ab[v];
-    errbits |= check_value(m) | check_sigma(sg);
+    nonfinite |= !isfinite(m) | !isfinite(sg);
+    negative |= sg < T(0);
     T b, a;
     tail_pair_lcp(m, sg, theta, b, a);
     bl[v] = b;
     ab[v] = a;
   }
+  const int errbits = (nonfinite ? kErrNonFinite : 0) | (negative ? kErrNegativeSigma : 0);
   __syncthreads();
-#pragma unroll
-  for (int ry = 0; ry < kLcpTY; ry += kLcpBY) {
-#pragma unroll
-    for (int rx = 0; rx < kLcpTX; rx += kLcpBX) {
-      const int x = threadIdx.x + rx, y = threadIdx.y + ry;
-      const int64_t ci = ci0 + x, cj = cj0 + y;
-      if (ci < nx - 1 && cj < ny - 1) {
-        // corners in lcp.py order: v00, v00+1, v00+nx, v00+nx+1
-        const T pb = A::mul(A::mul(A::mul(below[y][x], below[y][x + 1]), below[y + 1][x]), below[y + 1][x + 1]);
-        const T pa = A::mul(A::mul(A::mul(above[y][x], above[y][x + 1]), above[y + 1][x]), above[y + 1][x + 1]);
-        const T r = A::sub(T(1), A::add(pb, pa));
-        out[cj * (nx - 1) + ci] = r < T(0) ? T(0) : (r > T(1) ? T(1) : r);
-      }
-    }
-  }
+  lcp_tile_cells<T, L::W>(&below[0][0], &above[0][0], ci0, cj0, nx, ny, out);
   flush_error(err, errbits);
 }
 
@@ -367,23 +426,7 @@ lcp2d_fused_kernel(const __grid_constant__ CUtensorMap m_mu_u, const __grid_cons
     s.above[y][x] = a;
   }
   __syncthreads();
-#pragma unroll
-  for (int ry = 0; ry < kLcpTY; ry += kLcpBY) {
-#pragma unroll
-    for (int rx = 0; rx < kLcpTX; rx += kLcpBX) {
-      const int x = threadIdx.x + rx, y = threadIdx.y + ry;
-      const int64_t ci = i0 + x, cj = j0 + y;
-      if (ci < nx - 1 && cj < ny - 1) {
-        // corners in lcp.py order: v00, v00+1, v00+nx, v00+nx+1
-        const double pb = A::mul(A::mul(A::mul(s.below[y][x], s.below[y][x + 1]), s.below[y + 1][x]),
-                                 s.below[y + 1][x + 1]);
-        const double pa = A::mul(A::mul(A::mul(s.above[y][x], s.above[y][x + 1]), s.above[y + 1][x]),
-                                 s.above[y + 1][x + 1]);
-        const double r = A::sub(1.0, A::add(pb, pa));
-        p.out_lcp[cj * (nx - 1) + ci] = r < 0.0 ? 0.0 : (r > 1.0 ? 1.0 : r);
-      }
-    }
-  }
+  lcp_tile_cells<double, F::W>(&s.below[0][0], &s.above[0][0], i0, j0, nx, ny, p.out_lcp);
   flush_error(p.err, errbits);
 }
 
