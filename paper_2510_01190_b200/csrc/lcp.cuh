@@ -148,6 +148,23 @@ __device__ __forceinline__ void tail_pair_lcp(double mu, double sigma, double th
   above = x > 0.0 ? y : c;
 }
 
+// the pair stored in place: the larger tail c goes to `below` when x > 0 and
+// to `above` otherwise -- the store addresses are selected (2 integer selects)
+// instead of the two fp64 values (4 FSEL)
+__device__ __forceinline__ void tail_store_lcp(double mu, double sigma, double theta, double* below,
+                                               double* above) {
+  const double n = theta - mu;
+  const double xs = lcp_arg(n, sigma);
+  const double x = sigma == 0.0 ? (n >= 0.0 ? __longlong_as_double(0x7ff0000000000000ll)
+                                            : __longlong_as_double(0xfff0000000000000ll))
+                                : xs;
+  const double y = half_erfc_lcp(fabs(x));
+  const bool pos = x > 0.0;
+  *(pos ? above : below) = y;
+  *(pos ? below : above) = 1.0 - y;
+}
+__device__ __forceinline__ void tail_store_lcp(float mu, float sigma, float theta, float* below, float* above);
+
 template <typename T>
 __device__ __forceinline__ void tail_pair_lcp(T mu, T sigma, T theta, T& below, T& above) {
   using A = Arith<T>;
@@ -163,6 +180,16 @@ __device__ __forceinline__ void tail_pair_lcp(T mu, T sigma, T theta, T& below, 
   above = x > T(0) ? y : c;
 }
 
+__device__ __forceinline__ void tail_store_lcp(float mu, float sigma, float theta, float* below, float* above) {
+  float b, a;
+  tail_pair_lcp(mu, sigma, theta, b, a);
+  *below = b;
+  *above = a;
+}
+
+#ifndef DIVUQ_LCP_MINB
+#define DIVUQ_LCP_MINB 8
+#endif
 constexpr int kLcpTX = 64, kLcpTY = 16, kLcpBX = 32, kLcpBY = 8;
 
 // max(r, 0) keeping NaN: r = 1 - (pb + pa) is never -0, and the GPU's NaN
@@ -202,7 +229,7 @@ constexpr int kLcpV = (kLcpTX + 1) * (kLcpTY + 1);
 constexpr int kLcpNQ = (kLcpV + kLcpBX * kLcpBY - 1) / (kLcpBX * kLcpBY);
 
 template <typename T>
-__global__ void __launch_bounds__(kLcpBX * kLcpBY)
+__global__ void __launch_bounds__(kLcpBX * kLcpBY, DIVUQ_LCP_MINB)
 lcp2d_kernel(const T* __restrict__ mu, const T* __restrict__ sigma, int64_t nx, int64_t ny,
              T theta, T* __restrict__ out, int* err) {
   using A = Arith<T>;
@@ -210,7 +237,7 @@ lcp2d_kernel(const T* __restrict__ mu, const T* __restrict__ sigma, int64_t nx, 
   __shared__ T above[kLcpTY + 1][kLcpTX + 1];
   const int tid = threadIdx.y * kLcpBX + threadIdx.x;
   const int64_t ci0 = int64_t(blockIdx.x) * kLcpTX, cj0 = int64_t(blockIdx.y) * kLcpTY;
-  bool nonfinite = false, negative = false;   // validation flags (check_value / check_sigma)
+  int nonfinite = 0, negative = 0;   // validation flags (check_value / check_sigma)
   T* const bl = &below[0][0];
   T* const ab = &above[0][0];
   T mv[kLcpNQ], sv[kLcpNQ];
@@ -237,12 +264,9 @@ lcp2d_kernel(const T* __restrict__ mu, const T* __restrict__ sigma, int64_t nx, 
 #pragma unroll 1
   for (int v = tid; v < kLcpV; v += kLcpBX * kLcpBY) {   // own slots only: no barrier needed
     const T m = bl[v], sg = ab[v];
-    nonfinite |= !isfinite(m) | !isfinite(sg);
-    negative |= sg < T(0);
-    T b, a;
-    tail_pair_lcp(m, sg, theta, b, a);
-    bl[v] = b;
-    ab[v] = a;
+    nonfinite |= int(!isfinite(m)) | int(!isfinite(sg));
+    negative |= int(sg < T(0));
+    tail_store_lcp(m, sg, theta, bl + v, ab + v);
   }
   const int errbits = (nonfinite ? kErrNonFinite : 0) | (negative ? kErrNegativeSigma : 0);
   __syncthreads();
@@ -264,7 +288,7 @@ struct LcpTma {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(kLcpBX * kLcpBY)
+__global__ void __launch_bounds__(kLcpBX * kLcpBY, DIVUQ_LCP_MINB)
 lcp2d_tma_kernel(const __grid_constant__ CUtensorMap map_mu, const __grid_constant__ CUtensorMap map_sg,
                  int64_t nx, int64_t ny, T theta, T* __restrict__ out, int* err) {
   using A = Arith<T>;
@@ -283,18 +307,15 @@ lcp2d_tma_kernel(const __grid_constant__ CUtensorMap map_mu, const __grid_consta
   }
   __syncthreads();
   mbar_wait(&bar, 0);
-  bool nonfinite = false, negative = false;   // validation flags (check_value / check_sigma)
+  int nonfinite = 0, negative = 0;   // validation flags (check_value / check_sigma)
   T* const bl = &below[0][0];
   T* const ab = &above[0][0];
 #pragma unroll 1
   for (int v = tid; v < L::H * L::W; v += kLcpBX * kLcpBY) {   // own slots only: no barrier needed
     const T m = bl[v], sg = ab[v];
-    nonfinite |= !isfinite(m) | !isfinite(sg);
-    negative |= sg < T(0);
-    T b, a;
-    tail_pair_lcp(m, sg, theta, b, a);
-    bl[v] = b;
-    ab[v] = a;
+    nonfinite |= int(!isfinite(m)) | int(!isfinite(sg));
+    negative |= int(sg < T(0));
+    tail_store_lcp(m, sg, theta, bl + v, ab + v);
   }
   const int errbits = (nonfinite ? kErrNonFinite : 0) | (negative ? kErrNegativeSigma : 0);
   __syncthreads();
