@@ -1,5 +1,8 @@
-"""Small invocations of every kernel family for compute-sanitizer runs
-(memcheck / racecheck / synccheck): python tools/sanitize_probe.py."""
+"""Small invocations of every kernel family: python tools/sanitize_probe.py.
+Written for compute-sanitizer runs (memcheck / racecheck / synccheck); the GPU
+pool has since closed compute-sanitizer, so it now runs plainly as an
+every-kernel smoke (odd and aligned shapes, halos, slot merges) next to the
+bounds/validation tests in tests/."""
 import sys
 
 import numpy as np
@@ -40,6 +43,19 @@ dev.mc_divergence2d(*t, nx, ny, 0.5, 0.7, 40, 3, stream="reference")
 mu, sg = cu(rng.normal(size=130 * 70)), cu(rng.uniform(0.1, 1, 130 * 70))
 dev.lcp2d(mu, sg, 130, 70, 0.0)
 dev.gradient_ensemble2d(cu(rng.normal(size=(3, 2, 130 * 70))), 130, 70)
+dev.lcp2d(cu(rng.normal(size=131 * 33)), cu(rng.uniform(0, 1, 131 * 33)), 131, 33, 0.2)   # register LCP
+dev.tail_probs(mu, sg, 0.3)
+g4 = [cu(x) for x in (rng.normal(size=130 * 70), rng.normal(size=130 * 70),
+                      rng.uniform(0, 1, 130 * 70), rng.uniform(0, 1, 130 * 70))]
+dev.propagate_lcp2d(*g4, 130, 70, 0.5, 0.7, 0.1, moments=True)               # fused LCP (round 2)
+# K6 fused Red Sea chain (TMA: nx % 4 == 0; register-staged: odd nx), fp32 members
+for nx6, ny6 in ((132, 37), (129, 37)):
+    dev.gradient_ensemble_divergence2d(cu(rng.normal(size=(6, 2, nx6 * ny6)).astype(np.float32)),
+                                       nx6, ny6, 0.5, 0.5, 0.0, moments=True)
+# MC with more chunks than slots (Chan merge across a slot's chunks), then
+# the device error_metrics reduction on its output
+em, es = dev.mc_divergence2d(*t, nx, ny, 0.5, 0.7, 129 * 40, 5)
+dev.error_metrics(em, es, t[0], t[2])
 d.mc_histogram_1d(((1.0, 0.3), (2.0, 0.2), (0.5, 0.1), (1.5, 0.4)), (1.0, 1.0), d.McConfig(5000, seed=1), 17)
 torch.cuda.synchronize()
 print("sanitize probe: ok")
