@@ -1409,7 +1409,8 @@ int divuq_lcp2d_f64(const double* mu, const double* sigma, int64_t nx, int64_t n
       nx < (int64_t(1) << 31) && ny < (int64_t(1) << 31) &&
       make_map3d<double>(&mm, mu, nx, ny, 1, LcpTma<double>::W, LcpTma<double>::H, 0) &&
       make_map3d<double>(&ms, sigma, nx, ny, 1, LcpTma<double>::W, LcpTma<double>::H, 0)) {
-    lcp2d_tma_kernel<double><<<grid, dim3(kLcpBX, kLcpBY), 0, static_cast<cudaStream_t>(stream)>>>(
+    const dim3 gt(grid.x, unsigned((ny - 1 + kLcpTYT - 1) / kLcpTYT));
+    lcp2d_tma_kernel<double><<<gt, dim3(kLcpBX, kLcpBY), 0, static_cast<cudaStream_t>(stream)>>>(
         mm, ms, nx, ny, isovalue, out, err);
     return int(cudaGetLastError());
   }
