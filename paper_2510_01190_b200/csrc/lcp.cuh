@@ -398,6 +398,51 @@ struct LcpFusedParams {
   int* err;
 };
 
+// vertices (x, y) of the tile, x in [0, 65), y in [0, 17): global (i0 + x,
+// j0 + y) -> (mu, sigma) with K2's arithmetic -> tail pair into the tables
+template <bool EDGE>
+__device__ __forceinline__ int lcpf_vertices(LcpFusedSmem& s, const LcpFusedParams& p, int tid,
+                                             int64_t i0, int64_t j0) {
+  using A = Arith<double>;
+  using F = LcpFused;
+  using SM = StencilMath<double, false>;
+  const int64_t nx = p.nx, ny = p.ny;
+  int nonfinite = 0, negative = 0;
+#pragma unroll 1
+  for (int v = tid; v < F::H * (kLcpTX + 1); v += kLcpBX * kLcpBY) {
+    const int y = v / (kLcpTX + 1), x = v - y * (kLcpTX + 1);
+    const int64_t i = i0 + x, j = j0 + y;
+    if (EDGE && (i >= nx || j >= ny)) continue;
+    // stencils.py:46-51: the point itself at the global faces, c = 1/h there
+    const bool ilo = EDGE && i == 0, ihi = EDGE && i == nx - 1;
+    const bool jlo = EDGE && j == 0, jhi = EDGE && j == ny - 1;
+    const int ux = x + 2, vy = y + 1;            // this vertex in the u / v boxes
+    const double cx = (ilo || ihi) ? p.cx_bd : p.cx_in;
+    const double cy = (jlo || jhi) ? p.cy_bd : p.cy_in;
+    const int xl = ilo ? ux : ux - 1, xh = ihi ? ux : ux + 1;
+    const int yl = jlo ? vy : vy - 1, yh = jhi ? vy : vy + 1;
+    const double m = SM::mean(s.mu_u[y][xh], s.mu_u[y][xl], s.mu_v[yh][x], s.mu_v[yl][x], 0.0, 0.0,
+                              cx, cy, 0.0);
+    const double var = SM::var(s.s_u[y][xh], s.s_u[y][xl], s.s_v[yh][x], s.s_v[yl][x], 0.0, 0.0,
+                               cx, cy, 0.0);
+    const double sg = A::sqrt_(var);
+    // validation: every in-grid input point is some tile's vertex exactly once
+    const bool owned = (x < kLcpTX || (EDGE && i == nx - 1)) && (y < kLcpTY || (EDGE && j == ny - 1));
+    if (owned) {
+      const double mu = s.mu_u[y][ux], mv = s.mu_v[vy][x], su = s.s_u[y][ux], sv = s.s_v[vy][x];
+      nonfinite |= int(!isfinite(mu)) | int(!isfinite(mv)) | int(!isfinite(su)) | int(!isfinite(sv));
+      negative |= int(su < 0.0) | int(sv < 0.0);
+      if (p.out_mu || p.out_sigma) {
+        const int64_t o = j * nx + i;
+        if (p.out_mu) p.out_mu[o] = m;
+        if (p.out_sigma) p.out_sigma[o] = sg;
+      }
+    }
+    tail_store_lcp(m, sg, p.theta, &s.below[y][x], &s.above[y][x]);
+  }
+  return (nonfinite ? kErrNonFinite : 0) | (negative ? kErrNegativeSigma : 0);
+}
+
 __global__ void __launch_bounds__(kLcpBX * kLcpBY)
 lcp2d_fused_kernel(const __grid_constant__ CUtensorMap m_mu_u, const __grid_constant__ CUtensorMap m_s_u,
                    const __grid_constant__ CUtensorMap m_mu_v, const __grid_constant__ CUtensorMap m_s_v,
@@ -421,39 +466,11 @@ lcp2d_fused_kernel(const __grid_constant__ CUtensorMap m_mu_u, const __grid_cons
   __syncthreads();
   mbar_wait(&s.bar, 0);
   const int64_t nx = p.nx, ny = p.ny;
-  int errbits = 0;
-  // vertices (x, y) of the tile, x in [0, 65), y in [0, 17): global (i0 + x, j0 + y)
-#pragma unroll 1
-  for (int v = tid; v < F::H * (kLcpTX + 1); v += kLcpBX * kLcpBY) {
-    const int y = v / (kLcpTX + 1), x = v - y * (kLcpTX + 1);
-    const int64_t i = i0 + x, j = j0 + y;
-    if (i >= nx || j >= ny) continue;
-    // stencils.py:46-51: the point itself at the global faces, c = 1/h there
-    const bool ilo = i == 0, ihi = i == nx - 1, jlo = j == 0, jhi = j == ny - 1;
-    const int ux = x + 2, vy = y + 1;            // this vertex in the u / v boxes
-    const double cx = (ilo || ihi) ? p.cx_bd : p.cx_in;
-    const double cy = (jlo || jhi) ? p.cy_bd : p.cy_in;
-    const int xl = ilo ? ux : ux - 1, xh = ihi ? ux : ux + 1;
-    const int yl = jlo ? vy : vy - 1, yh = jhi ? vy : vy + 1;
-    const double m = SM::mean(s.mu_u[y][xh], s.mu_u[y][xl], s.mu_v[yh][x], s.mu_v[yl][x], 0.0, 0.0,
-                              cx, cy, 0.0);
-    const double var = SM::var(s.s_u[y][xh], s.s_u[y][xl], s.s_v[yh][x], s.s_v[yl][x], 0.0, 0.0,
-                               cx, cy, 0.0);
-    const double sg = A::sqrt_(var);
-    // validation: every in-grid input point is some tile's vertex exactly once
-    const bool owned = (x < kLcpTX || i == nx - 1) && (y < kLcpTY || j == ny - 1);
-    if (owned) {
-      errbits |= check_value(s.mu_u[y][ux]) | check_value(s.mu_v[vy][x]) |
-                 check_sigma(s.s_u[y][ux]) | check_sigma(s.s_v[vy][x]);
-      const int64_t o = j * nx + i;
-      if (p.out_mu) p.out_mu[o] = m;
-      if (p.out_sigma) p.out_sigma[o] = sg;
-    }
-    double b, a;
-    tail_pair_lcp(m, sg, p.theta, b, a);
-    s.below[y][x] = b;
-    s.above[y][x] = a;
-  }
+  // tiles clear of the global faces and of the grid's end take the path
+  // without boundary logic (CTA-uniform branch; same arithmetic)
+  const bool interior = i0 >= 1 && i0 + kLcpTX <= nx - 2 && j0 >= 1 && j0 + kLcpTY <= ny - 2;
+  const int errbits = interior ? lcpf_vertices<false>(s, p, tid, i0, j0)
+                               : lcpf_vertices<true>(s, p, tid, i0, j0);
   __syncthreads();
   lcp_tile_cells<double, F::W>(&s.below[0][0], &s.above[0][0], i0, j0, nx, ny, p.out_lcp);
   flush_error(p.err, errbits);
