@@ -63,6 +63,14 @@ constexpr uint32_t kGfStageBytes = 2 * kGfCompBytes;
 // (a magnitude slot per thread and pass, kGfRP = kGfNL * threads >= kGfR: the
 // region pass has no tail branch; the extra slots are never differenced)
 constexpr int kGfRP = kGfNL * kGfThreads;
+// the TMA path's last magnitude pass covers only the region's kGfR slots
+// (warp-uniform: kGfR - (kGfNL-1) * threads is a multiple of 32), and only the
+// first kGfHalo threads difference a halo slot -- no work on padding slots.
+// (Skipping the region's two outer columns each side too -- they only pad the
+// TMA box start to 16 bytes -- needs a per-thread slot table: 6 more
+// registers, which spill at 64.)
+static_assert((kGfR - (kGfNL - 1) * kGfThreads) % 32 == 0, "partial last pass is warp-uniform");
+static_assert(kGfHalo % 32 == 0, "the halo gradient slot is warp-uniform");
 constexpr uint32_t kGfMagOff = kGfS * kGfStageBytes;
 constexpr uint32_t kGfMagBytes = 2 * kGfRP * 8;
 constexpr uint32_t kGfBarOff = kGfMagOff + kGfMagBytes;
@@ -140,6 +148,7 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
   const int M = int(p.M);
   float a[kGfNL], b[kGfNL];
   int64_t ld_off[kGfNL];
+  const bool last_pass = tid + (kGfNL - 1) * kGfThreads < kGfR;
   if constexpr (TMA) {
     if (tid == 0) {
       for (int s = 0; s < kGfS; ++s) mbar_init(&full[s], 1);
@@ -189,7 +198,8 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
       const float* su = reinterpret_cast<const float*>(gf_smem + st * kGfStageBytes);
       const float* sv = reinterpret_cast<const float*>(gf_smem + st * kGfStageBytes + kGfCompBytes);
 #pragma unroll
-      for (int k = 0; k < kGfNL; ++k) {   // slots past kGfR read in-bounds garbage, never used
+      for (int k = 0; k < kGfNL; ++k) {
+        if (k == kGfNL - 1 && !last_pass) break;
         const int q = tid + k * kGfThreads;
         float h, l;
         mag_pair(su[q], sv[q], h, l);
@@ -223,6 +233,7 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
     }
 #pragma unroll
     for (int s = 0; s < kGfSlots; ++s) {
+      if (s == kGfSlots - 1 && tid >= kGfHalo) break;   // halo slot: the first kGfHalo threads
       float hh, hl, lh, ll;   // (hi, lo) of the high and the low neighbour
       asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+%3];" : "=f"(hh), "=f"(hl) : "r"(a_hi[s]), "n"(BUF * kGfRP * 8));
       asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+%3];" : "=f"(lh), "=f"(ll) : "r"(a_lo[s]), "n"(BUF * kGfRP * 8));

@@ -5,6 +5,7 @@ import numpy as np
 a = np.load('gpurun_out/abA.npz'); b = np.load('gpurun_out/abB.npz')
 for k in a.files:
     x, y = a[k], b[k]
-    same = np.array_equal(x.view(np.uint64), y.view(np.uint64))
-    print(k, 'bitwise' if same else 'DIFF max %.3g n=%d' % (np.nanmax(np.abs(x - y)), (x.view(np.uint64) != y.view(np.uint64)).sum()))
+    u = np.uint64 if x.dtype.itemsize == 8 else np.uint32
+    same = np.array_equal(x.view(u), y.view(u))
+    print(k, 'bitwise' if same else 'DIFF max %.3g n=%d' % (np.nanmax(np.abs(x - y)), (x.view(u) != y.view(u)).sum()))
 "
