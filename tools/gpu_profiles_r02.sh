@@ -48,4 +48,12 @@ prof lcp2d_fused lcp2d_fused --workload lcpfused --steps 3
 prof gradfused_redsea gradfused --workload redsea --steps 3
 prof fit_bulk fit_bulk --workload fit --steps 3
 prof gradient_tma gradient_tma --workload gradient --steps 3
+# the fp64 K2 of config 3's fp64 side line (launched after the fp32 timed loop)
+ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+  -k regex:"k2_tma_kernel<double" -s 3 -c 1 -o $O/prof_k2_tma_f64 \
+  python bench.py --config 3 --steps 3 --warmup 3 --no-e2e --no-cpu > $O/ncu_k2_tma_f64.log 2>&1
+python tools/ncu_summary.py $O/prof_k2_tma_f64.ncu-rep > $O/k2_tma_f64_summary.txt
+ncu -i $O/prof_k2_tma_f64.ncu-rep --page source --csv --print-source sass > $O/src_k2f64.csv 2>/dev/null
+python tools/sass_mix_csv.py $O/src_k2f64.csv > $O/k2_tma_f64_sassmix.txt 2>/dev/null
+rm -f $O/prof_k2_tma_f64.ncu-rep $O/src_k2f64.csv
 ls -la $O
