@@ -12,6 +12,7 @@
 #include "../../include/divuq_b200.h"
 #include "gen.cuh"
 #include "k2tma.cuh"
+#include "k2flat.cuh"
 #include "k3tma.cuh"
 #include "k3row.cuh"
 #include "divuq1.cuh"
@@ -377,16 +378,91 @@ int try_k3_tma(const StencilParams<float>& sp, int comps, cudaStream_t s, bool* 
   return int(cudaGetLastError());
 }
 
+// ---- K2 on 1D tensor maps (k2flat.cuh): shapes whose row pitch a tiled map
+// cannot take (fp32 nx % 4 != 0, fp64 nx odd) ---------------------------
+template <typename T>
+bool make_map1d(CUtensorMap* m, const T* base, int64_t n, int box) {
+  EncodeTiledFn fn = encode_tiled();
+  if (!fn || !base) return false;
+  const cuuint64_t dims[1] = {cuuint64_t(n)};
+  const cuuint64_t strides[1] = {0};
+  const cuuint32_t bx[1] = {cuuint32_t(box)};
+  const cuuint32_t es[1] = {1};
+  const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  return fn(m, dt, 1, const_cast<T*>(base), dims, strides, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <typename T, bool HAS_SIGMA>
+int launch_k2_flat(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
+  using C = FlatCfg<T>;
+  *used = false;
+  const int64_t n = sp.nx * sp.ny * sp.nzl;
+  const int64_t plane = sp.nx * sp.ny;
+  // element coordinates are int32: the furthest box (plane nzl, row ny) must fit
+  if (n + 2 * plane + C::UW >= (int64_t(1) << 31)) return DIVUQ_OK;
+  const int64_t sms = sm_count();
+  const int64_t tiles_x = (sp.nx + C::TX - 1) / C::TX;
+  int ty = C::TYMAX;
+  int64_t best = INT64_MAX;
+  for (int cand = C::TYMAX; cand >= 8; --cand) {
+    const int64_t tiles = tiles_x * ((sp.ny + cand - 1) / cand);
+    const int64_t cost = ((tiles + sms - 1) / sms) * cand;
+    if (cost < best) { best = cost; ty = cand; }
+  }
+  FlatMaps fm;
+  std::memset(&fm, 0, sizeof(fm));
+  const T* arrs[6] = {sp.mu_u, sp.s_u, sp.mu_v, sp.s_v, sp.mu_w, sp.s_w};
+  for (int a = 0; a < 6; ++a) {
+    if (!HAS_SIGMA && (a & 1)) { fm.m[a] = fm.m[a - 1]; continue; }
+    if (!make_map1d<T>(&fm.m[a], arrs[a], n, a < 2 ? C::UW : C::RWB)) return DIVUQ_OK;
+  }
+  FlatParams<T> p;
+  std::memset(&p, 0, sizeof(p));
+  p.mu_w = sp.mu_w; p.s_w = sp.s_w;
+  p.halo_lo_mu_w = sp.halo_lo_mu_w; p.halo_lo_s_w = sp.halo_lo_s_w;
+  p.halo_hi_mu_w = sp.halo_hi_mu_w; p.halo_hi_s_w = sp.halo_hi_s_w;
+  p.nzl = sp.nzl; p.z0 = sp.z0; p.nzg = sp.nzg; p.kbeg = sp.kbeg; p.kend = sp.kend;
+  p.nx = int(sp.nx); p.ny = int(sp.ny); p.ty = ty;
+  p.tiles_x = int(tiles_x);
+  p.n_tiles = int(tiles_x * ((sp.ny + ty - 1) / ty));
+  const uint32_t comps = HAS_SIGMA ? 2u : 1u;
+  p.stage_bytes = uint32_t((ty * (C::UW + C::RWB) + (ty + 2) * C::RWB) * sizeof(T)) * comps;
+  p.cx_in = sp.cx_in; p.cx_bd = sp.cx_bd; p.cy_in = sp.cy_in; p.cy_bd = sp.cy_bd;
+  p.cz_in = sp.cz_in; p.cz_bd = sp.cz_bd; p.theta = sp.theta;
+  p.out_mu = sp.out_mu; p.out_sigma = sp.out_sigma; p.out_psrc = sp.out_psrc; p.out_psnk = sp.out_psnk;
+  p.err = sp.err;
+  *used = true;
+  if (sp.kend <= sp.kbeg) return DIVUQ_OK;
+  auto kern = k2_flat_kernel<T, HAS_SIGMA>;
+  const size_t smem = sizeof(FlatStage<T>) * C::S + 2 * C::S * sizeof(uint64_t);
+  DIVUQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  const int64_t grid = std::min<int64_t>(p.n_tiles, sms);
+  kern<<<unsigned(grid), C::THREADS, smem, s>>>(fm, p);
+  return int(cudaGetLastError());
+}
+
+template <typename T>
+int try_k2_flat(const StencilParams<T>& p, bool has_sigma, cudaStream_t s, bool* used) {
+  *used = false;
+  if (env_int("DIVUQ_NO_FLAT", 0)) return DIVUQ_OK;
+  const void* ptrs[] = {p.mu_u, p.mu_v, p.mu_w, p.s_u, p.s_v, p.s_w};   // tensor-map bases
+  for (int a = 0; a < 6; ++a)
+    if ((has_sigma || a < 3) && !aligned(ptrs[a], 16)) return DIVUQ_OK;
+  return has_sigma ? launch_k2_flat<T, true>(p, s, used) : launch_k2_flat<T, false>(p, s, used);
+}
+
 template <typename T>
 int try_k2_tma(const StencilParams<T>& p, bool has_sigma, cudaStream_t s, bool* used) {
   *used = false;
   if (env_int("DIVUQ_NO_TMA", 0)) return DIVUQ_OK;
   constexpr int VW = TmaCfg<T>::VEC;
-  if (p.nx % VW) return DIVUQ_OK;
+  if (p.nx % VW) return try_k2_flat<T>(p, has_sigma, s, used);
   const void* ptrs[] = {p.mu_u, p.mu_v, p.mu_w, p.s_u, p.s_v, p.s_w, p.halo_lo_mu_w, p.halo_lo_s_w,
                         p.halo_hi_mu_w, p.halo_hi_s_w, p.out_mu, p.out_sigma, p.out_psrc, p.out_psnk};
   for (const void* q : ptrs)
-    if (!aligned(q, 16)) return DIVUQ_OK;
+    if (!aligned(q, 16)) return try_k2_flat<T>(p, has_sigma, s, used);   // vector accesses need 16 B
   if (p.nx > (int64_t(1) << 31) || p.ny > (int64_t(1) << 31) || p.nzl > (int64_t(1) << 31)) return DIVUQ_OK;
   return has_sigma ? launch_k2_tma<T, true>(p, s, used) : launch_k2_tma<T, false>(p, s, used);
 }

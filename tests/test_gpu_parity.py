@@ -578,3 +578,64 @@ def test_tma_pipeline_matches_register_kernel_bitwise(dev, dtype, rng, monkeypat
         monkeypatch.delenv("DIVUQ_NO_TMA")
         for k in a:
             assert torch.equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("shape", [(131, 9, 7), (510, 17, 5), (3, 2, 4), (257, 30, 3), (65, 1 + 14, 6)])
+def test_flat_tma_kernel_matches_generic_bitwise(dev, dtype, shape, rng, monkeypatch):
+    """K2 on 1D tensor maps (k2flat.cuh: row pitch not a multiple of 16 bytes)
+    == the generic register kernel bit for bit: whole domain, z-slabs with
+    halo planes, k ranges, the deterministic (mean-only) variant."""
+    nx, ny, nz = shape
+    if dtype == np.float64 and nx % 2 == 0:
+        nx += 1   # fp64 tiled maps take every even nx
+    plane = nx * ny
+    f = _model3d(nx, ny, nz, rng, dtype)
+    ins = [cu(x) for x in f]
+
+    def both(fn):
+        a = fn()
+        monkeypatch.setenv("DIVUQ_NO_FLAT", "1")
+        b = fn()
+        monkeypatch.delenv("DIVUQ_NO_FLAT")
+        for k in a:
+            assert torch.equal(a[k], b[k]), k
+        return a
+
+    for t in (0.0, 0.2):
+        both(lambda: dev.propagate3d(*ins, nx, ny, nz, 0.5, 1.5, 0.75, t))
+    both(lambda: dev.propagate3d(*ins, nx, ny, nz, 0.5, 1.5, 0.75, 0.0, outputs=("mu",)))
+    if nz >= 4:
+        z0, z1 = 1, nz - 1
+        sl = [cu(x[z0 * plane:z1 * plane]) for x in f]
+        lo = (cu(f[2][(z0 - 1) * plane:z0 * plane]), cu(f[5][(z0 - 1) * plane:z0 * plane]))
+        hi = (cu(f[2][z1 * plane:(z1 + 1) * plane]), cu(f[5][z1 * plane:(z1 + 1) * plane]))
+        full = dev.propagate3d(*ins, nx, ny, nz, 0.5, 1.5, 0.75, 0.1)
+        o = both(lambda: dev.propagate3d(*sl, nx, ny, z1 - z0, 0.5, 1.5, 0.75, 0.1, z0=z0, nz_global=nz,
+                                         halo_lo=lo, halo_hi=hi))
+        for k in o:
+            assert torch.equal(o[k], full[k][z0 * plane:z1 * plane]), k
+    if dtype == np.float64:   # and the reference order, bit for bit
+        o = dev.propagate3d(*ins, nx, ny, nz, 0.5, 1.5, 0.75, 0.0)
+        mu, sg = ref3d.propagate3d(*f, nx, ny, nz, 0.5, 1.5, 0.75)
+        assert np.array_equal(host(o["mu"]), mu) and np.array_equal(host(o["sigma"]), sg)
+
+
+def test_flat_tma_kernel_unaligned_outputs_and_validation(dev, rng):
+    """Aligned nx but outputs 4 bytes off a 16-byte boundary: the flat kernel
+    (scalar stores) takes it; a negative sigma still raises."""
+    nx, ny, nz = 128, 12, 6
+    n = nx * ny * nz
+    f = _model3d(nx, ny, nz, rng, np.float32)
+    ins = [cu(x) for x in f]
+    ref = dev.propagate3d(*ins, nx, ny, nz, 1.0, 1.0, 1.0, 0.0)
+    buf = {k: torch.empty(n + 1, dtype=torch.float32, device="cuda") for k in ref}
+    out = {k: v[1:] for k, v in buf.items()}
+    dev.propagate3d(*ins, nx, ny, nz, 1.0, 1.0, 1.0, 0.0, out=out)
+    for k in ref:
+        assert torch.equal(out[k], ref[k]), k
+    bad = [x.clone() for x in ins]
+    bad[4][n // 3] = -0.5
+    nx2 = 127
+    with pytest.raises(ValueError):
+        dev.propagate3d(*(x[: nx2 * ny * nz] for x in bad), nx2, ny, nz, 1.0, 1.0, 1.0, 0.0)
