@@ -32,7 +32,9 @@ routed functions return what the reference returns:
 ``DIVUQ_B200_LIB`` names the library (default: ``libdivuq_b200.so`` on the
 loader path); when it cannot be loaded ``install()`` leaves the reference
 untouched.  ``DIVUQ_B200_TRACE=<path>`` appends one line per routed call
-(the boundary test uses it to prove the GPU path ran).
+(the boundary test uses it to prove the GPU path ran).  ``install()`` warms
+the device up (CUDA context, library pools) at import so the first routed
+call is not charged for it; ``DIVUQ_B200_LAZY=1`` defers that to first use.
 """
 
 from __future__ import annotations
@@ -251,4 +253,10 @@ def install() -> bool:
         setattr(module, name, fn)            # callers inside the package
         if hasattr(divuq, name):
             setattr(divuq, name, fn)         # the public re-export (__init__.py:9-45)
+    if os.environ.get("DIVUQ_B200_LAZY", "0") != "1":
+        # create the CUDA context and stage the library's pools now, at import,
+        # not inside the first routed call (~1-3 s once per process)
+        one, zero = np.ones(1), np.zeros(1)
+        b_, a_ = np.empty(1), np.empty(1)
+        _lib.divuq_host_tail_probs_f64(_ptr(zero), _ptr(one), 1, 0.0, _ptr(b_), _ptr(a_), _DEVICE)
     return True
