@@ -106,6 +106,13 @@ int launch_stencil_impl(StencilParams<T> p, cudaStream_t s) {
   return int(cudaGetLastError());
 }
 
+template <typename T, bool HAS_SIGMA, int SRC>
+int launch_gather2d(const StencilParams<T>& p, cudaStream_t s) {
+  const dim3 grid(unsigned((p.nx + 255) / 256), unsigned(std::min<int64_t>(p.ny, 65535)));
+  stencil2d_gather_kernel<T, HAS_SIGMA, SRC><<<grid, 256, 0, s>>>(p);
+  return int(cudaGetLastError());
+}
+
 template <typename T, int VEC, bool HAS_W, int SRC>
 int dispatch_sigma(const StencilParams<T>& p, bool has_sigma, cudaStream_t s) {
   if constexpr (SRC == kResidual) {
@@ -130,6 +137,13 @@ int dispatch_vec(const StencilParams<T>& p, bool has_sigma, cudaStream_t s) {
   if (vec) {
     const int64_t tiles_vec = ((p.nx + 32 * VW - 1) / (32 * VW)) * ((p.ny + kStencilTY - 1) / kStencilTY);
     if (tiles_vec * (p.kend - p.kbeg) < sm_count()) vec = false;
+  }
+  if constexpr (!HAS_W) {   // 2D: the gather kernel where the vector kernel cannot run
+    if ((!vec || env_int("DIVUQ_GATHER2D", 0)) && !env_int("DIVUQ_NO_GATHER2D", 0) && p.kbeg == 0 &&
+        p.kend == 1) {
+      if (SRC == kResidual || has_sigma) return launch_gather2d<T, true, SRC>(p, s);
+      return launch_gather2d<T, false, SRC>(p, s);
+    }
   }
   if (vec) return dispatch_sigma<T, VW, HAS_W, SRC>(p, has_sigma, s);
   return dispatch_sigma<T, 1, HAS_W, SRC>(p, has_sigma, s);

@@ -308,6 +308,56 @@ struct StencilKernel {
   }
 };
 
+// 2D (no w) as a plain gather: one thread per point, the four stencil
+// neighbours (and the residuals' / sigmas' four) loaded straight from global
+// memory -- the x neighbours hit L1, the y neighbours L2 (adjacent rows run
+// in adjacent CTAs).  The z-marching kernel above degenerates in 2D (one
+// plane per work item: a barrier and a prologue per 256 points; 24 % of HBM
+// on the unaligned residual fallback).  Same StencilMath / Tails calls with
+// the same operands as StencilKernel<T, *, false, ...>: bitwise equal.
+template <typename T, bool HAS_SIGMA, int SRC>
+__global__ void __launch_bounds__(256)
+stencil2d_gather_kernel(const StencilParams<T> p) {
+  using SM = StencilMath<T, false>;
+  constexpr bool RES = (SRC == kResidual);
+  const int64_t nx = p.nx, ny = p.ny;
+  int errbits = 0;
+  const int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  if (i < nx) {
+    const bool ilo = i == 0, ihi = i == nx - 1;
+    const T cx = (ilo || ihi) ? p.cx_bd : p.cx_in;
+    for (int64_t j = blockIdx.y; j < ny; j += gridDim.y) {
+      const int64_t q = j * nx + i;
+      const bool jlo = j == 0, jhi = j == ny - 1;
+      const T cy = (jlo || jhi) ? p.cy_bd : p.cy_in;
+      const int64_t xl = ilo ? q : q - 1, xh = ihi ? q : q + 1;
+      const int64_t yl = jlo ? q : q - nx, yh = jhi ? q : q + nx;
+      T m;
+      if constexpr (RES) {
+        m = SM::mean_r(__ldg(p.mu_u + xh), __ldg(p.mu_u + xl), __ldg(p.r_u + xh), __ldg(p.r_u + xl),
+                       __ldg(p.mu_v + yh), __ldg(p.mu_v + yl), __ldg(p.r_v + yh), __ldg(p.r_v + yl),
+                       T(0), T(0), T(0), T(0), cx, cy, T(0));
+      } else {
+        m = SM::mean(__ldg(p.mu_u + xh), __ldg(p.mu_u + xl), __ldg(p.mu_v + yh), __ldg(p.mu_v + yl),
+                     T(0), T(0), cx, cy, T(0));
+      }
+      if (p.out_mu) p.out_mu[q] = m;
+      if (p.err) errbits |= check_value(__ldg(p.mu_u + q)) | check_value(__ldg(p.mu_v + q));
+      if constexpr (HAS_SIGMA) {
+        const T var = SM::var(__ldg(p.s_u + xh), __ldg(p.s_u + xl), __ldg(p.s_v + yh), __ldg(p.s_v + yl),
+                              T(0), T(0), cx, cy, T(0));
+        T sg, ps, pk;
+        Tails<T>::eval(m, var, p.theta, p.theta == T(0), sg, ps, pk);
+        if (p.out_sigma) p.out_sigma[q] = sg;
+        if (p.out_psrc) p.out_psrc[q] = ps;
+        if (p.out_psnk) p.out_psnk[q] = pk;
+        if (p.err) errbits |= check_sigma(__ldg(p.s_u + q)) | check_sigma(__ldg(p.s_v + q));
+      }
+    }
+  }
+  flush_error(p.err, errbits);
+}
+
 template <typename T, int VEC, bool HAS_W, bool HAS_SIGMA, int SRC>
 __global__ void __launch_bounds__(32 * kStencilTY, 2)
 stencil_kernel(const StencilParams<T> p) {

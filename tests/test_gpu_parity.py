@@ -639,3 +639,37 @@ def test_flat_tma_kernel_unaligned_outputs_and_validation(dev, rng):
     nx2 = 127
     with pytest.raises(ValueError):
         dev.propagate3d(*(x[: nx2 * ny * nz] for x in bad), nx2, ny, nz, 1.0, 1.0, 1.0, 0.0)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("shape", [(131, 9), (1023, 40), (3, 2), (257, 300)])
+def test_gather2d_matches_stencil_kernel_bitwise(dev, dtype, shape, rng, monkeypatch):
+    """2D on unaligned rows runs the gather kernel (stencil.cuh); the
+    z-marching register kernel is the same arithmetic, bit for bit: the
+    analytic map (with and without sigma) and the fused-ensemble fallback's
+    residual stencil."""
+    nx, ny = shape
+    n = nx * ny
+    a = [rng.normal(0, 2, n), rng.normal(0, 2, n), rng.uniform(0.05, 0.6, n), rng.uniform(0.05, 0.6, n)]
+    ins = [cu(x.astype(dtype)) for x in a]
+
+    def both(fn):
+        x = fn()
+        monkeypatch.setenv("DIVUQ_NO_GATHER2D", "1")
+        y = fn()
+        monkeypatch.delenv("DIVUQ_NO_GATHER2D")
+        for k in x:
+            assert torch.equal(x[k], y[k]), k
+
+    for t in (0.0, 0.3):
+        both(lambda: dev.propagate2d(*ins, nx, ny, 0.7, 1.3, t))
+    both(lambda: dev.propagate2d(*ins, nx, ny, 0.7, 1.3, 0.0, outputs=("mu",)))
+    if dtype == np.float32 and nx % 4:
+        mem = cu(rng.normal(size=(6, 2, n)).astype(np.float32))
+
+        def fused():
+            monkeypatch.setenv("DIVUQ_NO_ROWMARCH", "1")
+            o = dev.ensemble_divergence2d(mem, nx, ny, 0.5, 0.5, 0.1, moments=True)
+            monkeypatch.delenv("DIVUQ_NO_ROWMARCH")
+            return o
+        both(fused)
