@@ -43,3 +43,13 @@ for nx in (1024, 1022, 1023):
     mem = torch.randn(m, 2, nx * ny, device="cuda")
     ms = timeit(lambda: dev.ensemble_divergence2d(mem, nx, ny, 1.0, 1.0, 0.0, check=ERR))
     print(f"ensemble_divergence2d M=20 {nx}x{ny}: {ms * 1e3:.1f} us, {(160 + 16) * nx * ny / ms / 1e6 / PEAK * 100:.1f} % HBM")
+for nx in (1024, 1023):
+    ny, m = 1024, 20
+    mem = torch.randn(m, 2, nx * ny, device="cuda")
+    ms = timeit(lambda: dev.gradient_ensemble_divergence2d(mem, nx, ny, 1.0, 1.0, 0.0, check=ERR))
+    print(f"gradient_ensemble_divergence2d (K6) M=20 {nx}x{ny}: {ms * 1e3:.1f} us, {(160 + 16) * nx * ny / ms / 1e6 / PEAK * 100:.1f} % HBM")
+for nx in (4096, 4095):
+    ny = 4096
+    mu, sg = torch.randn(nx * ny, device="cuda", dtype=torch.float64), torch.rand(nx * ny, device="cuda", dtype=torch.float64)
+    ms = timeit(lambda: dev.lcp2d(mu, sg, nx, ny, 0.0, check=ERR))
+    print(f"lcp2d fp64 {nx}x{ny}: {ms * 1e3:.1f} us, {24 * (nx - 1) * (ny - 1) / ms / 1e6 / PEAK * 100:.1f} % HBM")
