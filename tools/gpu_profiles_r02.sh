@@ -57,3 +57,4 @@ ncu -i $O/prof_k2_tma_f64.ncu-rep --page source --csv --print-source sass > $O/s
 python tools/sass_mix_csv.py $O/src_k2f64.csv > $O/k2_tma_f64_sassmix.txt 2>/dev/null
 rm -f $O/prof_k2_tma_f64.ncu-rep $O/src_k2f64.csv
 ls -la $O
+python tools/dropin_probe.py > $O/dropin_probe.txt 2>&1
