@@ -1504,6 +1504,15 @@ int divuq_lcp2d_f64(const double* mu, const double* sigma, int64_t nx, int64_t n
         mm, ms, nx, ny, isovalue, out, err);
     return int(cudaGetLastError());
   }
+  // odd nx: row boxes on 1D tensor maps (lcp2d_flat_kernel)
+  if (!env_int("DIVUQ_NO_TMA", 0) && !env_int("DIVUQ_NO_FLAT", 0) && aligned(mu, 16) &&
+      aligned(sigma, 16) && nx * ny + 2 * nx + LcpFlat::BOX < (int64_t(1) << 31) &&
+      make_map1d<double>(&mm, mu, nx * ny, LcpFlat::BOX) && make_map1d<double>(&ms, sigma, nx * ny, LcpFlat::BOX)) {
+    const dim3 gf(grid.x, unsigned((ny - 1 + kLcpFTY - 1) / kLcpFTY));
+    lcp2d_flat_kernel<<<gf, dim3(kLcpBX, kLcpBY), 0, static_cast<cudaStream_t>(stream)>>>(
+        mm, ms, nx, ny, isovalue, out, err);
+    return int(cudaGetLastError());
+  }
   lcp2d_kernel<double><<<grid, dim3(kLcpBX, kLcpBY), 0, static_cast<cudaStream_t>(stream)>>>(
       mu, sigma, nx, ny, isovalue, out, err);
   return int(cudaGetLastError());

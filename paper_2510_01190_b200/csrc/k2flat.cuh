@@ -74,14 +74,6 @@ struct FlatParams {
   int* err;
 };
 
-__device__ __forceinline__ void tma_load_1d(void* dst, const CUtensorMap* map, uint64_t* bar, int x) {
-  asm volatile(
-      "cp.async.bulk.tensor.1d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2}], [%3];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(smem_u32(bar))
-      : "memory");
-}
-
 template <typename T, bool HAS_SIGMA>
 struct K2Flat {
   using C = FlatCfg<T>;

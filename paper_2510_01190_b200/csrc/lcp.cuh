@@ -331,6 +331,82 @@ lcp2d_tma_kernel(const __grid_constant__ CUtensorMap map_mu, const __grid_consta
   flush_error(err, errbits);
 }
 
+// Odd nx (fp64 rows not 16-byte aligned: no tiled tensor map): the same tile
+// on 1D tensor maps over the flat arrays, one row box per vertex row.  A box
+// must start on a 16-byte boundary, so row y's box starts one element early
+// when its offset is odd and the row sits at shift sh(y) = ((cj0 + y) nx) & 1
+// in its table row (cj0 + y parity for odd nx; ci0 is even).  Out-of-range
+// parts arrive as 0; a row's last two table columns hold the next row's
+// first values, read only by cells that are never written.
+constexpr int kLcpFTY = 32;   // cell rows per CTA (2 x 33 x 640 B tables: static shared memory)
+struct LcpFlat {
+  static constexpr int W = kLcpTX + 2;    // vertices per row used (65) rounded to even
+  static constexpr int BOX = W + 2;       // row box: + 1 element of start slack, even
+  static constexpr int P = 80;            // table pitch (640 B: 128-byte aligned rows)
+  static constexpr int H = kLcpFTY + 1;
+};
+
+__global__ void __launch_bounds__(kLcpBX * kLcpBY, DIVUQ_LCP_MINB)
+lcp2d_flat_kernel(const __grid_constant__ CUtensorMap map_mu, const __grid_constant__ CUtensorMap map_sg,
+                  int64_t nx, int64_t ny, double theta, double* __restrict__ out, int* err) {
+  using A = Arith<double>;
+  using L = LcpFlat;
+  __shared__ __align__(128) double below[L::H][L::P];
+  __shared__ __align__(128) double above[L::H][L::P];
+  __shared__ uint64_t bar;
+  const int tid = threadIdx.y * kLcpBX + threadIdx.x;
+  const int64_t ci0 = int64_t(blockIdx.x) * kLcpTX, cj0 = int64_t(blockIdx.y) * kLcpFTY;
+  const int odd = int(nx & 1);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    mbar_fence_init();
+    mbar_expect_tx(&bar, 2u * L::H * L::BOX * sizeof(double));
+  }
+  __syncthreads();
+  if (tid == 0 || tid == 32) {   // two issuing threads: one 1D load every ~72 cycles each
+    const CUtensorMap* map = tid == 0 ? &map_mu : &map_sg;
+    double* tab = tid == 0 ? &below[0][0] : &above[0][0];
+    for (int r = 0; r < L::H; ++r) {
+      const int64_t off = (cj0 + r) * nx + ci0;
+      tma_load_1d(tab + r * L::P, map, &bar, int(off & ~int64_t(1)));
+    }
+  }
+  mbar_wait(&bar, 0);
+  int nonfinite = 0, negative = 0;
+  double* const bl = &below[0][0];
+  double* const ab = &above[0][0];
+#pragma unroll kLcpUnroll
+  for (int v = tid; v < L::H * L::W; v += kLcpBX * kLcpBY) {
+    const int y = v / L::W, x = v - y * L::W;
+    const int idx = y * L::P + (odd & int(cj0 + y)) + x;
+    const double m = bl[idx], sg = ab[idx];
+    nonfinite |= int(!isfinite(m)) | int(!isfinite(sg));
+    negative |= int(sg < 0.0);
+    tail_store_lcp(m, sg, theta, bl + idx, ab + idx);
+  }
+  const int errbits = (nonfinite ? kErrNonFinite : 0) | (negative ? kErrNegativeSigma : 0);
+  __syncthreads();
+  const int xl = int(min(nx - 1 - ci0, int64_t(kLcpTX))), yl = int(min(ny - 1 - cj0, int64_t(kLcpFTY)));
+  const int64_t ld = nx - 1;
+  double* const o = out + cj0 * ld + ci0;
+#pragma unroll
+  for (int ry = 0; ry < kLcpFTY; ry += kLcpBY) {
+#pragma unroll
+    for (int rx = 0; rx < kLcpTX; rx += kLcpBX) {
+      const int x = threadIdx.x + rx, y = threadIdx.y + ry;
+      if (x < xl && y < yl) {
+        const int r0 = y * L::P + (odd & int(cj0 + y)) + x;
+        const int r1 = (y + 1) * L::P + (odd & int(cj0 + y + 1)) + x;
+        // corners in lcp.py order: v00, v00+1, v00+nx, v00+nx+1
+        const double pb = A::mul(A::mul(A::mul(bl[r0], bl[r0 + 1]), bl[r1]), bl[r1 + 1]);
+        const double pa = A::mul(A::mul(A::mul(ab[r0], ab[r0 + 1]), ab[r1]), ab[r1 + 1]);
+        o[int64_t(y) * ld + x] = lcp_clip0(A::sub(1.0, A::add(pb, pa)));
+      }
+    }
+  }
+  flush_error(err, errbits);
+}
+
 // stacked cells: mu4 / sigma4 are (n, 4) row-major, corners in order
 template <typename T>
 __global__ void cell_crossing_kernel(const T* __restrict__ mu4, const T* __restrict__ sigma4,

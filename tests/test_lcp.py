@@ -152,3 +152,28 @@ def test_propagate_lcp_fused(gpu, rng, shape):
     bad[2][n // 2] = -1.0
     with pytest.raises(ValueError):
         dev.propagate_lcp2d(*bad, nx, ny, 0.7, 1.3, 0.0)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(1031, 517), (65, 33), (3, 70), (4095, 41)])
+def test_lcp_flat_kernel_matches_register_kernel(gpu, rng, shape, monkeypatch):
+    """Odd nx runs the 1D-tensor-map LCP kernel (row boxes at 16-byte-aligned
+    starts); the register kernel is the same arithmetic, bit for bit."""
+    import torch
+
+    from paper_2510_01190_b200 import device as dev
+
+    nx, ny = shape
+    n = nx * ny
+    mu = rng.normal(0, 1.5, n)
+    sg = rng.uniform(0, 2, n)
+    sg[rng.random(n) < 0.05] = 0.0
+    mu[rng.random(n) < 0.02] = 0.25
+    m, s = torch.from_numpy(mu).cuda(), torch.from_numpy(sg).cuda()
+    for t in (0.0, 0.25):
+        a = dev.lcp2d(m, s, nx, ny, t)
+        monkeypatch.setenv("DIVUQ_NO_FLAT", "1")
+        b = dev.lcp2d(m, s, nx, ny, t)
+        monkeypatch.delenv("DIVUQ_NO_FLAT")
+        assert torch.equal(a, b)
+        assert np.abs(a.cpu().numpy() - ref2d.lcp(mu, sg, nx, ny, t)).max() <= 1e-12
