@@ -38,6 +38,17 @@
 #include "common.cuh"
 #include "tma.cuh"
 
+#ifndef DIVUQ_K2_TYMAX
+#define DIVUQ_K2_TYMAX 15
+#endif
+// fp64: 14 consumer rows keep the CTA at 16 warps, where the register
+// allocation allows 128 per thread (17 warps: 96, and the fp64 consumers
+// spilled); config 3's tile height is 14 either way.  fp64 config 3:
+// 2.03 -> 1.91 ms.  (fp32 keeps 15: measured no better at 14.)
+#ifndef DIVUQ_K2_TYMAX_F64
+#define DIVUQ_K2_TYMAX_F64 14
+#endif
+
 namespace divuq {
 
 template <typename T>
@@ -45,7 +56,7 @@ struct TmaCfg {
   static constexpr int VEC = 16 / int(sizeof(T));  // 4 x fp32 or 2 x fp64 per lane
   static constexpr int TX = 32 * VEC;               // tile width (points)
   static constexpr int PAD = VEC;                    // x-halo box width (16 bytes)
-  static constexpr int TYMAX = 15;  // consumer warps (tile rows, max): 16 warps/CTA -> 128 regs
+  static constexpr int TYMAX = sizeof(T) == 8 ? DIVUQ_K2_TYMAX_F64 : DIVUQ_K2_TYMAX;   // consumer warps
   static constexpr int S = 4;                        // pipeline stages
   static constexpr int D = 3;                        // max stages the halo boxes may trail (runtime hdelay)
   static constexpr int THREADS = 32 * (TYMAX + 2);  // + producer warp + pacer warp
