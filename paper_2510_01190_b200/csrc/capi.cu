@@ -1556,7 +1556,7 @@ int divuq_propagate_lcp2d_f64(const double* mu_u, const double* mu_v, const doub
   p.cy_in = 1.0 / (2.0 * dy); p.cy_bd = 1.0 / dy;
   p.theta = isovalue;
   p.out_mu = out_mu; p.out_sigma = out_sigma; p.out_lcp = out_lcp; p.err = err;
-  const dim3 grid(unsigned((nx - 1 + kLcpTX - 1) / kLcpTX), unsigned((ny - 1 + kLcpTY - 1) / kLcpTY));
+  const dim3 grid(unsigned((nx - 1 + kLcpTX - 1) / kLcpTX), unsigned((ny - 1 + kLcpFY - 1) / kLcpFY));
   if (grid.y > 65535) return DIVUQ_EGRID;
   DIVUQ_CUDA(cudaFuncSetAttribute(lcp2d_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(sizeof(LcpFusedSmem))));

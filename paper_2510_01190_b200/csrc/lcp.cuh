@@ -450,11 +450,21 @@ namespace divuq {
 // (66 wide).  Out-of-grid slots arrive as 0 and feed only vertices that are
 // never written and cells that are never written.
 // ---------------------------------------------------------------------------
+#ifndef DIVUQ_LCPF_TY
+#define DIVUQ_LCPF_TY 16
+#endif
+#ifndef DIVUQ_LCPF_ALIAS
+#define DIVUQ_LCPF_ALIAS 0
+#endif
+constexpr int kLcpFY = DIVUQ_LCPF_TY;           // cell rows per CTA of the fused kernel
+constexpr bool kLcpFAlias = DIVUQ_LCPF_ALIAS;   // tail tables over the u boxes (tails held in registers)
 struct LcpFused {
-  static constexpr int UW = kLcpTX + 4, UH = kLcpTY + 1;   // u box: x from i0 - 2
-  static constexpr int VW = kLcpTX + 2, VH = kLcpTY + 3;   // v box: y from j0 - 1
-  static constexpr int W = kLcpTX + 2, H = kLcpTY + 1;     // vertex / tail tables
+  static constexpr int UW = kLcpTX + 4, UH = kLcpFY + 1;   // u box: x from i0 - 2
+  static constexpr int VW = kLcpTX + 2, VH = kLcpFY + 3;   // v box: y from j0 - 1
+  static constexpr int W = kLcpTX + 2, H = kLcpFY + 1;     // vertex / tail tables
+  static constexpr int NV = (H * (kLcpTX + 1) + kLcpBX * kLcpBY - 1) / (kLcpBX * kLcpBY);
   static constexpr uint32_t kBytes = uint32_t(2 * UW * UH + 2 * VW * VH) * 8u;
+  static_assert(H * W <= UH * UW, "a tail table fits in a u box");
 };
 
 struct LcpFusedSmem {
@@ -462,8 +472,10 @@ struct LcpFusedSmem {
   alignas(128) double s_u[LcpFused::UH][LcpFused::UW];
   alignas(128) double mu_v[LcpFused::VH][LcpFused::VW];
   alignas(128) double s_v[LcpFused::VH][LcpFused::VW];
+#if !DIVUQ_LCPF_ALIAS
   alignas(16) double below[LcpFused::H][LcpFused::W];
   alignas(16) double above[LcpFused::H][LcpFused::W];
+#endif
   uint64_t bar;
 };
 
@@ -478,14 +490,19 @@ struct LcpFusedParams {
 // j0 + y) -> (mu, sigma) with K2's arithmetic -> tail pair into the tables
 template <bool EDGE>
 __device__ __forceinline__ int lcpf_vertices(LcpFusedSmem& s, const LcpFusedParams& p, int tid,
-                                             int64_t i0, int64_t j0) {
+                                             int64_t i0, int64_t j0, double* tb, double* ta) {
   using A = Arith<double>;
   using F = LcpFused;
   using SM = StencilMath<double, false>;
   const int64_t nx = p.nx, ny = p.ny;
   int nonfinite = 0, negative = 0;
-#pragma unroll 1
-  for (int v = tid; v < F::H * (kLcpTX + 1); v += kLcpBX * kLcpBY) {
+  double rb[kLcpFAlias ? F::NV : 1], ra[kLcpFAlias ? F::NV : 1];   // tails held until the boxes are free
+#pragma unroll
+  for (int k = 0; k < (kLcpFAlias ? F::NV : 1); ++k) { rb[k] = 0.0; ra[k] = 0.0; }
+#pragma unroll (kLcpFAlias ? F::NV : 1)
+  for (int k = 0; k < F::NV; ++k) {
+    const int v = tid + k * kLcpBX * kLcpBY;
+    if (v >= F::H * (kLcpTX + 1)) break;
     const int y = v / (kLcpTX + 1), x = v - y * (kLcpTX + 1);
     const int64_t i = i0 + x, j = j0 + y;
     if (EDGE && (i >= nx || j >= ny)) continue;
@@ -503,7 +520,7 @@ __device__ __forceinline__ int lcpf_vertices(LcpFusedSmem& s, const LcpFusedPara
                                cx, cy, 0.0);
     const double sg = A::sqrt_(var);
     // validation: every in-grid input point is some tile's vertex exactly once
-    const bool owned = (x < kLcpTX || (EDGE && i == nx - 1)) && (y < kLcpTY || (EDGE && j == ny - 1));
+    const bool owned = (x < kLcpTX || (EDGE && i == nx - 1)) && (y < kLcpFY || (EDGE && j == ny - 1));
     if (owned) {
       const double mu = s.mu_u[y][ux], mv = s.mu_v[vy][x], su = s.s_u[y][ux], sv = s.s_v[vy][x];
       nonfinite |= int(!isfinite(mu)) | int(!isfinite(mv)) | int(!isfinite(su)) | int(!isfinite(sv));
@@ -514,7 +531,22 @@ __device__ __forceinline__ int lcpf_vertices(LcpFusedSmem& s, const LcpFusedPara
         if (p.out_sigma) p.out_sigma[o] = sg;
       }
     }
-    tail_store_lcp(m, sg, p.theta, &s.below[y][x], &s.above[y][x]);
+    if constexpr (kLcpFAlias) {
+      tail_pair_lcp(m, sg, p.theta, rb[k], ra[k]);
+    } else {
+      tail_store_lcp(m, sg, p.theta, tb + y * F::W + x, ta + y * F::W + x);
+    }
+  }
+  if constexpr (kLcpFAlias) {
+    __syncthreads();   // every box read is done: the tables take over the u boxes
+#pragma unroll
+    for (int k = 0; k < F::NV; ++k) {
+      const int v = tid + k * kLcpBX * kLcpBY;
+      if (v >= F::H * (kLcpTX + 1)) break;
+      const int y = v / (kLcpTX + 1), x = v - y * (kLcpTX + 1);
+      tb[y * F::W + x] = rb[k];
+      ta[y * F::W + x] = ra[k];
+    }
   }
   return (nonfinite ? kErrNonFinite : 0) | (negative ? kErrNegativeSigma : 0);
 }
@@ -529,7 +561,7 @@ lcp2d_fused_kernel(const __grid_constant__ CUtensorMap m_mu_u, const __grid_cons
   extern __shared__ __align__(128) unsigned char lf_smem[];
   LcpFusedSmem& s = *reinterpret_cast<LcpFusedSmem*>(lf_smem);
   const int tid = threadIdx.y * kLcpBX + threadIdx.x;
-  const int64_t i0 = int64_t(blockIdx.x) * kLcpTX, j0 = int64_t(blockIdx.y) * kLcpTY;
+  const int64_t i0 = int64_t(blockIdx.x) * kLcpTX, j0 = int64_t(blockIdx.y) * kLcpFY;
   if (tid == 0) {
     mbar_init(&s.bar, 1);
     mbar_fence_init();
@@ -544,11 +576,18 @@ lcp2d_fused_kernel(const __grid_constant__ CUtensorMap m_mu_u, const __grid_cons
   const int64_t nx = p.nx, ny = p.ny;
   // tiles clear of the global faces and of the grid's end take the path
   // without boundary logic (CTA-uniform branch; same arithmetic)
-  const bool interior = i0 >= 1 && i0 + kLcpTX <= nx - 2 && j0 >= 1 && j0 + kLcpTY <= ny - 2;
-  const int errbits = interior ? lcpf_vertices<false>(s, p, tid, i0, j0)
-                               : lcpf_vertices<true>(s, p, tid, i0, j0);
+  const bool interior = i0 >= 1 && i0 + kLcpTX <= nx - 2 && j0 >= 1 && j0 + kLcpFY <= ny - 2;
+#if DIVUQ_LCPF_ALIAS
+  double* const tb = &s.mu_u[0][0];
+  double* const ta = &s.s_u[0][0];
+#else
+  double* const tb = &s.below[0][0];
+  double* const ta = &s.above[0][0];
+#endif
+  const int errbits = interior ? lcpf_vertices<false>(s, p, tid, i0, j0, tb, ta)
+                               : lcpf_vertices<true>(s, p, tid, i0, j0, tb, ta);
   __syncthreads();
-  lcp_tile_cells<double, F::W>(&s.below[0][0], &s.above[0][0], i0, j0, nx, ny, p.out_lcp);
+  lcp_tile_cells<double, F::W, kLcpFY>(tb, ta, i0, j0, nx, ny, p.out_lcp);
   flush_error(p.err, errbits);
 }
 
