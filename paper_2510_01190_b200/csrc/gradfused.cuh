@@ -174,14 +174,6 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
     }
   }
 
-  // shared-window addresses of the differenced magnitudes in mag buffer 0;
-  // buffer 1 is an immediate offset (the member loop is unrolled by two)
-  uint32_t a_hi[kGfSlots], a_lo[kGfSlots];
-#pragma unroll
-  for (int s = 0; s < kGfSlots; ++s) {
-    a_hi[s] = smem_u32(mag + g_hi[s]);
-    a_lo[s] = smem_u32(mag + g_lo[s]);
-  }
   ShiftedMoments<1> acc[kGfSlots];
   // non-finite input: u or v inf/NaN makes its magnitude pair NaN (mag_pair),
   // every gradient differencing it NaN, and so the divergence mean of some
@@ -235,8 +227,10 @@ gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
     for (int s = 0; s < kGfSlots; ++s) {
       if (s == kGfSlots - 1 && tid >= kGfHalo) break;   // halo slot: the first kGfHalo threads
       float hh, hl, lh, ll;   // (hi, lo) of the high and the low neighbour
-      asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+%3];" : "=f"(hh), "=f"(hl) : "r"(a_hi[s]), "n"(BUF * kGfRP * 8));
-      asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+%3];" : "=f"(lh), "=f"(ll) : "r"(a_lo[s]), "n"(BUF * kGfRP * 8));
+      // plain shared loads (volatile asm measured the same: 61.9 vs 62.1 us);
+      // BUF folds into the load's immediate offset
+      const float2 ph = mg[g_hi[s]], pl = mg[g_lo[s]];
+      hh = ph.x; hl = ph.y; lh = pl.x; ll = pl.y;
       const float g = grad_diff_pair(hh, lh, hl, ll, g_c[s]);   // stencils.py:87-96
       acc[s].add(FIRST ? 0 : 1, &g);   // member 0 sets the shift
     }
