@@ -451,7 +451,9 @@ def _mc_model():
 def test_mc_matches_philox_oracle_same_stream(dev):
     g, nx, ny, dx, dy = _mc_model()
     ins = [cu(g[k]) for k in ("mu_u", "mu_v", "s_u", "s_v")]
-    for n in (2, 300, 513):
+    # 4396 and 12345: more 128-sample chunks than the 32 slots, so slots fold
+    # several chunks with Chan's formula before the cross-slot merge
+    for n in (2, 300, 513, 4396, 12345):
         mean, std = dev.mc_divergence2d(*ins, nx, ny, dx, dy, n, 77)
         om, os_ = philox.mc_divergence(g["mu_u"], g["mu_v"], g["s_u"], g["s_v"], nx, ny, dx, dy, n, 77)
         # same counters and merge order; only libdevice vs numpy log/sincos ulps differ
