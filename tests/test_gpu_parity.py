@@ -644,7 +644,7 @@ def test_flat_tma_kernel_unaligned_outputs_and_validation(dev, rng):
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
-@pytest.mark.parametrize("shape", [(131, 9), (1023, 40), (3, 2), (257, 300)])
+@pytest.mark.parametrize("shape", [(131, 9), (1023, 40), (3, 2), (257, 300), (3, 70001)])
 def test_gather2d_matches_stencil_kernel_bitwise(dev, dtype, shape, rng, monkeypatch):
     """2D on unaligned rows runs the gather kernel (stencil.cuh); the
     z-marching register kernel is the same arithmetic, bit for bit: the
