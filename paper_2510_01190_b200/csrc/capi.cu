@@ -232,6 +232,19 @@ cudaError_t progress_flags(unsigned long long** flags_out, unsigned long long* e
   return cudaSuccess;
 }
 
+// Small planes (fewer tile columns than SMs): split each column's z range
+// into chunks so every SM gets a work item; each chunk restarts the z-march
+// (two w planes by plain loads), so chunks stay >= 16 planes.  Results are
+// the same bits: every point's arithmetic is unchanged.
+void z_chunks(int n_tiles, int64_t nk, int64_t sms, int* n_chunks, int64_t* zchunk) {
+  int64_t nch = 1;
+  if (n_tiles > 0 && n_tiles < sms && !env_int("DIVUQ_NO_ZCHUNK", 0))
+    nch = std::max<int64_t>(1, std::min<int64_t>(sms / n_tiles, nk / 16));   // one wave of items
+  const int64_t zc = std::max<int64_t>(1, (nk + nch - 1) / nch);
+  *zchunk = zc;
+  *n_chunks = int(std::max<int64_t>(1, (nk + zc - 1) / zc));
+}
+
 template <typename T, bool HAS_SIGMA>
 int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
   using C = TmaCfg<T>;
@@ -276,6 +289,7 @@ int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
   p.ty = ty;
   p.tiles_x = int(tiles_x);
   p.n_tiles = int(tiles_x * ((sp.ny + ty - 1) / ty));
+  z_chunks(p.n_tiles, sp.kend - sp.kbeg, sms, &p.n_chunks, &p.zchunk);
   p.hdelay = int(std::max<int64_t>(0, std::min<int64_t>(C::D, env_int("DIVUQ_K2_HDELAY", 2))));
   p.halo_off = int(env_int("DIVUQ_K2_HALO_OFF", 0));   // diagnostics only (wrong edge points)
   p.sync_w = int(env_int("DIVUQ_K2_SYNC_W", 8));
@@ -303,7 +317,7 @@ int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
   const size_t smem = sizeof(TmaStage<T>) * C::S + 2 * C::S * sizeof(uint64_t);
   // function attributes are per device context: set on every launch (cheap)
   DIVUQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  const int64_t grid = std::min<int64_t>(p.n_tiles, sms);
+  const int64_t grid = std::min<int64_t>(int64_t(p.n_tiles) * p.n_chunks, sms);
   kern<<<unsigned(grid), C::THREADS, smem, s>>>(tm, p);
   *used = true;
   return int(cudaGetLastError());
@@ -366,6 +380,7 @@ int try_k3_tma(const StencilParams<float>& sp, int comps, cudaStream_t s, bool* 
   p.comp_stride = sp.comp_stride;
   p.nx = int(sp.nx); p.ny = int(sp.ny); p.ty = ty; p.tiles_x = int(tiles_x);
   p.n_tiles = int(tiles_x * ((sp.ny + ty - 1) / ty));
+  z_chunks(p.n_tiles, sp.kend - sp.kbeg, sms, &p.n_chunks, &p.zchunk);
   p.M = int(sp.n_members);
   p.has_w = comps == 3;
   p.sync_w = int(env_int("DIVUQ_K3_SYNC_W", 0));   // lockstep off: no gain measured for K3
@@ -387,7 +402,7 @@ int try_k3_tma(const StencilParams<float>& sp, int comps, cudaStream_t s, bool* 
   const size_t smem = sizeof(K3Stage) * C::S + sizeof(K3Xchg) + 2 * C::S * sizeof(uint64_t);
   // function attributes are per device context: set on every launch (cheap)
   DIVUQ_CUDA(cudaFuncSetAttribute(k3_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  const int64_t grid = std::min<int64_t>(p.n_tiles, sms);
+  const int64_t grid = std::min<int64_t>(int64_t(p.n_tiles) * p.n_chunks, sms);
   k3_tma_kernel<<<unsigned(grid), C::THREADS, smem, s>>>(tm, p);
   return int(cudaGetLastError());
 }
@@ -441,6 +456,7 @@ int launch_k2_flat(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
   p.nx = int(sp.nx); p.ny = int(sp.ny); p.ty = ty;
   p.tiles_x = int(tiles_x);
   p.n_tiles = int(tiles_x * ((sp.ny + ty - 1) / ty));
+  z_chunks(p.n_tiles, sp.kend - sp.kbeg, sms, &p.n_chunks, &p.zchunk);
   const uint32_t comps = HAS_SIGMA ? 2u : 1u;
   p.stage_bytes = uint32_t((ty * (C::UW + C::RWB) + (ty + 2) * C::RWB) * sizeof(T)) * comps;
   p.cx_in = sp.cx_in; p.cx_bd = sp.cx_bd; p.cy_in = sp.cy_in; p.cy_bd = sp.cy_bd;
@@ -452,7 +468,7 @@ int launch_k2_flat(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
   auto kern = k2_flat_kernel<T, HAS_SIGMA>;
   const size_t smem = sizeof(FlatStage<T>) * C::S + 2 * C::S * sizeof(uint64_t);
   DIVUQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-  const int64_t grid = std::min<int64_t>(p.n_tiles, sms);
+  const int64_t grid = std::min<int64_t>(int64_t(p.n_tiles) * p.n_chunks, sms);
   kern<<<unsigned(grid), C::THREADS, smem, s>>>(fm, p);
   return int(cudaGetLastError());
 }

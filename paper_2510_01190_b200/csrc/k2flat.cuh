@@ -67,6 +67,8 @@ struct FlatParams {
   const T* halo_hi_mu_w; const T* halo_hi_s_w;
   int64_t nzl, z0, nzg, kbeg, kend;
   int nx, ny, ty, tiles_x, n_tiles;
+  int n_chunks;                                      // z-chunks per tile column (small planes: > 1)
+  int64_t zchunk;
   uint32_t stage_bytes;
   T cx_in, cx_bd, cy_in, cy_bd, cz_in, cz_bd;
   T theta;
@@ -126,10 +128,12 @@ struct K2Flat {
     const uint32_t my_bytes = (na * (C::UW + C::RWB) + nb * C::RWB) * uint32_t(sizeof(T)) * comps;
     int s = 0;
     uint32_t ph = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+    for (int item = blockIdx.x; item < p.n_tiles * p.n_chunks; item += gridDim.x) {
+      const int tile = item % p.n_tiles, chunk = item / p.n_tiles;
+      const int64_t kb = p.kbeg + chunk * p.zchunk, ke = min(p.kend, kb + p.zchunk);
       const int x0 = (tile % p.tiles_x) * TX;
       const int y0 = (tile / p.tiles_x) * p.ty;
-      for (int64_t k = p.kbeg; k < p.kend; ++k) {
+      for (int64_t k = kb; k < ke; ++k) {
         mbar_wait_backoff<DIVUQ_FLAT_NS>(&empty[s], ph ^ 1u);
         mbar_expect_tx(&full[s], my_bytes);
         Stage& S_ = st[s];
@@ -166,7 +170,9 @@ struct K2Flat {
     int nonfinite = 0, negative = 0;
     int s = 0;
     uint32_t ph = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+    for (int item = blockIdx.x; item < p.n_tiles * p.n_chunks; item += gridDim.x) {
+      const int tile = item % p.n_tiles, chunk = item / p.n_tiles;
+      const int64_t kb = p.kbeg + chunk * p.zchunk, ke = min(p.kend, kb + p.zchunk);
       const int x0 = (tile % p.tiles_x) * TX;
       const int j = (tile / p.tiles_x) * p.ty + ty;
       const bool row_act = j < p.ny;
@@ -174,10 +180,10 @@ struct K2Flat {
       const bool jlo = j == 0, jhi = j == p.ny - 1;
       const T cy = (jlo || jhi) ? p.cy_bd : p.cy_in;
       V wm, w0, swm, sw0;
-      load_w(p, p.kbeg - 1, off2d, x0 + lane, row_act, wm, swm);
-      load_w(p, p.kbeg, off2d, x0 + lane, row_act, w0, sw0);
-      int64_t o = p.kbeg * plane + off2d;
-      for (int64_t k = p.kbeg; k < p.kend; ++k, o += plane) {
+      load_w(p, kb - 1, off2d, x0 + lane, row_act, wm, swm);
+      load_w(p, kb, off2d, x0 + lane, row_act, w0, sw0);
+      int64_t o = kb * plane + off2d;
+      for (int64_t k = kb; k < ke; ++k, o += plane) {
         mbar_wait(&full[s], ph);
         const Stage& S_ = st[s];
         // warp-uniform shifts of this warp's rows inside their boxes

@@ -98,6 +98,8 @@ struct TmaParams {
   const T* halo_hi_mu_w; const T* halo_hi_s_w;
   int64_t nzl, z0, nzg, kbeg, kend;
   int nx, ny, ty, tiles_x, n_tiles;
+  int n_chunks;                                      // z-chunks per tile column (small planes: > 1)
+  int64_t zchunk;                                    // planes per chunk
   uint32_t stage_bytes;                              // TMA bytes per stage (depends on ty)
   int hdelay;                                        // halo boxes trail the main boxes by this many stages (<= D)
   int halo_off;                                      // diagnostics only: skip halo boxes (wrong edges; traffic attribution)
@@ -208,17 +210,20 @@ struct K2Tma {
     uint32_t ph = 0;
     const int hd = p.hdelay;
     // loose lockstep: only when every tile has its own resident CTA
-    const bool sync = p.progress != nullptr && p.n_tiles <= int(gridDim.x);
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+    const bool sync = p.progress != nullptr && p.n_tiles <= int(gridDim.x) && p.n_chunks == 1;
+    for (int item = blockIdx.x; item < p.n_tiles * p.n_chunks; item += gridDim.x) {
+      const int tile = item % p.n_tiles, chunk = item / p.n_tiles;
       const int x0 = (tile % p.tiles_x) * TX;
       const int y0 = (tile / p.tiles_x) * p.ty;
-      for (int k = int(p.kbeg); k < int(p.kend); ++k) {
+      const int kb = int(p.kbeg + chunk * p.zchunk);
+      const int ke = int(min(p.kend, p.kbeg + (chunk + 1) * p.zchunk));
+      for (int k = kb; k < ke; ++k) {
         if (sync)   // the pacer warp grants planes (neighbour-progress window)
           while (int(k - p.kbeg) >= *permit) __nanosleep(32);
         if (p.pf_dist > 0) {   // keep pf_dist planes of this tile on their way into L2
-          if (k == int(p.kbeg))
-            for (int q = 1; q < p.pf_dist && k + q < int(p.kend); ++q) prefetch_main(tm, x0, y0, k + q);
-          if (k + p.pf_dist < int(p.kend)) prefetch_main(tm, x0, y0, k + p.pf_dist);
+          if (k == kb)
+            for (int q = 1; q < p.pf_dist && k + q < ke; ++q) prefetch_main(tm, x0, y0, k + q);
+          if (k + p.pf_dist < ke) prefetch_main(tm, x0, y0, k + p.pf_dist);
         }
         mbar_wait_backoff(&empty[s], ph ^ 1u);
         mbar_expect_tx(&full[s], p.stage_bytes);
@@ -282,11 +287,13 @@ struct K2Tma {
     const bool validate = p.err != nullptr;
     const bool t_zero = (p.theta == T(0));
     const bool top = ty == 0, bot = ty == p.ty - 1;
-    const bool sync = p.progress != nullptr && p.n_tiles <= int(gridDim.x);
+    const bool sync = p.progress != nullptr && p.n_tiles <= int(gridDim.x) && p.n_chunks == 1;
     int errbits = 0;
     int s = 0;
     uint32_t ph = 0;
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+    for (int item = blockIdx.x; item < p.n_tiles * p.n_chunks; item += gridDim.x) {
+      const int tile = item % p.n_tiles, chunk = item / p.n_tiles;
+      const int64_t kb = p.kbeg + chunk * p.zchunk, ke = min(p.kend, kb + p.zchunk);
       const int x0 = (tile % p.tiles_x) * TX;
       const int j = (tile / p.tiles_x) * p.ty + ty;
       const int xi = x0 + cx0;
@@ -320,10 +327,10 @@ struct K2Tma {
       const uint32_t off_svlo = (!jlo && top) ? off_vlo + d_svhalo : off_vlo + d_sv;
       const uint32_t off_svhi = (!jhi && bot) ? off_vhi + d_svhalo : off_vhi + d_sv;
       V wm, w0, swm, sw0;
-      load_w(p, p.kbeg - 1, off2d, act, wm, swm);
-      load_w(p, p.kbeg, off2d, act, w0, sw0);
-      int64_t o = p.kbeg * plane + off2d;
-      for (int64_t k = p.kbeg; k < p.kend; ++k, o += plane) {
+      load_w(p, kb - 1, off2d, act, wm, swm);
+      load_w(p, kb, off2d, act, w0, sw0);
+      int64_t o = kb * plane + off2d;
+      for (int64_t k = kb; k < ke; ++k, o += plane) {
         mbar_wait(&full[s], ph);
         const Stage& S_ = st[s];
         const char* sb = reinterpret_cast<const char*>(&S_);
@@ -431,7 +438,7 @@ k2_tma_kernel(const __grid_constant__ TmaMaps tm, const TmaParams<T> p) {
   if (warp == C::TYMAX && (threadIdx.x & 31) < kNumMaps) tma_prefetch_desc(&tm.m[threadIdx.x & 31]);
   __syncthreads();
   __shared__ int permit;
-  const bool sync = p.progress != nullptr && p.n_tiles <= int(gridDim.x);
+  const bool sync = p.progress != nullptr && p.n_tiles <= int(gridDim.x) && p.n_chunks == 1;
   if (threadIdx.x == 0) permit = sync ? 0 : 0x7fffffff;
   __syncthreads();
   if (warp == C::TYMAX) {

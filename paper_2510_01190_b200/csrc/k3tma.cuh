@@ -95,6 +95,8 @@ struct K3Params {
   int64_t nzl, z0, nzg, kbeg, kend;
   int64_t comp_stride;                                   // Nl = nx*ny*nzl
   int nx, ny, ty, tiles_x, n_tiles, M;
+  int n_chunks;                                      // z-chunks per tile column (small planes: > 1)
+  int64_t zchunk;
   int has_w;                                             // 0: 2D ensemble (u, v only)
   unsigned long long* progress;                          // per-tile progress flags (nullptr: no lockstep)
   unsigned long long epoch;                              // launch tag in the flags' high word
@@ -145,10 +147,12 @@ struct K3 {
       }
       if (++s == S) { s = 0; ph ^= 1u; }
     };
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+    for (int wi = blockIdx.x; wi < p.n_tiles * p.n_chunks; wi += gridDim.x) {
+      const int tile = wi % p.n_tiles, chunk = wi / p.n_tiles;
+      const int ke = int(min(p.kend, p.kbeg + (chunk + 1) * p.zchunk));
       const int x0 = (tile % p.tiles_x) * TX;
       const int y0 = (tile / p.tiles_x) * p.ty;
-      const int kb = int(p.kbeg);
+      const int kb = int(p.kbeg + chunk * p.zchunk);
       const int nb = n_blocks(p);
       if (p.has_w) {
         if (kb - 1 >= 0)
@@ -158,7 +162,7 @@ struct K3 {
       // loose inter-CTA lockstep (as K2): before plane k, wait (bounded) until
       // every neighbour tile has consumed plane k - W, so the delayed halo
       // boxes find the neighbour's bytes in L2
-      const bool sync = p.progress != nullptr && p.n_tiles <= int(gridDim.x);
+      const bool sync = p.progress != nullptr && p.n_tiles <= int(gridDim.x) && p.n_chunks == 1;
       const int tcol = tile % p.tiles_x;
       int nbr[4], n_nbr = 0;
       if (tcol > 0) nbr[n_nbr++] = tile - 1;
@@ -166,7 +170,7 @@ struct K3 {
       if (tile >= p.tiles_x) nbr[n_nbr++] = tile - p.tiles_x;
       if (tile + p.tiles_x < p.n_tiles) nbr[n_nbr++] = tile + p.tiles_x;
       int seen = -1;   // min consumed planes over the neighbours, as last observed
-      for (int k = kb; k < int(p.kend); ++k) {
+      for (int k = kb; k < ke; ++k) {
         const int need = (k - kb) - p.sync_w;
         for (int spin = 0; sync && seen < need && spin < p.sync_spin; ++spin) {
           unsigned long long f[4];
@@ -294,10 +298,12 @@ struct K3 {
     const int side = lane / p.ty, row = lane % p.ty;
     const bool has_x = lane < 2 * p.ty;
     const int nb = n_blocks(p);
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
-      const int kb = int(p.kbeg);
+    for (int wi = blockIdx.x; wi < p.n_tiles * p.n_chunks; wi += gridDim.x) {
+      const int tile = wi % p.n_tiles, chunk = wi / p.n_tiles;
+      const int ke = int(min(p.kend, p.kbeg + (chunk + 1) * p.zchunk));
+      const int kb = int(p.kbeg + chunk * p.zchunk);
       if (p.has_w) r.skip((kb - 1 >= 0 ? nb : 0) + nb, lane);
-      for (int k = kb; k < int(p.kend); ++k) {
+      for (int k = kb; k < ke; ++k) {
         {  // u: the 2*TY x-halo points
           ShiftedMoments<1> acc;
 #pragma unroll 1
@@ -375,7 +381,9 @@ struct K3 {
     Ring r{st, full, empty, 0, 0u};
     int xbuf = 0;
     const uint2 zr = make_uint2(0u, 0u);
-    for (int tile = blockIdx.x; tile < p.n_tiles; tile += gridDim.x) {
+    for (int wi = blockIdx.x; wi < p.n_tiles * p.n_chunks; wi += gridDim.x) {
+      const int tile = wi % p.n_tiles, chunk = wi / p.n_tiles;
+      const int ke = int(min(p.kend, p.kbeg + (chunk + 1) * p.zchunk));
       const int x0 = (tile % p.tiles_x) * TX;
       const int j = (tile / p.tiles_x) * p.ty + ty;
       const int xi = x0 + cx0;
@@ -383,7 +391,7 @@ struct K3 {
       const int64_t off2d = int64_t(j) * p.nx + xi;
       const bool jlo = j == 0, jhi = j == p.ny - 1;
       const float cy = (jlo || jhi) ? p.cy_bd : p.cy_in;
-      const int kb = int(p.kbeg);
+      const int kb = int(p.kbeg + chunk * p.zchunk);
       V4 w0_mu = V4{{0.f, 0.f, 0.f, 0.f}}, w0_sg = w0_mu;
       uint2 w0_r = zr;
       {
@@ -399,7 +407,7 @@ struct K3 {
       }
       if (p.has_w) row_moments(p, r, ty, cx0, lane, validate, err, w0_mu, w0_r, w0_sg);
       int64_t o = int64_t(kb) * plane + off2d;
-      for (int k = kb; k < int(p.kend); ++k, o += plane) {
+      for (int k = kb; k < ke; ++k, o += plane) {
         const int64_t kg = p.z0 + k;
         // 2D: no z terms (w moments are zero, so c*(0-0) adds exactly 0)
         const bool klo = p.has_w && kg == 0, khi = p.has_w && kg == p.nzg - 1;
@@ -525,7 +533,7 @@ struct K3 {
           if (p.out_psrc) st_stream<float, 4>(p.out_psrc + o, ops);
           if (p.out_psnk) st_stream<float, 4>(p.out_psnk + o, opk);
         }
-        if (ty == 0 && lane == 0 && p.progress != nullptr && p.n_tiles <= int(gridDim.x))
+        if (ty == 0 && lane == 0 && p.progress != nullptr && p.n_tiles <= int(gridDim.x) && p.n_chunks == 1)
           st_relaxed_u64(p.progress + size_t(tile) * kFlagStride,   // planes consumed, for the pacing
                          ((p.epoch & 0xffffffffull) << 32) | (unsigned long long)(k - kb + 1));
       }

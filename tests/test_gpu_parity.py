@@ -675,3 +675,28 @@ def test_gather2d_matches_stencil_kernel_bitwise(dev, dtype, shape, rng, monkeyp
             monkeypatch.delenv("DIVUQ_NO_ROWMARCH")
             return o
         both(fused)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("shape", [(128, 40, 70), (127, 40, 70), (64, 16, 300)])
+def test_zchunked_tma_kernels_bitwise(dev, dtype, shape, rng, monkeypatch):
+    """Small planes (fewer tile columns than SMs): the TMA K2 / flat K2 / K3
+    kernels split each column's z range into chunks that restart the
+    z-march; the bits are the unchunked ones."""
+    nx, ny, nz = shape
+    f = _model3d(nx, ny, nz, rng, dtype)
+    ins = [cu(x) for x in f]
+
+    def both(fn):
+        a = fn()
+        monkeypatch.setenv("DIVUQ_NO_ZCHUNK", "1")
+        b = fn()
+        monkeypatch.delenv("DIVUQ_NO_ZCHUNK")
+        for k in a:
+            assert torch.equal(a[k], b[k]), k
+
+    both(lambda: dev.propagate3d(*ins, nx, ny, nz, 0.5, 1.5, 0.75, 0.1))
+    both(lambda: dev.propagate3d(*ins, nx, ny, nz, 0.5, 1.5, 0.75, 0.1, k_range=(3, nz - 2)))
+    if dtype == np.float32:
+        mem = cu(rng.normal(size=(4, 3, nx * ny * nz)).astype(np.float32))
+        both(lambda: dev.ensemble_divergence3d(mem, nx, ny, nz, 1.0, 1.0, 1.0, 0.1, moments=True))

@@ -53,3 +53,15 @@ for nx in (4096, 4095):
     mu, sg = torch.randn(nx * ny, device="cuda", dtype=torch.float64), torch.rand(nx * ny, device="cuda", dtype=torch.float64)
     ms = timeit(lambda: dev.lcp2d(mu, sg, nx, ny, 0.0, check=ERR))
     print(f"lcp2d fp64 {nx}x{ny}: {ms * 1e3:.1f} us, {24 * (nx - 1) * (ny - 1) / ms / 1e6 / PEAK * 100:.1f} % HBM")
+for nx in (512, 511):
+    ny, nz, m = 128, 64, 16
+    mem = torch.randn(m, 3, nx * ny * nz, device="cuda")
+    ms = timeit(lambda: dev.ensemble_divergence3d(mem, nx, ny, nz, 1.0, 1.0, 1.0, 0.1, check=ERR))
+    print(f"ensemble_divergence3d M=16 {nx}x{ny}x{nz}: {ms * 1e3:.1f} us, {(192 + 16) * nx * ny * nz / ms / 1e6 / PEAK * 100:.1f} % HBM")
+for nx in (128, 127):
+    ny, nz = 128, 1024
+    n = nx * ny * nz
+    f = [torch.randn(n, device="cuda") for _ in range(3)] + [torch.rand(n, device="cuda") * 0.3 + 0.05 for _ in range(3)]
+    out = {k: torch.empty(n, device="cuda") for k in dev.ALL_OUTPUTS}
+    ms = timeit(lambda: dev.propagate3d(*f, nx, ny, nz, 1.0, 1.0, 1.0, 0.0, out=out, check=ERR))
+    print(f"propagate3d fp32 small planes {nx}x{ny}x{nz}: {ms * 1e3:.1f} us, {40 * n / ms / 1e6 / PEAK * 100:.1f} % HBM")
