@@ -245,6 +245,24 @@ void z_chunks(int n_tiles, int64_t nk, int64_t sms, int* n_chunks, int64_t* zchu
   *n_chunks = int(std::max<int64_t>(1, (nk + zc - 1) / zc));
 }
 
+// Tile height for the persistent TMA kernels: minimise the rows x planes the
+// busiest SM marches, counting z-chunks (z_chunks above) when the tile
+// columns do not fill the GPU; ties go to the taller tile (more warps).
+int pick_ty(int64_t tiles_x, int64_t ny, int64_t nk, int tymax, int64_t sms) {
+  int ty = tymax;
+  int64_t best = INT64_MAX;
+  for (int cand = tymax; cand >= 8; --cand) {
+    const int64_t tiles = tiles_x * ((ny + cand - 1) / cand);
+    int nch = 1;
+    int64_t zc = nk;
+    z_chunks(int(std::min<int64_t>(tiles, INT32_MAX)), nk, sms, &nch, &zc);
+    const int64_t items = tiles * nch;
+    const int64_t cost = ((items + sms - 1) / sms) * cand * zc;
+    if (cost < best) { best = cost; ty = cand; }
+  }
+  return ty;
+}
+
 template <typename T, bool HAS_SIGMA>
 int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
   using C = TmaCfg<T>;
@@ -253,13 +271,7 @@ int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
   // lockstep, so pick TY minimising (waves of tiles) x (rows per tile)
   const int64_t sms = sm_count();
   const int64_t tiles_x = (sp.nx + C::TX - 1) / C::TX;
-  int ty = C::TYMAX;
-  int64_t best = INT64_MAX;
-  for (int cand = C::TYMAX; cand >= 8; --cand) {
-    const int64_t tiles = tiles_x * ((sp.ny + cand - 1) / cand);
-    const int64_t cost = ((tiles + sms - 1) / sms) * cand;
-    if (cost < best) { best = cost; ty = cand; }
-  }
+  int ty = pick_ty(tiles_x, sp.ny, sp.kend - sp.kbeg, C::TYMAX, sms);
   if (const int64_t forced = env_int("DIVUQ_TMA_TY", 0)) ty = int(std::max<int64_t>(1, std::min<int64_t>(forced, C::TYMAX)));
   // main boxes: whole 512-byte rows, L2 fill promotion on; halo boxes: 16-byte
   // columns / single rows, no promotion (they are L2 hits by design)
@@ -355,13 +367,7 @@ int try_k3_tma(const StencilParams<float>& sp, int comps, cudaStream_t s, bool* 
   if (sp.nx > (int64_t(1) << 30) || sp.ny > (int64_t(1) << 30) || sp.nzl > (int64_t(1) << 30)) return DIVUQ_OK;
   const int64_t sms = sm_count();
   const int64_t tiles_x = (sp.nx + C::TX - 1) / C::TX;
-  int ty = C::TYMAX;
-  int64_t best = INT64_MAX;
-  for (int cand = C::TYMAX; cand >= 8; --cand) {
-    const int64_t tiles = tiles_x * ((sp.ny + cand - 1) / cand);
-    const int64_t cost = ((tiles + sms - 1) / sms) * cand;
-    if (cost < best) { best = cost; ty = cand; }
-  }
+  int ty = pick_ty(tiles_x, sp.ny, sp.kend - sp.kbeg, C::TYMAX, sms);
   if (const int64_t forced = env_int("DIVUQ_TMA_TY", 0)) ty = int(std::max<int64_t>(1, std::min<int64_t>(forced, C::TYMAX)));
   K3Maps tm;
   std::memset(&tm, 0, sizeof(tm));
@@ -433,13 +439,7 @@ int launch_k2_flat(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
   if (n + 2 * plane + C::UW >= (int64_t(1) << 31)) return DIVUQ_OK;
   const int64_t sms = sm_count();
   const int64_t tiles_x = (sp.nx + C::TX - 1) / C::TX;
-  int ty = C::TYMAX;
-  int64_t best = INT64_MAX;
-  for (int cand = C::TYMAX; cand >= 8; --cand) {
-    const int64_t tiles = tiles_x * ((sp.ny + cand - 1) / cand);
-    const int64_t cost = ((tiles + sms - 1) / sms) * cand;
-    if (cost < best) { best = cost; ty = cand; }
-  }
+  int ty = pick_ty(tiles_x, sp.ny, sp.kend - sp.kbeg, C::TYMAX, sms);
   FlatMaps fm;
   std::memset(&fm, 0, sizeof(fm));
   const T* arrs[6] = {sp.mu_u, sp.s_u, sp.mu_v, sp.s_v, sp.mu_w, sp.s_w};

@@ -65,3 +65,9 @@ for nx in (128, 127):
     out = {k: torch.empty(n, device="cuda") for k in dev.ALL_OUTPUTS}
     ms = timeit(lambda: dev.propagate3d(*f, nx, ny, nz, 1.0, 1.0, 1.0, 0.0, out=out, check=ERR))
     print(f"propagate3d fp32 small planes {nx}x{ny}x{nz}: {ms * 1e3:.1f} us, {40 * n / ms / 1e6 / PEAK * 100:.1f} % HBM")
+for nx, ny, nz in ((256, 256, 512), (256, 200, 300), (512, 512, 512)):
+    n = nx * ny * nz
+    f = [torch.randn(n, device="cuda") for _ in range(3)] + [torch.rand(n, device="cuda") * 0.3 + 0.05 for _ in range(3)]
+    out = {k: torch.empty(n, device="cuda") for k in dev.ALL_OUTPUTS}
+    ms = timeit(lambda: dev.propagate3d(*f, nx, ny, nz, 1.0, 1.0, 1.0, 0.0, out=out, check=ERR))
+    print(f"propagate3d fp32 {nx}x{ny}x{nz}: {ms * 1e3:.1f} us, {40 * n / ms / 1e6 / PEAK * 100:.1f} % HBM")
