@@ -232,15 +232,29 @@ cudaError_t progress_flags(unsigned long long** flags_out, unsigned long long* e
   return cudaSuccess;
 }
 
-// Small planes (fewer tile columns than SMs): split each column's z range
-// into chunks so every SM gets a work item; each chunk restarts the z-march
-// (two w planes by plain loads), so chunks stay >= 16 planes.  Results are
-// the same bits: every point's arithmetic is unchanged.
+// Work items for the persistent TMA kernels: whole tile columns, or -- when
+// the columns do not spread evenly over the SMs (fewer columns than SMs, or
+// a last wave mostly empty) -- columns cut into z-chunks.  Each chunk restarts
+// the z-march (two w planes by plain loads, a pipeline fill: ~2 planes of
+// cost) and runs without the neighbour lockstep, so chunking is taken only
+// when it cuts the busiest SM's planes by more than 15 %.  Results are the
+// same bits: every point's arithmetic is unchanged.
 void z_chunks(int n_tiles, int64_t nk, int64_t sms, int* n_chunks, int64_t* zchunk) {
-  int64_t nch = 1;
-  if (n_tiles > 0 && n_tiles < sms && !env_int("DIVUQ_NO_ZCHUNK", 0))
-    nch = std::max<int64_t>(1, std::min<int64_t>(sms / n_tiles, nk / 16));   // one wave of items
-  const int64_t zc = std::max<int64_t>(1, (nk + nch - 1) / nch);
+  int64_t best_n = 1;
+  if (n_tiles > 0 && nk > 0 && !env_int("DIVUQ_NO_ZCHUNK", 0)) {
+    auto cost = [&](int64_t nch) {
+      const int64_t zc = (nk + nch - 1) / nch;
+      return ((int64_t(n_tiles) * nch + sms - 1) / sms) * (zc + 2);
+    };
+    const int64_t c1 = cost(1);
+    int64_t best = c1;
+    for (int64_t nch = 2; nch <= nk / 16; ++nch) {
+      const int64_t c = cost(nch);
+      if (c < best) { best = c; best_n = nch; }
+    }
+    if (best * 100 > c1 * 85) best_n = 1;
+  }
+  const int64_t zc = std::max<int64_t>(1, (nk + best_n - 1) / best_n);
   *zchunk = zc;
   *n_chunks = int(std::max<int64_t>(1, (nk + zc - 1) / zc));
 }
@@ -257,7 +271,9 @@ int pick_ty(int64_t tiles_x, int64_t ny, int64_t nk, int tymax, int64_t sms) {
     int64_t zc = nk;
     z_chunks(int(std::min<int64_t>(tiles, INT32_MAX)), nk, sms, &nch, &zc);
     const int64_t items = tiles * nch;
-    const int64_t cost = ((items + sms - 1) / sms) * cand * zc;
+    // a CTA with fewer than 12 consumer rows streams less than a full one:
+    // count short tiles as 12 rows
+    const int64_t cost = ((items + sms - 1) / sms) * std::max(cand, 12) * (nch > 1 ? zc + 2 : zc);
     if (cost < best) { best = cost; ty = cand; }
   }
   return ty;
