@@ -138,9 +138,12 @@ int dispatch_vec(const StencilParams<T>& p, bool has_sigma, cudaStream_t s) {
     const int64_t tiles_vec = ((p.nx + 32 * VW - 1) / (32 * VW)) * ((p.ny + kStencilTY - 1) / kStencilTY);
     if (tiles_vec * (p.kend - p.kbeg) < sm_count()) vec = false;
   }
-  if constexpr (!HAS_W) {   // 2D: the gather kernel where the vector kernel cannot run
-    if ((!vec || env_int("DIVUQ_GATHER2D", 0)) && !env_int("DIVUQ_NO_GATHER2D", 0) && p.kbeg == 0 &&
-        p.kend == 1) {
+  if constexpr (!HAS_W) {   // 2D: the gather kernel where the vector kernel cannot run,
+                            // and for fp64 from 512^2 up (tools/p2d_probe.py: 4096^2
+                            // 377 -> 299 us; the vector kernel stays ahead below)
+    const bool big64 = sizeof(T) == 8 && p.nx * p.ny >= (int64_t(1) << 18);
+    if ((!vec || big64 || env_int("DIVUQ_GATHER2D", 0)) && !env_int("DIVUQ_NO_GATHER2D", 0) &&
+        p.kbeg == 0 && p.kend == 1) {
       if (SRC == kResidual || has_sigma) return launch_gather2d<T, true, SRC>(p, s);
       return launch_gather2d<T, false, SRC>(p, s);
     }
