@@ -159,6 +159,9 @@ StencilParams<T> blank_params() {
   return p;
 }
 
+template <typename T, bool HAS_SIGMA, bool HAS_W = true>
+int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used);   // below
+
 template <typename T>
 int propagate2d(const T* mu_u, const T* mu_v, const T* s_u, const T* s_v, int64_t nx, int64_t ny,
                 double dx, double dy, double t, T* out_mu, T* out_sigma, T* out_ps, T* out_pk,
@@ -174,6 +177,22 @@ int propagate2d(const T* mu_u, const T* mu_v, const T* s_u, const T* s_v, int64_
   p.theta = T(t);
   p.out_mu = out_mu; p.out_sigma = out_sigma; p.out_psrc = out_ps; p.out_psnk = out_pk;
   p.err = err;
+  // large 2D grids: the 3D TMA pipeline without w (one "plane", tiles as work
+  // items); small ones stay on the register kernels (launch-latency bound)
+  if (!env_int("DIVUQ_NO_TMA", 0) && !env_int("DIVUQ_NO_TMA2D", 0) && nx * ny >= (int64_t(1) << 18) &&
+      nx % TmaCfg<T>::VEC == 0 && nx < (int64_t(1) << 31) && ny < (int64_t(1) << 31)) {
+    bool ok = true;
+    for (const void* q : {(const void*)mu_u, (const void*)mu_v, (const void*)s_u, (const void*)s_v,
+                          (const void*)out_mu, (const void*)out_sigma, (const void*)out_ps, (const void*)out_pk})
+      ok = ok && aligned(q, 16);
+    if (ok) {
+      bool used = false;
+      const cudaStream_t cs = static_cast<cudaStream_t>(stream);
+      const int r = has_sigma ? launch_k2_tma<T, true, false>(p, cs, &used)
+                              : launch_k2_tma<T, false, false>(p, cs, &used);
+      if (r || used) return r;
+    }
+  }
   return dispatch_vec<T, false, kMoments>(p, has_sigma, static_cast<cudaStream_t>(stream));
 }
 
@@ -282,7 +301,7 @@ int pick_ty(int64_t tiles_x, int64_t ny, int64_t nk, int tymax, int64_t sms) {
   return ty;
 }
 
-template <typename T, bool HAS_SIGMA>
+template <typename T, bool HAS_SIGMA, bool HAS_W>
 int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
   using C = TmaCfg<T>;
   *used = false;
@@ -298,8 +317,10 @@ int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
   TmaMaps tm;
   std::memset(&tm, 0, sizeof(tm));
   const T* arrs[6] = {sp.mu_u, sp.mu_v, sp.mu_w, sp.s_u, sp.s_v, sp.s_w};
-  for (int a = 0; a < (HAS_SIGMA ? 6 : 3); ++a)
+  for (int a = 0; a < (HAS_SIGMA ? 6 : 3); ++a) {
+    if (!HAS_W && (a == 2 || a == 5)) { tm.m[kMapU + a] = tm.m[kMapU + a - 2]; continue; }   // 2D: no w
     if (!make_map3d<T>(&tm.m[kMapU + a], arrs[a], sp.nx, sp.ny, sp.nzl, C::TX, ty, promo)) return DIVUQ_OK;
+  }
   if (!make_map3d<T>(&tm.m[kMapUH], sp.mu_u, sp.nx, sp.ny, sp.nzl, C::PAD, ty, 0)) return DIVUQ_OK;
   if (!make_map3d<T>(&tm.m[kMapVH], sp.mu_v, sp.nx, sp.ny, sp.nzl, C::TX, 1, 0)) return DIVUQ_OK;
   if (HAS_SIGMA) {
@@ -336,7 +357,7 @@ int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
   const int64_t min_planes = env_int("DIVUQ_K2_SYNC_MIN_PLANES", 64);
   if (p.sync_w > 0 && p.n_tiles <= kMaxFlagTiles && sp.kend - sp.kbeg >= min_planes)
     DIVUQ_CUDA(progress_flags(&p.progress, &p.epoch));
-  p.stage_bytes = uint32_t((3 * ty * C::TX + (p.halo_off ? 0 : 2 * ty * C::PAD + 2 * C::TX)) *
+  p.stage_bytes = uint32_t(((HAS_W ? 3 : 2) * ty * C::TX + (p.halo_off ? 0 : 2 * ty * C::PAD + 2 * C::TX)) *
                            sizeof(T)) * (HAS_SIGMA ? 2u : 1u);
   const int64_t n_work = int64_t(p.n_tiles) * (sp.kend - sp.kbeg);
   p.cx_in = sp.cx_in; p.cx_bd = sp.cx_bd; p.cy_in = sp.cy_in; p.cy_bd = sp.cy_bd;
@@ -344,7 +365,7 @@ int launch_k2_tma(const StencilParams<T>& sp, cudaStream_t s, bool* used) {
   p.out_mu = sp.out_mu; p.out_sigma = sp.out_sigma; p.out_psrc = sp.out_psrc; p.out_psnk = sp.out_psnk;
   p.err = sp.err;
   if (n_work <= 0) { *used = true; return DIVUQ_OK; }
-  auto kern = k2_tma_kernel<T, HAS_SIGMA>;
+  auto kern = k2_tma_kernel<T, HAS_SIGMA, HAS_W>;
   const size_t smem = sizeof(TmaStage<T>) * C::S + 2 * C::S * sizeof(uint64_t);
   // function attributes are per device context: set on every launch (cheap)
   DIVUQ_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));

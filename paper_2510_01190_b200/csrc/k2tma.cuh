@@ -116,7 +116,7 @@ struct TmaParams {
   int* err;
 };
 
-template <typename T, bool HAS_SIGMA>
+template <typename T, bool HAS_SIGMA, bool HAS_W = true>
 struct K2Tma {
   using C = TmaCfg<T>;
   using V = Vec<T, C::VEC>;
@@ -157,7 +157,7 @@ struct K2Tma {
                                                T wh, T sl, T sh, T svl, T svh, T swl, T swh,
                                                T cx, T cy, T cz, bool t_zero, T& m, T& sg, T& ps,
                                                T& pk) {
-    using SM = StencilMath<T, true>;
+    using SM = StencilMath<T, HAS_W>;   // 2D (HAS_W false): the reference's 2D order
     m = SM::mean(uh, ul, vh, vl, wh, wl, cx, cy, cz);
     if constexpr (HAS_SIGMA)
       Tails<T>::eval(m, SM::var(sh, sl, svh, svl, swh, swl, cx, cy, cz), p.theta, t_zero, sg, ps, pk);
@@ -169,22 +169,22 @@ struct K2Tma {
                                                     int x0, int y0, int k) {
     tma_load_3d(&st.u[0][0], &tm.m[kMapU], bar, x0, y0, k);
     tma_load_3d(&st.v[0][0], &tm.m[kMapV], bar, x0, y0, k);
-    tma_load_3d(&st.w[0][0], &tm.m[kMapW], bar, x0, y0, k + 1);
+    if constexpr (HAS_W) tma_load_3d(&st.w[0][0], &tm.m[kMapW], bar, x0, y0, k + 1);
     if constexpr (HAS_SIGMA) {
       tma_load_3d(&st.su[0][0], &tm.m[kMapSU], bar, x0, y0, k);
       tma_load_3d(&st.sv[0][0], &tm.m[kMapSV], bar, x0, y0, k);
-      tma_load_3d(&st.sw[0][0], &tm.m[kMapSW], bar, x0, y0, k + 1);
+      if constexpr (HAS_W) tma_load_3d(&st.sw[0][0], &tm.m[kMapSW], bar, x0, y0, k + 1);
     }
   }
 
   static __device__ __forceinline__ void prefetch_main(const TmaMaps& tm, int x0, int y0, int k) {
     tma_prefetch_l2_3d(&tm.m[kMapU], x0, y0, k);
     tma_prefetch_l2_3d(&tm.m[kMapV], x0, y0, k);
-    tma_prefetch_l2_3d(&tm.m[kMapW], x0, y0, k + 1);
+    if constexpr (HAS_W) tma_prefetch_l2_3d(&tm.m[kMapW], x0, y0, k + 1);
     if constexpr (HAS_SIGMA) {
       tma_prefetch_l2_3d(&tm.m[kMapSU], x0, y0, k);
       tma_prefetch_l2_3d(&tm.m[kMapSV], x0, y0, k);
-      tma_prefetch_l2_3d(&tm.m[kMapSW], x0, y0, k + 1);
+      if constexpr (HAS_W) tma_prefetch_l2_3d(&tm.m[kMapSW], x0, y0, k + 1);
     }
   }
 
@@ -326,9 +326,11 @@ struct K2Tma {
                                          reinterpret_cast<const char*>(&st[0].v_top[0]));
       const uint32_t off_svlo = (!jlo && top) ? off_vlo + d_svhalo : off_vlo + d_sv;
       const uint32_t off_svhi = (!jhi && bot) ? off_vhi + d_svhalo : off_vhi + d_sv;
-      V wm, w0, swm, sw0;
-      load_w(p, kb - 1, off2d, act, wm, swm);
-      load_w(p, kb, off2d, act, w0, sw0);
+      V wm = zero(), w0 = zero(), swm = zero(), sw0 = zero();
+      if constexpr (HAS_W) {
+        load_w(p, kb - 1, off2d, act, wm, swm);
+        load_w(p, kb, off2d, act, w0, sw0);
+      }
       int64_t o = kb * plane + off2d;
       for (int64_t k = kb; k < ke; ++k, o += plane) {
         mbar_wait(&full[s], ph);
@@ -338,7 +340,7 @@ struct K2Tma {
         const V v_own = validate ? lds(&S_.v[ty][cx0]) : zero();   // validation only
         const V v_lo = lds(reinterpret_cast<const T*>(sb + off_vlo));
         const V v_hi = lds(reinterpret_cast<const T*>(sb + off_vhi));
-        V wp = lds(&S_.w[ty][cx0]);
+        V wp = HAS_W ? lds(&S_.w[ty][cx0]) : zero();
         T u_l = __shfl_up_sync(0xffffffffu, u_own.v[VEC - 1], 1);
         T u_r = __shfl_down_sync(0xffffffffu, u_own.v[0], 1);
         if (lane == 0) u_l = S_.u_l[ty][PAD - 1];
@@ -350,7 +352,7 @@ struct K2Tma {
           if (validate) sv_own = lds(&S_.sv[ty][cx0]);
           sv_lo = lds(reinterpret_cast<const T*>(sb + off_svlo));
           sv_hi = lds(reinterpret_cast<const T*>(sb + off_svhi));
-          swp = lds(&S_.sw[ty][cx0]);
+          if constexpr (HAS_W) swp = lds(&S_.sw[ty][cx0]);
           s_l = __shfl_up_sync(0xffffffffu, su_own.v[VEC - 1], 1);
           s_r = __shfl_down_sync(0xffffffffu, su_own.v[0], 1);
           if (lane == 0) s_l = S_.su_l[ty][PAD - 1];
@@ -362,7 +364,7 @@ struct K2Tma {
           st_relaxed_u64(p.progress + size_t(tile) * kFlagStride,
                          ((p.epoch & 0xffffffffull) << 32) | (unsigned long long)(k - p.kbeg + 1));
         if (++s == S) { s = 0; ph ^= 1u; }
-        if (k + 1 == p.nzl) load_w(p, k + 1, off2d, act, wp, swp);  // past the slab: halo or none
+        if (HAS_W && k + 1 == p.nzl) load_w(p, k + 1, off2d, act, wp, swp);  // past the slab: halo or none
 
         if (act && p.diag_null) {   // diagnostics: pipeline + stores only, no math
           V z;
@@ -401,6 +403,7 @@ struct K2Tma {
               errbits |= check_value(u_own.v[e]) | check_value(v_own.v[e]) | check_value(w0.v[e]);
               if constexpr (HAS_SIGMA)
                 errbits |= check_sigma(su_own.v[e]) | check_sigma(sv_own.v[e]) | check_sigma(sw0.v[e]);
+              // (2D: w0 / sw0 are zeros, so their checks never fire)
             }
           }
           if (p.out_mu) st_stream<T, VEC>(p.out_mu + o, omu);
@@ -418,7 +421,7 @@ struct K2Tma {
   }
 };
 
-template <typename T, bool HAS_SIGMA>
+template <typename T, bool HAS_SIGMA, bool HAS_W = true>
 __global__ void __launch_bounds__(TmaCfg<T>::THREADS, 1)
 k2_tma_kernel(const __grid_constant__ TmaMaps tm, const TmaParams<T> p) {
   using C = TmaCfg<T>;
@@ -442,15 +445,15 @@ k2_tma_kernel(const __grid_constant__ TmaMaps tm, const TmaParams<T> p) {
   if (threadIdx.x == 0) permit = sync ? 0 : 0x7fffffff;
   __syncthreads();
   if (warp == C::TYMAX) {
-    if ((threadIdx.x & 31) == 0) K2Tma<T, HAS_SIGMA>::produce(p, tm, st, full, empty, &permit);
+    if ((threadIdx.x & 31) == 0) K2Tma<T, HAS_SIGMA, HAS_W>::produce(p, tm, st, full, empty, &permit);
     return;
   }
   if (warp == C::TYMAX + 1) {
-    if ((threadIdx.x & 31) == 0 && sync) K2Tma<T, HAS_SIGMA>::pace(p, &permit);
+    if ((threadIdx.x & 31) == 0 && sync) K2Tma<T, HAS_SIGMA, HAS_W>::pace(p, &permit);
     return;
   }
   if (warp >= p.ty) return;  // tile shorter than TYMAX: spare warps sit out
-  K2Tma<T, HAS_SIGMA>::consume(p, st, full, empty);
+  K2Tma<T, HAS_SIGMA, HAS_W>::consume(p, st, full, empty);
 }
 
 }  // namespace divuq

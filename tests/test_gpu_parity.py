@@ -700,3 +700,35 @@ def test_zchunked_tma_kernels_bitwise(dev, dtype, shape, rng, monkeypatch):
     if dtype == np.float32:
         mem = cu(rng.normal(size=(4, 3, nx * ny * nz)).astype(np.float32))
         both(lambda: dev.ensemble_divergence3d(mem, nx, ny, nz, 1.0, 1.0, 1.0, 0.1, moments=True))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("shape", [(640, 512), (1024, 600), (512, 1030)])
+def test_tma2d_matches_register_kernels_bitwise(dev, dtype, shape, rng, monkeypatch):
+    """Large 2D grids run the 3D TMA pipeline without w (K2Tma<T, *, false>);
+    the register / gather kernels are the same arithmetic, bit for bit, and
+    fp64 equals the reference order (oracle) bit for bit."""
+    nx, ny = shape
+    n = nx * ny
+    a = [rng.normal(0, 2, n), rng.normal(0, 2, n), rng.uniform(0.05, 0.6, n), rng.uniform(0.05, 0.6, n)]
+    ins = [cu(x.astype(dtype)) for x in a]
+
+    def both(fn):
+        x = fn()
+        monkeypatch.setenv("DIVUQ_NO_TMA2D", "1")
+        y = fn()
+        monkeypatch.delenv("DIVUQ_NO_TMA2D")
+        for k in x:
+            assert torch.equal(x[k], y[k]), k
+        return x
+
+    for t in (0.0, 0.3):
+        o = both(lambda: dev.propagate2d(*ins, nx, ny, 0.7, 1.3, t))
+    both(lambda: dev.propagate2d(*ins, nx, ny, 0.7, 1.3, 0.0, outputs=("mu",)))
+    if dtype == np.float64:
+        mu, sg = ref2d.propagate2d(*a, nx, ny, 0.7, 1.3)
+        assert np.array_equal(host(o["mu"]), mu) and np.array_equal(host(o["sigma"]), sg)
+    bad = [x.clone() for x in ins]
+    bad[3][n // 2] = -1.0
+    with pytest.raises(ValueError):
+        dev.propagate2d(*bad, nx, ny, 0.7, 1.3, 0.0)
