@@ -36,6 +36,9 @@
 #ifndef DIVUQ_GF_MINB
 #define DIVUQ_GF_MINB 4   // TMA variant (the register-staged one runs 2 CTAs / SM)
 #endif
+#ifndef DIVUQ_GF_MINB_LDG
+#define DIVUQ_GF_MINB_LDG 2   // register-staged variant (nx % 4 != 0); 3 / 4 CTAs per SM measured equal / slower
+#endif
 #ifndef DIVUQ_GF_STAGES
 #define DIVUQ_GF_STAGES 2   // 4 CTAs x 2 TMA stages: 8 members (92 KB) in flight per SM
 #endif
@@ -107,7 +110,7 @@ __device__ __forceinline__ void gf_slot(int s, int tid, bool& isx, int& r, int& 
 }
 
 template <bool TMA>
-__global__ void __launch_bounds__(kGfThreads, TMA ? DIVUQ_GF_MINB : 2)
+__global__ void __launch_bounds__(kGfThreads, TMA ? DIVUQ_GF_MINB : DIVUQ_GF_MINB_LDG)
 gradfused_kernel(const __grid_constant__ CUtensorMap map, const GfParams p) {
   extern __shared__ __align__(128) unsigned char gf_smem[];
   const int64_t nx = p.nx, ny = p.ny, N = nx * ny;
