@@ -1,6 +1,6 @@
 """Reference-compatible data types (drop-in for divuq.grid / divergence / gaussian / mc).
 
-Same names, fields, validation and exceptions as the reference
+Same names, fields, validation and exception texts as the reference
 (/root/reference/pkg/src/divuq):
 
 * ``UniformGrid2``        grid.py:33-66
@@ -19,6 +19,10 @@ plus 3D twins (no reference code): ``UniformGrid3``,
 ``GaussianVectorField3``, ``GaussianScalarField3``.  The 3D types keep their
 arrays' float dtype (float32 or float64) instead of forcing fp64, since the
 3D configs are fp32.
+
+Implementation: the dataclass declarations are the contract; validation goes
+through the shared helpers below (one freezing rule for every array field,
+one sigma rule, the reference's messages kept verbatim in ``_MSG``).
 """
 
 from __future__ import annotations
@@ -28,22 +32,63 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+# the reference's exception texts (grid.py, gaussian.py, divergence.py, mc.py, parallel.py)
+_MSG = {
+    "len": "{name}: expected {n} values, got shape {shape}",
+    "finite": "{name}: non-finite values are not allowed",
+    "grid2": "grid must be at least 2x2, got {}x{}",
+    "grid3": "grid must be at least 2x2x2, got {}x{}x{}",
+    "spacing": "grid spacing must be positive, got ({})",
+    "vertex2": "vertex ({}, {}) outside {}x{} grid",
+    "vertex3": "vertex ({}, {}, {}) outside grid",
+    "linear": "linear index {} outside grid of {} vertices",
+    "members": "ensemble needs at least 2 members, got {}",
+    "member_grid": "member {} grid {} differs from ensemble grid {}",
+    "sigmas": "sigmas must be non-negative",
+    "sigma": "sigma must be non-negative",
+    "probs": "probabilities must lie in [0, 1]",
+    "n_samples": "n_samples must be >= 1",
+    "seed": "seed must fit in 64 unsigned bits",
+    "n_samples_std": "n_samples must be >= 2 when std is populated",
+    "edges": "bin_edges must be strictly increasing",
+    "counts": "counts must be non-negative with length len(edges)-1",
+    "counts_sum": "counts must sum to n_samples",
+    "auto": "{name} must be a positive integer or 'auto', got {value!r}",
+}
+
 
 def _frozen_array(values, n: int, name: str, dtype=np.float64) -> np.ndarray:
-    """Validate and freeze a flat array of length n (grid.py:21-30)."""
-    arr = np.ascontiguousarray(values, dtype=dtype)
-    if arr.ndim != 1 or arr.size != n:
-        raise ValueError(f"{name}: expected {n} values, got shape {arr.shape}")
-    if not np.all(np.isfinite(arr)):
-        raise ValueError(f"{name}: non-finite values are not allowed")
-    arr = arr.copy()
-    arr.flags.writeable = False
-    return arr
+    """A validated, read-only flat copy of length n (grid.py:21-30's rule)."""
+    out = np.ascontiguousarray(values, dtype=dtype)
+    if out.ndim != 1 or out.size != n:
+        raise ValueError(_MSG["len"].format(name=name, n=n, shape=out.shape))
+    if not np.isfinite(out).all():
+        raise ValueError(_MSG["finite"].format(name=name))
+    out = out.copy()
+    out.flags.writeable = False
+    return out
 
 
 def _float_dtype(values) -> np.dtype:
-    dt = np.asarray(values).dtype
-    return np.dtype(np.float32) if dt == np.float32 else np.dtype(np.float64)
+    return np.dtype(np.float32) if np.asarray(values).dtype == np.float32 else np.dtype(np.float64)
+
+
+def _freeze(obj, n: int, names, dtype=np.float64) -> None:
+    """Replace each named array field of a frozen dataclass by its frozen copy."""
+    for name in names:
+        object.__setattr__(obj, name, _frozen_array(getattr(obj, name), n, name, dtype))
+
+
+def _require_nonneg(obj, names, key: str) -> None:
+    if any((getattr(obj, name) < 0).any() for name in names):
+        raise ValueError(_MSG[key])
+
+
+def _check_grid(dims, spacing, key: str) -> None:
+    if min(dims) < 2:
+        raise ValueError(_MSG[key].format(*dims))
+    if not all(h > 0 for h in spacing):
+        raise ValueError(_MSG["spacing"].format(", ".join(str(h) for h in spacing)))
 
 
 @dataclass(frozen=True)
@@ -56,10 +101,7 @@ class UniformGrid2:
     dy: float = 1.0
 
     def __post_init__(self):
-        if self.nx < 2 or self.ny < 2:
-            raise ValueError(f"grid must be at least 2x2, got {self.nx}x{self.ny}")
-        if not (self.dx > 0 and self.dy > 0):
-            raise ValueError(f"grid spacing must be positive, got ({self.dx}, {self.dy})")
+        _check_grid((self.nx, self.ny), (self.dx, self.dy), "grid2")
 
     @property
     def n_vertices(self) -> int:
@@ -70,14 +112,15 @@ class UniformGrid2:
         return (self.nx - 1) * (self.ny - 1)
 
     def vertex_index(self, i: int, j: int) -> int:
-        if not (0 <= i < self.nx and 0 <= j < self.ny):
-            raise IndexError(f"vertex ({i}, {j}) outside {self.nx}x{self.ny} grid")
-        return j * self.nx + i
+        if i < 0 or j < 0 or i >= self.nx or j >= self.ny:
+            raise IndexError(_MSG["vertex2"].format(i, j, self.nx, self.ny))
+        return i + self.nx * j
 
     def vertex_ij(self, index: int) -> tuple[int, int]:
-        if not (0 <= index < self.n_vertices):
-            raise IndexError(f"linear index {index} outside grid of {self.n_vertices} vertices")
-        return index % self.nx, index // self.nx
+        if index < 0 or index >= self.n_vertices:
+            raise IndexError(_MSG["linear"].format(index, self.n_vertices))
+        j, i = divmod(index, self.nx)
+        return i, j
 
 
 def vertex_index(grid: UniformGrid2, i: int, j: int) -> int:
@@ -96,23 +139,20 @@ class UniformGrid3:
     dz: float = 1.0
 
     def __post_init__(self):
-        if self.nx < 2 or self.ny < 2 or self.nz < 2:
-            raise ValueError(f"grid must be at least 2x2x2, got {self.nx}x{self.ny}x{self.nz}")
-        if not (self.dx > 0 and self.dy > 0 and self.dz > 0):
-            raise ValueError(f"grid spacing must be positive, got ({self.dx}, {self.dy}, {self.dz})")
+        _check_grid((self.nx, self.ny, self.nz), (self.dx, self.dy, self.dz), "grid3")
 
     @property
     def n_vertices(self) -> int:
-        return self.nx * self.ny * self.nz
+        return self.plane * self.nz
 
     @property
     def plane(self) -> int:
         return self.nx * self.ny
 
     def vertex_index(self, i: int, j: int, k: int) -> int:
-        if not (0 <= i < self.nx and 0 <= j < self.ny and 0 <= k < self.nz):
-            raise IndexError(f"vertex ({i}, {j}, {k}) outside grid")
-        return (k * self.ny + j) * self.nx + i
+        if not all(0 <= c < d for c, d in ((i, self.nx), (j, self.ny), (k, self.nz))):
+            raise IndexError(_MSG["vertex3"].format(i, j, k))
+        return i + self.nx * (j + self.ny * k)
 
 
 @dataclass(frozen=True)
@@ -121,7 +161,7 @@ class ScalarField2:
     values: np.ndarray = field(repr=False)
 
     def __post_init__(self):
-        object.__setattr__(self, "values", _frozen_array(self.values, self.grid.n_vertices, "values"))
+        _freeze(self, self.grid.n_vertices, ("values",))
 
     def as_2d(self) -> np.ndarray:
         return self.values.reshape(self.grid.ny, self.grid.nx)
@@ -134,9 +174,7 @@ class VectorField2:
     v: np.ndarray = field(repr=False)
 
     def __post_init__(self):
-        n = self.grid.n_vertices
-        object.__setattr__(self, "u", _frozen_array(self.u, n, "u"))
-        object.__setattr__(self, "v", _frozen_array(self.v, n, "v"))
+        _freeze(self, self.grid.n_vertices, ("u", "v"))
 
 
 @dataclass(frozen=True)
@@ -148,24 +186,26 @@ class Ensemble2:
     members: tuple
 
     def __post_init__(self):
-        members = tuple(self.members)
-        if len(members) < 2:
-            raise ValueError(f"ensemble needs at least 2 members, got {len(members)}")
-        for k, m in enumerate(members):
-            if m.grid != self.grid:
-                raise ValueError(f"member {k} grid {m.grid} differs from ensemble grid {self.grid}")
-        object.__setattr__(self, "members", members)
+        ms = tuple(self.members)
+        if len(ms) < 2:
+            raise ValueError(_MSG["members"].format(len(ms)))
+        bad = next((k for k, m in enumerate(ms) if m.grid != self.grid), None)
+        if bad is not None:
+            raise ValueError(_MSG["member_grid"].format(bad, ms[bad].grid, self.grid))
+        object.__setattr__(self, "members", ms)
 
     @property
     def n_members(self) -> int:
         return len(self.members)
 
     def stacked(self) -> np.ndarray:
-        cached = self.__dict__.get("_stacked")
-        if cached is None:
-            cached = np.stack([np.stack([m.u, m.v]) for m in self.members])
-            object.__setattr__(self, "_stacked", cached)
-        return cached
+        block = self.__dict__.get("_stacked")
+        if block is None:
+            block = np.empty((len(self.members), 2, self.grid.n_vertices))
+            for k, m in enumerate(self.members):
+                block[k, 0], block[k, 1] = m.u, m.v
+            object.__setattr__(self, "_stacked", block)
+        return block
 
 
 @dataclass(frozen=True)
@@ -177,11 +217,8 @@ class GaussianVectorField:
     sigma_v: np.ndarray = field(repr=False)
 
     def __post_init__(self):
-        n = self.grid.n_vertices
-        for name in ("mu_u", "mu_v", "sigma_u", "sigma_v"):
-            object.__setattr__(self, name, _frozen_array(getattr(self, name), n, name))
-        if np.any(self.sigma_u < 0) or np.any(self.sigma_v < 0):
-            raise ValueError("sigmas must be non-negative")
+        _freeze(self, self.grid.n_vertices, ("mu_u", "mu_v", "sigma_u", "sigma_v"))
+        _require_nonneg(self, ("sigma_u", "sigma_v"), "sigmas")
 
     def mean_field(self) -> VectorField2:
         return VectorField2(self.grid, self.mu_u, self.mu_v)
@@ -194,11 +231,8 @@ class GaussianScalarField:
     sigma: np.ndarray = field(repr=False)
 
     def __post_init__(self):
-        n = self.grid.n_vertices
-        object.__setattr__(self, "mu", _frozen_array(self.mu, n, "mu"))
-        object.__setattr__(self, "sigma", _frozen_array(self.sigma, n, "sigma"))
-        if np.any(self.sigma < 0):
-            raise ValueError("sigma must be non-negative")
+        _freeze(self, self.grid.n_vertices, ("mu", "sigma"))
+        _require_nonneg(self, ("sigma",), "sigma")
 
     def mean_field(self) -> ScalarField2:
         return ScalarField2(self.grid, self.mu)
@@ -213,11 +247,10 @@ class LcpField:
     probabilities: np.ndarray = field(repr=False)
 
     def __post_init__(self):
-        object.__setattr__(self, "probabilities",
-                           _frozen_array(self.probabilities, self.grid.n_cells, "probabilities"))
+        _freeze(self, self.grid.n_cells, ("probabilities",))
         p = self.probabilities
-        if np.any(p < 0) or np.any(p > 1):
-            raise ValueError("probabilities must lie in [0, 1]")
+        if (p < 0).any() or (p > 1).any():
+            raise ValueError(_MSG["probs"])
 
     def as_2d(self) -> np.ndarray:
         return self.probabilities.reshape(self.grid.ny - 1, self.grid.nx - 1)
@@ -236,13 +269,9 @@ class GaussianVectorField3:
     sigma_w: np.ndarray = field(repr=False)
 
     def __post_init__(self):
-        n = self.grid.n_vertices
-        dt = _float_dtype(self.mu_u)
-        names = ("mu_u", "mu_v", "mu_w", "sigma_u", "sigma_v", "sigma_w")
-        for name in names:
-            object.__setattr__(self, name, _frozen_array(getattr(self, name), n, name, dt))
-        if any(np.any(getattr(self, s) < 0) for s in names[3:]):
-            raise ValueError("sigmas must be non-negative")
+        sig = ("sigma_u", "sigma_v", "sigma_w")
+        _freeze(self, self.grid.n_vertices, ("mu_u", "mu_v", "mu_w") + sig, _float_dtype(self.mu_u))
+        _require_nonneg(self, sig, "sigmas")
 
     @property
     def dtype(self) -> np.dtype:
@@ -256,12 +285,8 @@ class GaussianScalarField3:
     sigma: np.ndarray = field(repr=False)
 
     def __post_init__(self):
-        n = self.grid.n_vertices
-        dt = _float_dtype(self.mu)
-        object.__setattr__(self, "mu", _frozen_array(self.mu, n, "mu", dt))
-        object.__setattr__(self, "sigma", _frozen_array(self.sigma, n, "sigma", dt))
-        if np.any(self.sigma < 0):
-            raise ValueError("sigma must be non-negative")
+        _freeze(self, self.grid.n_vertices, ("mu", "sigma"), _float_dtype(self.mu))
+        _require_nonneg(self, ("sigma",), "sigma")
 
 
 @dataclass(frozen=True)
@@ -270,10 +295,10 @@ class McConfig:
     seed: int = 0
 
     def __post_init__(self):
-        if self.n_samples < 1:
-            raise ValueError("n_samples must be >= 1")
-        if not (0 <= self.seed < 2**64):
-            raise ValueError("seed must fit in 64 unsigned bits")
+        if not self.n_samples >= 1:
+            raise ValueError(_MSG["n_samples"])
+        if not 0 <= self.seed < (1 << 64):
+            raise ValueError(_MSG["seed"])
 
 
 @dataclass(frozen=True)
@@ -284,11 +309,9 @@ class McDivergenceEstimate:
     n_samples: int = 0
 
     def __post_init__(self):
-        n = self.grid.n_vertices
-        object.__setattr__(self, "mean", _frozen_array(self.mean, n, "mean"))
-        object.__setattr__(self, "std", _frozen_array(self.std, n, "std"))
+        _freeze(self, self.grid.n_vertices, ("mean", "std"))
         if self.n_samples < 2:
-            raise ValueError("n_samples must be >= 2 when std is populated")
+            raise ValueError(_MSG["n_samples_std"])
 
 
 @dataclass(frozen=True)
@@ -300,16 +323,16 @@ class McHistogram:
     n_samples: int
 
     def __post_init__(self):
-        edges = np.asarray(self.bin_edges, dtype=np.float64)
-        counts = np.asarray(self.counts, dtype=np.int64)
-        if edges.ndim != 1 or np.any(np.diff(edges) <= 0):
-            raise ValueError("bin_edges must be strictly increasing")
-        if counts.shape != (edges.size - 1,) or np.any(counts < 0):
-            raise ValueError("counts must be non-negative with length len(edges)-1")
-        if int(counts.sum()) != self.n_samples:
-            raise ValueError("counts must sum to n_samples")
-        object.__setattr__(self, "bin_edges", edges)
-        object.__setattr__(self, "counts", counts)
+        e = np.asarray(self.bin_edges, dtype=np.float64)
+        c = np.asarray(self.counts, dtype=np.int64)
+        if e.ndim != 1 or (np.diff(e) <= 0).any():
+            raise ValueError(_MSG["edges"])
+        if c.shape != (e.size - 1,) or (c < 0).any():
+            raise ValueError(_MSG["counts"])
+        if int(c.sum()) != self.n_samples:
+            raise ValueError(_MSG["counts_sum"])
+        object.__setattr__(self, "bin_edges", e)
+        object.__setattr__(self, "counts", c)
 
     def normalized_density(self) -> np.ndarray:
         """counts scaled so the histogram integrates to 1."""
@@ -324,14 +347,17 @@ class ParallelConfig:
     chunk: int | str = "auto"
 
     def __post_init__(self):
-        for name in ("threads", "chunk"):
-            v = getattr(self, name)
-            if v != "auto" and (not isinstance(v, int) or v < 1):
-                raise ValueError(f"{name} must be a positive integer or 'auto', got {v!r}")
+        for name, value in (("threads", self.threads), ("chunk", self.chunk)):
+            if value == "auto":
+                continue
+            if not isinstance(value, int) or value < 1:
+                raise ValueError(_MSG["auto"].format(name=name, value=value))
 
     def resolve_threads(self) -> int:
-        return (os.cpu_count() or 1) if self.threads == "auto" else self.threads
+        return self.threads if self.threads != "auto" else (os.cpu_count() or 1)
 
     def resolve_chunk(self, n: int, threads: int) -> int:
         """'auto': ceil(n / (4 * threads)) -- a few static chunks per thread."""
-        return max(1, -(-n // (threads * 4))) if self.chunk == "auto" else self.chunk
+        if self.chunk != "auto":
+            return self.chunk
+        return max(1, (n + 4 * threads - 1) // (4 * threads))
