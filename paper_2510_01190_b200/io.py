@@ -76,23 +76,37 @@ def read_payload_f32(path) -> tuple[UniformGrid2, np.ndarray]:
     return grid, out
 
 
-def write_members(grid: UniformGrid2, members, path) -> None:
-    """Byte-identical to io.py:43-55 (fp64 members rounded to fp32)."""
-    members = tuple(members)
-    block = np.empty((len(members), 2, grid.n_vertices), dtype=np.float32)
-    for k, mb in enumerate(members):
-        block[k, 0] = mb.u
-        block[k, 1] = mb.v
+def _write_planes(grid: UniformGrid2, planes, path) -> None:
+    """(u, v) plane pairs -> one DIVUQ1 file (fp64 values rounded to fp32)."""
+    planes = list(planes)
+    block = np.empty((len(planes), 2, grid.n_vertices), dtype=np.float32)
+    for k, (u, v) in enumerate(planes):
+        block[k] = (u, v)
     _raise(lib.divuq_divuq1_write_f32(os.fsencode(path), grid.nx, grid.ny, float(grid.dx),
-                                      float(grid.dy), len(members), block.ctypes.data),
+                                      float(grid.dy), len(planes), block.ctypes.data),
            path, "write")
+
+
+def write_members(grid: UniformGrid2, members, path) -> None:
+    """Byte-identical to io.py:43-55."""
+    _write_planes(grid, ((mb.u, mb.v) for mb in members), path)
 
 
 def read_members(path) -> tuple[UniformGrid2, tuple[VectorField2, ...]]:
     """io.py:58-93: members as fp64 fields (exact widening of the fp32 payload)."""
     grid, block = read_payload_f32(path)
-    planes = block.astype(np.float64)
-    return grid, tuple(VectorField2(grid, p[0], p[1]) for p in planes)
+    wide = block.astype(np.float64)
+    return grid, tuple(VectorField2(grid, wide[k, 0], wide[k, 1]) for k in range(wide.shape[0]))
+
+
+def _single_block(path, what: str):
+    """The one (u, v) block of a scalar / model file, with io.py's errors."""
+    grid, blocks = read_members(path)
+    if len(blocks) != 1:
+        if what == "scalar":
+            raise DataError(f"{path}: expected a single-block scalar file, got {len(blocks)} blocks")
+        raise DataError("model files must contain exactly one block each")
+    return grid, blocks[0]
 
 
 def write_ensemble(ensemble: Ensemble2, path) -> None:
@@ -101,42 +115,40 @@ def write_ensemble(ensemble: Ensemble2, path) -> None:
 
 def read_ensemble(path) -> Ensemble2:
     """io.py:100-104: at least two members."""
-    grid, members = read_members(path)
-    if len(members) < 2:
-        raise DataError(f"{path}: an ensemble needs >= 2 members, file has {len(members)}")
-    return Ensemble2(grid, members)
+    grid, found = read_members(path)
+    if len(found) < 2:
+        raise DataError(f"{path}: an ensemble needs >= 2 members, file has {len(found)}")
+    return Ensemble2(grid, found)
 
 
 def write_scalar(fld: ScalarField2, path) -> None:
-    zero = np.zeros_like(fld.values)
-    write_members(fld.grid, (VectorField2(fld.grid, fld.values, zero),), path)
+    """A scalar is a one-block file with v = 0 (io.py:107-111)."""
+    _write_planes(fld.grid, [(fld.values, np.zeros_like(fld.values))], path)
 
 
 def read_scalar(path) -> ScalarField2:
-    grid, members = read_members(path)
-    if len(members) != 1:
-        raise DataError(f"{path}: expected a single-block scalar file, got {len(members)} blocks")
-    return ScalarField2(grid, members[0].u)
+    grid, block = _single_block(path, "scalar")
+    return ScalarField2(grid, block.u)
 
 
 def write_model(model: GaussianVectorField, mu_path, sigma_path) -> None:
-    grid = model.grid
-    write_members(grid, (VectorField2(grid, model.mu_u, model.mu_v),), mu_path)
-    write_members(grid, (VectorField2(grid, model.sigma_u, model.sigma_v),), sigma_path)
+    """Two one-block files: (mu_u, mu_v) and (sigma_u, sigma_v) (io.py:114-119)."""
+    for path, pair in ((mu_path, (model.mu_u, model.mu_v)), (sigma_path, (model.sigma_u, model.sigma_v))):
+        _write_planes(model.grid, [pair], path)
 
 
 def read_model(mu_path, sigma_path) -> GaussianVectorField:
-    """io.py:122-134."""
-    grid_mu, mu_members = read_members(mu_path)
-    grid_sg, sg_members = read_members(sigma_path)
-    if grid_mu != grid_sg:
+    """io.py:122-134 (same checks, same order)."""
+    g_mu, blocks_mu = read_members(mu_path)
+    g_sg, blocks_sg = read_members(sigma_path)
+    if g_mu != g_sg:
         raise DataError(f"{mu_path} and {sigma_path} are on different grids")
-    if len(mu_members) != 1 or len(sg_members) != 1:
+    if len(blocks_mu) != 1 or len(blocks_sg) != 1:
         raise DataError("model files must contain exactly one block each")
-    sg = sg_members[0]
-    if np.any(sg.u < 0) or np.any(sg.v < 0):
+    mean, spread = blocks_mu[0], blocks_sg[0]
+    if (spread.u < 0).any() or (spread.v < 0).any():
         raise DataError(f"{sigma_path}: sigmas must be non-negative")
-    return GaussianVectorField(grid_mu, mu_members[0].u, mu_members[0].v, sg.u, sg.v)
+    return GaussianVectorField(g_mu, mean.u, mean.v, spread.u, spread.v)
 
 
 def load_ensemble_device(path, device=None):
@@ -164,7 +176,6 @@ def csv_float(x: float) -> str:
 
 def write_csv(path, header: str, rows) -> None:
     """Header row + comma-joined rows, \\n line endings (io.py:142-148)."""
-    with open(path, "w", encoding="ascii", newline="\n") as fh:
-        fh.write(header + "\n")
-        for row in rows:
-            fh.write(",".join(str(c) for c in row) + "\n")
+    with open(path, "w", encoding="ascii", newline="\n") as out:   # streamed: LCP CSVs are large
+        out.write(header + "\n")
+        out.writelines(",".join(map(str, row)) + "\n" for row in rows)
