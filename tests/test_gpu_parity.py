@@ -697,6 +697,16 @@ def test_zchunked_tma_kernels_bitwise(dev, dtype, shape, rng, monkeypatch):
 
     both(lambda: dev.propagate3d(*ins, nx, ny, nz, 0.5, 1.5, 0.75, 0.1))
     both(lambda: dev.propagate3d(*ins, nx, ny, nz, 0.5, 1.5, 0.75, 0.1, k_range=(3, nz - 2)))
+    # a z-slab with halo planes, chunked: bitwise the whole-domain run's planes
+    plane = nx * ny
+    z0, z1 = 5, nz - 4
+    full = dev.propagate3d(*ins, nx, ny, nz, 0.5, 1.5, 0.75, 0.1)
+    sl = [cu(x[z0 * plane:z1 * plane]) for x in f]
+    lo = (cu(f[2][(z0 - 1) * plane:z0 * plane]), cu(f[5][(z0 - 1) * plane:z0 * plane]))
+    hi = (cu(f[2][z1 * plane:(z1 + 1) * plane]), cu(f[5][z1 * plane:(z1 + 1) * plane]))
+    o = dev.propagate3d(*sl, nx, ny, z1 - z0, 0.5, 1.5, 0.75, 0.1, z0=z0, nz_global=nz, halo_lo=lo, halo_hi=hi)
+    for k in o:
+        assert torch.equal(o[k], full[k][z0 * plane:z1 * plane]), k
     if dtype == np.float32:
         mem = cu(rng.normal(size=(4, 3, nx * ny * nz)).astype(np.float32))
         both(lambda: dev.ensemble_divergence3d(mem, nx, ny, nz, 1.0, 1.0, 1.0, 0.1, moments=True))
