@@ -1032,6 +1032,111 @@ int d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   return status;
 }
 
+// Several arrays of one call as ONE staged stream: the per-array decision
+// above sends an 8 MB fp64 map through the driver's pageable path, so a 1024^2
+// propagate_divergence paid 4 + 2 such copies back to back.  Here the spans'
+// chunks share the ring, so span k's host copy overlaps span k-1's DMA; used
+// when the pageable bytes of the call reach kStageManyH2D / kStageManyD2H.  Non-pageable spans
+// and small totals go straight to cudaMemcpyAsync.  Leaves the stream drained.
+struct Span { void* dev; const void* host; size_t bytes; };
+// same-box A/B (tools/dropin_probe.py): 2 x 8 MB in was slower staged, 4 x 8 MB
+// faster; pageable D2H is the slow direction and gains from 12 MB up
+constexpr size_t kStageManyH2D = size_t(32) << 20, kStageManyD2H = size_t(12) << 20;
+
+int h2d_many(const Span* sp, int n, cudaStream_t s) {
+  size_t paged = 0;
+  for (int i = 0; i < n; ++i)
+    if (sp[i].host && sp[i].bytes && pageable(sp[i].host)) paged += sp[i].bytes;
+  if (paged < kStageManyH2D || env_int("DIVUQ_NO_STAGE_MANY", 0)) {
+    for (int i = 0; i < n; ++i)
+      if (sp[i].host && sp[i].bytes)
+        if (int r = h2d(sp[i].dev, sp[i].host, sp[i].bytes, s)) return r;
+    return 0;
+  }
+  io::Staging& st = io::staging();
+  std::lock_guard<std::mutex> lock(st.mu);
+  if (int r = st.ensure()) return r;
+  cudaEvent_t done[io::Staging::kBuffers] = {};
+  int status = 0;
+  for (auto& e : done)
+    if (!status) status = int(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  int b = 0;
+  for (int i = 0; i < n && !status; ++i) {
+    if (!sp[i].host || !sp[i].bytes) continue;
+    if (!pageable(sp[i].host)) {
+      status = int(cudaMemcpyAsync(sp[i].dev, sp[i].host, sp[i].bytes, cudaMemcpyHostToDevice, s));
+      continue;
+    }
+    const char* in = static_cast<const char*>(sp[i].host);
+    char* out = static_cast<char*>(sp[i].dev);
+    for (size_t off = 0; !status && off < sp[i].bytes; off += io::Staging::kChunk, b = (b + 1) % io::Staging::kBuffers) {
+      const int64_t len = int64_t(std::min<size_t>(io::Staging::kChunk, sp[i].bytes - off));
+      if ((status = int(cudaEventSynchronize(done[b])))) break;
+      memcpy_parallel(st.buf[b], in + off, len);
+      if ((status = int(cudaMemcpyAsync(out + off, st.buf[b], size_t(len), cudaMemcpyHostToDevice, s)))) break;
+      status = int(cudaEventRecord(done[b], s));
+    }
+  }
+  if (!status) status = int(cudaStreamSynchronize(s));
+  for (auto& e : done)
+    if (e) cudaEventDestroy(e);
+  return status;
+}
+
+// device -> host for several arrays; `host` is the destination here
+int d2h_many(const Span* sp, int n, cudaStream_t s) {
+  size_t paged = 0;
+  for (int i = 0; i < n; ++i)
+    if (sp[i].host && sp[i].bytes && pageable(sp[i].host)) paged += sp[i].bytes;
+  if (paged < kStageManyD2H || env_int("DIVUQ_NO_STAGE_MANY", 0)) {
+    for (int i = 0; i < n; ++i)
+      if (sp[i].host && sp[i].bytes)
+        if (int r = d2h(const_cast<void*>(sp[i].host), sp[i].dev, sp[i].bytes, s)) return r;
+    return 0;
+  }
+  io::Staging& st = io::staging();
+  std::lock_guard<std::mutex> lock(st.mu);
+  if (int r = st.ensure()) return r;
+  struct Chunk { char* dst; const char* src; size_t len; };
+  std::vector<Chunk> chunks;
+  for (int i = 0; i < n; ++i) {
+    if (!sp[i].host || !sp[i].bytes) continue;
+    if (!pageable(sp[i].host)) {
+      if (int r = int(cudaMemcpyAsync(const_cast<void*>(sp[i].host), sp[i].dev, sp[i].bytes,
+                                      cudaMemcpyDeviceToHost, s)))
+        return r;
+      continue;
+    }
+    for (size_t off = 0; off < sp[i].bytes; off += io::Staging::kChunk)
+      chunks.push_back({static_cast<char*>(const_cast<void*>(sp[i].host)) + off,
+                        static_cast<const char*>(sp[i].dev) + off,
+                        std::min<size_t>(io::Staging::kChunk, sp[i].bytes - off)});
+  }
+  const int nb = io::Staging::kBuffers;
+  cudaEvent_t done[io::Staging::kBuffers] = {};
+  int status = 0;
+  for (auto& e : done)
+    if (!status) status = int(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  const size_t nc = chunks.size();
+  for (size_t c = 0; !status && c < nc + nb - 1; ++c) {
+    if (c < nc) {
+      if ((status = int(cudaMemcpyAsync(st.buf[c % nb], chunks[c].src, chunks[c].len, cudaMemcpyDeviceToHost, s)))) break;
+      if ((status = int(cudaEventRecord(done[c % nb], s)))) break;
+    }
+    if (c + 1 >= size_t(nb)) {
+      const size_t d = c + 1 - nb;
+      if (d < nc) {
+        if ((status = int(cudaEventSynchronize(done[d % nb])))) break;
+        memcpy_parallel(chunks[d].dst, st.buf[d % nb], int64_t(chunks[d].len));
+      }
+    }
+  }
+  if (!status) status = int(cudaStreamSynchronize(s));
+  for (auto& e : done)
+    if (e) cudaEventDestroy(e);
+  return status;
+}
+
 // The host entry points run on a per-(thread, device) pair of non-blocking
 // streams created once: creating and destroying a stream per call cost more
 // than a small call's copies and kernel.  The guard only drains the stream.
@@ -1818,20 +1923,18 @@ int divuq_host_propagate2d_f64(const double* mu_u, const double* mu_v, const dou
   double* outs[4] = {base + 4 * n, base + 5 * n, base + 6 * n, base + 7 * n};
   int32_t* derr = reinterpret_cast<int32_t*>(base + 8 * n);
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
-  DIVUQ_CUDA(h2d(dmu, mu_u, b, sg.s));
-  DIVUQ_CUDA(h2d(dmv, mu_v, b, sg.s));
-  if (has_sigma) {
-    DIVUQ_CUDA(h2d(dsu, s_u, b, sg.s));
-    DIVUQ_CUDA(h2d(dsv, s_v, b, sg.s));
-  }
+  const Span ins[4] = {{dmu, mu_u, b}, {dmv, mu_v, b}, {dsu, has_sigma ? s_u : nullptr, b},
+                       {dsv, has_sigma ? s_v : nullptr, b}};
+  DIVUQ_CUDA(h2d_many(ins, 4, sg.s));
   double* host_out[4] = {out_mu, out_sigma, out_p_src, out_p_snk};
   int r = propagate2d<double>(dmu, dmv, has_sigma ? dsu : nullptr, has_sigma ? dsv : nullptr, nx, ny,
                               dx, dy, t, out_mu ? outs[0] : nullptr, out_sigma ? outs[1] : nullptr,
                               out_p_src ? outs[2] : nullptr, out_p_snk ? outs[3] : nullptr, derr,
                               sg.s);
   if (r) return r;
-  for (int q = 0; q < 4; ++q)
-    if (host_out[q]) DIVUQ_CUDA(d2h(host_out[q], outs[q], b, sg.s));
+  Span res[4];
+  for (int q = 0; q < 4; ++q) res[q] = Span{outs[q], host_out[q], host_out[q] ? b : 0};
+  DIVUQ_CUDA(d2h_many(res, 4, sg.s));
   int status = 0;
   DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
   return status;
@@ -1850,13 +1953,13 @@ int divuq_host_tail_probs_f64(const double* mu, const double* sigma, int64_t n, 
   double* base = d.as<double>();
   int32_t* derr = reinterpret_cast<int32_t*>(base + 4 * n);
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
-  DIVUQ_CUDA(h2d(base, mu, b, sg.s));
-  DIVUQ_CUDA(h2d(base + n, sigma, b, sg.s));
+  const Span ins[2] = {{base, mu, b}, {base + n, sigma, b}};
+  DIVUQ_CUDA(h2d_many(ins, 2, sg.s));
   if (int r = tail_probs<double>(base, base + n, n, theta, out_below ? base + 2 * n : nullptr,
                                  out_above ? base + 3 * n : nullptr, derr, sg.s))
     return r;
-  if (out_below) DIVUQ_CUDA(d2h(out_below, base + 2 * n, b, sg.s));
-  if (out_above) DIVUQ_CUDA(d2h(out_above, base + 3 * n, b, sg.s));
+  const Span res[2] = {{base + 2 * n, out_below, out_below ? b : 0}, {base + 3 * n, out_above, out_above ? b : 0}};
+  DIVUQ_CUDA(d2h_many(res, 2, sg.s));
   int status = 0;
   DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
   return status;
@@ -1881,14 +1984,17 @@ int divuq_host_propagate_lcp2d_f64(const double* mu_u, const double* mu_v, const
   int32_t* derr = reinterpret_cast<int32_t*>(dout + nc);
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
   const double* ins[4] = {mu_u, mu_v, s_u, s_v};
-  for (int k = 0; k < 4; ++k) DIVUQ_CUDA(h2d(din + k * n, ins[k], size_t(n) * sizeof(double), sg.s));
+  Span spans[4];
+  for (int k = 0; k < 4; ++k) spans[k] = Span{din + k * n, ins[k], size_t(n) * sizeof(double)};
+  DIVUQ_CUDA(h2d_many(spans, 4, sg.s));
   if (int r = divuq_propagate_lcp2d_f64(din, din + n, din + 2 * n, din + 3 * n, nx, ny, dx, dy, isovalue,
                                         out_mu ? dmu : nullptr, out_sigma ? dsg : nullptr, dout, derr,
                                         sg.s))
     return r;
-  if (out_mu) DIVUQ_CUDA(d2h(out_mu, dmu, size_t(n) * sizeof(double), sg.s));
-  if (out_sigma) DIVUQ_CUDA(d2h(out_sigma, dsg, size_t(n) * sizeof(double), sg.s));
-  DIVUQ_CUDA(d2h(out_lcp, dout, size_t(nc) * sizeof(double), sg.s));
+  const Span res[3] = {{dmu, out_mu, out_mu ? size_t(n) * sizeof(double) : 0},
+                       {dsg, out_sigma, out_sigma ? size_t(n) * sizeof(double) : 0},
+                       {dout, out_lcp, size_t(nc) * sizeof(double)}};
+  DIVUQ_CUDA(d2h_many(res, 3, sg.s));
   int status = 0;
   DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
   return status;
@@ -1909,8 +2015,8 @@ int divuq_host_lcp2d_f64(const double* mu, const double* sigma, int64_t nx, int6
   double* dout = dsg + n;
   int32_t* derr = reinterpret_cast<int32_t*>(dout + nc);
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
-  DIVUQ_CUDA(h2d(dmu, mu, size_t(n) * sizeof(double), sg.s));
-  DIVUQ_CUDA(h2d(dsg, sigma, size_t(n) * sizeof(double), sg.s));
+  const Span ins[2] = {{dmu, mu, size_t(n) * sizeof(double)}, {dsg, sigma, size_t(n) * sizeof(double)}};
+  DIVUQ_CUDA(h2d_many(ins, 2, sg.s));
   if (int r = divuq_lcp2d_f64(dmu, dsg, nx, ny, isovalue, dout, derr, sg.s)) return r;
   DIVUQ_CUDA(d2h(out, dout, size_t(nc) * sizeof(double), sg.s));
   int status = 0;
@@ -2067,15 +2173,13 @@ int divuq_host_mc_divergence2d_f64(const double* mu_u, const double* mu_v, const
   int32_t* derr = reinterpret_cast<int32_t*>(base + 6 * n);
   void* dscr = reinterpret_cast<char*>(base + 6 * n) + 256;
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
-  DIVUQ_CUDA(h2d(dmu, mu_u, b, sg.s));
-  DIVUQ_CUDA(h2d(dmv, mu_v, b, sg.s));
-  DIVUQ_CUDA(h2d(dsu, s_u, b, sg.s));
-  DIVUQ_CUDA(h2d(dsv, s_v, b, sg.s));
+  const Span ins[4] = {{dmu, mu_u, b}, {dmv, mu_v, b}, {dsu, s_u, b}, {dsv, s_v, b}};
+  DIVUQ_CUDA(h2d_many(ins, 4, sg.s));
   int r = divuq_mc_divergence2d_f64(dmu, dmv, dsu, dsv, nx, ny, dx, dy, n_samples, seed, 0, ny, dmean,
                                     dstd, dscr, derr, sg.s);
   if (r) return r;
-  DIVUQ_CUDA(d2h(out_mean, dmean, b, sg.s));
-  DIVUQ_CUDA(d2h(out_std, dstd, b, sg.s));
+  const Span res[2] = {{dmean, out_mean, b}, {dstd, out_std, b}};
+  DIVUQ_CUDA(d2h_many(res, 2, sg.s));
   int status = 0;
   DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
   return status;
