@@ -31,6 +31,7 @@ from .types import (
     ScalarField2,
     UniformGrid3,
     VectorField2,
+    adopt,
 )
 
 _DEVICE = 0
@@ -43,7 +44,7 @@ def set_device(ordinal: int) -> None:
 
 
 def _p(a):
-    return None if a is None else a.ctypes.data
+    return None if a is None else a.__array_interface__["data"][0]
 
 
 def _c64(a):
@@ -60,7 +61,7 @@ def fit_gaussian(ensemble: Ensemble2) -> GaussianVectorField:
     mu = np.empty((c, n))
     sg = np.empty((c, n))
     _check(lib.divuq_host_fit_gaussian_f64(_p(stacked), m, c, n, _p(mu), _p(sg), _DEVICE))
-    return GaussianVectorField(ensemble.grid, mu[0], mu[1], sg[0], sg[1])
+    return adopt(GaussianVectorField, ensemble.grid, mu[0], mu[1], sg[0], sg[1])
 
 
 def propagate_divergence(model, config: ParallelConfig | None = None):
@@ -99,7 +100,7 @@ def propagate_with_probabilities(model: GaussianVectorField, t: float = 0.0, *,
     _check(lib.divuq_host_propagate2d_f64(
         _p(model.mu_u), _p(model.mu_v), _p(model.sigma_u), _p(model.sigma_v), g.nx, g.ny,
         float(g.dx), float(g.dy), float(t), _p(mu), _p(sg), _p(ps), _p(pk), _DEVICE))
-    return Propagation(GaussianScalarField(g, mu, sg), ps, pk)
+    return Propagation(adopt(GaussianScalarField, g, mu, sg), ps, pk)
 
 
 def propagate_with_probabilities3d(model: GaussianVectorField3, t: float = 0.0, *,
@@ -132,7 +133,7 @@ def propagate_with_probabilities3d(model: GaussianVectorField3, t: float = 0.0, 
             if probabilities:
                 ps[:] = o["p_src"].cpu().numpy()
                 pk[:] = o["p_snk"].cpu().numpy()
-    return Propagation(GaussianScalarField3(g, mu, sg), ps, pk)
+    return Propagation(adopt(GaussianScalarField3, g, mu, sg), ps, pk)
 
 
 def divergence_deterministic(fld: VectorField2) -> ScalarField2:
@@ -142,7 +143,7 @@ def divergence_deterministic(fld: VectorField2) -> ScalarField2:
     _check(lib.divuq_host_propagate2d_f64(
         _p(fld.u), _p(fld.v), None, None, g.nx, g.ny, float(g.dx), float(g.dy), 0.0, _p(out),
         None, None, None, _DEVICE))
-    return ScalarField2(g, out)
+    return adopt(ScalarField2, g, out)
 
 
 def stencil_distribution(neighbors, spacing: tuple[float, float]) -> tuple[float, float]:
@@ -204,7 +205,7 @@ def mc_divergence(model: GaussianVectorField, config: McConfig, *,
         _p(model.mu_u), _p(model.mu_v), _p(model.sigma_u), _p(model.sigma_v), g.nx, g.ny,
         float(g.dx), float(g.dy), int(config.n_samples), int(config.seed), _p(mean), _p(std),
         _DEVICE))
-    return McDivergenceEstimate(g, mean, std, config.n_samples)
+    return adopt(McDivergenceEstimate, g, mean, std, config.n_samples)
 
 
 def _neighbors8(neighbors) -> np.ndarray:
@@ -334,7 +335,7 @@ def ensemble_divergence3d(members, grid: UniformGrid3, t: float = 0.0, *, z0: in
     _check(lib.divuq_host_ensemble_divergence3d_f32(
         _p(mem), m, g.nx, g.ny, g.nz, int(z0), nzg, _p(lo), _p(hi), stride, float(g.dx),
         float(g.dy), float(g.dz), float(t), *(_p(a) for a in o), int(chunk_planes), _DEVICE))
-    return Propagation(GaussianScalarField3(g, o[0], o[1]), o[2], o[3])
+    return Propagation(adopt(GaussianScalarField3, g, o[0], o[1]), o[2], o[3])
 
 
 def gradient_ensemble_divergence(ensemble: Ensemble2, t: float = 0.0) -> EnsembleDivergence:
@@ -362,7 +363,7 @@ def velocity_magnitude(member: VectorField2) -> ScalarField2:
     out = np.empty(g.n_vertices)
     _check(lib.divuq_host_velocity_magnitude_f64(_p(member.u), _p(member.v), g.n_vertices, _p(out),
                                                  _DEVICE))
-    return ScalarField2(g, out)
+    return adopt(ScalarField2, g, out)
 
 
 def gradient(fld: ScalarField2) -> VectorField2:
@@ -371,7 +372,7 @@ def gradient(fld: ScalarField2) -> VectorField2:
     out = np.empty((2, g.n_vertices))
     _check(lib.divuq_host_gradient2d_f64(_p(fld.values), g.nx, g.ny, float(g.dx), float(g.dy),
                                          _p(out), _DEVICE))
-    return VectorField2(g, out[0], out[1])
+    return adopt(VectorField2, g, out[0], out[1])
 
 
 def gradient_ensemble(ensemble: Ensemble2) -> Ensemble2:
@@ -382,7 +383,7 @@ def gradient_ensemble(ensemble: Ensemble2) -> Ensemble2:
     out = np.empty_like(stacked)
     _check(lib.divuq_host_gradient_ensemble2d_f64(_p(stacked), stacked.shape[0], g.nx, g.ny,
                                                   float(g.dx), float(g.dy), _p(out), _DEVICE))
-    return Ensemble2(g, tuple(VectorField2(g, o[0], o[1]) for o in out))
+    return Ensemble2(g, tuple(adopt(VectorField2, g, o[0], o[1]) for o in out))
 
 
 def cell_crossing_probability(mu, sigma, isovalue: float) -> np.ndarray:
@@ -408,7 +409,7 @@ def propagate_lcp(model, isovalue: float) -> tuple[GaussianScalarField, LcpField
     _check(lib.divuq_host_propagate_lcp2d_f64(
         _p(model.mu_u), _p(model.mu_v), _p(model.sigma_u), _p(model.sigma_v), g.nx, g.ny,
         float(g.dx), float(g.dy), float(isovalue), _p(mu), _p(sg), _p(out), _DEVICE))
-    return GaussianScalarField(g, mu, sg), LcpField(g, isovalue, out)
+    return adopt(GaussianScalarField, g, mu, sg), adopt(LcpField, g, isovalue, out)
 
 
 def lcp(fld: GaussianScalarField, isovalue: float, config: ParallelConfig | None = None) -> LcpField:
@@ -417,4 +418,4 @@ def lcp(fld: GaussianScalarField, isovalue: float, config: ParallelConfig | None
     out = np.empty(g.n_cells)
     _check(lib.divuq_host_lcp2d_f64(_p(fld.mu), _p(fld.sigma), g.nx, g.ny, float(isovalue), _p(out),
                                     _DEVICE))
-    return LcpField(g, isovalue, out)
+    return adopt(LcpField, g, isovalue, out)

@@ -930,16 +930,30 @@ cudaError_t library_pool(cudaMemPool_t* out) {
   return cudaSuccess;
 }
 
-// RAII device scratch from the library pool; released with a synchronising
-// cudaFree so no stream of the call can still be using it
+// RAII device scratch from the library pool.  alloc(): released with a
+// synchronising cudaFree, so no stream of the call can still be using it
+// (the multi-stream 3D pipelines).  alloc_on(): every use is on stream st, so
+// the release is stream-ordered there (cudaFreeAsync: no device-wide sync --
+// ~5 us of a small drop-in call, and a hidden sync in device-API fallbacks).
 struct DevBuf {
   void* p = nullptr;
+  cudaStream_t only = nullptr;
+  bool one_stream = false;
   cudaError_t alloc(size_t bytes, cudaStream_t st) {
     cudaMemPool_t pool;
     if (cudaError_t e = library_pool(&pool)) return e;
     return cudaMallocFromPoolAsync(&p, bytes ? bytes : 1, pool, st);
   }
-  ~DevBuf() { if (p) cudaFree(p); }
+  cudaError_t alloc_on(size_t bytes, cudaStream_t st) {
+    only = st;
+    one_stream = true;
+    return alloc(bytes, st);
+  }
+  ~DevBuf() {
+    if (!p) return;
+    if (one_stream) cudaFreeAsync(p, only);
+    else cudaFree(p);
+  }
   template <typename T> T* as() const { return static_cast<T*>(p); }
 };
 
@@ -1137,6 +1151,207 @@ int d2h_many(const Span* sp, int n, cudaStream_t s) {
   return status;
 }
 
+// Small calls (the paper's own grids: 68^2 wind, 500^2 Red Sea) are latency
+// bound: every pageable cudaMemcpyAsync is a synchronous driver copy, and a
+// 68^2 propagate_divergence paid four of them in, two out, one for the
+// validation word and a stream sync per output (~100 us of a 170 us call).
+// Here a call's pageable inputs are packed into ONE per-thread pinned arena
+// and go down as async DMAs (adjacent device spans merged into one copy);
+// its outputs and the validation word come back into the arena, ONE stream
+// sync, then memcpy out.  The arena is append-only until a sync on its
+// stream (d2h side) or until it fills (then the stream is drained), so no
+// bytes are overwritten while a DMA may still read them.
+struct Bounce {
+  char* buf = nullptr;
+  size_t cap = 0, cur = 0;
+  cudaStream_t stream = nullptr;
+};
+static Bounce& bounce() {
+  thread_local Bounce b;
+  return b;
+}
+static size_t bounce_max() {
+  static const size_t v = size_t(std::max<int64_t>(0, env_int("DIVUQ_BOUNCE_MAX_KB", 16384))) << 10;
+  return v;
+}
+// room for `bytes` more on stream s; returns the arena offset or -1 (use the
+// regular path)
+static int64_t bounce_reserve(size_t bytes, cudaStream_t s, int* status) {
+  Bounce& b = bounce();
+  const size_t need = (bytes + 255) & ~size_t(255);
+  if (need > bounce_max()) return -1;
+  if (b.stream != s || b.cur + need > b.cap) {   // drain what may still use the arena
+    if (b.stream && b.cur)
+      if ((*status = int(cudaStreamSynchronize(b.stream)))) return -1;
+    b.cur = 0;
+    b.stream = s;
+  }
+  if (need > b.cap) {
+    if (b.buf) cudaFreeHost(b.buf);
+    b.buf = nullptr;
+    b.cap = 0;
+    size_t cap = size_t(1) << 20;
+    while (cap < need) cap <<= 1;
+    cap = std::min(cap, bounce_max());
+    if ((*status = int(cudaHostAlloc(reinterpret_cast<void**>(&b.buf), cap, cudaHostAllocPortable)))) {
+      b.buf = nullptr;
+      return -1;
+    }
+    b.cap = cap;
+  }
+  const int64_t off = int64_t(b.cur);
+  b.cur += need;
+  return off;
+}
+
+// several (dst, src, len) copies as one job: from 512 KB on the bytes are
+// split evenly over the host workers (a 500^2 call moves 8 MB in and 4 MB out:
+// one thread per array ran at memcpy speed, ~1 ms)
+struct Seg { char* dst; const char* src; size_t len; };
+static void memcpy_segs(const Seg* sg, int n) {
+  size_t total = 0;
+  for (int i = 0; i < n; ++i) total += sg[i].len;
+  const int64_t hw = std::max(1u, std::thread::hardware_concurrency());
+  const int nt = total < (size_t(512) << 10) ? 1
+                 : int(std::min<int64_t>({16, hw, int64_t(total / (size_t(256) << 10))}));
+  if (nt <= 1) {
+    for (int i = 0; i < n; ++i) std::memcpy(sg[i].dst, sg[i].src, sg[i].len);
+    return;
+  }
+  const size_t per = (total + nt - 1) / nt;
+  io::HostPool::get().run(nt, [&](int t) {
+    size_t a = size_t(t) * per, b = std::min(total, a + per), base = 0;
+    for (int i = 0; i < n && a < b; ++i) {
+      const size_t e = base + sg[i].len;
+      if (a < e) {
+        const size_t lo = a - base, hi = std::min(b, e) - base;
+        std::memcpy(sg[i].dst + lo, sg[i].src + lo, hi - lo);
+        a = base + hi;
+      }
+      base = e;
+    }
+  });
+}
+
+// pageable spans of a call through the arena (async); false: not taken
+static bool bounce_h2d(const Span* sp, int n, cudaStream_t s, int* status) {
+  size_t total = 0;
+  for (int i = 0; i < n; ++i)
+    if (sp[i].host && sp[i].bytes) total += (sp[i].bytes + 255) & ~size_t(255);
+  if (total == 0) return false;
+  const int64_t base = bounce_reserve(total, s, status);
+  if (base < 0) return false;
+  char* arena = bounce().buf + base;
+  {   // pack every span first (one parallel job), then the DMAs
+    std::vector<Seg> segs;
+    size_t o = 0;
+    for (int i = 0; i < n; ++i) {
+      if (!sp[i].host || !sp[i].bytes) continue;
+      segs.push_back({arena + o, static_cast<const char*>(sp[i].host), sp[i].bytes});
+      o += (sp[i].bytes + 255) & ~size_t(255);
+    }
+    memcpy_segs(segs.data(), int(segs.size()));
+  }
+  size_t off = 0;
+  const char* run_dev = nullptr;   // a run of spans adjacent in device memory -> one DMA
+  const char* run_host = nullptr;
+  size_t run_len = 0;
+  auto flush = [&]() {
+    if (run_len && !*status)
+      *status = int(cudaMemcpyAsync(const_cast<char*>(run_dev), run_host, run_len, cudaMemcpyHostToDevice, s));
+    run_len = 0;
+  };
+  for (int i = 0; i < n && !*status; ++i) {
+    if (!sp[i].host || !sp[i].bytes) continue;
+    const char* dev = static_cast<const char*>(sp[i].dev);
+    if (run_len && run_dev + run_len == dev && run_host + run_len == arena + off) {
+      run_len += sp[i].bytes;
+    } else {
+      flush();
+      run_dev = dev;
+      run_host = arena + off;
+      run_len = sp[i].bytes;
+    }
+    off += (sp[i].bytes + 255) & ~size_t(255);
+  }
+  flush();
+  return true;
+}
+
+// outputs (host = destination) and the validation word: one sync
+static bool bounce_d2h(const Span* sp, int n, const int32_t* derr, cudaStream_t s, int* code,
+                       int* status) {
+  size_t total = derr ? 256 : 0;
+  for (int i = 0; i < n; ++i)
+    if (sp[i].host && sp[i].bytes) total += (sp[i].bytes + 255) & ~size_t(255);
+  const int64_t base = bounce_reserve(total, s, status);
+  if (base < 0) return false;
+  char* arena = bounce().buf + base;
+  size_t off = derr ? 256 : 0;
+  if (derr && !*status)
+    *status = int(cudaMemcpyAsync(arena, derr, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  for (int i = 0; i < n && !*status; ++i) {
+    if (!sp[i].host || !sp[i].bytes) continue;
+    *status = int(cudaMemcpyAsync(arena + off, sp[i].dev, sp[i].bytes, cudaMemcpyDeviceToHost, s));
+    off += (sp[i].bytes + 255) & ~size_t(255);
+  }
+  if (!*status) *status = int(cudaStreamSynchronize(s));
+  if (*status) return true;
+  bounce().cur = 0;   // the stream is drained: the whole arena is free
+  off = derr ? 256 : 0;
+  std::vector<Seg> segs;
+  for (int i = 0; i < n; ++i) {
+    if (!sp[i].host || !sp[i].bytes) continue;
+    segs.push_back({static_cast<char*>(const_cast<void*>(sp[i].host)), arena + off, sp[i].bytes});
+    off += (sp[i].bytes + 255) & ~size_t(255);
+  }
+  memcpy_segs(segs.data(), int(segs.size()));
+  if (derr) {
+    int32_t h;
+    std::memcpy(&h, arena, sizeof(h));
+    *code = (h & DIVUQ_ERRBIT_NONFINITE) ? DIVUQ_ENONFINITE
+            : (h & DIVUQ_ERRBIT_NEGSIGMA) ? DIVUQ_ENEGSIGMA : DIVUQ_OK;
+  }
+  return true;
+}
+
+// inputs of a call: small pageable totals through the arena, else h2d_many
+int h2d_in(const Span* sp, int n, cudaStream_t s) {
+  size_t paged = 0;
+  bool any_pinned = false;
+  for (int i = 0; i < n; ++i)
+    if (sp[i].host && sp[i].bytes) {
+      if (pageable(sp[i].host)) paged += sp[i].bytes;
+      else any_pinned = true;
+    }
+  if (!any_pinned && paged) {
+    int status = 0;
+    if (bounce_h2d(sp, n, s, &status)) return status;
+    if (status) return status;
+  }
+  return h2d_many(sp, n, s);
+}
+
+// outputs of a call + the validation word -> *code (DIVUQ_OK / ENONFINITE /
+// ENEGSIGMA); returns a CUDA status.  Leaves the stream drained.
+int d2h_out(const Span* sp, int n, const int32_t* derr, cudaStream_t s, int* code) {
+  *code = DIVUQ_OK;
+  size_t paged = 0;
+  bool any_pinned = false;
+  for (int i = 0; i < n; ++i)
+    if (sp[i].host && sp[i].bytes) {
+      if (pageable(sp[i].host)) paged += sp[i].bytes;
+      else any_pinned = true;
+    }
+  if (!any_pinned) {
+    int status = 0;
+    if (bounce_d2h(sp, n, derr, s, code, &status)) return status;
+    if (status) return status;
+  }
+  if (int r = d2h_many(sp, n, s)) return r;
+  return derr ? check_err_word(derr, s, code) : 0;
+}
+
 // The host entry points run on a per-(thread, device) pair of non-blocking
 // streams created once: creating and destroying a stream per call cost more
 // than a small call's copies and kernel.  The guard only drains the stream.
@@ -1238,24 +1453,25 @@ static int host_gradient_common(int kind, const double* a, const double* b, int6
   const int64_t in_elems = kind == 0 ? 2 * n : kind == 1 ? n : 2 * M * n;
   const int64_t out_elems = kind == 0 ? n : kind == 1 ? 2 * n : 2 * M * n;
   DevBuf d;
-  DIVUQ_CUDA(d.alloc(size_t(in_elems + out_elems) * sizeof(double) + 256, sg.s));
+  DIVUQ_CUDA(d.alloc_on(size_t(in_elems + out_elems) * sizeof(double) + 256, sg.s));
   double* din = d.as<double>();
   double* dout = din + in_elems;
   int32_t* derr = reinterpret_cast<int32_t*>(dout + out_elems);
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
   if (kind == 0) {
-    DIVUQ_CUDA(h2d(din, a, size_t(n) * 8, sg.s));
-    DIVUQ_CUDA(h2d(din + n, b, size_t(n) * 8, sg.s));
+    const Span ins[2] = {{din, a, size_t(n) * 8}, {din + n, b, size_t(n) * 8}};
+    DIVUQ_CUDA(h2d_in(ins, 2, sg.s));
     if (int r = divuq_velocity_magnitude_f64(din, din + n, n, dout, derr, sg.s)) return r;
   } else {
-    DIVUQ_CUDA(h2d(din, a, size_t(in_elems) * 8, sg.s));
+    const Span ins[1] = {{din, a, size_t(in_elems) * 8}};
+    DIVUQ_CUDA(h2d_in(ins, 1, sg.s));
     const int r = kind == 1 ? divuq_gradient2d_f64(din, nx, ny, dx, dy, dout, derr, sg.s)
                             : divuq_gradient_ensemble2d_f64(din, M, nx, ny, dx, dy, dout, derr, sg.s);
     if (r) return r;
   }
-  DIVUQ_CUDA(d2h(out, dout, size_t(out_elems) * 8, sg.s));
+  const Span res1[1] = {{dout, out, size_t(out_elems) * 8}};
   int status = 0;
-  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  DIVUQ_CUDA(d2h_out(res1, 1, derr, sg.s, &status));
   return status;
 }
 
@@ -1473,7 +1689,7 @@ static int ensemble_fallback(StencilParams<float> p, int comps, cudaStream_t s) 
   const int64_t nl = p.comp_stride;
   const bool own = p.out_mom_mu != nullptr;
   DevBuf scratch;
-  DIVUQ_CUDA(scratch.alloc(size_t(comps) * nl * (own ? 1 : 3) * sizeof(float), s));
+  DIVUQ_CUDA(scratch.alloc_on(size_t(comps) * nl * (own ? 1 : 3) * sizeof(float), s));
   float* r = scratch.as<float>();
   float* mu = own ? p.out_mom_mu : r + comps * nl;
   float* sg = own ? p.out_mom_sigma : r + 2 * comps * nl;
@@ -1702,7 +1918,7 @@ int divuq_propagate_lcp2d_f64(const double* mu_u, const double* mu_v, const doub
     double* mu = out_mu;
     double* sg = out_sigma;
     if (!mu || !sg) {
-      DIVUQ_CUDA(scratch.alloc(size_t(2 * n) * sizeof(double), s));
+      DIVUQ_CUDA(scratch.alloc_on(size_t(2 * n) * sizeof(double), s));
       if (!mu) mu = scratch.as<double>();
       if (!sg) sg = scratch.as<double>() + n;
     }
@@ -1917,7 +2133,7 @@ int divuq_host_propagate2d_f64(const double* mu_u, const double* mu_v, const dou
   const int64_t n = nx * ny;
   const size_t b = size_t(n) * sizeof(double);
   DevBuf d;
-  DIVUQ_CUDA(d.alloc(8 * b + 256, sg.s));
+  DIVUQ_CUDA(d.alloc_on(8 * b + 256, sg.s));
   double* base = d.as<double>();
   double *dmu = base, *dmv = base + n, *dsu = base + 2 * n, *dsv = base + 3 * n;
   double* outs[4] = {base + 4 * n, base + 5 * n, base + 6 * n, base + 7 * n};
@@ -1925,7 +2141,7 @@ int divuq_host_propagate2d_f64(const double* mu_u, const double* mu_v, const dou
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
   const Span ins[4] = {{dmu, mu_u, b}, {dmv, mu_v, b}, {dsu, has_sigma ? s_u : nullptr, b},
                        {dsv, has_sigma ? s_v : nullptr, b}};
-  DIVUQ_CUDA(h2d_many(ins, 4, sg.s));
+  DIVUQ_CUDA(h2d_in(ins, 4, sg.s));
   double* host_out[4] = {out_mu, out_sigma, out_p_src, out_p_snk};
   int r = propagate2d<double>(dmu, dmv, has_sigma ? dsu : nullptr, has_sigma ? dsv : nullptr, nx, ny,
                               dx, dy, t, out_mu ? outs[0] : nullptr, out_sigma ? outs[1] : nullptr,
@@ -1934,9 +2150,8 @@ int divuq_host_propagate2d_f64(const double* mu_u, const double* mu_v, const dou
   if (r) return r;
   Span res[4];
   for (int q = 0; q < 4; ++q) res[q] = Span{outs[q], host_out[q], host_out[q] ? b : 0};
-  DIVUQ_CUDA(d2h_many(res, 4, sg.s));
   int status = 0;
-  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  DIVUQ_CUDA(d2h_out(res, 4, derr, sg.s, &status));
   return status;
 }
 
@@ -1949,19 +2164,18 @@ int divuq_host_tail_probs_f64(const double* mu, const double* sigma, int64_t n, 
   DIVUQ_CUDA(cached_stream(0, &sg.s));
   const size_t b = size_t(n) * sizeof(double);
   DevBuf d;
-  DIVUQ_CUDA(d.alloc(4 * b + 256, sg.s));
+  DIVUQ_CUDA(d.alloc_on(4 * b + 256, sg.s));
   double* base = d.as<double>();
   int32_t* derr = reinterpret_cast<int32_t*>(base + 4 * n);
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
   const Span ins[2] = {{base, mu, b}, {base + n, sigma, b}};
-  DIVUQ_CUDA(h2d_many(ins, 2, sg.s));
+  DIVUQ_CUDA(h2d_in(ins, 2, sg.s));
   if (int r = tail_probs<double>(base, base + n, n, theta, out_below ? base + 2 * n : nullptr,
                                  out_above ? base + 3 * n : nullptr, derr, sg.s))
     return r;
   const Span res[2] = {{base + 2 * n, out_below, out_below ? b : 0}, {base + 3 * n, out_above, out_above ? b : 0}};
-  DIVUQ_CUDA(d2h_many(res, 2, sg.s));
   int status = 0;
-  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  DIVUQ_CUDA(d2h_out(res, 2, derr, sg.s, &status));
   return status;
 }
 
@@ -1976,7 +2190,7 @@ int divuq_host_propagate_lcp2d_f64(const double* mu_u, const double* mu_v, const
   DIVUQ_CUDA(cached_stream(0, &sg.s));
   const int64_t n = nx * ny, nc = (nx - 1) * (ny - 1);
   DevBuf d;
-  DIVUQ_CUDA(d.alloc(size_t(6 * n + nc) * sizeof(double) + 256, sg.s));
+  DIVUQ_CUDA(d.alloc_on(size_t(6 * n + nc) * sizeof(double) + 256, sg.s));
   double* din = d.as<double>();
   double* dmu = din + 4 * n;
   double* dsg = dmu + n;
@@ -1986,7 +2200,7 @@ int divuq_host_propagate_lcp2d_f64(const double* mu_u, const double* mu_v, const
   const double* ins[4] = {mu_u, mu_v, s_u, s_v};
   Span spans[4];
   for (int k = 0; k < 4; ++k) spans[k] = Span{din + k * n, ins[k], size_t(n) * sizeof(double)};
-  DIVUQ_CUDA(h2d_many(spans, 4, sg.s));
+  DIVUQ_CUDA(h2d_in(spans, 4, sg.s));
   if (int r = divuq_propagate_lcp2d_f64(din, din + n, din + 2 * n, din + 3 * n, nx, ny, dx, dy, isovalue,
                                         out_mu ? dmu : nullptr, out_sigma ? dsg : nullptr, dout, derr,
                                         sg.s))
@@ -1994,9 +2208,8 @@ int divuq_host_propagate_lcp2d_f64(const double* mu_u, const double* mu_v, const
   const Span res[3] = {{dmu, out_mu, out_mu ? size_t(n) * sizeof(double) : 0},
                        {dsg, out_sigma, out_sigma ? size_t(n) * sizeof(double) : 0},
                        {dout, out_lcp, size_t(nc) * sizeof(double)}};
-  DIVUQ_CUDA(d2h_many(res, 3, sg.s));
   int status = 0;
-  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  DIVUQ_CUDA(d2h_out(res, 3, derr, sg.s, &status));
   return status;
 }
 
@@ -2009,18 +2222,18 @@ int divuq_host_lcp2d_f64(const double* mu, const double* sigma, int64_t nx, int6
   DIVUQ_CUDA(cached_stream(0, &sg.s));
   const int64_t n = nx * ny, nc = (nx - 1) * (ny - 1);
   DevBuf d;
-  DIVUQ_CUDA(d.alloc(size_t(2 * n + nc) * sizeof(double) + 256, sg.s));
+  DIVUQ_CUDA(d.alloc_on(size_t(2 * n + nc) * sizeof(double) + 256, sg.s));
   double* dmu = d.as<double>();
   double* dsg = dmu + n;
   double* dout = dsg + n;
   int32_t* derr = reinterpret_cast<int32_t*>(dout + nc);
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
   const Span ins[2] = {{dmu, mu, size_t(n) * sizeof(double)}, {dsg, sigma, size_t(n) * sizeof(double)}};
-  DIVUQ_CUDA(h2d_many(ins, 2, sg.s));
+  DIVUQ_CUDA(h2d_in(ins, 2, sg.s));
   if (int r = divuq_lcp2d_f64(dmu, dsg, nx, ny, isovalue, dout, derr, sg.s)) return r;
-  DIVUQ_CUDA(d2h(out, dout, size_t(nc) * sizeof(double), sg.s));
+  const Span res1[1] = {{dout, out, size_t(nc) * sizeof(double)}};
   int status = 0;
-  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  DIVUQ_CUDA(d2h_out(res1, 1, derr, sg.s, &status));
   return status;
 }
 
@@ -2032,18 +2245,19 @@ int divuq_host_cell_crossing_f64(const double* mu4, const double* sigma4, int64_
   StreamGuard sg;
   DIVUQ_CUDA(cached_stream(0, &sg.s));
   DevBuf d;
-  DIVUQ_CUDA(d.alloc(size_t(9 * n_cells) * sizeof(double) + 256, sg.s));
+  DIVUQ_CUDA(d.alloc_on(size_t(9 * n_cells) * sizeof(double) + 256, sg.s));
   double* dmu = d.as<double>();
   double* dsg = dmu + 4 * n_cells;
   double* dout = dsg + 4 * n_cells;
   int32_t* derr = reinterpret_cast<int32_t*>(dout + n_cells);
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
-  DIVUQ_CUDA(h2d(dmu, mu4, size_t(4 * n_cells) * sizeof(double), sg.s));
-  DIVUQ_CUDA(h2d(dsg, sigma4, size_t(4 * n_cells) * sizeof(double), sg.s));
+  const Span ins[2] = {{dmu, mu4, size_t(4 * n_cells) * sizeof(double)},
+                       {dsg, sigma4, size_t(4 * n_cells) * sizeof(double)}};
+  DIVUQ_CUDA(h2d_in(ins, 2, sg.s));
   if (int r = divuq_cell_crossing_f64(dmu, dsg, n_cells, isovalue, dout, derr, sg.s)) return r;
-  DIVUQ_CUDA(d2h(out, dout, size_t(n_cells) * sizeof(double), sg.s));
+  const Span res1[1] = {{dout, out, size_t(n_cells) * sizeof(double)}};
   int status = 0;
-  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  DIVUQ_CUDA(d2h_out(res1, 1, derr, sg.s, &status));
   return status;
 }
 
@@ -2056,18 +2270,18 @@ int divuq_host_fit_gaussian_f64(const double* members, int64_t M, int64_t C, int
   DIVUQ_CUDA(cached_stream(0, &sg.s));
   const size_t in_b = size_t(M * C * N) * sizeof(double), out_b = size_t(C * N) * sizeof(double);
   DevBuf d;
-  DIVUQ_CUDA(d.alloc(in_b + 2 * out_b + 256, sg.s));
+  DIVUQ_CUDA(d.alloc_on(in_b + 2 * out_b + 256, sg.s));
   double* dm = d.as<double>();
   double* dmu = dm + M * C * N;
   double* dsg = dmu + C * N;
   int32_t* derr = reinterpret_cast<int32_t*>(dsg + C * N);
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
-  DIVUQ_CUDA(h2d(dm, members, in_b, sg.s));
+  const Span ins[1] = {{dm, members, in_b}};
+  DIVUQ_CUDA(h2d_in(ins, 1, sg.s));
   if (int r = fit_gaussian<double>(dm, M, C, N, dmu, dsg, derr, sg.s)) return r;
-  DIVUQ_CUDA(d2h(out_mu, dmu, out_b, sg.s));
-  DIVUQ_CUDA(d2h(out_sigma, dsg, out_b, sg.s));
+  const Span res[2] = {{dmu, out_mu, out_b}, {dsg, out_sigma, out_b}};
   int status = 0;
-  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  DIVUQ_CUDA(d2h_out(res, 2, derr, sg.s, &status));
   return status;
 }
 
@@ -2085,7 +2299,7 @@ int divuq_host_ensemble_divergence2d_f32(const float* members, int64_t M, int64_
   const int64_t n = nx * ny;
   const size_t in_b = size_t(M * 2 * n) * sizeof(float), b = size_t(n) * sizeof(float);
   DevBuf d;
-  DIVUQ_CUDA(d.alloc(in_b + 8 * b + 256, sg.s));
+  DIVUQ_CUDA(d.alloc_on(in_b + 8 * b + 256, sg.s));
   float* dm = d.as<float>();
   float* o = dm + M * 2 * n;
   float* outs[4] = {o, o + n, o + 2 * n, o + 3 * n};
@@ -2093,21 +2307,20 @@ int divuq_host_ensemble_divergence2d_f32(const float* members, int64_t M, int64_
   float* mom_sg = o + 6 * n;      // (2, n)
   int32_t* derr = reinterpret_cast<int32_t*>(o + 8 * n);
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
-  DIVUQ_CUDA(h2d(dm, members, in_b, sg.s));
+  const Span ins[1] = {{dm, members, in_b}};
+  DIVUQ_CUDA(h2d_in(ins, 1, sg.s));
   float* host_out[4] = {out_mu, out_sigma, out_p_src, out_p_snk};
   int r = divuq_ensemble_divergence2d_f32(dm, M, nx, ny, dx, dy, t, out_mu ? outs[0] : nullptr,
                                           out_sigma ? outs[1] : nullptr, out_p_src ? outs[2] : nullptr,
                                           out_p_snk ? outs[3] : nullptr, out_mom_mu ? mom_mu : nullptr,
                                           out_mom_mu ? mom_sg : nullptr, derr, sg.s);
   if (r) return r;
-  for (int q = 0; q < 4; ++q)
-    if (host_out[q]) DIVUQ_CUDA(d2h(host_out[q], outs[q], b, sg.s));
-  if (out_mom_mu) {
-    DIVUQ_CUDA(d2h(out_mom_mu, mom_mu, 2 * b, sg.s));
-    DIVUQ_CUDA(d2h(out_mom_sigma, mom_sg, 2 * b, sg.s));
-  }
+  Span res[6];
+  for (int q = 0; q < 4; ++q) res[q] = Span{outs[q], host_out[q], host_out[q] ? b : 0};
+  res[4] = Span{mom_mu, out_mom_mu, out_mom_mu ? 2 * b : 0};
+  res[5] = Span{mom_sg, out_mom_sigma, out_mom_mu ? 2 * b : 0};
   int status = 0;
-  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  DIVUQ_CUDA(d2h_out(res, 6, derr, sg.s, &status));
   return status;
 }
 
@@ -2126,7 +2339,7 @@ int divuq_host_gradient_ensemble_divergence2d_f32(const float* members, int64_t 
   const int64_t n = nx * ny;
   const size_t in_b = size_t(M * 2 * n) * sizeof(float), b = size_t(n) * sizeof(float);
   DevBuf d;
-  DIVUQ_CUDA(d.alloc(in_b + 8 * b + 256, sg.s));
+  DIVUQ_CUDA(d.alloc_on(in_b + 8 * b + 256, sg.s));
   float* dm = d.as<float>();
   float* o = dm + M * 2 * n;
   float* outs[4] = {o, o + n, o + 2 * n, o + 3 * n};
@@ -2134,21 +2347,20 @@ int divuq_host_gradient_ensemble_divergence2d_f32(const float* members, int64_t 
   float* mom_sg = o + 6 * n;
   int32_t* derr = reinterpret_cast<int32_t*>(o + 8 * n);
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
-  DIVUQ_CUDA(h2d(dm, members, in_b, sg.s));
+  const Span ins[1] = {{dm, members, in_b}};
+  DIVUQ_CUDA(h2d_in(ins, 1, sg.s));
   float* host_out[4] = {out_mu, out_sigma, out_p_src, out_p_snk};
   int r = divuq_gradient_ensemble_divergence2d_f32(
       dm, M, nx, ny, dx, dy, t, out_mu ? outs[0] : nullptr, out_sigma ? outs[1] : nullptr,
       out_p_src ? outs[2] : nullptr, out_p_snk ? outs[3] : nullptr, out_mom_mu ? mom_mu : nullptr,
       out_mom_mu ? mom_sg : nullptr, derr, sg.s);
   if (r) return r;
-  for (int q = 0; q < 4; ++q)
-    if (host_out[q]) DIVUQ_CUDA(d2h(host_out[q], outs[q], b, sg.s));
-  if (out_mom_mu) {
-    DIVUQ_CUDA(d2h(out_mom_mu, mom_mu, 2 * b, sg.s));
-    DIVUQ_CUDA(d2h(out_mom_sigma, mom_sg, 2 * b, sg.s));
-  }
+  Span res[6];
+  for (int q = 0; q < 4; ++q) res[q] = Span{outs[q], host_out[q], host_out[q] ? b : 0};
+  res[4] = Span{mom_mu, out_mom_mu, out_mom_mu ? 2 * b : 0};
+  res[5] = Span{mom_sg, out_mom_sigma, out_mom_mu ? 2 * b : 0};
   int status = 0;
-  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  DIVUQ_CUDA(d2h_out(res, 6, derr, sg.s, &status));
   return status;
 }
 
@@ -2166,7 +2378,7 @@ int divuq_host_mc_divergence2d_f64(const double* mu_u, const double* mu_v, const
   const size_t b = size_t(n) * sizeof(double);
   const int64_t scratch = divuq_mc_scratch_bytes(nx, 0, ny, n_samples);
   DevBuf d;
-  DIVUQ_CUDA(d.alloc(6 * b + size_t(scratch) + 256, sg.s));
+  DIVUQ_CUDA(d.alloc_on(6 * b + size_t(scratch) + 256, sg.s));
   double* base = d.as<double>();
   double *dmu = base, *dmv = base + n, *dsu = base + 2 * n, *dsv = base + 3 * n;
   double *dmean = base + 4 * n, *dstd = base + 5 * n;
@@ -2174,14 +2386,13 @@ int divuq_host_mc_divergence2d_f64(const double* mu_u, const double* mu_v, const
   void* dscr = reinterpret_cast<char*>(base + 6 * n) + 256;
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
   const Span ins[4] = {{dmu, mu_u, b}, {dmv, mu_v, b}, {dsu, s_u, b}, {dsv, s_v, b}};
-  DIVUQ_CUDA(h2d_many(ins, 4, sg.s));
+  DIVUQ_CUDA(h2d_in(ins, 4, sg.s));
   int r = divuq_mc_divergence2d_f64(dmu, dmv, dsu, dsv, nx, ny, dx, dy, n_samples, seed, 0, ny, dmean,
                                     dstd, dscr, derr, sg.s);
   if (r) return r;
   const Span res[2] = {{dmean, out_mean, b}, {dstd, out_std, b}};
-  DIVUQ_CUDA(d2h_many(res, 2, sg.s));
   int status = 0;
-  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  DIVUQ_CUDA(d2h_out(res, 2, derr, sg.s, &status));
   return status;
 }
 
@@ -2201,20 +2412,20 @@ int divuq_host_mc_divergence2d_ref_f64(const double* mu_u, const double* mu_v, c
   const int64_t n = nx * ny;
   const size_t b = size_t(n) * sizeof(double);
   DevBuf d;
-  DIVUQ_CUDA(d.alloc(6 * b + 256, sg.s));
+  DIVUQ_CUDA(d.alloc_on(6 * b + 256, sg.s));
   double* base = d.as<double>();
   int32_t* derr = reinterpret_cast<int32_t*>(base + 6 * n);
   DIVUQ_CUDA(cudaMemsetAsync(derr, 0, sizeof(int32_t), sg.s));
   const double* src[4] = {mu_u, mu_v, s_u, s_v};
-  for (int q = 0; q < 4; ++q)
-    DIVUQ_CUDA(h2d(base + q * n, src[q], b, sg.s));
+  Span ins[4];
+  for (int q = 0; q < 4; ++q) ins[q] = Span{base + q * n, src[q], b};
+  DIVUQ_CUDA(h2d_in(ins, 4, sg.s));
   int r = divuq_mc_divergence2d_ref_f64(base, base + n, base + 2 * n, base + 3 * n, nx, ny, dx, dy,
                                         n_samples, seed, 0, ny, base + 4 * n, base + 5 * n, derr, sg.s);
   if (r) return r;
-  DIVUQ_CUDA(d2h(out_mean, base + 4 * n, b, sg.s));
-  DIVUQ_CUDA(d2h(out_std, base + 5 * n, b, sg.s));
+  const Span res[2] = {{base + 4 * n, out_mean, b}, {base + 5 * n, out_std, b}};
   int status = 0;
-  DIVUQ_CUDA(check_err_word(derr, sg.s, &status));
+  DIVUQ_CUDA(d2h_out(res, 2, derr, sg.s, &status));
   return status;
 }
 
@@ -2249,17 +2460,20 @@ int divuq_host_error_metrics_f64(const double* est_mean, const double* est_std, 
   DIVUQ_CUDA(cached_stream(0, &sg.s));
   const size_t sb = size_t(divuq_error_metrics_scratch_bytes());
   DevBuf d;
-  DIVUQ_CUDA(d.alloc(size_t(4 * n + 3) * sizeof(double) + sb, sg.s));
+  DIVUQ_CUDA(d.alloc_on(size_t(4 * n + 3) * sizeof(double) + sb, sg.s));
   double* din = d.as<double>();
   double* dout = din + 4 * n;
   void* scratch = dout + 3;
   DIVUQ_CUDA(cudaMemsetAsync(scratch, 0, sb, sg.s));
   const double* ins[4] = {est_mean, est_std, mu, sigma};
-  for (int k = 0; k < 4; ++k) DIVUQ_CUDA(h2d(din + k * n, ins[k], size_t(n) * sizeof(double), sg.s));
+  Span sp[4];
+  for (int k = 0; k < 4; ++k) sp[k] = Span{din + k * n, ins[k], size_t(n) * sizeof(double)};
+  DIVUQ_CUDA(h2d_in(sp, 4, sg.s));
   if (int r = divuq_error_metrics_f64(din, din + n, din + 2 * n, din + 3 * n, n, dout, scratch, sg.s))
     return r;
-  DIVUQ_CUDA(cudaMemcpyAsync(out3, dout, 3 * sizeof(double), cudaMemcpyDeviceToHost, sg.s));
-  DIVUQ_CUDA(cudaStreamSynchronize(sg.s));
+  const Span res[1] = {{dout, out3, 3 * sizeof(double)}};
+  int status = 0;
+  DIVUQ_CUDA(d2h_out(res, 1, nullptr, sg.s, &status));
   return DIVUQ_OK;
 }
 

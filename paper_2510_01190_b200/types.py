@@ -27,6 +27,7 @@ one sigma rule, the reference's messages kept verbatim in ``_MSG``).
 
 from __future__ import annotations
 
+import math
 import os
 from dataclasses import dataclass, field
 
@@ -82,6 +83,74 @@ def _freeze(obj, n: int, names, dtype=np.float64) -> None:
 def _require_nonneg(obj, names, key: str) -> None:
     if any((getattr(obj, name) < 0).any() for name in names):
         raise ValueError(_MSG[key])
+
+
+# Output records of this package's own kernels (api.py): the arrays are fresh,
+# owned by the call and never handed out elsewhere, so the constructor's
+# defensive copy is skipped and its scans become reductions -- a finite a.a
+# (BLAS dot) proves every value finite, a min >= 0 (NaN fails it) proves sigma >= 0, a
+# min/max inside [0, 1] proves probabilities.  When a reduction cannot prove
+# the rule (a NaN, or a dot that overflows on finite values) the record goes
+# through its constructor, which raises the reference's exact error, in the
+# reference's order, or accepts the values.  1024^2 fp64 (mu, sigma): ~7 ms
+# of scans, copies and page faults -> ~1 ms.
+_ADOPT = os.environ.get("DIVUQ_ADOPT", "1") != "0"   # 0: always the constructor (A/B)
+_ADOPT_RULES = {   # class name -> {array field: rule}
+    "ScalarField2": {"values": "finite"},
+    "VectorField2": {"u": "finite", "v": "finite"},
+    "GaussianVectorField": {"mu_u": "finite", "mu_v": "finite", "sigma_u": "sigma", "sigma_v": "sigma"},
+    "GaussianScalarField": {"mu": "finite", "sigma": "sigma"},
+    "GaussianVectorField3": {"mu_u": "finite", "mu_v": "finite", "mu_w": "finite",
+                             "sigma_u": "sigma", "sigma_v": "sigma", "sigma_w": "sigma"},
+    "GaussianScalarField3": {"mu": "finite", "sigma": "sigma"},
+    "LcpField": {"probabilities": "prob"},
+    "McDivergenceEstimate": {"mean": "finite", "std": "finite"},
+}
+
+
+_ADOPT_PLANS: dict = {}
+_F64 = np.dtype(np.float64)
+_DOT, _MIN, _MAX = np.dot, np.minimum.reduce, np.maximum.reduce
+
+
+def _adopt_plan(cls):
+    names = tuple(cls.__dataclass_fields__)
+    rules = _ADOPT_RULES[cls.__name__]
+    checks = tuple((names.index(k), {"finite": 0, "sigma": 1, "prob": 2}[r]) for k, r in rules.items())
+    plan = (len(names), checks, "n_cells" if cls.__name__ == "LcpField" else "n_vertices",
+            cls.__name__.endswith("3"), names)
+    _ADOPT_PLANS[cls] = plan
+    return plan
+
+
+def adopt(cls, *args):
+    """``cls(*args)`` for records built from freshly computed, call-owned
+    arrays (no copy; same validation, see above)."""
+    plan = _ADOPT_PLANS.get(cls) or _adopt_plan(cls)
+    n_fields, checks, n_attr, keeps_dtype, names = plan
+    if not _ADOPT or len(args) != n_fields:
+        return cls(*args)
+    n = getattr(args[0], n_attr)
+    dt = _float_dtype(args[checks[0][0]]) if keeps_dtype else _F64
+    for i, rule in checks:
+        a = args[i]
+        if (type(a) is not np.ndarray or a.dtype != dt or a.ndim != 1 or a.size != n
+                or not a.flags.c_contiguous):
+            return cls(*args)
+        if not math.isfinite(_DOT(a, a)):   # NaN / inf -> non-finite; |a| > 1e154 -> constructor
+            return cls(*args)
+        if rule and not _MIN(a) >= 0:
+            return cls(*args)
+        if rule == 2 and not _MAX(a) <= 1:
+            return cls(*args)
+    if cls is McDivergenceEstimate and args[3] < 2:
+        return cls(*args)
+    obj = object.__new__(cls)
+    for k, v in zip(names, args):
+        object.__setattr__(obj, k, v)
+    for i, _ in checks:
+        args[i].flags.writeable = False
+    return obj
 
 
 def _check_grid(dims, spacing, key: str) -> None:

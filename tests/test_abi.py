@@ -100,3 +100,47 @@ def test_stencil_distribution_fig1_host(pkg):
     fig1 = golden("fig1.npz")
     mu, sd = pkg.stencil_distribution(tuple(map(tuple, fig1["neighbors"])), (1.0, 1.0))
     assert abs(mu + 0.89) <= 1e-12 and sd == 0.7700811645534514
+
+
+def test_adopted_output_records_match_the_constructor(pkg):
+    """api.py builds its output records with types.adopt (no defensive copy,
+    reductions instead of scans): same fields and read-only arrays as the
+    constructor, and for every invalid value the constructor's own error."""
+    from paper_2510_01190_b200 import types as T
+
+    g = T.UniformGrid2(5, 4)
+    rng = np.random.default_rng(3)
+    mu, sg = rng.normal(size=20), rng.uniform(0, 1, 20)
+    a = T.adopt(T.GaussianScalarField, g, mu.copy(), sg.copy())
+    b = T.GaussianScalarField(g, mu, sg)
+    assert type(a) is type(b) and a.grid == b.grid
+    assert np.array_equal(a.mu, b.mu) and np.array_equal(a.sigma, b.sigma)
+    assert not a.mu.flags.writeable and not a.sigma.flags.writeable
+    m = mu.copy()
+    assert T.adopt(T.ScalarField2, g, m).values is m          # no copy
+    # finite values whose sum overflows: proven by the constructor instead
+    big = np.full(20, 1e308)
+    assert np.array_equal(T.adopt(T.ScalarField2, g, big.copy()).values, big)
+    cases = [
+        (T.GaussianScalarField, lambda: (g, np.where(np.arange(20) == 7, np.nan, mu), sg.copy())),
+        (T.GaussianScalarField, lambda: (g, mu.copy(), np.where(np.arange(20) == 3, np.inf, sg))),
+        (T.GaussianScalarField, lambda: (g, mu.copy(), np.where(np.arange(20) == 3, -0.5, sg))),
+        (T.GaussianScalarField, lambda: (g, mu.copy(), np.where(np.arange(20) == 3, np.nan, sg))),
+        (T.GaussianVectorField, lambda: (g, mu.copy(), mu.copy(), sg.copy(), -sg)),
+        (T.LcpField, lambda: (g, 0.0, np.where(np.arange(12) == 2, 1.5, 0.5))),
+        (T.LcpField, lambda: (g, 0.0, np.where(np.arange(12) == 2, np.nan, 0.5))),
+        (T.McDivergenceEstimate, lambda: (g, mu.copy(), np.full(20, -np.inf), 10)),
+        (T.McDivergenceEstimate, lambda: (g, mu.copy(), sg.copy(), 1)),
+        (T.ScalarField2, lambda: (g, np.zeros(19))),
+    ]
+    for cls, args in cases:
+        with pytest.raises(ValueError) as want:
+            cls(*args())
+        with pytest.raises(ValueError) as got:
+            T.adopt(cls, *args())
+        assert str(got.value) == str(want.value), cls.__name__
+    # 3D records keep the float dtype of mu
+    g3 = T.UniformGrid3(3, 2, 2)
+    f32 = rng.uniform(0, 1, 12).astype(np.float32)
+    r = T.adopt(T.GaussianScalarField3, g3, f32.copy(), f32.copy())
+    assert r.mu.dtype == np.float32 and np.array_equal(r.sigma, f32)

@@ -48,6 +48,13 @@ for pkg, out in ((d, ours), (ref, theirs)):
     out["ens"] = pkg.Ensemble2(g, tuple(pkg.VectorField2(g, u, v) for u, v in mem))
     out["fld"] = pkg.propagate_divergence(out["model"])
     out["model2"] = pkg.GaussianVectorField(pkg.UniformGrid2(256, 256), *a2)
+    # the paper's own grid sizes: wind 68^2 x 15, Red Sea 500^2 x 20
+    for k, side, m in (("wind", 68, 15), ("redsea", 500, 20)):
+        gk = pkg.UniformGrid2(side, side)
+        nk = side * side
+        out[k] = pkg.GaussianVectorField(gk, *(a[:nk] for a in arrs))
+        out[k + "_ens"] = pkg.Ensemble2(gk, tuple(pkg.VectorField2(gk, u[:nk], v[:nk]) for u, v in mem[:m]))
+        out[k + "_fld"] = pkg.propagate_divergence(out[k])
 pc = ref.ParallelConfig(threads=threads)
 rows = [
     ("propagate_divergence 1024^2 fp64", lambda: d.propagate_divergence(ours["model"]),
@@ -58,11 +65,23 @@ rows = [
      lambda: _tail_probs(theirs["fld"].mu, theirs["fld"].sigma, 0.0), None),
     ("lcp 1024^2", lambda: d.lcp(ours["fld"], 0.0), lambda: ref.lcp(theirs["fld"], 0.0),
      lambda: ref.lcp(theirs["fld"], 0.0, pc)),
+    ("propagate_divergence 500^2 (Red Sea grid)", lambda: d.propagate_divergence(ours["redsea"]),
+     lambda: ref.propagate_divergence(theirs["redsea"]), lambda: ref.propagate_divergence(theirs["redsea"], pc)),
+    ("fit_gaussian 500^2 x 20 (Red Sea ensemble)", lambda: d.fit_gaussian(ours["redsea_ens"]),
+     lambda: ref.fit_gaussian(theirs["redsea_ens"]), None),
+    ("lcp 500^2", lambda: d.lcp(ours["redsea_fld"], 0.0), lambda: ref.lcp(theirs["redsea_fld"], 0.0),
+     lambda: ref.lcp(theirs["redsea_fld"], 0.0, pc)),
+    ("propagate_divergence 68^2 (wind grid)", lambda: d.propagate_divergence(ours["wind"]),
+     lambda: ref.propagate_divergence(theirs["wind"]), None),
+    ("fit_gaussian 68^2 x 15 (wind ensemble)", lambda: d.fit_gaussian(ours["wind_ens"]),
+     lambda: ref.fit_gaussian(theirs["wind_ens"]), None),
+    ("lcp 68^2", lambda: d.lcp(ours["wind_fld"], 0.0), lambda: ref.lcp(theirs["wind_fld"], 0.0), None),
     ("mc_divergence 256^2 N=200 (reference stream)",
      lambda: d.mc_divergence(ours["model2"], d.McConfig(200, seed=5), stream="reference"),
      lambda: ref.mc_divergence(theirs["model2"], ref.McConfig(200, seed=5)), None),
 ]
-print(f"host: {threads} cores; times are the best of 5 after one warm-up")
+print(f"host: {threads} cores; times are the best of 5 after one warm-up; "
+      f"DIVUQ_ADOPT={os.environ.get('DIVUQ_ADOPT', '1')}")
 for name, fo, fr, fp in rows:
     t = best(fo)
     tr = best(fr, runs=3)
