@@ -1233,27 +1233,30 @@ static void memcpy_segs(const Seg* sg, int n) {
   });
 }
 
-// pageable spans of a call through the arena (async); false: not taken
-static bool bounce_h2d(const Span* sp, int n, cudaStream_t s, int* status) {
+// A call's spans through the arena (async): pageable ones are packed (one
+// parallel job) and go down as DMAs from the arena -- a run of spans adjacent
+// in device memory as one copy -- pinned ones DMA straight from the caller's
+// buffer.  `paged[i]`: span i is pageable.  false: not taken (too large).
+static bool bounce_h2d(const Span* sp, const bool* paged, int n, cudaStream_t s, int* status) {
   size_t total = 0;
   for (int i = 0; i < n; ++i)
-    if (sp[i].host && sp[i].bytes) total += (sp[i].bytes + 255) & ~size_t(255);
-  if (total == 0) return false;
-  const int64_t base = bounce_reserve(total, s, status);
-  if (base < 0) return false;
-  char* arena = bounce().buf + base;
-  {   // pack every span first (one parallel job), then the DMAs
+    if (paged[i]) total += (sp[i].bytes + 255) & ~size_t(255);
+  char* arena = nullptr;
+  if (total) {
+    const int64_t base = bounce_reserve(total, s, status);
+    if (base < 0) return false;
+    arena = bounce().buf + base;
     std::vector<Seg> segs;
     size_t o = 0;
     for (int i = 0; i < n; ++i) {
-      if (!sp[i].host || !sp[i].bytes) continue;
+      if (!paged[i]) continue;
       segs.push_back({arena + o, static_cast<const char*>(sp[i].host), sp[i].bytes});
       o += (sp[i].bytes + 255) & ~size_t(255);
     }
     memcpy_segs(segs.data(), int(segs.size()));
   }
   size_t off = 0;
-  const char* run_dev = nullptr;   // a run of spans adjacent in device memory -> one DMA
+  const char* run_dev = nullptr;   // a run of arena spans adjacent in device memory -> one DMA
   const char* run_host = nullptr;
   size_t run_len = 0;
   auto flush = [&]() {
@@ -1263,6 +1266,10 @@ static bool bounce_h2d(const Span* sp, int n, cudaStream_t s, int* status) {
   };
   for (int i = 0; i < n && !*status; ++i) {
     if (!sp[i].host || !sp[i].bytes) continue;
+    if (!paged[i]) {
+      *status = int(cudaMemcpyAsync(sp[i].dev, sp[i].host, sp[i].bytes, cudaMemcpyHostToDevice, s));
+      continue;
+    }
     const char* dev = static_cast<const char*>(sp[i].dev);
     if (run_len && run_dev + run_len == dev && run_host + run_len == arena + off) {
       run_len += sp[i].bytes;
@@ -1278,30 +1285,40 @@ static bool bounce_h2d(const Span* sp, int n, cudaStream_t s, int* status) {
   return true;
 }
 
-// outputs (host = destination) and the validation word: one sync
-static bool bounce_d2h(const Span* sp, int n, const int32_t* derr, cudaStream_t s, int* code,
-                       int* status) {
+// outputs (host = destination) and the validation word, ONE stream sync:
+// pinned destinations are written by the DMA, pageable ones (and the word)
+// land in the arena and are copied out after the sync
+static bool bounce_d2h(const Span* sp, const bool* paged, int n, const int32_t* derr, cudaStream_t s,
+                       int* code, int* status) {
   size_t total = derr ? 256 : 0;
   for (int i = 0; i < n; ++i)
-    if (sp[i].host && sp[i].bytes) total += (sp[i].bytes + 255) & ~size_t(255);
-  const int64_t base = bounce_reserve(total, s, status);
-  if (base < 0) return false;
-  char* arena = bounce().buf + base;
+    if (paged[i]) total += (sp[i].bytes + 255) & ~size_t(255);
+  char* arena = nullptr;
+  if (total) {
+    const int64_t base = bounce_reserve(total, s, status);
+    if (base < 0) return false;
+    arena = bounce().buf + base;
+  }
   size_t off = derr ? 256 : 0;
   if (derr && !*status)
     *status = int(cudaMemcpyAsync(arena, derr, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   for (int i = 0; i < n && !*status; ++i) {
     if (!sp[i].host || !sp[i].bytes) continue;
+    if (!paged[i]) {
+      *status = int(cudaMemcpyAsync(const_cast<void*>(sp[i].host), sp[i].dev, sp[i].bytes,
+                                    cudaMemcpyDeviceToHost, s));
+      continue;
+    }
     *status = int(cudaMemcpyAsync(arena + off, sp[i].dev, sp[i].bytes, cudaMemcpyDeviceToHost, s));
     off += (sp[i].bytes + 255) & ~size_t(255);
   }
   if (!*status) *status = int(cudaStreamSynchronize(s));
   if (*status) return true;
-  bounce().cur = 0;   // the stream is drained: the whole arena is free
+  if (total) bounce().cur = 0;   // the stream is drained: the whole arena is free
   off = derr ? 256 : 0;
   std::vector<Seg> segs;
   for (int i = 0; i < n; ++i) {
-    if (!sp[i].host || !sp[i].bytes) continue;
+    if (!paged[i]) continue;
     segs.push_back({static_cast<char*>(const_cast<void*>(sp[i].host)), arena + off, sp[i].bytes});
     off += (sp[i].bytes + 255) & ~size_t(255);
   }
@@ -1315,18 +1332,19 @@ static bool bounce_d2h(const Span* sp, int n, const int32_t* derr, cudaStream_t 
   return true;
 }
 
-// inputs of a call: small pageable totals through the arena, else h2d_many
+constexpr int kMaxSpans = 8;
+static void classify(const Span* sp, int n, bool* paged) {
+  for (int i = 0; i < n; ++i) paged[i] = sp[i].host && sp[i].bytes && pageable(sp[i].host);
+}
+
+// inputs of a call: through the arena when its pageable part is small, else
+// h2d_many (the staged ring for large pageable totals)
 int h2d_in(const Span* sp, int n, cudaStream_t s) {
-  size_t paged = 0;
-  bool any_pinned = false;
-  for (int i = 0; i < n; ++i)
-    if (sp[i].host && sp[i].bytes) {
-      if (pageable(sp[i].host)) paged += sp[i].bytes;
-      else any_pinned = true;
-    }
-  if (!any_pinned && paged) {
+  if (n <= kMaxSpans) {
+    bool paged[kMaxSpans];
+    classify(sp, n, paged);
     int status = 0;
-    if (bounce_h2d(sp, n, s, &status)) return status;
+    if (bounce_h2d(sp, paged, n, s, &status)) return status;
     if (status) return status;
   }
   return h2d_many(sp, n, s);
@@ -1336,16 +1354,11 @@ int h2d_in(const Span* sp, int n, cudaStream_t s) {
 // ENEGSIGMA); returns a CUDA status.  Leaves the stream drained.
 int d2h_out(const Span* sp, int n, const int32_t* derr, cudaStream_t s, int* code) {
   *code = DIVUQ_OK;
-  size_t paged = 0;
-  bool any_pinned = false;
-  for (int i = 0; i < n; ++i)
-    if (sp[i].host && sp[i].bytes) {
-      if (pageable(sp[i].host)) paged += sp[i].bytes;
-      else any_pinned = true;
-    }
-  if (!any_pinned) {
+  if (n <= kMaxSpans) {
+    bool paged[kMaxSpans];
+    classify(sp, n, paged);
     int status = 0;
-    if (bounce_d2h(sp, n, derr, s, code, &status)) return status;
+    if (bounce_d2h(sp, paged, n, derr, s, code, &status)) return status;
     if (status) return status;
   }
   if (int r = d2h_many(sp, n, s)) return r;

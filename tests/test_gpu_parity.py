@@ -742,3 +742,38 @@ def test_tma2d_matches_register_kernels_bitwise(dev, dtype, shape, rng, monkeypa
     bad[3][n // 2] = -1.0
     with pytest.raises(ValueError):
         dev.propagate2d(*bad, nx, ny, 0.7, 1.3, 0.0)
+
+
+@pytest.mark.parametrize("side", [68, 500, 1024])
+def test_host_entry_staging_paths_bitwise(dev, side, rng):
+    """The host-buffer entry points stage pageable spans through the pinned
+    bounce arena (small calls) or the staged ring (large ones) and DMA pinned
+    spans directly; any mix of pinned and pageable inputs/outputs, repeated
+    calls on the warm arena, and the validation word read in the same sync
+    give the device path's bits."""
+    from paper_2510_01190_b200._lib import lib
+
+    n = side * side
+    mu_u, mu_v, s_u, s_v = random_model_arrays(n, rng)
+    want = dev.propagate2d(cu(mu_u), cu(mu_v), cu(s_u), cu(s_v), side, side, 1.0, 1.0, 0.0)
+    want = {k: host(v) for k, v in want.items()}
+    pinned = [torch.from_numpy(a.copy()).pin_memory() for a in (mu_u, mu_v, s_u, s_v)]
+    for mask in (0b0000, 0b0101, 0b1111):
+        ins = [pinned[k].data_ptr() if mask >> k & 1 else a.__array_interface__["data"][0]
+               for k, a in enumerate((mu_u, mu_v, s_u, s_v))]
+        outs_np = [np.full(n, np.nan) for _ in range(4)]
+        outs_pin = [torch.full((n,), float("nan"), dtype=torch.float64).pin_memory() for _ in range(4)]
+        ptrs = [outs_pin[k].data_ptr() if mask >> k & 1 else outs_np[k].__array_interface__["data"][0]
+                for k in range(4)]
+        for _ in range(2):   # second call: warm arena / ring
+            assert lib.divuq_host_propagate2d_f64(*ins, side, side, 1.0, 1.0, 0.0, *ptrs, 0) == 0
+        got = [outs_pin[k].numpy() if mask >> k & 1 else outs_np[k] for k in range(4)]
+        for k, key in enumerate(("mu", "sigma", "p_src", "p_snk")):
+            assert np.array_equal(got[k], want[key]), (side, mask, key)
+    bad = s_v.copy()
+    bad[n // 2] = -1.0
+    o = [np.empty(n) for _ in range(4)]
+    st = lib.divuq_host_propagate2d_f64(*(a.__array_interface__["data"][0] for a in (mu_u, mu_v, s_u, bad)),
+                                        side, side, 1.0, 1.0, 0.0,
+                                        *(a.__array_interface__["data"][0] for a in o), 0)
+    assert st != 0
