@@ -1171,7 +1171,7 @@ static Bounce& bounce() {
   return b;
 }
 static size_t bounce_max() {
-  static const size_t v = size_t(std::max<int64_t>(0, env_int("DIVUQ_BOUNCE_MAX_KB", 16384))) << 10;
+  static const size_t v = size_t(std::max<int64_t>(0, env_int("DIVUQ_BOUNCE_MAX_KB", 32832))) << 10;
   return v;
 }
 // room for `bytes` more on stream s; returns the arena offset or -1 (use the

@@ -777,3 +777,21 @@ def test_host_entry_staging_paths_bitwise(dev, side, rng):
                                         side, side, 1.0, 1.0, 0.0,
                                         *(a.__array_interface__["data"][0] for a in o), 0)
     assert st != 0
+
+
+def test_device_api_launches_on_torch_current_stream(dev, rng):
+    """The device API enqueues on torch's current stream (raw-handle getter):
+    same handle as the public object, inside a stream context too, and a
+    launch on a side stream is ordered there."""
+    assert dev._stream() == torch.cuda.current_stream().cuda_stream
+    side = torch.cuda.Stream()
+    n = 256 * 256
+    arrs = [cu(a) for a in random_model_arrays(n, rng)]
+    base = dev.propagate2d(*arrs, 256, 256, 1.0, 1.0, 0.0)
+    with torch.cuda.stream(side):
+        assert dev._stream() == side.cuda_stream
+        side.wait_stream(torch.cuda.default_stream())
+        o = dev.propagate2d(*arrs, 256, 256, 1.0, 1.0, 0.0, check=False)
+    side.synchronize()
+    for k in base:
+        assert torch.equal(o[k], base[k])
