@@ -255,7 +255,11 @@ int divuq_divuq1_format_real(double x, char* out, int64_t cap);
 
 /* ---- host-buffer entry points (the reference-facing path) ----------------
  * Same semantics as the device versions; synchronous; `device` = CUDA
- * ordinal.  Host buffers may be pinned (direct DMA) or pageable.  The 3D
+ * ordinal.  Host buffers may be pinned (direct DMA) or pageable, mixed in
+ * one call.  Pageable spans of a call up to DIVUQ_BOUNCE_MAX_KB (32 MB) are
+ * packed into a per-thread pinned arena (adjacent device spans as one DMA);
+ * outputs and the validation word come back with one stream sync; larger
+ * pageable totals go through a staged ring of pinned buffers.  The 3D
  * variant pipelines z-chunks: host->device copies, the kernel and
  * device->host copies of consecutive chunks overlap on separate streams. */
 int divuq_host_propagate2d_f64(const double* mu_u, const double* mu_v,
