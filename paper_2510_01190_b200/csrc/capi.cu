@@ -1163,6 +1163,7 @@ int d2h_many(const Span* sp, int n, cudaStream_t s) {
 // bytes are overwritten while a DMA may still read them.
 struct Bounce {
   char* buf = nullptr;
+  char* dbuf = nullptr;   // the arena as the device sees it (mapped pinned memory)
   size_t cap = 0, cur = 0;
   cudaStream_t stream = nullptr;
 };
@@ -1193,9 +1194,14 @@ static int64_t bounce_reserve(size_t bytes, cudaStream_t s, int* status) {
     size_t cap = size_t(1) << 20;
     while (cap < need) cap <<= 1;
     cap = std::min(cap, bounce_max());
-    if ((*status = int(cudaHostAlloc(reinterpret_cast<void**>(&b.buf), cap, cudaHostAllocPortable)))) {
+    if ((*status = int(cudaHostAlloc(reinterpret_cast<void**>(&b.buf), cap,
+                                     cudaHostAllocPortable | cudaHostAllocMapped)))) {
       b.buf = nullptr;
       return -1;
+    }
+    if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&b.dbuf), b.buf, 0) != cudaSuccess) {
+      cudaGetLastError();
+      b.dbuf = nullptr;   // no zero-copy: the DMA paths still work
     }
     b.cap = cap;
   }
@@ -1233,27 +1239,93 @@ static void memcpy_segs(const Seg* sg, int n) {
   });
 }
 
+// Small calls: ONE copy kernel instead of one DMA per span.  A DMA of
+// <= 128 KB costs ~5 us of copy-engine time (config 0's e2e call was nine of
+// them around a 2.8 us kernel, tools/host_entry_trace.py); a grid of CTAs
+// reading mapped pinned memory (the arena, or the caller's pinned buffers)
+// keeps ~100 KB of PCIe reads in flight, so a whole call's inputs -- or its
+// outputs plus the validation word -- move in one launch.  Host-side sources
+// are read with ld.global.cv (never served from a cache line of an earlier
+// call); writes to host memory are visible after the stream sync.
+constexpr int kCopyMax = 10;
+struct CopyList {
+  const char* src[kCopyMax];
+  char* dst[kCopyMax];
+  int64_t bytes[kCopyMax];
+  int n;
+};
+template <typename V>
+__device__ __forceinline__ void copy_run(const char* a, char* b, int64_t nb, int64_t tid, int64_t nt) {
+  const int64_t nv = nb / int64_t(sizeof(V));
+  const V* av = reinterpret_cast<const V*>(a);
+  V* bv = reinterpret_cast<V*>(b);
+  for (int64_t i = tid; i < nv; i += nt) bv[i] = __ldcv(av + i);
+  for (int64_t i = nv * int64_t(sizeof(V)) + tid; i < nb; i += nt) b[i] = __ldcv(a + i);
+}
+__global__ void __launch_bounds__(256) copy_spans_kernel(const CopyList L) {
+  const int64_t tid = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t nt = int64_t(gridDim.x) * blockDim.x;
+  for (int s = 0; s < L.n; ++s) {
+    const uintptr_t al = reinterpret_cast<uintptr_t>(L.src[s]) | reinterpret_cast<uintptr_t>(L.dst[s]);
+    if ((al & 15) == 0) copy_run<int4>(L.src[s], L.dst[s], L.bytes[s], tid, nt);
+    else if ((al & 7) == 0) copy_run<long long>(L.src[s], L.dst[s], L.bytes[s], tid, nt);
+    else if ((al & 3) == 0) copy_run<int>(L.src[s], L.dst[s], L.bytes[s], tid, nt);
+    else copy_run<char>(L.src[s], L.dst[s], L.bytes[s], tid, nt);
+  }
+}
+static size_t zc_max() {
+  static const size_t v = size_t(std::max<int64_t>(0, env_int("DIVUQ_ZC_MAX_KB", 4096))) << 10;
+  return v;
+}
+static int launch_copy(const CopyList& L, size_t total, cudaStream_t s) {
+  if (L.n == 0) return 0;
+  const int64_t vecs = int64_t((total + 15) / 16);
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((vecs + 255) / 256, 2 * int64_t(sm_count())));
+  copy_spans_kernel<<<unsigned(grid), 256, 0, s>>>(L);
+  return int(cudaGetLastError());
+}
+
 // A call's spans through the arena (async): pageable ones are packed (one
-// parallel job) and go down as DMAs from the arena -- a run of spans adjacent
-// in device memory as one copy -- pinned ones DMA straight from the caller's
-// buffer.  `paged[i]`: span i is pageable.  false: not taken (too large).
-static bool bounce_h2d(const Span* sp, const bool* paged, int n, cudaStream_t s, int* status) {
-  size_t total = 0;
-  for (int i = 0; i < n; ++i)
-    if (paged[i]) total += (sp[i].bytes + 255) & ~size_t(255);
+// parallel job); then either ONE copy kernel moves every span (small calls,
+// zc_max()) or DMAs do -- from the arena, a run of spans adjacent in device
+// memory as one copy, and pinned spans straight from the caller's buffer.
+// `hdev[i]`: span i's host buffer as the device sees it when it is pinned,
+// nullptr when pageable.  false: not taken (too large for the arena).
+static bool bounce_h2d(const Span* sp, const char* const* hdev, int n, cudaStream_t s, int* status) {
+  size_t total = 0, all = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!sp[i].host || !sp[i].bytes) continue;
+    all += sp[i].bytes;
+    if (!hdev[i]) total += (sp[i].bytes + 255) & ~size_t(255);
+  }
   char* arena = nullptr;
+  const char* darena = nullptr;
   if (total) {
     const int64_t base = bounce_reserve(total, s, status);
     if (base < 0) return false;
     arena = bounce().buf + base;
+    darena = bounce().dbuf ? bounce().dbuf + base : nullptr;
     std::vector<Seg> segs;
     size_t o = 0;
     for (int i = 0; i < n; ++i) {
-      if (!paged[i]) continue;
+      if (!sp[i].host || !sp[i].bytes || hdev[i]) continue;
       segs.push_back({arena + o, static_cast<const char*>(sp[i].host), sp[i].bytes});
       o += (sp[i].bytes + 255) & ~size_t(255);
     }
     memcpy_segs(segs.data(), int(segs.size()));
+  }
+  if (all <= zc_max() && n <= kCopyMax && (darena || !total)) {
+    CopyList L{};
+    size_t off = 0;
+    for (int i = 0; i < n; ++i) {
+      if (!sp[i].host || !sp[i].bytes) continue;
+      L.src[L.n] = hdev[i] ? hdev[i] : darena + off;
+      L.dst[L.n] = static_cast<char*>(sp[i].dev);
+      L.bytes[L.n++] = int64_t(sp[i].bytes);
+      if (!hdev[i]) off += (sp[i].bytes + 255) & ~size_t(255);
+    }
+    *status = launch_copy(L, all, s);
+    return true;
   }
   size_t off = 0;
   const char* run_dev = nullptr;   // a run of arena spans adjacent in device memory -> one DMA
@@ -1266,7 +1338,7 @@ static bool bounce_h2d(const Span* sp, const bool* paged, int n, cudaStream_t s,
   };
   for (int i = 0; i < n && !*status; ++i) {
     if (!sp[i].host || !sp[i].bytes) continue;
-    if (!paged[i]) {
+    if (hdev[i]) {
       *status = int(cudaMemcpyAsync(sp[i].dev, sp[i].host, sp[i].bytes, cudaMemcpyHostToDevice, s));
       continue;
     }
@@ -1286,39 +1358,63 @@ static bool bounce_h2d(const Span* sp, const bool* paged, int n, cudaStream_t s,
 }
 
 // outputs (host = destination) and the validation word, ONE stream sync:
-// pinned destinations are written by the DMA, pageable ones (and the word)
-// land in the arena and are copied out after the sync
-static bool bounce_d2h(const Span* sp, const bool* paged, int n, const int32_t* derr, cudaStream_t s,
-                       int* code, int* status) {
-  size_t total = derr ? 256 : 0;
-  for (int i = 0; i < n; ++i)
-    if (paged[i]) total += (sp[i].bytes + 255) & ~size_t(255);
+// pinned destinations are written directly, pageable ones (and the word)
+// land in the arena and are copied out after the sync; small calls move
+// everything with one copy kernel
+static bool bounce_d2h(const Span* sp, const char* const* hdev, int n, const int32_t* derr,
+                       cudaStream_t s, int* code, int* status) {
+  size_t total = derr ? 256 : 0, all = derr ? sizeof(int32_t) : 0;
+  for (int i = 0; i < n; ++i) {
+    if (!sp[i].host || !sp[i].bytes) continue;
+    all += sp[i].bytes;
+    if (!hdev[i]) total += (sp[i].bytes + 255) & ~size_t(255);
+  }
   char* arena = nullptr;
+  char* darena = nullptr;
   if (total) {
     const int64_t base = bounce_reserve(total, s, status);
     if (base < 0) return false;
     arena = bounce().buf + base;
+    darena = bounce().dbuf ? bounce().dbuf + base : nullptr;
   }
-  size_t off = derr ? 256 : 0;
-  if (derr && !*status)
-    *status = int(cudaMemcpyAsync(arena, derr, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  for (int i = 0; i < n && !*status; ++i) {
-    if (!sp[i].host || !sp[i].bytes) continue;
-    if (!paged[i]) {
-      *status = int(cudaMemcpyAsync(const_cast<void*>(sp[i].host), sp[i].dev, sp[i].bytes,
-                                    cudaMemcpyDeviceToHost, s));
-      continue;
+  if (all <= zc_max() && n + 1 <= kCopyMax && (darena || !total)) {
+    CopyList L{};
+    if (derr) {
+      L.src[L.n] = reinterpret_cast<const char*>(derr);
+      L.dst[L.n] = darena;
+      L.bytes[L.n++] = sizeof(int32_t);
     }
-    *status = int(cudaMemcpyAsync(arena + off, sp[i].dev, sp[i].bytes, cudaMemcpyDeviceToHost, s));
-    off += (sp[i].bytes + 255) & ~size_t(255);
+    size_t off = derr ? 256 : 0;
+    for (int i = 0; i < n; ++i) {
+      if (!sp[i].host || !sp[i].bytes) continue;
+      L.src[L.n] = static_cast<const char*>(sp[i].dev);
+      L.dst[L.n] = hdev[i] ? const_cast<char*>(hdev[i]) : darena + off;
+      L.bytes[L.n++] = int64_t(sp[i].bytes);
+      if (!hdev[i]) off += (sp[i].bytes + 255) & ~size_t(255);
+    }
+    *status = launch_copy(L, all, s);
+  } else {
+    size_t off = derr ? 256 : 0;
+    if (derr && !*status)
+      *status = int(cudaMemcpyAsync(arena, derr, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    for (int i = 0; i < n && !*status; ++i) {
+      if (!sp[i].host || !sp[i].bytes) continue;
+      if (hdev[i]) {
+        *status = int(cudaMemcpyAsync(const_cast<void*>(sp[i].host), sp[i].dev, sp[i].bytes,
+                                      cudaMemcpyDeviceToHost, s));
+        continue;
+      }
+      *status = int(cudaMemcpyAsync(arena + off, sp[i].dev, sp[i].bytes, cudaMemcpyDeviceToHost, s));
+      off += (sp[i].bytes + 255) & ~size_t(255);
+    }
   }
   if (!*status) *status = int(cudaStreamSynchronize(s));
   if (*status) return true;
   if (total) bounce().cur = 0;   // the stream is drained: the whole arena is free
-  off = derr ? 256 : 0;
+  size_t off = derr ? 256 : 0;
   std::vector<Seg> segs;
   for (int i = 0; i < n; ++i) {
-    if (!paged[i]) continue;
+    if (!sp[i].host || !sp[i].bytes || hdev[i]) continue;
     segs.push_back({static_cast<char*>(const_cast<void*>(sp[i].host)), arena + off, sp[i].bytes});
     off += (sp[i].bytes + 255) & ~size_t(255);
   }
@@ -1333,18 +1429,30 @@ static bool bounce_d2h(const Span* sp, const bool* paged, int n, const int32_t* 
 }
 
 constexpr int kMaxSpans = 8;
-static void classify(const Span* sp, int n, bool* paged) {
-  for (int i = 0; i < n; ++i) paged[i] = sp[i].host && sp[i].bytes && pageable(sp[i].host);
+// hdev[i]: the device view of span i's host buffer when it is pinned (or
+// registered) host memory, nullptr when it is pageable or empty
+static void classify(const Span* sp, int n, const char** hdev) {
+  for (int i = 0; i < n; ++i) {
+    hdev[i] = nullptr;
+    if (!sp[i].host || !sp[i].bytes) continue;
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, sp[i].host) != cudaSuccess) { cudaGetLastError(); continue; }
+    if (a.type == cudaMemoryTypeUnregistered) continue;
+    // device memory passed as a "host" span: let the DMA path handle it
+    hdev[i] = a.type == cudaMemoryTypeHost && a.devicePointer ? static_cast<const char*>(a.devicePointer)
+                                                              : nullptr;
+    if (!hdev[i]) hdev[i] = static_cast<const char*>(sp[i].host);   // pinned but unmapped: DMA only
+  }
 }
 
-// inputs of a call: through the arena when its pageable part is small, else
+// inputs of a call: through the arena / one copy kernel when small, else
 // h2d_many (the staged ring for large pageable totals)
 int h2d_in(const Span* sp, int n, cudaStream_t s) {
   if (n <= kMaxSpans) {
-    bool paged[kMaxSpans];
-    classify(sp, n, paged);
+    const char* hdev[kMaxSpans];
+    classify(sp, n, hdev);
     int status = 0;
-    if (bounce_h2d(sp, paged, n, s, &status)) return status;
+    if (bounce_h2d(sp, hdev, n, s, &status)) return status;
     if (status) return status;
   }
   return h2d_many(sp, n, s);
@@ -1355,10 +1463,10 @@ int h2d_in(const Span* sp, int n, cudaStream_t s) {
 int d2h_out(const Span* sp, int n, const int32_t* derr, cudaStream_t s, int* code) {
   *code = DIVUQ_OK;
   if (n <= kMaxSpans) {
-    bool paged[kMaxSpans];
-    classify(sp, n, paged);
+    const char* hdev[kMaxSpans];
+    classify(sp, n, hdev);
     int status = 0;
-    if (bounce_d2h(sp, paged, n, derr, s, code, &status)) return status;
+    if (bounce_d2h(sp, hdev, n, derr, s, code, &status)) return status;
     if (status) return status;
   }
   if (int r = d2h_many(sp, n, s)) return r;
