@@ -258,7 +258,9 @@ int divuq_divuq1_format_real(double x, char* out, int64_t cap);
  * ordinal.  Host buffers may be pinned (direct DMA) or pageable, mixed in
  * one call.  Pageable spans of a call up to DIVUQ_BOUNCE_MAX_KB (32 MB) are
  * packed into a per-thread pinned arena (adjacent device spans as one DMA);
- * outputs and the validation word come back with one stream sync; larger
+ * outputs and the validation word come back with one stream sync; calls up
+ * to DIVUQ_ZC_MAX_KB (4 MB) per direction move all their spans with one copy
+ * kernel over mapped pinned memory instead of one DMA each; larger
  * pageable totals go through a staged ring of pinned buffers.  The 3D
  * variant pipelines z-chunks: host->device copies, the kernel and
  * device->host copies of consecutive chunks overlap on separate streams. */
