@@ -257,7 +257,9 @@ int divuq_divuq1_format_real(double x, char* out, int64_t cap);
  * Same semantics as the device versions; synchronous; `device` = CUDA
  * ordinal.  Host buffers may be pinned (direct DMA) or pageable, mixed in
  * one call.  Pageable spans of a call up to DIVUQ_BOUNCE_MAX_KB (32 MB) are
- * packed into a per-thread pinned arena (adjacent device spans as one DMA);
+ * packed into a per-thread pinned arena (adjacent device spans as one DMA;
+ * each calling thread keeps its arena, sized to its largest such call, for
+ * the life of the process -- set DIVUQ_BOUNCE_MAX_KB=0 to never allocate it);
  * outputs and the validation word come back with one stream sync; calls up
  * to DIVUQ_ZC_MAX_KB (4 MB) per direction move all their spans with one copy
  * kernel over mapped pinned memory instead of one DMA each; larger
