@@ -1,6 +1,7 @@
 // C ABI of the divergence-uncertainty hot path: launchers + host pipelines.
 // Declarations and reference citations: include/divuq_b200.h.
 #include <cuda_runtime.h>
+#include <emmintrin.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -966,16 +967,45 @@ struct DevBuf {
 // drop-in probe, tools/dropin_probe.py): pageable D2H is the slower direction
 constexpr size_t kStageMinH2D = size_t(64) << 20, kStageMinD2H = size_t(12) << 20;
 
+// Host copies of the staged paths.  Every staged byte is read by the host
+// copy, written to the staging buffer and read again by the DMA, so these
+// paths are bound by host DRAM bandwidth (tools/host_membw_probe.py, ~45 GB/s
+// on the B200 boxes).  Streaming (non-temporal) stores drop the
+// read-for-ownership of each destination line: one DRAM pass fewer per byte.
+static void copy_lines(char* dst, const char* src, size_t n) {
+  static const bool streaming = env_int("DIVUQ_NT_COPY", 1) != 0;
+  if (!streaming || n < (size_t(64) << 10)) { std::memcpy(dst, src, n); return; }
+  const size_t head = std::min(n, (16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & size_t(15));
+  std::memcpy(dst, src, head);
+  dst += head; src += head; n -= head;
+  const size_t v = n / 64;
+  for (size_t i = 0; i < v; ++i, src += 64, dst += 64) {
+    const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src));
+    const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + 16));
+    const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + 32));
+    const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + 48));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst), a);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + 16), b);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + 32), c);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + 48), d);
+  }
+  std::memcpy(dst, src, n - v * 64);
+  _mm_sfence();   // the streamed lines are globally visible before the DMA / the caller reads them
+}
+static int copy_threads() {
+  static const int v = int(std::max<int64_t>(1, std::min<int64_t>(16, env_int("DIVUQ_COPY_THREADS", 16))));
+  return v;
+}
+
 static void memcpy_parallel(char* dst, const char* src, int64_t len) {
-  constexpr int kMaxThreads = 16;
   const int64_t kSlice = int64_t(2) << 20;
   const int64_t hw = std::max(1u, std::thread::hardware_concurrency());
-  const int nt = int(std::min<int64_t>(std::min<int64_t>(kMaxThreads, hw), (len + kSlice - 1) / kSlice));
-  if (nt <= 1) { std::memcpy(dst, src, size_t(len)); return; }
+  const int nt = int(std::min<int64_t>(std::min<int64_t>(copy_threads(), hw), (len + kSlice - 1) / kSlice));
+  if (nt <= 1) { copy_lines(dst, src, size_t(len)); return; }
   const int64_t per = (len + nt - 1) / nt;
   io::HostPool::get().run(nt, [&](int t) {
     const int64_t a = t * per, n = std::min(per, len - a);
-    if (n > 0) std::memcpy(dst + a, src + a, size_t(n));
+    if (n > 0) copy_lines(dst + a, src + a, size_t(n));
   });
 }
 
@@ -1219,9 +1249,9 @@ static void memcpy_segs(const Seg* sg, int n) {
   for (int i = 0; i < n; ++i) total += sg[i].len;
   const int64_t hw = std::max(1u, std::thread::hardware_concurrency());
   const int nt = total < (size_t(512) << 10) ? 1
-                 : int(std::min<int64_t>({16, hw, int64_t(total / (size_t(256) << 10))}));
+                 : int(std::min<int64_t>({int64_t(copy_threads()), hw, int64_t(total / (size_t(256) << 10))}));
   if (nt <= 1) {
-    for (int i = 0; i < n; ++i) std::memcpy(sg[i].dst, sg[i].src, sg[i].len);
+    for (int i = 0; i < n; ++i) copy_lines(sg[i].dst, sg[i].src, sg[i].len);
     return;
   }
   const size_t per = (total + nt - 1) / nt;
@@ -1231,7 +1261,7 @@ static void memcpy_segs(const Seg* sg, int n) {
       const size_t e = base + sg[i].len;
       if (a < e) {
         const size_t lo = a - base, hi = std::min(b, e) - base;
-        std::memcpy(sg[i].dst + lo, sg[i].src + lo, hi - lo);
+        copy_lines(sg[i].dst + lo, sg[i].src + lo, hi - lo);
         a = base + hi;
       }
       base = e;
