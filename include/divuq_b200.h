@@ -366,6 +366,12 @@ int divuq_fit_gaussian_strided_f32(const float* members, int64_t n_members, int6
                                    int64_t n_points, float* out_mu, float* out_sigma,
                                    float* out_r, int32_t* err_word, void* stream);
 
+/* Page-lock (portable, mapped) / release caller-owned host memory: the
+ * drop-in layer pins its pooled output blocks once so host entries write
+ * results straight into them (cudaHostRegister / cudaHostUnregister). */
+int divuq_host_register(void* ptr, int64_t bytes);
+int divuq_host_unregister(void* ptr);
+
 /* Peer memory (CUDA IPC) for the z-slab exchange over NVLink: export the
  * allocation holding `ptr` (handle: divuq_ipc_handle_bytes() bytes, plus the
  * offset of ptr inside it); import maps a neighbour's export (peer access

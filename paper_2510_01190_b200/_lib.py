@@ -99,6 +99,8 @@ SIGNATURES = {
     "divuq_host_mc_divergence2d_ref_f64": (
         _int, [_p] * 4 + [_i64, _i64, _f64, _f64, _i64, _u64, _p, _p, _int]),
     "divuq_fit_gaussian_strided_f32": (_int, [_p, _i64, _i64, _i64, _p, _p, _p, _p, _p]),
+    "divuq_host_register": (_int, [_p, _i64]),
+    "divuq_host_unregister": (_int, [_p]),
     "divuq_ipc_handle_bytes": (_i64, []),
     "divuq_ipc_export": (_int, [_p, _p, _p]),
     "divuq_ipc_import": (_int, [_p, _i64, _p, _p]),

@@ -11,6 +11,7 @@ package does not import.
 
 from __future__ import annotations
 
+import sys
 from typing import NamedTuple
 
 import numpy as np
@@ -37,6 +38,78 @@ from .types import (
 _DEVICE = 0
 
 
+class _OutputPool:
+    """Page-locked host blocks for the large results of the drop-in calls.
+
+    A fresh ``np.empty`` result of megabytes is unpopulated memory: the copy
+    that fills it page-faults every 4 KB (fit_gaussian 1024^2 x 20: 8.7 ms in
+    the C entry with warm outputs, 17 ms with fresh ones).  Results of at
+    least ``MIN_BYTES`` are instead views of pooled blocks that were pinned
+    once (``divuq_host_register``): the host entries DMA -- or, for small
+    calls, copy-kernel -- straight into them.  A block is reused only when no
+    array refers to it any more (every result is a view whose ``.base`` is
+    the block, so the block's reference count says whether one is alive).
+    Pinned bytes are capped (``DIVUQ_OUT_POOL_MB``, default 512; 0 disables
+    the pool): past the cap free blocks are released, then plain ``np.empty``
+    is used.  Same values, shapes and dtypes either way.
+    """
+
+    MIN_BYTES = 4 << 20
+
+    def __init__(self):
+        import os
+        import threading
+
+        self._cap = int(os.environ.get("DIVUQ_OUT_POOL_MB", "512")) << 20
+        self._blocks: list = []
+        self._sentinel = [np.empty(1, np.uint8)]
+        self._bytes = 0
+        self._lock = threading.Lock()
+
+    def empty(self, shape, dtype=np.float64):
+        dt = np.dtype(dtype)
+        nbytes = int(np.prod(shape)) * dt.itemsize
+        if self._cap <= 0 or nbytes < self.MIN_BYTES:
+            return np.empty(shape, dt)
+        with self._lock:
+            # a block nothing else refers to has the reference count of the
+            # never-handed-out sentinel, measured the same way (no guess at
+            # the interpreter's own references)
+            idle = _refs(self._sentinel, 0)
+            for i in range(len(self._blocks)):
+                if self._blocks[i].nbytes == nbytes and _refs(self._blocks, i) == idle:
+                    block = self._blocks.pop(i)    # most recently used last
+                    self._blocks.append(block)
+                    return block.view(dt).reshape(shape)
+            i = 0
+            while self._bytes + nbytes > self._cap and i < len(self._blocks):
+                if _refs(self._blocks, i) == idle:
+                    block = self._blocks.pop(i)
+                    lib.divuq_host_unregister(_p(block))
+                    self._bytes -= block.nbytes
+                    del block
+                else:
+                    i += 1
+            if self._bytes + nbytes > self._cap:
+                return np.empty(shape, dt)
+            block = np.empty(nbytes, np.uint8)
+            if lib.divuq_host_register(_p(block), nbytes) != 0:
+                return np.empty(shape, dt)
+            self._blocks.append(block)
+            self._bytes += nbytes
+            return block.view(dt).reshape(shape)
+
+
+def _refs(lst, i):
+    """Reference count of lst[i] as seen from here (same for every list)."""
+    for b in lst[i:i + 1]:
+        return sys.getrefcount(b)
+
+
+_POOL = _OutputPool()
+_out = _POOL.empty
+
+
 def set_device(ordinal: int) -> None:
     """CUDA device used by the host-buffer entry points (default 0)."""
     global _DEVICE
@@ -58,8 +131,8 @@ def fit_gaussian(ensemble: Ensemble2) -> GaussianVectorField:
     """
     stacked = _c64(ensemble.stacked())  # (M, 2, N)
     m, c, n = stacked.shape
-    mu = np.empty((c, n))
-    sg = np.empty((c, n))
+    mu = _out((c, n))
+    sg = _out((c, n))
     _check(lib.divuq_host_fit_gaussian_f64(_p(stacked), m, c, n, _p(mu), _p(sg), _DEVICE))
     return adopt(GaussianVectorField, ensemble.grid, mu[0], mu[1], sg[0], sg[1])
 
@@ -93,10 +166,10 @@ def propagate_with_probabilities(model: GaussianVectorField, t: float = 0.0, *,
     """
     g = model.grid
     n = g.n_vertices
-    mu = np.empty(n)
-    sg = np.empty(n)
-    ps = np.empty(n) if probabilities else None
-    pk = np.empty(n) if probabilities else None
+    mu = _out(n)
+    sg = _out(n)
+    ps = _out(n) if probabilities else None
+    pk = _out(n) if probabilities else None
     _check(lib.divuq_host_propagate2d_f64(
         _p(model.mu_u), _p(model.mu_v), _p(model.sigma_u), _p(model.sigma_v), g.nx, g.ny,
         float(g.dx), float(g.dy), float(t), _p(mu), _p(sg), _p(ps), _p(pk), _DEVICE))
@@ -163,8 +236,8 @@ def tail_probs(mu, sigma, isovalue: float):
     sigma = _c64(sigma)
     if mu.shape != sigma.shape:
         raise ValueError("mu and sigma must have the same shape")
-    below = np.empty_like(mu)
-    above = np.empty_like(mu)
+    below = _out(mu.shape, mu.dtype)
+    above = _out(mu.shape, mu.dtype)
     _check(lib.divuq_host_tail_probs_f64(_p(mu), _p(sigma), mu.size, float(isovalue), _p(below),
                                          _p(above), _DEVICE))
     return below, above
@@ -197,8 +270,8 @@ def mc_divergence(model: GaussianVectorField, config: McConfig, *,
         raise ValueError("stream must be 'philox' or 'reference'")
     g = model.grid
     n = g.n_vertices
-    mean = np.empty(n)
-    std = np.empty(n)
+    mean = _out(n)
+    std = _out(n)
     fn = (lib.divuq_host_mc_divergence2d_f64 if stream == "philox"
           else lib.divuq_host_mc_divergence2d_ref_f64)
     _check(fn(
@@ -405,7 +478,7 @@ def propagate_lcp(model, isovalue: float) -> tuple[GaussianScalarField, LcpField
     divergence field through host memory in between."""
     g = model.grid
     n = g.n_vertices
-    mu, sg, out = np.empty(n), np.empty(n), np.empty(g.n_cells)
+    mu, sg, out = _out(n), _out(n), _out(g.n_cells)
     _check(lib.divuq_host_propagate_lcp2d_f64(
         _p(model.mu_u), _p(model.mu_v), _p(model.sigma_u), _p(model.sigma_v), g.nx, g.ny,
         float(g.dx), float(g.dy), float(isovalue), _p(mu), _p(sg), _p(out), _DEVICE))
@@ -415,7 +488,7 @@ def propagate_lcp(model, isovalue: float) -> tuple[GaussianScalarField, LcpField
 def lcp(fld: GaussianScalarField, isovalue: float, config: ParallelConfig | None = None) -> LcpField:
     """Crossing probability of the isovalue for every grid cell (lcp.py:80-100)."""
     g = fld.grid
-    out = np.empty(g.n_cells)
+    out = _out(g.n_cells)
     _check(lib.divuq_host_lcp2d_f64(_p(fld.mu), _p(fld.sigma), g.nx, g.ny, float(isovalue), _p(out),
                                     _DEVICE))
     return adopt(LcpField, g, isovalue, out)

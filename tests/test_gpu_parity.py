@@ -795,3 +795,37 @@ def test_device_api_launches_on_torch_current_stream(dev, rng):
     side.synchronize()
     for k in base:
         assert torch.equal(o[k], base[k])
+
+
+def test_dropin_output_pool_never_hands_out_live_memory(dev, rng):
+    """Large drop-in results are views of pooled pinned blocks (api._OutputPool):
+    a block is reused only after every array (and view) of an earlier result
+    is gone; results stay bitwise equal to fresh numpy outputs."""
+    import paper_2510_01190_b200 as d
+    from paper_2510_01190_b200 import api
+
+    side = 1024
+    g = d.UniformGrid2(side, side)
+    model = d.GaussianVectorField(g, *random_model_arrays(side * side, rng))
+    r1 = d.propagate_divergence(model)
+    mu1, sg1 = r1.mu.copy(), r1.sigma.copy()
+    assert r1.mu.base is not None and api._POOL._bytes > 0   # pooled, pinned
+    r2 = d.propagate_divergence(model)
+    assert not np.shares_memory(r1.mu, r2.mu) and not np.shares_memory(r1.sigma, r2.sigma)
+    view = r2.mu[::3]
+    keep = view.copy()
+    del r2
+    r3 = d.propagate_divergence(model)
+    assert not np.shares_memory(view, r3.mu) and not np.shares_memory(view, r3.sigma)
+    assert np.array_equal(view, keep)
+    del view
+    r4 = d.propagate_divergence(model)   # free blocks are reused from here on
+    for r in (r1, r3, r4):
+        assert np.array_equal(r.mu, mu1) and np.array_equal(r.sigma, sg1)
+        assert not r.mu.flags.writeable
+    p = d.source_probability(r4, 0.0)
+    q = d.source_probability(r4, 0.0)
+    assert not np.shares_memory(p, q) and np.array_equal(p, q)
+    est = d.fit_gaussian(d.Ensemble2(g, tuple(d.VectorField2(g, *random_model_arrays(side * side, rng)[:2])
+                                               for _ in range(3))))
+    assert np.all(est.sigma_u >= 0) and not np.shares_memory(est.mu_u, r4.mu)
