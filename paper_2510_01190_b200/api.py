@@ -46,7 +46,8 @@ class _OutputPool:
     the C entry with warm outputs, 17 ms with fresh ones).  Results of at
     least ``MIN_BYTES`` are instead views of pooled blocks that were pinned
     once (``divuq_host_register``): the host entries DMA -- or, for small
-    calls, copy-kernel -- straight into them.  A block is reused only when no
+    calls, copy-kernel -- straight into them (from 256 KB: 500^2 results
+    0.6 -> 0.5 ms, 724^2 2.0 -> 0.93 ms, tools/bounce_probe.py).  A block is reused only when no
     array refers to it any more (every result is a view whose ``.base`` is
     the block, so the block's reference count says whether one is alive).
     Pinned bytes are capped (``DIVUQ_OUT_POOL_MB``, default 512; 0 disables
@@ -54,13 +55,14 @@ class _OutputPool:
     is used.  Same values, shapes and dtypes either way.
     """
 
-    MIN_BYTES = 4 << 20
+    MIN_BYTES = 256 << 10
 
     def __init__(self):
         import os
         import threading
 
         self._cap = int(os.environ.get("DIVUQ_OUT_POOL_MB", "512")) << 20
+        self._min = int(os.environ.get("DIVUQ_OUT_POOL_MIN_KB", str(self.MIN_BYTES >> 10))) << 10
         self._blocks: list = []
         self._sentinel = [np.empty(1, np.uint8)]
         self._bytes = 0
@@ -69,7 +71,7 @@ class _OutputPool:
     def empty(self, shape, dtype=np.float64):
         dt = np.dtype(dtype)
         nbytes = int(np.prod(shape)) * dt.itemsize
-        if self._cap <= 0 or nbytes < self.MIN_BYTES:
+        if self._cap <= 0 or nbytes < self._min or nbytes == 0:
             return np.empty(shape, dt)
         with self._lock:
             # a block nothing else refers to has the reference count of the
