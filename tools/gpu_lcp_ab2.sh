@@ -1,0 +1,4 @@
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -x 2>&1 | tail -2
+for rep in 1 2; do for w in lcp lcpfused; do
+  python bench.py --workload $w --steps 50 --no-e2e --no-cpu 2>/dev/null | python3 -c "import json,sys;d=json.loads(sys.stdin.read());print('$w', round(d['ms_per_step']*1e3,1),'us', round(d['roofline']['frac'],3))"
+done; done
