@@ -39,3 +39,18 @@ with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
         call()
 print(prof.key_averages().table(sort_by="self_cpu_time_total", row_limit=8))
 print(prof.key_averages().table(sort_by="self_cuda_time_total", row_limit=6))
+
+# the same call through the drop-in API (types, output records)
+import paper_2510_01190_b200 as d  # noqa: E402
+
+g = d.UniformGrid2(1024, 1024)
+ens = d.Ensemble2(g, tuple(d.VectorField2(g, stacked[k, 0], stacked[k, 1]) for k in range(M)))
+d.fit_gaussian(ens)
+for label, fn in (("drop-in fit_gaussian", lambda: d.fit_gaussian(ens)),
+                  ("np.empty x2 + C entry", lambda: (np.empty((2, N)), np.empty((2, N)), call()))):
+    ts = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        fn()
+        ts.append(time.perf_counter() - t0)
+    print(f"{label}: best {min(ts) * 1e3:.2f} ms, all {[round(t * 1e3, 2) for t in ts]}")

@@ -1,7 +1,7 @@
 # Late-round-2 refresh on one B200 (kernels unchanged since the ncu captures in
 # profiles/r02): GPU tests, smoke, every bench line (ours + reference arm),
-# drop-in / host-path probes.  Output: gpurun_out/r02b/.
-O=gpurun_out/r02b
+# drop-in / host-path probes.  Output: gpurun_out/r02c/.
+O=gpurun_out/r02c
 mkdir -p $O
 nvidia-smi --query-gpu=name,driver_version,clocks.max.sm,memory.total,power.limit --format=csv > $O/box.txt
 lscpu | grep -E "Model name|^CPU\(s\)|Socket" >> $O/box.txt
@@ -24,3 +24,4 @@ timeout 600 python tools/bounce_probe.py > $O/bounce_probe.txt 2>&1
 timeout 600 python tools/device_call_probe.py > $O/device_call_probe.txt 2>&1
 timeout 600 python tools/host_entry_trace.py 128 > $O/host_entry_trace.txt 2>&1
 ls -la $O
+timeout 600 python tools/fit_trace.py 2>&1 | grep -E "ms, all" > $O/fit_trace.txt
