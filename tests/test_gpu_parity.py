@@ -829,3 +829,40 @@ def test_dropin_output_pool_never_hands_out_live_memory(dev, rng):
     est = d.fit_gaussian(d.Ensemble2(g, tuple(d.VectorField2(g, *random_model_arrays(side * side, rng)[:2])
                                                for _ in range(3))))
     assert np.all(est.sigma_u >= 0) and not np.shares_memory(est.mu_u, r4.mu)
+
+
+def test_dropin_calls_from_concurrent_threads(dev, rng):
+    """Host entries from several Python threads at once (ctypes drops the
+    GIL): per-thread streams and bounce arenas, the shared staging ring and
+    host workers, the output pool's lock -- every result bitwise equal to the
+    same call made alone."""
+    import threading
+
+    import paper_2510_01190_b200 as d
+
+    models = []
+    for side in (68, 500, 1024, 300):
+        g = d.UniformGrid2(side, side)
+        models.append(d.GaussianVectorField(g, *random_model_arrays(side * side, rng)))
+    want = [(d.propagate_divergence(m), d.lcp(d.propagate_divergence(m), 0.0)) for m in models]
+    want = [(f.mu.copy(), f.sigma.copy(), c.probabilities.copy()) for f, c in want]
+    errors = []
+
+    def worker(k):
+        try:
+            for _ in range(4):
+                f = d.propagate_divergence(models[k])
+                c = d.lcp(f, 0.0)
+                mu, sg, pr = want[k]
+                if not (np.array_equal(f.mu, mu) and np.array_equal(f.sigma, sg)
+                        and np.array_equal(c.probabilities, pr)):
+                    errors.append(k)
+        except Exception as e:   # noqa: BLE001 -- surfaced below
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=worker, args=(k % 4,)) for k in range(8)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
