@@ -241,7 +241,7 @@ constexpr int kLcpUnroll = DIVUQ_LCP_UNROLL;
 #endif
 constexpr int kLcpTX = 64, kLcpTY = 16, kLcpBX = 32, kLcpBY = 8;
 #ifndef DIVUQ_LCP_TMA_TY
-#define DIVUQ_LCP_TMA_TY 40   // 16: 121.5 us, 24: 114.8, 32: 113.7, 40: 112.6 (4096^2)
+#define DIVUQ_LCP_TMA_TY 32   // fit tails: 16: 121.5 us, 24: 114.8, 32: 113.7, 40: 112.6; table tails + row-run epilogue: 32: 100.5, 40: 101.0 (4096^2)
 #endif
 constexpr int kLcpTYT = DIVUQ_LCP_TMA_TY;   // cell rows per CTA of lcp2d_tma_kernel
 
@@ -505,11 +505,13 @@ namespace divuq {
 // (66 wide).  Out-of-grid slots arrive as 0 and feed only vertices that are
 // never written and cells that are never written.
 // ---------------------------------------------------------------------------
+// row-run epilogue (lcp_tile_cells): 16 rows 172.2 us, 24 rows aliased 167.7,
+// 32 aliased 178.8 (4096^2; before it: 16 rows 180.4, 24 aliased 179.8)
 #ifndef DIVUQ_LCPF_TY
-#define DIVUQ_LCPF_TY 16
+#define DIVUQ_LCPF_TY 24
 #endif
 #ifndef DIVUQ_LCPF_ALIAS
-#define DIVUQ_LCPF_ALIAS 0
+#define DIVUQ_LCPF_ALIAS 1
 #endif
 constexpr int kLcpFY = DIVUQ_LCPF_TY;           // cell rows per CTA of the fused kernel
 constexpr bool kLcpFAlias = DIVUQ_LCPF_ALIAS;   // tail tables over the u boxes (tails held in registers)
