@@ -274,11 +274,20 @@ inline bool pread_span(int fd, char* dst, int64_t len, int64_t off) {
   return true;
 }
 
+inline int io_threads() {   // DIVUQ_IO_THREADS (1..16, default 16)
+  static const int v = [] {
+    const char* e = std::getenv("DIVUQ_IO_THREADS");
+    const int n = e ? std::atoi(e) : 16;
+    return n < 1 ? 1 : (n > 16 ? 16 : n);
+  }();
+  return v;
+}
+
 inline bool pread_parallel(int fd, char* dst, int64_t len, int64_t off) {
   constexpr int kMaxThreads = 16;
   const int64_t kSlice = int64_t(1) << 20;
   const int64_t hw = std::max(1u, std::thread::hardware_concurrency());
-  const int nt = int(std::min<int64_t>(std::min<int64_t>(kMaxThreads, hw), (len + kSlice - 1) / kSlice));
+  const int nt = int(std::min<int64_t>(std::min<int64_t>(io_threads(), hw), (len + kSlice - 1) / kSlice));
   if (nt <= 1) return pread_span(fd, dst, len, off);
   const int64_t per = (len + nt - 1) / nt;
   bool ok[kMaxThreads] = {};
