@@ -245,14 +245,27 @@ def tail_probs(mu, sigma, isovalue: float):
     return below, above
 
 
+def _one_tail(mu, sigma, isovalue: float, above: bool) -> np.ndarray:
+    """One of tail_probs' two maps: only that map is computed and copied back."""
+    mu = _c64(mu)
+    sigma = _c64(sigma)
+    if mu.shape != sigma.shape:
+        raise ValueError("mu and sigma must have the same shape")
+    out = _out(mu.shape, mu.dtype)
+    _check(lib.divuq_host_tail_probs_f64(_p(mu), _p(sigma), mu.size, float(isovalue),
+                                         None if above else _p(out), _p(out) if above else None,
+                                         _DEVICE))
+    return out
+
+
 def source_probability(fld: GaussianScalarField, t: float = 0.0) -> np.ndarray:
     """P(div > t) per vertex: the reference's 'above' tail at isovalue t."""
-    return tail_probs(fld.mu, fld.sigma, t)[1]
+    return _one_tail(fld.mu, fld.sigma, t, above=True)
 
 
 def sink_probability(fld: GaussianScalarField, t: float = 0.0) -> np.ndarray:
     """P(div < -t) per vertex (P(div <= -t) on the sigma == 0 tie, lcp.py:56-59)."""
-    return tail_probs(fld.mu, fld.sigma, -t)[0]
+    return _one_tail(fld.mu, fld.sigma, -t, above=False)
 
 
 def mc_divergence(model: GaussianVectorField, config: McConfig, *,

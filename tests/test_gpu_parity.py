@@ -866,3 +866,21 @@ def test_dropin_calls_from_concurrent_threads(dev, rng):
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("side", [64, 700])
+def test_single_tail_dropins_equal_the_pair(dev, side, rng):
+    """source/sink_probability compute and copy back only their own map: bitwise
+    the matching half of tail_probs (lcp.py:48-68), sigma = 0 ties included."""
+    import paper_2510_01190_b200 as d
+
+    g = d.UniformGrid2(side, side)
+    mu_u, mu_v, s_u, s_v = random_model_arrays(side * side, rng)
+    s_u[::7] = 0.0
+    s_v[::7] = 0.0
+    f = d.propagate_divergence(d.GaussianVectorField(g, mu_u, mu_v, s_u, s_v))
+    for t in (0.0, 0.25):
+        below_neg, _ = d.tail_probs(f.mu, f.sigma, -t)
+        _, above = d.tail_probs(f.mu, f.sigma, t)
+        assert np.array_equal(d.source_probability(f, t), above)
+        assert np.array_equal(d.sink_probability(f, t), below_neg)
