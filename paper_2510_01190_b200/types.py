@@ -58,15 +58,27 @@ _MSG = {
 }
 
 
-def _frozen_array(values, n: int, name: str, dtype=np.float64) -> np.ndarray:
-    """A validated, read-only flat copy of length n (grid.py:21-30's rule)."""
+def _frozen_array(values, n: int, name: str, dtype=np.float64, pinned: bool = False) -> np.ndarray:
+    """A validated, read-only flat copy of length n (grid.py:21-30's rule);
+    ``pinned``: the copy goes to a pooled pinned block when large."""
     out = np.ascontiguousarray(values, dtype=dtype)
     if out.ndim != 1 or out.size != n:
         raise ValueError(_MSG["len"].format(name=name, n=n, shape=out.shape))
     if not np.isfinite(out).all():
         raise ValueError(_MSG["finite"].format(name=name))
-    out = out.copy()
+    out = _pinned_copy(out) if pinned else out.copy()
     out.flags.writeable = False
+    return out
+
+
+def _pinned_copy(a: np.ndarray) -> np.ndarray:
+    """The constructor's defensive copy, made into a pooled pinned block when
+    it is large (_pool.py): the host entries then DMA the model straight from
+    it on every call instead of staging it through host memory again."""
+    from . import _pool
+
+    out = _pool.empty(a.shape, a.dtype)
+    np.copyto(out, a)
     return out
 
 
@@ -74,10 +86,11 @@ def _float_dtype(values) -> np.dtype:
     return np.dtype(np.float32) if np.asarray(values).dtype == np.float32 else np.dtype(np.float64)
 
 
-def _freeze(obj, n: int, names, dtype=np.float64) -> None:
-    """Replace each named array field of a frozen dataclass by its frozen copy."""
+def _freeze(obj, n: int, names, dtype=np.float64, pinned: bool = False) -> None:
+    """Replace each named array field of a frozen dataclass by its frozen copy
+    (``pinned``: for the models the host entries read on every call)."""
     for name in names:
-        object.__setattr__(obj, name, _frozen_array(getattr(obj, name), n, name, dtype))
+        object.__setattr__(obj, name, _frozen_array(getattr(obj, name), n, name, dtype, pinned))
 
 
 def _require_nonneg(obj, names, key: str) -> None:
@@ -270,7 +283,9 @@ class Ensemble2:
     def stacked(self) -> np.ndarray:
         block = self.__dict__.get("_stacked")
         if block is None:
-            block = np.empty((len(self.members), 2, self.grid.n_vertices))
+            from . import _pool   # pinned when large: fit_gaussian DMAs it directly
+
+            block = _pool.empty((len(self.members), 2, self.grid.n_vertices))
             for k, m in enumerate(self.members):
                 block[k, 0], block[k, 1] = m.u, m.v
             object.__setattr__(self, "_stacked", block)
@@ -286,7 +301,7 @@ class GaussianVectorField:
     sigma_v: np.ndarray = field(repr=False)
 
     def __post_init__(self):
-        _freeze(self, self.grid.n_vertices, ("mu_u", "mu_v", "sigma_u", "sigma_v"))
+        _freeze(self, self.grid.n_vertices, ("mu_u", "mu_v", "sigma_u", "sigma_v"), pinned=True)
         _require_nonneg(self, ("sigma_u", "sigma_v"), "sigmas")
 
     def mean_field(self) -> VectorField2:
@@ -300,7 +315,7 @@ class GaussianScalarField:
     sigma: np.ndarray = field(repr=False)
 
     def __post_init__(self):
-        _freeze(self, self.grid.n_vertices, ("mu", "sigma"))
+        _freeze(self, self.grid.n_vertices, ("mu", "sigma"), pinned=True)
         _require_nonneg(self, ("sigma",), "sigma")
 
     def mean_field(self) -> ScalarField2:
@@ -339,7 +354,7 @@ class GaussianVectorField3:
 
     def __post_init__(self):
         sig = ("sigma_u", "sigma_v", "sigma_w")
-        _freeze(self, self.grid.n_vertices, ("mu_u", "mu_v", "mu_w") + sig, _float_dtype(self.mu_u))
+        _freeze(self, self.grid.n_vertices, ("mu_u", "mu_v", "mu_w") + sig, _float_dtype(self.mu_u), True)
         _require_nonneg(self, sig, "sigmas")
 
     @property
@@ -354,7 +369,7 @@ class GaussianScalarField3:
     sigma: np.ndarray = field(repr=False)
 
     def __post_init__(self):
-        _freeze(self, self.grid.n_vertices, ("mu", "sigma"), _float_dtype(self.mu))
+        _freeze(self, self.grid.n_vertices, ("mu", "sigma"), _float_dtype(self.mu), True)
         _require_nonneg(self, ("sigma",), "sigma")
 
 
