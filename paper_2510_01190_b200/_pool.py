@@ -19,7 +19,7 @@ def _p(a):
 
 
 class OutputPool:
-    """Page-locked host blocks for the large results of the drop-in calls.
+    """Page-locked host blocks for the drop-in layer's large arrays.
 
     A fresh ``np.empty`` result of megabytes is unpopulated memory: the copy
     that fills it page-faults every 4 KB (fit_gaussian 1024^2 x 20: 8.7 ms in

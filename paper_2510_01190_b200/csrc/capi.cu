@@ -1224,8 +1224,9 @@ static int64_t bounce_reserve(size_t bytes, cudaStream_t s, int* status) {
     size_t cap = size_t(1) << 20;
     while (cap < need) cap <<= 1;
     cap = std::min(cap, bounce_max());
-    if ((*status = int(cudaHostAlloc(reinterpret_cast<void**>(&b.buf), cap,
-                                     cudaHostAllocPortable | cudaHostAllocMapped)))) {
+    if (cudaHostAlloc(reinterpret_cast<void**>(&b.buf), cap, cudaHostAllocPortable | cudaHostAllocMapped) !=
+        cudaSuccess) {   // no pinned arena (limit reached): the regular paths, not an error
+      cudaGetLastError();
       b.buf = nullptr;
       return -1;
     }
@@ -1738,15 +1739,19 @@ int divuq_fit_gaussian_strided_f32(const float* members, int64_t M, int64_t memb
 // into the returned arrays -- no staging copy, no page faults on fresh
 // output pages (fit_gaussian 1024^2 x 20: 8.7 ms in the C entry, 17 ms with
 // fresh numpy outputs, tools/fit_trace.py).
+// a refusal (no device, the pinned-memory limit) is reported and cleared, so
+// it never surfaces later as a launch's cudaGetLastError
 int divuq_host_register(void* ptr, int64_t bytes) {
   if (!ptr || bytes <= 0) return DIVUQ_EINVAL;
-  DIVUQ_CUDA(cudaHostRegister(ptr, size_t(bytes), cudaHostRegisterPortable | cudaHostRegisterMapped));
-  return DIVUQ_OK;
+  const cudaError_t e = cudaHostRegister(ptr, size_t(bytes), cudaHostRegisterPortable | cudaHostRegisterMapped);
+  if (e != cudaSuccess) cudaGetLastError();
+  return int(e);
 }
 int divuq_host_unregister(void* ptr) {
   if (!ptr) return DIVUQ_EINVAL;
-  DIVUQ_CUDA(cudaHostUnregister(ptr));
-  return DIVUQ_OK;
+  const cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess) cudaGetLastError();
+  return int(e);
 }
 
 // ---- peer memory (CUDA IPC) for the z-slab exchange over NVLink ----------
