@@ -884,3 +884,38 @@ def test_single_tail_dropins_equal_the_pair(dev, side, rng):
         _, above = d.tail_probs(f.mu, f.sigma, t)
         assert np.array_equal(d.source_probability(f, t), above)
         assert np.array_equal(d.sink_probability(f, t), below_neg)
+
+
+def test_dropin_staging_knobs_off_give_the_same_bits(dev, rng, tmp_path):
+    """With the output pool, the bounce arena, the copy kernel and the
+    streaming stores all switched off (the driver's pageable copies and plain
+    numpy outputs), the drop-in results are bitwise the defaults'."""
+    import os
+    import subprocess
+    import sys
+
+    import paper_2510_01190_b200 as d
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    side = 600
+    arrs = random_model_arrays(side * side, rng)
+    np.savez(tmp_path / "in.npz", *arrs)
+    g = d.UniformGrid2(side, side)
+    m = d.GaussianVectorField(g, *arrs)
+    f = d.propagate_divergence(m)
+    want = [f.mu, f.sigma, d.lcp(f, 0.0).probabilities, d.source_probability(f, 0.2)]
+    script = (
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "import paper_2510_01190_b200 as d\n"
+        f"z = np.load({str(tmp_path / 'in.npz')!r}); a = [z[k] for k in sorted(z.files)]\n"
+        f"g = d.UniformGrid2({side}, {side}); f = d.propagate_divergence(d.GaussianVectorField(g, *a))\n"
+        f"np.savez({str(tmp_path / 'out.npz')!r}, f.mu, f.sigma, d.lcp(f, 0.0).probabilities,"
+        " d.source_probability(f, 0.2))\n")
+    env = dict(os.environ, DIVUQ_OUT_POOL_MB="0", DIVUQ_BOUNCE_MAX_KB="0", DIVUQ_ZC_MAX_KB="0",
+               DIVUQ_NT_COPY="0", DIVUQ_ADOPT="0")
+    subprocess.run([sys.executable, "-c", script], env=env, check=True, timeout=300)
+    z = np.load(tmp_path / "out.npz")
+    got = [z[k] for k in sorted(z.files, key=lambda s: int(s.split("_")[1]))]
+    for a, b in zip(got, want):
+        assert np.array_equal(a, b)
